@@ -1,0 +1,127 @@
+/*
+ * hodlr_b200.h -- C ABI of the B200-native HODLR factorize/solve engine.
+ *
+ * Plain pointers, sizes and a cudaStream_t (passed as void*); no torch types.
+ * Every entry point is stream-ordered, allocates nothing (workspace is passed
+ * in) and returns a hodlr_status.  Device pointers are column-major buffers in
+ * the reference's layout (Fig. 3):
+ *   D   leaf a at a*m*m (m x m, ld m)
+ *   U/Y N x rL slab, ld N, level l' in 1..L at columns [(l'-1) r, l' r)
+ *   V   same as U
+ *   K   level l (0..L-1) at ((2^l)-1)*(2r)^2, parent p at +p*(2r)^2 (2r x 2r)
+ *
+ * Each entry point replaces a reference interface (file:line under
+ * /root/reference); see INTEGRATION.md for the Python/ctypes binding.
+ */
+#ifndef HODLR_B200_H
+#define HODLR_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HODLR_OK = 0,
+  HODLR_ERR_ARG = 1,      /* bad argument (shape, size, layout)             */
+  HODLR_ERR_SHAPE = 2,    /* operand shapes disagree                        */
+  HODLR_ERR_SINGULAR = 3, /* a block was flagged singular (see info arrays) */
+  HODLR_ERR_CUDA = 4,     /* CUDA launch / runtime error                    */
+  HODLR_ERR_NCCL = 5      /* collective failure (distributed entry points)  */
+} hodlr_status;
+
+/* dtype tags */
+#define HODLR_F64 0
+#define HODLR_F32 1
+
+/* Library version + last CUDA error string (thread-local, for diagnostics). */
+const char* hodlr_version(void);
+const char* hodlr_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * Batched kernels (reference batched-kernel layer, backend.py)
+ * --------------------------------------------------------------------- */
+
+/* Batched right-looking partial-pivot LU, in place, bit-identical to the
+ * reference (first-max pivot, true division, separately rounded multiply and
+ * subtract, singular guard |piv| <= eps*s*max|orig col|).
+ * Replaces backend.py:481 batched_lu_factor_inplace / :444 _lu_factor_stack.
+ * A: batch blocks of s x s at A + b*strideA (ld lda).
+ * swaps/perm: int32 [batch*s] (0-based, LAPACK-style swaps; P A = A[perm]).
+ * info: int32 [batch], 1 = flagged singular.
+ * Ainv (optional, may be NULL): explicit inverse A^-1 = U^-1 L^-1 P written at
+ * Ainv + b*strideInv (ld ldinv) -- used by the DMMA solve GEMMs. */
+hodlr_status hodlr_getrf_batched(int dtype, int s, int batch, void* A, int64_t lda, int64_t strideA,
+                                 int32_t* swaps, int32_t* perm, int32_t* info, void* Ainv,
+                                 int64_t ldinv, int64_t strideInv, void* stream);
+
+/* Batched LU solve from stored factors: rhs <- A^-1 rhs (gather by perm,
+ * unit-L forward, U backward with true division).
+ * Replaces backend.py:570 batched_lu_solve_inplace / :532 lu_solve_stacks. */
+hodlr_status hodlr_getrs_batched(int dtype, int s, int nrhs, int batch, const void* LU, int64_t lda,
+                                 int64_t strideA, const int32_t* perm, void* B, int64_t ldb,
+                                 int64_t strideB, void* stream);
+
+/* Batched GEMM  C_b <- alpha op(A_b) B_b + beta C_b,  op in {N, T}.
+ * Operand b lives at X + (b / bdiv) * strideX_hi + (b % bdiv) * strideX_lo,
+ * which covers the reference's constant-stride fast path (bdiv = 1) and the
+ * paired-child layouts of the level GEMMs (bdiv = 2).  The product is formed
+ * first and combined afterwards (tmp = op(A)B; C = beta C + alpha tmp),
+ * as in backend.py:282-303.  C may alias B when the whole of C's rows fit
+ * one tile (M <= 64) -- used for in-place inverse applications.
+ * Replaces backend.py:320 batched_gemm, :266 gemm_stacks, :367
+ * grouped_gemm_large (split-K with a fixed reduction order for huge K). */
+hodlr_status hodlr_gemm_batched(int dtype, int transA, int M, int N, int K, double alpha,
+                                const void* A, int64_t lda, int64_t sA_hi, int64_t sA_lo,
+                                const void* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double beta,
+                                void* C, int64_t ldc, int64_t sC_hi, int64_t sC_lo, int batch, int bdiv,
+                                void* work, size_t work_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Whole-phase entry points (SPEC factorization / solver modules)
+ * --------------------------------------------------------------------- */
+
+typedef struct {
+  int64_t n;     /* matrix dimension N = m * 2^L                   */
+  int32_t m;     /* leaf size                                      */
+  int32_t r;     /* uniform off-diagonal rank (ragged -> zero-pad) */
+  int32_t L;     /* tree depth                                     */
+  int32_t dtype; /* HODLR_F64 / HODLR_F32                          */
+} hodlr_desc;
+
+/* Device buffers of a factorization (all owned by the caller). */
+typedef struct {
+  void* D;        /* in: leaf blocks; out: leaf LU                       */
+  void* Dinv;     /* out: leaf inverses (2^L m^2)                        */
+  void* Y;        /* in: U slab; out: Y slab                             */
+  void* V;        /* in: V slab                                          */
+  void* K;        /* out: K LU per level ((2^L - 1) (2r)^2)              */
+  void* Kinv;     /* out: K inverses, same layout                        */
+  int32_t* dswaps; /* out: 2^L m                                          */
+  int32_t* dperm;  /* out: 2^L m                                          */
+  int32_t* dinfo;  /* out: 2^L                                            */
+  int32_t* kswaps; /* out: (2^L - 1) 2r                                   */
+  int32_t* kperm;  /* out: (2^L - 1) 2r                                   */
+  int32_t* kinfo;  /* out: 2^L - 1                                        */
+} hodlr_factors;
+
+/* Workspace bytes for factorize / solve with nrhs columns. */
+size_t hodlr_factorize_workspace(const hodlr_desc* d);
+size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs);
+
+/* Alg. 3.  Singularity is reported in the
+ * info arrays (the host wrapper raises naming level and node). */
+hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* work,
+                             size_t work_bytes, void* stream);
+
+/* Alg. 4: X (N x nrhs, ld ldx) is
+ * overwritten with A^-1 X. */
+hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f, void* X, int64_t ldx, int nrhs,
+                         void* work, size_t work_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HODLR_B200_H */

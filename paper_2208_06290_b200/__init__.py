@@ -1,0 +1,38 @@
+"""B200-native HODLR factorize/solve engine (arXiv 2208.06290 hot path).
+
+Public API mirrors the reference package ``hodlr`` (tree + batched kernel
+layer) and its SPEC factorization/solver contracts; all arithmetic runs in
+hand-written sm_100a CUDA kernels behind the C ABI in ``include/hodlr_b200.h``.
+"""
+
+from .tree import ClusterTree, IndexRange, build_tree, sibling_pairs  # noqa: F401
+from .backend import (  # noqa: F401
+    SERIAL,
+    BlockBatch,
+    BlockRef,
+    LuPivots,
+    SingularBlockError,
+    ThreadedExecutor,
+    as_stack,
+    batched_gemm,
+    batched_lu_factor_inplace,
+    batched_lu_solve_inplace,
+    gemm_stacks,
+    grouped_gemm_large,
+    lu_solve_stacks,
+    parse_executor,
+)
+from .hodlr import (  # noqa: F401
+    HodlrFactorization,
+    HodlrMatrix,
+    HodlrSingularError,
+    factorize,
+    flop_report,
+    logdet,
+    random_hodlr,
+    solve,
+    solve_flops,
+)
+from ._lib import HodlrNativeError, LIB_PATH  # noqa: F401
+
+__version__ = "0.1.0"

@@ -1,0 +1,250 @@
+// C ABI + level-wise factorize / solve drivers (Alg. 3/4).
+//
+// Everything is enqueued on the caller's stream; no allocation, no host sync.
+// Device layout is the reference's (include/hodlr_b200.h).  The factor keeps
+// the reference outputs (leaf LU + pivots, Y slab, K LU + pivots per level) and
+// additionally the explicit inverses D^-1 and K^-1, so every triangular solve of
+// the factor and solve phases becomes a batched DMMA GEMM.
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace hodlr {
+template <typename T>
+hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
+                          int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, cudaStream_t st);
+template <typename T>
+hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
+                          const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX, int identity,
+                          cudaStream_t st);
+hodlr_status gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA_hi,
+                      int64_t sA_lo, const double* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double beta,
+                      double* C, int64_t ldc, int64_t sC_hi, int64_t sC_lo, int batch, int bdiv, void* work,
+                      size_t work_bytes, cudaStream_t st);
+}  // namespace hodlr
+
+using namespace hodlr;
+
+static thread_local std::string g_last_error;
+
+hodlr_status hodlr_set_cuda_error(cudaError_t e) {
+  g_last_error = cudaGetErrorString(e);
+  return HODLR_ERR_CUDA;
+}
+
+extern "C" const char* hodlr_version(void) { return "hodlr_b200 0.1 (sm_100a, fp64 DMMA)"; }
+extern "C" const char* hodlr_last_error(void) { return g_last_error.c_str(); }
+
+static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+// split-K partial-sum area reserved inside every workspace
+static constexpr size_t kSplitBytes = size_t(64) << 20;
+
+static inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------------------------
+// batched kernels
+// ---------------------------------------------------------------------------
+
+extern "C" hodlr_status hodlr_getrf_batched(int dtype, int s, int batch, void* A, int64_t lda, int64_t strideA,
+                                            int32_t* swaps, int32_t* perm, int32_t* info, void* Ainv, int64_t ldinv,
+                                            int64_t strideInv, void* stream) {
+  if (s < 0 || batch < 0 || (s > 0 && lda < s)) return HODLR_ERR_ARG;
+  hodlr_status st;
+  if (dtype == HODLR_F64) {
+    st = launch_getrf<double>(s, batch, 0, (const double*)A, lda, strideA, (double*)A, lda, strideA, swaps, perm, info,
+                              S(stream));
+    if (st == HODLR_OK && Ainv)
+      st = launch_getrs<double>(s, s, batch, (const double*)A, lda, strideA, perm, nullptr, 0, 0, (double*)Ainv, ldinv,
+                                strideInv, 1, S(stream));
+  } else if (dtype == HODLR_F32) {
+    st = launch_getrf<float>(s, batch, 0, (const float*)A, lda, strideA, (float*)A, lda, strideA, swaps, perm, info,
+                             S(stream));
+    if (st == HODLR_OK && Ainv)
+      st = launch_getrs<float>(s, s, batch, (const float*)A, lda, strideA, perm, nullptr, 0, 0, (float*)Ainv, ldinv,
+                               strideInv, 1, S(stream));
+  } else {
+    return HODLR_ERR_ARG;
+  }
+  return st;
+}
+
+extern "C" hodlr_status hodlr_getrs_batched(int dtype, int s, int nrhs, int batch, const void* LU, int64_t lda,
+                                            int64_t strideA, const int32_t* perm, void* B, int64_t ldb,
+                                            int64_t strideB, void* stream) {
+  if (s < 0 || nrhs < 0 || batch < 0) return HODLR_ERR_ARG;
+  if (dtype == HODLR_F64)
+    return launch_getrs<double>(s, nrhs, batch, (const double*)LU, lda, strideA, perm, (const double*)B, ldb, strideB,
+                                (double*)B, ldb, strideB, 0, S(stream));
+  if (dtype == HODLR_F32)
+    return launch_getrs<float>(s, nrhs, batch, (const float*)LU, lda, strideA, perm, (const float*)B, ldb, strideB,
+                               (float*)B, ldb, strideB, 0, S(stream));
+  return HODLR_ERR_ARG;
+}
+
+extern "C" hodlr_status hodlr_gemm_batched(int dtype, int transA, int M, int N, int K, double alpha, const void* A,
+                                           int64_t lda, int64_t sA_hi, int64_t sA_lo, const void* B, int64_t ldb,
+                                           int64_t sB_hi, int64_t sB_lo, double beta, void* C, int64_t ldc,
+                                           int64_t sC_hi, int64_t sC_lo, int batch, int bdiv, void* work,
+                                           size_t work_bytes, void* stream) {
+  if (dtype != HODLR_F64) return HODLR_ERR_ARG;
+  return gemm_f64(transA, M, N, K, alpha, (const double*)A, lda, sA_hi, sA_lo, (const double*)B, ldb, sB_hi, sB_lo,
+                  beta, (double*)C, ldc, sC_hi, sC_lo, batch, bdiv, work, work_bytes, S(stream));
+}
+
+// ---------------------------------------------------------------------------
+// factorize / solve
+// ---------------------------------------------------------------------------
+
+static bool desc_ok(const hodlr_desc* d) {
+  if (!d || d->m < 1 || d->r < 0 || d->L < 0 || d->L > 30) return false;
+  return d->n == (int64_t)d->m << d->L;
+}
+
+// workspace layout (factorize): [split-K | TW | W | leaf tmp (m > 64 only)]
+struct FactWs {
+  size_t split, tw, w, tmp, total;
+};
+static FactWs fact_ws(const hodlr_desc* d) {
+  const int64_t n = d->n, r = d->r, L = d->L;
+  FactWs w{};
+  w.split = kSplitBytes;
+  w.tw = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * r * L);
+  w.w = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * r * (L > 0 ? L - 1 : 0));
+  w.tmp = (d->m > 64) ? align_up(sizeof(double) * (size_t)n * r * L) : 0;
+  w.total = w.split + w.tw + w.w + w.tmp;
+  return w;
+}
+
+extern "C" size_t hodlr_factorize_workspace(const hodlr_desc* d) { return desc_ok(d) ? fact_ws(d).total : 0; }
+
+extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
+  if (!desc_ok(d) || nrhs < 0) return 0;
+  // split-K | w | w2 | tmp (m > 64)
+  const size_t wsz = align_up(sizeof(double) * (size_t)((int64_t)1 << d->L) * d->r * nrhs);
+  const size_t tmp = (d->m > 64) ? align_up(sizeof(double) * (size_t)d->n * nrhs) : 0;
+  return kSplitBytes + 2 * wsz + tmp;
+}
+
+#define TRY(x)                            \
+  do {                                    \
+    hodlr_status s_ = (x);                \
+    if (s_ != HODLR_OK) return s_;        \
+  } while (0)
+
+// X_a <- Dinv_a X_a for all leaves (rows a*m.., ncols columns, ld ldx).
+static hodlr_status apply_leaf_inverse(const hodlr_desc* d, const double* Dinv, double* X, int64_t ldx, int ncols,
+                                       void* split, size_t split_bytes, double* tmp, cudaStream_t st) {
+  const int m = d->m;
+  const int64_t nleaf = (int64_t)1 << d->L;
+  if (m <= 64) {  // whole tile column per CTA: in place is safe
+    return gemm_f64(0, m, ncols, m, 1.0, Dinv, m, (int64_t)m * m, 0, X, ldx, m, 0, 0.0, X, ldx, m, 0, (int)nleaf, 1,
+                    split, split_bytes, st);
+  }
+  TRY(gemm_f64(0, m, ncols, m, 1.0, Dinv, m, (int64_t)m * m, 0, X, ldx, m, 0, 0.0, tmp, d->n, m, 0, (int)nleaf, 1,
+               split, split_bytes, st));
+  if (cudaMemcpy2DAsync(X, ldx * sizeof(double), tmp, d->n * sizeof(double), d->n * sizeof(double), ncols,
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return hodlr_set_cuda_error(cudaGetLastError());
+  return HODLR_OK;
+}
+
+extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* work, size_t work_bytes,
+                                        void* stream) {
+  if (!desc_ok(d) || !f) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
+  const FactWs ws = fact_ws(d);
+  if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
+  cudaStream_t st = S(stream);
+  char* wp = static_cast<char*>(work);
+  void* split = wp;
+  double* TW = reinterpret_cast<double*>(wp + ws.split);
+  double* W = reinterpret_cast<double*>(wp + ws.split + ws.tw);
+  double* tmp = ws.tmp ? reinterpret_cast<double*>(wp + ws.split + ws.tw + ws.w) : nullptr;
+
+  const int64_t n = d->n;
+  const int m = d->m, r = d->r, L = d->L;
+  const int64_t nleaf = (int64_t)1 << L;
+  double* D = (double*)f->D;
+  double* Dinv = (double*)f->Dinv;
+  double* Y = (double*)f->Y;
+  const double* V = (const double*)f->V;
+  double* K = (double*)f->K;
+  double* Kinv = (double*)f->Kinv;
+
+  // (1) leaf getrf (bit-exact) + explicit inverse          Alg.3 l.2
+  TRY(launch_getrf<double>(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, m, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo,
+                           st));
+  TRY(launch_getrs<double>(m, m, (int)nleaf, D, m, (int64_t)m * m, f->dperm, nullptr, 0, 0, Dinv, m, (int64_t)m * m, 1,
+                           st));
+  if (L == 0 || r == 0) return HODLR_OK;
+  // (2) Y(I_a, :) <- D_a^-1 U(I_a, :) for all levels at once       Alg.3 l.3
+  TRY(apply_leaf_inverse(d, Dinv, Y, n, r * L, split, ws.split, tmp, st));
+
+  // (3) levels                                                     Alg.3 l.4-10
+  for (int lv = L - 1; lv >= 0; --lv) {
+    const int nch = 1 << (lv + 1), npar = 1 << lv;
+    const int64_t nc = n >> (lv + 1);
+    const int ncol = r * (lv + 1), wc = r * lv;
+    const int64_t koff = ((int64_t)npar - 1) * 4 * r * r;
+    // [W|T]_c = V_c^T Y(I_c, 0:r(l+1)), paired per parent: 2r x ncol, ld 2r
+    TRY(gemm_f64(1, r, ncol, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, Y, n, 2 * nc, nc, 0.0, TW, 2 * r,
+                 (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
+    // K_p = [[T_2p, I], [I, T_2p+1]] assembled + factored (bit-exact) + inverted
+    TRY(launch_getrf<double>(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff, 2 * r,
+                             (int64_t)4 * r * r, f->kswaps + ((int64_t)npar - 1) * 2 * r,
+                             f->kperm + ((int64_t)npar - 1) * 2 * r, f->kinfo + (npar - 1), st));
+    TRY(launch_getrs<double>(2 * r, 2 * r, npar, K + koff, 2 * r, (int64_t)4 * r * r,
+                             f->kperm + ((int64_t)npar - 1) * 2 * r, nullptr, 0, 0, Kinv + koff, 2 * r,
+                             (int64_t)4 * r * r, 1, st));
+    if (lv == 0) break;
+    // W_p <- K_p^-1 [W_2p; W_2p+1]
+    TRY(gemm_f64(0, 2 * r, wc, 2 * r, 1.0, Kinv + koff, 2 * r, (int64_t)4 * r * r, 0, TW, 2 * r,
+                 (int64_t)2 * r * ncol, 0, 0.0, W, 2 * r, (int64_t)2 * r * wc, 0, npar, 1, split, ws.split, st));
+    // Y(I_c, 0:rl) -= Y_c^{l+1} W_c
+    TRY(gemm_f64(0, (int)nc, wc, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, W, 2 * r, (int64_t)2 * r * wc, r,
+                 1.0, Y, n, 2 * nc, nc, nch, 2, split, ws.split, st));
+  }
+  return HODLR_OK;
+}
+
+extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f, void* Xv, int64_t ldx, int nrhs,
+                                    void* work, size_t work_bytes, void* stream) {
+  if (!desc_ok(d) || !f || nrhs < 0 || ldx < d->n) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
+  if (nrhs == 0) return HODLR_OK;
+  const size_t need = hodlr_solve_workspace(d, nrhs);
+  if (work_bytes < need || !work) return HODLR_ERR_ARG;
+  cudaStream_t st = S(stream);
+  const int64_t n = d->n;
+  const int m = d->m, r = d->r, L = d->L;
+  const size_t wsz = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * nrhs);
+  char* wp = static_cast<char*>(work);
+  void* split = wp;
+  double* w = reinterpret_cast<double*>(wp + kSplitBytes);
+  double* w2 = reinterpret_cast<double*>(wp + kSplitBytes + wsz);
+  double* tmp = (m > 64) ? reinterpret_cast<double*>(wp + kSplitBytes + 2 * wsz) : nullptr;
+  double* X = (double*)Xv;
+  const double* Y = (const double*)f->Y;
+  const double* V = (const double*)f->V;
+  const double* Kinv = (const double*)f->Kinv;
+
+  TRY(apply_leaf_inverse(d, (const double*)f->Dinv, X, ldx, nrhs, split, kSplitBytes, tmp, st));
+  if (r == 0) return HODLR_OK;
+  for (int lv = L - 1; lv >= 0; --lv) {
+    const int nch = 1 << (lv + 1), npar = 1 << lv;
+    const int64_t nc = n >> (lv + 1);
+    const int64_t koff = ((int64_t)npar - 1) * 4 * r * r;
+    // w_c = V_c^T x_c  (paired per parent, 2r x nrhs, ld 2r)
+    TRY(gemm_f64(1, r, nrhs, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w, 2 * r,
+                 (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
+    // w_p <- K_p^-1 w_p
+    TRY(gemm_f64(0, 2 * r, nrhs, 2 * r, 1.0, Kinv + koff, 2 * r, (int64_t)4 * r * r, 0, w, 2 * r,
+                 (int64_t)2 * r * nrhs, 0, 0.0, w2, 2 * r, (int64_t)2 * r * nrhs, 0, npar, 1, split, kSplitBytes, st));
+    // x_c -= Y_c w_c
+    TRY(gemm_f64(0, (int)nc, nrhs, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, w2, 2 * r, (int64_t)2 * r * nrhs,
+                 r, 1.0, X, ldx, 2 * nc, nc, nch, 2, split, kSplitBytes, st));
+  }
+  return HODLR_OK;
+}

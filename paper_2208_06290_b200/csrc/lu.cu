@@ -1,0 +1,250 @@
+// Batched LU factor (bit-exact replay of the reference) and LU solve / inverse.
+//
+//   getrf_kernel  <- backend.py:444-478 _lu_factor_stack (one CTA per block)
+//   getrs_kernel  <- backend.py:546-567 _lu_solve_stack (also builds A^-1 = U^-1 L^-1 P
+//                    by solving against the permuted identity)
+//
+// The factor is computed in shared memory.  Bit-exactness with numpy comes from
+// replaying the same IEEE operations in the same order: first-max pivot (NaN
+// wins, first index on ties, as np.argmax), whole-row swaps, true division by
+// the pivot (0 -> 1), and the outer-product update rounded as a separate
+// multiply then subtract (__dmul_rn / __dsub_rn: no FMA contraction).
+#include "common.cuh"
+
+namespace hodlr {
+
+template <typename T>
+__device__ __forceinline__ bool is_nan(T v) {
+  return v != v;
+}
+
+template <typename T>
+__device__ __forceinline__ T nan_max(T a, T b) {
+  if (is_nan(a)) return a;
+  if (is_nan(b)) return b;
+  return a > b ? a : b;
+}
+
+// np.argmax order on (|value|, index): NaN first, then larger, then smaller index.
+template <typename T>
+__device__ __forceinline__ bool pivot_better(T v, int i, T best, int bi) {
+  if (bi < 0) return true;
+  bool vn = is_nan(v), bn = is_nan(best);
+  if (bn) return vn && i < bi;
+  if (vn) return true;
+  return v > best || (v == best && i < bi);
+}
+
+// Input modes: 0 = plain strided blocks; 1 = K-block assembly
+//   K_p = [[T_2p, I], [I, T_2p+1]] from the paired [W|T] panel of parent p
+//   (2r x .. , ld lds): T block for row half h sits at src[h*r + i + j*lds].
+template <typename T>
+__global__ void __launch_bounds__(256) getrf_kernel(int s, int mode, const T* __restrict__ src, int64_t lds,
+                                                    int64_t strides, T* out, int64_t ldo, int64_t strideo,
+                                                    int32_t* __restrict__ swaps, int32_t* __restrict__ perm,
+                                                    int32_t* __restrict__ info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* a = reinterpret_cast<T*>(smem_raw);  // s x s, column-major, ld s
+  T* colmax = a + s * s;
+  int* pm = reinterpret_cast<int*>(colmax + s);
+  __shared__ int piv_row;
+  __shared__ int singular;
+
+  const int64_t blk = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const T* g = src + blk * strides;
+
+  if (mode == 0) {
+    for (int j = warp; j < s; j += 8)
+      for (int i = lane; i < s; i += 32) a[i + j * s] = g[i + j * lds];
+  } else {
+    const int r = s >> 1;
+    for (int j = warp; j < s; j += 8)
+      for (int i = lane; i < s; i += 32) {
+        T v;
+        if (i < r && j < r)
+          v = g[i + j * lds];
+        else if (i >= r && j >= r)
+          v = g[i + (j - r) * lds];
+        else
+          v = (i < r) ? (T)(i == j - r) : (T)(i - r == j);
+        a[i + j * s] = v;
+      }
+  }
+  if (t < s) pm[t] = t;
+  if (t == 0) singular = 0;
+  __syncthreads();
+  // original per-column magnitudes (np.abs(a).max(axis=1), NaN-propagating)
+  for (int j = warp; j < s; j += 8) {
+    T m = (T)0;
+    for (int i = lane; i < s; i += 32) m = nan_max(m, (T)fabs((double)a[i + j * s]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) colmax[j] = m;
+  }
+  __syncthreads();
+
+  const T thr_scale = mul_rn(Eps<T>::v, (T)s);
+  for (int k = 0; k < s; ++k) {
+    if (warp == 0) {
+      T best = (T)0;
+      int bi = -1;
+      for (int i = k + lane; i < s; i += 32) {
+        T v = (T)fabs((double)a[i + k * s]);
+        if (pivot_better(v, i, best, bi)) {
+          best = v;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        T ov = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi >= 0 && pivot_better(ov, oi, best, bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) piv_row = bi;
+    }
+    __syncthreads();
+    const int p = piv_row;
+    if (p != k) {
+      for (int j = t; j < s; j += 256) {
+        T x = a[k + j * s];
+        a[k + j * s] = a[p + j * s];
+        a[p + j * s] = x;
+      }
+      if (t == 0) {
+        int q = pm[k];
+        pm[k] = pm[p];
+        pm[p] = q;
+      }
+    }
+    if (t == 0) swaps[blk * s + k] = p;
+    __syncthreads();
+    const T piv = a[k + k * s];
+    if (t == 0 && (T)fabs((double)piv) <= mul_rn(thr_scale, colmax[k])) singular = 1;
+    if (k + 1 < s) {
+      const T d = (piv == (T)0) ? (T)1 : piv;
+      for (int i = k + 1 + t; i < s; i += 256) a[i + k * s] = div_rn(a[i + k * s], d);
+      __syncthreads();
+      for (int j = k + 1 + warp; j < s; j += 8) {
+        const T u = a[k + j * s];
+        for (int i = k + 1 + lane; i < s; i += 32) a[i + j * s] = sub_rn(a[i + j * s], mul_rn(a[i + k * s], u));
+      }
+      __syncthreads();
+    }
+  }
+  T* o = out + blk * strideo;
+  for (int j = warp; j < s; j += 8)
+    for (int i = lane; i < s; i += 32) o[i + j * ldo] = a[i + j * s];
+  if (t < s) perm[blk * s + t] = pm[t];
+  if (t == 0) info[blk] = singular;
+}
+
+// X_chunk <- A^-1 B_chunk from stored LU + perm.  identity=1 uses B = I, so the
+// result is the explicit inverse U^-1 L^-1 P.  One CTA per (block, column chunk).
+template <typename T>
+__global__ void __launch_bounds__(256) getrs_kernel(int s, int nrhs, int cw, const T* __restrict__ LU, int64_t lda,
+                                                    int64_t strideA, const int32_t* __restrict__ perm, const T* B,
+                                                    int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX,
+                                                    int identity) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* lu = reinterpret_cast<T*>(smem_raw);  // s x s ld s
+  T* x = lu + s * s;                       // cw columns, ld s
+  int* pm = reinterpret_cast<int*>(x + cw * s);
+  const int nchunk = (nrhs + cw - 1) / cw;
+  const int64_t blk = blockIdx.x / nchunk;
+  const int c0 = (blockIdx.x % nchunk) * cw;
+  const int ncols = min(cw, nrhs - c0);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+  const T* g = LU + blk * strideA;
+  for (int j = warp; j < s; j += 8)
+    for (int i = lane; i < s; i += 32) lu[i + j * s] = g[i + j * lda];
+  if (t < s) pm[t] = perm[blk * s + t];
+  __syncthreads();
+  if (identity) {
+    for (int c = warp; c < ncols; c += 8)
+      for (int i = lane; i < s; i += 32) x[c * s + i] = (T)(pm[i] == c0 + c);
+  } else {
+    const T* gb = B + blk * strideB;
+    for (int c = warp; c < ncols; c += 8)
+      for (int i = lane; i < s; i += 32) x[c * s + i] = gb[pm[i] + (int64_t)(c0 + c) * ldb];
+  }
+  __syncthreads();
+  for (int j = 0; j + 1 < s; ++j) {
+    for (int c = warp; c < ncols; c += 8) {
+      const T xj = x[c * s + j];
+      for (int i = j + 1 + lane; i < s; i += 32) x[c * s + i] -= lu[i + j * s] * xj;
+    }
+    __syncthreads();
+  }
+  for (int j = s - 1; j >= 0; --j) {
+    if (t < ncols) x[t * s + j] = x[t * s + j] / lu[j + j * s];
+    __syncthreads();
+    for (int c = warp; c < ncols; c += 8) {
+      const T xj = x[c * s + j];
+      for (int i = lane; i < j; i += 32) x[c * s + i] -= lu[i + j * s] * xj;
+    }
+    __syncthreads();
+  }
+  T* gx = X + blk * strideX;
+  for (int c = warp; c < ncols; c += 8)
+    for (int i = lane; i < s; i += 32) gx[i + (int64_t)(c0 + c) * ldx] = x[c * s + i];
+}
+
+template <typename T>
+static size_t getrf_smem(int s) {
+  return (size_t)s * s * sizeof(T) + s * sizeof(T) + s * sizeof(int) + 16;
+}
+template <typename T>
+static size_t getrs_smem(int s, int cw) {
+  return (size_t)s * s * sizeof(T) + (size_t)cw * s * sizeof(T) + s * sizeof(int) + 16;
+}
+
+template <typename T>
+hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
+                          int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, cudaStream_t st) {
+  if (batch == 0 || s == 0) return HODLR_OK;
+  size_t sm = getrf_smem<T>(s);
+  if (sm > 227 * 1024) return HODLR_ERR_ARG;
+  cudaFuncSetAttribute(getrf_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  getrf_kernel<T><<<batch, 256, sm, st>>>(s, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+template <typename T>
+hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
+                          const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX, int identity,
+                          cudaStream_t st) {
+  if (batch == 0 || s == 0 || nrhs == 0) return HODLR_OK;
+  int cw = nrhs < 64 ? nrhs : 64;
+  size_t sm = getrs_smem<T>(s, cw);
+  while (sm > 227 * 1024 && cw > 8) {
+    cw >>= 1;
+    sm = getrs_smem<T>(s, cw);
+  }
+  if (sm > 227 * 1024) return HODLR_ERR_ARG;
+  const int64_t grid = (int64_t)batch * ((nrhs + cw - 1) / cw);
+  if (grid > 2147483647LL) return HODLR_ERR_ARG;
+  cudaFuncSetAttribute(getrs_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  getrs_kernel<T><<<(unsigned)grid, 256, sm, st>>>(s, nrhs, cw, LU, lda, strideA, perm, B, ldb, strideB, X, ldx,
+                                                    strideX, identity);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+template hodlr_status launch_getrf<double>(int, int, int, const double*, int64_t, int64_t, double*, int64_t, int64_t,
+                                           int32_t*, int32_t*, int32_t*, cudaStream_t);
+template hodlr_status launch_getrf<float>(int, int, int, const float*, int64_t, int64_t, float*, int64_t, int64_t,
+                                          int32_t*, int32_t*, int32_t*, cudaStream_t);
+template hodlr_status launch_getrs<double>(int, int, int, const double*, int64_t, int64_t, const int32_t*,
+                                           const double*, int64_t, int64_t, double*, int64_t, int64_t, int,
+                                           cudaStream_t);
+template hodlr_status launch_getrs<float>(int, int, int, const float*, int64_t, int64_t, const int32_t*, const float*,
+                                          int64_t, int64_t, float*, int64_t, int64_t, int, cudaStream_t);
+
+}  // namespace hodlr

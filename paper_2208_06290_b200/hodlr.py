@@ -1,0 +1,395 @@
+"""HODLR container, factorization and solver on the B200 (SPEC modules
+``hodlr_matrix`` / ``factorization`` / ``solver``).
+
+Same operation names and semantics as the reference's SPEC API:
+
+* :class:`HodlrMatrix` -- D_big (leaf blocks, leaf order), U_big / V_big
+  level-concatenated N x rL column-major slabs (Fig. 3), uniform
+  rank r, N = m 2^L; device-resident flat torch tensors.
+* :func:`factorize` (PAPER Alg. 3) consumes ``h``: Y
+  overwrites U in place and D holds its LU factors.
+* :func:`solve` (PAPER Alg. 4) never mutates ``b``.
+* :func:`logdet`, :func:`flop_report`, :func:`storage_report`.
+
+All arithmetic runs in the sm_100a library through the C ABI; this module only
+allocates device buffers and checks status / singular flags.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .backend import LuPivots, lu_factor_flops, lu_solve_flops, gemm_flops
+from .tree import ClusterTree, build_tree
+
+VARIANTS = ("pivoted_standard",)
+
+
+class HodlrSingularError(RuntimeError):
+    """A leaf block or K_gamma is singular to working precision."""
+
+    def __init__(self, what: str, level: int, nodes):
+        self.what, self.level, self.nodes = what, level, list(nodes)
+        super().__init__(f"singular {what} block at level {level}, node(s) {self.nodes}")
+
+
+def _torch():
+    return _lib.require_cuda()
+
+
+def _dtype_tag(t) -> int:
+    import torch
+
+    if t.dtype == torch.float64:
+        return _lib.F64
+    if t.dtype == torch.float32:
+        return _lib.F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+@dataclass
+class HodlrMatrix:
+    """Uniform-rank HODLR matrix in the concatenated big-matrix layout."""
+
+    tree: ClusterTree
+    rank: int
+    D: "object"  # torch (2^L m^2,)  leaf a at a*m*m, column-major
+    U: "object"  # torch (N r L,)   ld N, level l' at columns (l'-1) r
+    V: "object"  # torch (N r L,)
+
+    @property
+    def n(self) -> int:
+        return self.tree.n
+
+    @property
+    def L(self) -> int:
+        return self.tree.depth
+
+    @property
+    def m(self) -> int:
+        return self.tree.n >> self.tree.depth
+
+    @property
+    def dtype(self):
+        return self.D.dtype
+
+    def desc(self) -> _lib.Desc:
+        return _lib.Desc(self.n, self.m, self.rank, self.L, _dtype_tag(self.D))
+
+    @classmethod
+    def from_buffers(cls, n: int, m: int, r: int, D, U, V, device="cuda") -> "HodlrMatrix":
+        """Wrap flat buffers (numpy or torch) in the reference layout; copies to ``device``."""
+        torch = _torch()
+        L = int(round(math.log2(n // m))) if n >= m else 0
+        if n != m << L:
+            raise ValueError(f"GPU layout needs N = m 2^L (got N={n}, m={m})")
+        tree = ClusterTree(n, L)
+
+        def dev(x, size, name):
+            t = torch.as_tensor(x).reshape(-1).to(device)
+            if t.numel() != size:
+                raise ValueError(f"{name} has {t.numel()} entries, expected {size}")
+            return t.contiguous()
+
+        return cls(tree, r, dev(D, (1 << L) * m * m, "D"), dev(U, n * r * L, "U"), dev(V, n * r * L, "V"))
+
+    def clone(self) -> "HodlrMatrix":
+        return HodlrMatrix(self.tree, self.rank, self.D.clone(), self.U.clone(), self.V.clone())
+
+    def storage_report(self) -> dict:
+        """Scalar counts vs Thm. 2: diag m N, bases 2 r N L."""
+        n, m, r, L = self.n, self.m, self.rank, self.L
+        es = self.D.element_size()
+        return {
+            "scalars_diagonal": m * n,
+            "scalars_bases": 2 * r * n * L,
+            "bytes_diagonal": m * n * es,
+            "bytes_bases": 2 * r * n * L * es,
+            "formula_prediction": m * n + 2 * r * n * L,
+            "factorization_scalars_thm2": m * n + r * n * L,
+        }
+
+    def matvec(self, x):
+        """A x on the device (block-wise U (V^T x)); x is (N,) or (N, k) torch."""
+        torch = _torch()
+        n, m, r, L = self.n, self.m, self.rank, self.L
+        X = x.reshape(n, -1)
+        Dm = self.D.view(1 << L, m, m).transpose(1, 2)  # row-major view of column-major blocks
+        y = torch.bmm(Dm, X.view(1 << L, m, -1)).reshape(n, -1)
+        for lv in range(1, L + 1):
+            nl = n >> lv
+            U = self.U[(lv - 1) * r * n : lv * r * n].view(r, n).t()  # (n, r)
+            V = self.V[(lv - 1) * r * n : lv * r * n].view(r, n).t()
+            Ub = U.reshape(1 << (lv - 1), 2, nl, r)
+            Vb = V.reshape(1 << (lv - 1), 2, nl, r)
+            Xb = X.reshape(1 << (lv - 1), 2, nl, -1)
+            w = torch.einsum("pcir,pcik->pcrk", Vb, Xb)  # V_c^T x_c
+            # A[I_a, I_b] = U_a V_b^T: child 0 receives U_0 w_1, child 1 receives U_1 w_0
+            contrib = torch.einsum("pcir,pcrk->pcik", Ub, w.flip(1))
+            y += contrib.reshape(n, -1)
+        return y.reshape(x.shape)
+
+    def reconstruct_dense(self):
+        torch = _torch()
+        n = self.n
+        if n > 8192:
+            raise ValueError("reconstruct_dense size guard (n > 8192)")
+        return self.matvec(torch.eye(n, dtype=self.dtype, device=self.D.device))
+
+
+@dataclass
+class HodlrFactorization:
+    """In-place product form plus the explicit inverses."""
+
+    tree: ClusterTree
+    rank: int
+    D: "object"     # leaf LU
+    Dinv: "object"  # leaf inverses
+    Y: "object"     # Y slab (overwrote U)
+    V: "object"
+    K: "object"     # K LU, level l at (2^l - 1)(2r)^2
+    Kinv: "object"
+    dswaps: "object"
+    dperm: "object"
+    dinfo: "object"
+    kswaps: "object"
+    kperm: "object"
+    kinfo: "object"
+    variant: str = "pivoted_standard"
+    flops: dict = field(default_factory=dict)
+
+    @property
+    def n(self):
+        return self.tree.n
+
+    @property
+    def L(self):
+        return self.tree.depth
+
+    @property
+    def m(self):
+        return self.tree.n >> self.tree.depth
+
+    def desc(self) -> _lib.Desc:
+        return _lib.Desc(self.n, self.m, self.rank, self.L, _dtype_tag(self.D))
+
+    def cfactors(self) -> _lib.Factors:
+        p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        return _lib.Factors(
+            p(self.D), p(self.Dinv), p(self.Y), p(self.V), p(self.K), p(self.Kinv),
+            p(self.dswaps), p(self.dperm), p(self.dinfo), p(self.kswaps), p(self.kperm), p(self.kinfo),
+        )
+
+    def leaf_pivots(self) -> LuPivots:
+        nl, m = 1 << self.L, self.m
+        sw = self.dswaps.view(nl, m).cpu().numpy().astype(np.int64)
+        pm = self.dperm.view(nl, m).cpu().numpy().astype(np.int64)
+        return LuPivots(sw, pm, [int(i) for i in np.flatnonzero(self.dinfo.cpu().numpy())])
+
+    def k_pivots(self, level: int) -> LuPivots:
+        r2, npar = 2 * self.rank, 1 << level
+        lo = (npar - 1) * r2
+        sw = self.kswaps[lo : lo + npar * r2].view(npar, r2).cpu().numpy().astype(np.int64)
+        pm = self.kperm[lo : lo + npar * r2].view(npar, r2).cpu().numpy().astype(np.int64)
+        info = self.kinfo[npar - 1 : 2 * npar - 1].cpu().numpy()
+        return LuPivots(sw, pm, [int(i) for i in np.flatnonzero(info)])
+
+    def k_block(self, level: int):
+        r2, npar = 2 * self.rank, 1 << level
+        lo = (npar - 1) * r2 * r2
+        return self.K[lo : lo + npar * r2 * r2]
+
+
+_WS_CACHE: dict = {}
+
+
+def _workspace(nbytes: int, device):
+    """Reusable device workspace (bytes), grown on demand."""
+    torch = _torch()
+    key = (str(device),)
+    buf = _WS_CACHE.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+    return buf
+
+
+def flop_report(n: int, m: int, r: int) -> dict:
+    """Per-phase factor flops with the reference counters (backend.py:240-251)."""
+    L = int(round(math.log2(n // m)))
+    nl = 1 << L
+    rep = {
+        "leaf_getrf": lu_factor_flops(m) * nl,
+        "leaf_getrs": lu_solve_flops(m, r * L) * nl if L else 0,
+        "tw_gemm": 0, "k_getrf": 0, "k_getrs": 0, "update_gemm": 0, "per_level_gemm": {},
+    }
+    for lv in range(L):
+        nc = n >> (lv + 1)
+        tw = gemm_flops(r, nc, r * (lv + 1)) * (1 << (lv + 1))
+        up = gemm_flops(nc, r, r * lv) * (1 << (lv + 1)) if lv else 0
+        rep["tw_gemm"] += tw
+        rep["update_gemm"] += up
+        rep["k_getrf"] += lu_factor_flops(2 * r) * (1 << lv)
+        rep["k_getrs"] += lu_solve_flops(2 * r, r * lv) * (1 << lv) if lv else 0
+        rep["per_level_gemm"][lv] = tw + up
+    rep["total"] = sum(v for k, v in rep.items() if k != "per_level_gemm")
+    return rep
+
+
+def solve_flops(n: int, m: int, r: int, nrhs: int = 1) -> int:
+    """2mN + 4rNL + 8r^2(2^L - 1) per column (Thm. 4 plus the K term)."""
+    L = int(round(math.log2(n // m)))
+    return nrhs * (2 * m * n + 4 * r * n * L + 8 * r * r * ((1 << L) - 1))
+
+
+def factorize(h: HodlrMatrix, variant: str = "pivoted_standard", check: bool = True, stream=None) -> HodlrFactorization:
+    """Level-wise batched factorization (PAPER Alg. 3).  Consumes ``h``.
+
+    Raises :class:`HodlrSingularError` naming level and node when a leaf or
+    K_gamma block is flagged singular.
+    """
+    torch = _torch()
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r} (supported: {VARIANTS})")
+    if h.D.dtype != torch.float64:
+        raise NotImplementedError("the factorization path is fp64 in this build")
+    lib = _lib.load()
+    dev = h.D.device
+    n, m, r, L = h.n, h.m, h.rank, h.L
+    nl = 1 << L
+    nk = nl - 1
+    i32 = dict(dtype=torch.int32, device=dev)
+    f = HodlrFactorization(
+        tree=h.tree, rank=r, D=h.D, Dinv=torch.empty_like(h.D), Y=h.U, V=h.V,
+        K=torch.empty(nk * 4 * r * r, dtype=h.D.dtype, device=dev),
+        Kinv=torch.empty(nk * 4 * r * r, dtype=h.D.dtype, device=dev),
+        dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
+        kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
+        kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r),
+    )
+    desc = h.desc()
+    wsb = lib.hodlr_factorize_workspace(C.byref(desc))
+    ws = _workspace(wsb, dev)
+    st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    cf = f.cfactors()
+    _lib.check(lib.hodlr_factorize(C.byref(desc), C.byref(cf), C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st)),
+               "hodlr_factorize")
+    if check:
+        _raise_if_singular(f)
+    return f
+
+
+def _raise_if_singular(f: HodlrFactorization) -> None:
+    torch = _torch()
+    flags = torch.cat([f.dinfo, f.kinfo]).cpu().numpy()
+    if not flags.any():
+        return
+    nl = 1 << f.L
+    bad = np.flatnonzero(flags[:nl])
+    if bad.size:
+        raise HodlrSingularError("leaf", f.L, bad.tolist())
+    kf = flags[nl:]
+    for lv in range(f.L):
+        seg = kf[(1 << lv) - 1 : (2 << lv) - 1]
+        if seg.any():
+            raise HodlrSingularError("K", lv, np.flatnonzero(seg).tolist())
+
+
+def solve(fact: HodlrFactorization, b, stream=None):
+    """x = A^-1 b (PAPER Alg. 4).  ``b``: (N,) or (N, k), torch (device or host)
+    or numpy; the result has the same kind/shape and ``b`` is not modified."""
+    torch = _torch()
+    lib = _lib.load()
+    is_np = isinstance(b, np.ndarray)
+    bt = torch.from_numpy(np.ascontiguousarray(b)) if is_np else b
+    n = fact.n
+    if bt.shape[0] != n or bt.dim() not in (1, 2):
+        raise ValueError(f"rhs must have {n} rows (got shape {tuple(bt.shape)})")
+    nrhs = 1 if bt.dim() == 1 else bt.shape[1]
+    dev = fact.D.device
+    # column-major device copy: (nrhs, n) row-major == (n, nrhs) column-major
+    x = bt.reshape(n, nrhs).t().to(device=dev, dtype=fact.D.dtype).contiguous()
+    if x.data_ptr() == bt.data_ptr():
+        x = x.clone()
+    desc = fact.desc()
+    wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
+    ws = _workspace(wsb, dev)
+    st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    cf = fact.cfactors()
+    _lib.check(
+        lib.hodlr_solve(C.byref(desc), C.byref(cf), C.c_void_p(x.data_ptr()), n, nrhs, C.c_void_p(ws.data_ptr()),
+                        wsb, C.c_void_p(st)),
+        "hodlr_solve",
+    )
+    out = x.t().reshape(bt.shape)
+    if is_np:
+        return out.cpu().numpy()
+    return out.to(bt.device) if bt.device != dev else out
+
+
+def logdet(fact: HodlrFactorization):
+    """(log|det A|, sign) from the stored LU diagonals.
+
+    det(I + Z X^T) = det(I + X^T Z) = det(K_p) (-1)^{r_a r_b}: K_p is
+    I + X^T Z with its two r-wide block columns exchanged.
+    """
+    torch = _torch()
+    n, m, r, L = fact.n, fact.m, fact.rank, fact.L
+    nl = 1 << L
+    dd = fact.D.view(nl, m, m).diagonal(dim1=1, dim2=2)
+    logabs = torch.log(dd.abs()).sum()
+    neg = (dd < 0).sum()
+    ar = torch.arange(m, device=dd.device, dtype=torch.int32)
+    nswap = (fact.dswaps.view(nl, m) != ar).sum()
+    if L:
+        nk, r2 = nl - 1, 2 * r
+        kd = fact.K.view(nk, r2, r2).diagonal(dim1=1, dim2=2)
+        logabs = logabs + torch.log(kd.abs()).sum()
+        neg = neg + (kd < 0).sum()
+        ak = torch.arange(r2, device=dd.device, dtype=torch.int32)
+        nswap = nswap + (fact.kswaps[: nk * r2].view(nk, r2) != ak).sum()
+        blockswap = nk * (r * r % 2)
+    else:
+        blockswap = 0
+    parity = (int(neg) + int(nswap) + blockswap) % 2
+    return float(logabs), (-1.0 if parity else 1.0)
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs (SURVEY.md §8d exact-HODLR stand-in), generated on device
+# ---------------------------------------------------------------------------
+
+
+def random_hodlr(n: int, m: int, r: int, seed: int = 0, s: float = 1.0, device="cuda", dtype=None) -> HodlrMatrix:
+    """Seeded exact uniform-rank HODLR generated directly in HBM.
+
+    D_a = N(0,1)/sqrt(m) + 4 I; level-l U ~ N(0, s^2/n_l), V ~ N(0, 1/n_l).
+    (Same distribution as the oracle's numpy generator; different stream.)
+    """
+    torch = _torch()
+    dtype = dtype or torch.float64
+    L = int(round(math.log2(n // m)))
+    if n != m << L:
+        raise ValueError("need N = m 2^L")
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    nl = 1 << L
+    D = torch.randn(nl * m * m, generator=g, device=device, dtype=dtype).mul_(1.0 / math.sqrt(m))
+    D.view(nl, m, m).diagonal(dim1=1, dim2=2).add_(4.0)
+    U = torch.randn(n * r * L, generator=g, device=device, dtype=dtype)
+    V = torch.randn(n * r * L, generator=g, device=device, dtype=dtype)
+    for lv in range(1, L + 1):
+        nlv = n >> lv
+        sl = slice((lv - 1) * r * n, lv * r * n)
+        U[sl].mul_(s / math.sqrt(nlv))
+        V[sl].mul_(1.0 / math.sqrt(nlv))
+    return HodlrMatrix(ClusterTree(n, L), r, D, U, V)
+
+
+def tree_for(n: int, leaf_size: int) -> ClusterTree:
+    return build_tree(n, leaf_size)

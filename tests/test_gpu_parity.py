@@ -1,0 +1,167 @@
+"""GPU parity: the sm_100a path vs the CPU oracle and the reference golden vectors.
+
+Bars (BASELINE.json north_star): leaf/K pivot indices bit-exact, leaf LU
+factors bit-exact (the kernel replays the reference's IEEE op order), Y / K /
+x within 1e-10 relative (fp64) of the oracle, which is itself bit-identical to
+the reference kernels (tests/golden/make_golden.py).
+"""
+
+from __future__ import annotations
+
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import hodlr_oracle as orc  # noqa: E402
+import paper_2208_06290_b200 as hb  # noqa: E402
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+TOL = 1e-10  # fp64 solution / factor agreement (north_star)
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def to_gpu(h: orc.HodlrData) -> hb.HodlrMatrix:
+    return hb.HodlrMatrix.from_buffers(h.lay.n, h.lay.m, h.lay.r, h.D, h.U, h.V)
+
+
+def golden_cases():
+    return sorted(p for p in GOLDEN.glob("n*.npz"))
+
+
+@pytest.mark.parametrize("path", golden_cases(), ids=lambda p: p.stem)
+def test_golden_factor_and_solve(path):
+    g = np.load(path)
+    n, m, r = int(g["n"]), int(g["m"]), int(g["r"])
+    h = orc.make_exact_hodlr(n, m, r, seed=int(g["seed"]), s=float(g["s"]))
+    f = hb.factorize(to_gpu(h))
+    L = f.L
+    # leaf LU: factors and pivots bit-exact
+    assert np.array_equal(f.D.cpu().numpy(), g["D_lu"])
+    assert np.array_equal(f.dperm.cpu().numpy().reshape(-1, m), g["d_perm"])
+    assert np.array_equal(f.dswaps.cpu().numpy().reshape(-1, m), g["d_swaps"])
+    # K pivots bit-exact, Y and K factors to tolerance
+    assert np.array_equal(f.kswaps.cpu().numpy().reshape(-1, 2 * r), g["k_swaps"])
+    assert np.array_equal(f.kperm.cpu().numpy().reshape(-1, 2 * r), g["k_perm"])
+    assert rel(f.Y.cpu().numpy(), g["Y"]) <= TOL
+    assert rel(f.K.cpu().numpy(), g["K"]) <= TOL
+    x = hb.solve(f, g["b"])
+    assert rel(x, g["x"]) <= TOL
+    la, sg = hb.logdet(f)
+    assert sg == float(g["logdet_sign"])
+    assert abs(la - float(g["logdet"])) <= 1e-10 * abs(float(g["logdet"]))
+    assert L == int(round(math.log2(n // m)))
+
+
+def test_spec_2x2_worked_example():
+    # [[2,1],[1,2]], tree(2,1)
+    h = hb.HodlrMatrix.from_buffers(2, 1, 1, np.array([2.0, 2.0]), np.array([1.0, 1.0]), np.array([1.0, 1.0]))
+    f = hb.factorize(h)
+    assert f.Y.cpu().tolist() == [0.5, 0.5]
+    g = np.load(GOLDEN / "spec_2x2.npz")
+    assert f.K.cpu().numpy().tolist() == g["K_lu"].tolist()
+    x = hb.solve(f, np.array([3.0, 3.0]))
+    assert np.allclose(x, [1.0, 1.0], rtol=0, atol=1e-15)
+    la, sg = hb.logdet(f)
+    assert abs(la - math.log(3.0)) < 1e-15 and sg == 1.0
+
+
+def test_identity_hodlr_solves_to_b():
+    n, m, r = 256, 32, 4
+    L = 3
+    D = np.zeros((1 << L) * m * m)
+    for a in range(1 << L):
+        D[a * m * m + np.arange(m) * (m + 1)] = 1.0
+    U = np.zeros(n * r * L)
+    V = np.zeros(n * r * L)
+    f = hb.factorize(hb.HodlrMatrix.from_buffers(n, m, r, D, U, V))
+    b = np.random.default_rng(0).standard_normal(n)
+    assert np.array_equal(hb.solve(f, b), b)
+    assert hb.logdet(f) == (0.0, 1.0)
+
+
+@pytest.mark.parametrize(
+    "n,m,r,s",
+    [(1 << 14, 64, 32, 16.0), (1 << 13, 64, 16, 1.0), (1 << 12, 32, 8, 16.0), (1 << 11, 16, 32, 16.0)],
+)
+def test_random_vs_oracle(n, m, r, s):
+    h = orc.make_exact_hodlr(n, m, r, seed=n + r, s=s)
+    f = hb.factorize(to_gpu(h))
+    fo = orc.factorize(h.copy(), threads=8)
+    assert np.array_equal(f.D.cpu().numpy(), fo.D)
+    assert np.array_equal(f.dperm.cpu().numpy().reshape(-1, m), fo.dpiv.perm)
+    ks = f.kswaps.cpu().numpy().reshape(-1, 2 * r)
+    assert np.array_equal(ks, np.concatenate([kp.swaps for kp in fo.kpiv]))
+    assert rel(f.Y.cpu().numpy(), fo.Y) <= TOL
+    assert rel(f.K.cpu().numpy(), np.concatenate(fo.K)) <= TOL
+    b = np.random.default_rng(1).standard_normal((n, 2))
+    x = hb.solve(f, b)
+    assert rel(x, orc.solve(fo, b, threads=8)) <= TOL
+    # relative residual against the HODLR operator itself
+    hm = to_gpu(h)
+    xt = torch.from_numpy(x).cuda()
+    res = hm.matvec(xt) - torch.from_numpy(b).cuda()
+    relres = float(torch.linalg.norm(res) / torch.linalg.norm(torch.from_numpy(b)))
+    assert relres < 1e-12
+
+
+def test_multi_rhs_columns_bitwise_equal_single():
+    # column j of a blocked solve == single-vector solve, bit for bit
+    n, m, r = 1 << 13, 64, 32
+    h = hb.random_hodlr(n, m, r, seed=3, s=16.0)
+    f = hb.factorize(h)
+    B = torch.randn(n, 5, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+    X = hb.solve(f, B)
+    for j in range(5):
+        xj = hb.solve(f, B[:, j].contiguous())
+        assert torch.equal(X[:, j], xj)
+
+
+def test_solve_does_not_mutate_b_and_is_linear():
+    n, m, r = 1 << 12, 64, 16
+    f = hb.factorize(hb.random_hodlr(n, m, r, seed=4))
+    g = torch.Generator("cuda").manual_seed(5)
+    b1 = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    b2 = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    keep = b1.clone()
+    x1, x2 = hb.solve(f, b1), hb.solve(f, b2)
+    assert torch.equal(b1, keep)
+    x12 = hb.solve(f, 2.0 * b1 - 3.0 * b2)
+    assert float(torch.linalg.norm(x12 - (2 * x1 - 3 * x2)) / torch.linalg.norm(x12)) < 1e-12
+
+
+def test_factorize_deterministic_run_to_run():
+    n, m, r = 1 << 14, 64, 32
+    h1 = hb.random_hodlr(n, m, r, seed=9, s=16.0)
+    h2 = h1.clone()
+    f1, f2 = hb.factorize(h1), hb.factorize(h2)
+    assert torch.equal(f1.Y, f2.Y) and torch.equal(f1.K, f2.K) and torch.equal(f1.kswaps, f2.kswaps)
+
+
+def test_single_leaf_tree():
+    # L = 0: the whole matrix is one dense leaf block
+    n = m = 48
+    rng = np.random.default_rng(6)
+    D = rng.standard_normal(m * m) + 8 * np.eye(m).ravel()
+    f = hb.factorize(hb.HodlrMatrix.from_buffers(n, m, 4, D, np.zeros(0), np.zeros(0)))
+    b = rng.standard_normal(n)
+    x = hb.solve(f, b)
+    A = D.reshape(m, m).T
+    assert rel(x, np.linalg.solve(A, b)) < 1e-13
+
+
+def test_singular_leaf_raises_with_level_and_node():
+    n, m, r = 256, 32, 4
+    h = orc.make_exact_hodlr(n, m, r, seed=1)
+    h.D[3 * m * m : 4 * m * m] = 0.0  # leaf 3 is the zero matrix
+    with pytest.raises(hb.HodlrSingularError, match=r"leaf block at level 3, node\(s\) \[3\]"):
+        hb.factorize(to_gpu(h))

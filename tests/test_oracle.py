@@ -1,0 +1,131 @@
+"""CPU: the oracle against the reference golden vectors and known answers.
+
+The golden vectors were produced by the reference's own kernels
+(tests/golden/make_golden.py); the oracle must reproduce them BIT-FOR-BIT.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import hodlr_oracle as orc
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("path", sorted(GOLDEN.glob("n*.npz")), ids=lambda p: p.stem)
+def test_oracle_reproduces_reference_bitwise(path):
+    g = np.load(path)
+    h = orc.make_exact_hodlr(int(g["n"]), int(g["m"]), int(g["r"]), seed=int(g["seed"]), s=float(g["s"]))
+    assert digest(h.D, h.U, h.V) == str(g["input_sha256"]), "generator drifted"
+    f = orc.factorize(h.copy())
+    assert f.D.tobytes() == g["D_lu"].tobytes()
+    assert f.Y.tobytes() == g["Y"].tobytes()
+    assert np.array_equal(f.dpiv.swaps, g["d_swaps"]) and np.array_equal(f.dpiv.perm, g["d_perm"])
+    assert np.concatenate(f.K).tobytes() == g["K"].tobytes()
+    assert np.array_equal(np.concatenate([p.swaps for p in f.kpiv]), g["k_swaps"])
+    x = orc.solve(f, g["b"])
+    assert x.tobytes() == g["x"].tobytes()
+    la, sg = orc.logdet(f)
+    assert la == float(g["logdet"]) and sg == float(g["logdet_sign"])
+
+
+def test_threads_bit_identical():
+    h = orc.make_exact_hodlr(1024, 32, 8, seed=3, s=16.0)
+    f1 = orc.factorize(h.copy(), threads=1)
+    f4 = orc.factorize(h.copy(), threads=4)
+    assert f1.Y.tobytes() == f4.Y.tobytes() and f1.D.tobytes() == f4.D.tobytes()
+    b = np.random.default_rng(0).standard_normal((1024, 3))
+    assert orc.solve(f1, b, 1).tobytes() == orc.solve(f4, b, 4).tobytes()
+
+
+def test_spec_2x2_worked_example():
+    h = orc.HodlrData(orc.Layout(2, 1, 1), np.array([2.0, 2.0]), np.array([1.0, 1.0]), np.array([1.0, 1.0]))
+    f = orc.factorize(h)
+    assert f.Y.tolist() == [0.5, 0.5]
+    g = np.load(GOLDEN / "spec_2x2.npz")
+    assert f.K[0].tolist() == g["K_lu"].tolist()
+    x = orc.solve(f, np.array([3.0, 3.0]))
+    assert x.tolist() == [1.0, 1.0]
+    la, sg = orc.logdet(f)
+    assert abs(la - math.log(3.0)) < 1e-15 and sg == 1.0
+
+
+def test_dense_equivalence_and_flops():
+    n, m, r = 1024, 64, 8
+    h = orc.make_exact_hodlr(n, m, r, seed=5, s=16.0)
+    A = orc.dense(h)
+    f = orc.factorize(h.copy())
+    b = np.random.default_rng(1).standard_normal(n)
+    x = orc.solve(f, b)
+    assert np.linalg.norm(x - np.linalg.solve(A, b)) / np.linalg.norm(x) < 1e-11
+    assert sum(f.flops.values()) == orc.factor_flops(n, m, r)
+    # SPEC acceptance 5: per-level GEMM term 4 r^2 N l
+    L = h.lay.L
+    assert f.flops["tw_gemm"] + f.flops["update_gemm"] == sum(
+        2 * r * r * n + 4 * r * r * n * lv for lv in range(L)
+    )
+
+
+def test_cfg2_closed_form_flops():
+    # 538.24 GFLOP at N=2^20, m=64, r=32; 3.18 at N=2^14
+    assert round(orc.factor_flops(1 << 20, 64, 32) / 1e9, 2) == 538.24
+    assert round(orc.factor_flops(1 << 14, 64, 32) / 1e9, 2) == 3.18
+    assert round(orc.solve_flops(1 << 20, 64, 32) / 1e9, 3) == 2.147
+
+
+def test_lu_known_answers():
+    a = np.array([0.0, 1.0, 1.0, 0.0])  # [[0,1],[1,0]] column-major
+    p = orc.lu_factor(orc.sview(a, 0, 4, 1, 2, 2, 2))
+    assert p.swaps.tolist() == [[1, 1]] and a.tolist() == [1.0, 0.0, 0.0, 1.0] and p.sign()[0] == -1.0
+    bad = np.array([1.0, 2.0, 2.0, 4.0])
+    assert orc.lu_factor(orc.sview(bad, 0, 4, 1, 2, 2, 2)).singular.tolist() == [True]
+
+
+def test_lu_reconstruction_and_solve():
+    rng = np.random.default_rng(37)
+    s, nb = 32, 6
+    mats = rng.standard_normal((nb, s, s))
+    buf = np.concatenate([np.asfortranarray(x).ravel(order="F") for x in mats])
+    st = orc.sview(buf, 0, s * s, nb, s, s, s)
+    p = orc.lu_factor(st)
+    for i in range(nb):
+        lu = st[i]
+        lo, up = np.tril(lu, -1) + np.eye(s), np.triu(lu)
+        assert np.linalg.norm(mats[i][p.perm[i]] - lo @ up) / np.linalg.norm(mats[i]) <= 1e-13
+    rhs = rng.standard_normal((nb, s, 3))
+    x = rhs.copy()
+    orc.lu_solve(st, p.perm, x)
+    for i in range(nb):
+        assert np.linalg.norm(x[i] - np.linalg.solve(mats[i], rhs[i])) <= 1e-12 * np.linalg.norm(x[i])
+
+
+def test_identity_and_singular_leaf():
+    n, m, r = 128, 16, 2
+    h = orc.make_exact_hodlr(n, m, r, seed=0)
+    h.U[:] = 0.0
+    h.V[:] = 0.0
+    L = h.lay.L
+    h.D[:] = 0.0
+    for a in range(1 << L):
+        h.D[a * m * m + np.arange(m) * (m + 1)] = 1.0
+    f = orc.factorize(h)
+    b = np.arange(n, dtype=float)
+    assert orc.solve(f, b).tolist() == b.tolist()
+    assert orc.logdet(f) == (0.0, 1.0)
+    h2 = orc.make_exact_hodlr(n, m, r, seed=0)
+    h2.D[:m * m] = 0.0
+    with pytest.raises(orc.SingularError, match="level 3"):
+        orc.factorize(h2)
