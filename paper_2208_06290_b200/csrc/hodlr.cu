@@ -3,8 +3,9 @@
 // Everything is enqueued on the caller's stream; no allocation, no host sync.
 // Device layout is the reference's (include/hodlr_b200.h).  The factor keeps
 // the reference outputs (leaf LU + pivots, Y slab, K LU + pivots per level) and
-// additionally the explicit inverses D^-1 and K^-1, so every triangular solve of
-// the factor and solve phases becomes a batched DMMA GEMM.
+// additionally the packed triangular inverses strict_lower(L^-1) + upper(U^-1)
+// of every leaf and K block, so every triangular solve of the factor and solve
+// phases becomes a pair of batched DMMA GEMMs (apply.cu).
 #include <cstdio>
 #include <string>
 
@@ -13,7 +14,11 @@
 namespace hodlr {
 template <typename T>
 hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
-                          int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, cudaStream_t st);
+                          int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
+                          int64_t stridei, cudaStream_t st);
+hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int64_t ldi, int64_t strideT,
+                           const int32_t* perm, const double* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double* X,
+                           int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st);
 template <typename T>
 hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
                           const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX, int identity,
@@ -54,16 +59,10 @@ extern "C" hodlr_status hodlr_getrf_batched(int dtype, int s, int batch, void* A
   hodlr_status st;
   if (dtype == HODLR_F64) {
     st = launch_getrf<double>(s, batch, 0, (const double*)A, lda, strideA, (double*)A, lda, strideA, swaps, perm, info,
-                              S(stream));
-    if (st == HODLR_OK && Ainv)
-      st = launch_getrs<double>(s, s, batch, (const double*)A, lda, strideA, perm, nullptr, 0, 0, (double*)Ainv, ldinv,
-                                strideInv, 1, S(stream));
+                              (double*)Ainv, ldinv, strideInv, S(stream));
   } else if (dtype == HODLR_F32) {
     st = launch_getrf<float>(s, batch, 0, (const float*)A, lda, strideA, (float*)A, lda, strideA, swaps, perm, info,
-                             S(stream));
-    if (st == HODLR_OK && Ainv)
-      st = launch_getrs<float>(s, s, batch, (const float*)A, lda, strideA, perm, nullptr, 0, 0, (float*)Ainv, ldinv,
-                               strideInv, 1, S(stream));
+                             (float*)Ainv, ldinv, strideInv, S(stream));
   } else {
     return HODLR_ERR_ARG;
   }
@@ -97,9 +96,32 @@ extern "C" hodlr_status hodlr_gemm_batched(int dtype, int transA, int M, int N, 
 // factorize / solve
 // ---------------------------------------------------------------------------
 
+static bool tri_size_ok(int s) { return s == 16 || s == 32 || s == 64 || s == 128; }
+
 static bool desc_ok(const hodlr_desc* d) {
   if (!d || d->m < 1 || d->r < 0 || d->L < 0 || d->L > 30) return false;
+  if (d->m > 119 && !tri_size_ok(d->m)) return false;
+  if (d->L > 0 && 2 * d->r > 119 && !tri_size_ok(2 * d->r)) return false;
   return d->n == (int64_t)d->m << d->L;
+}
+
+// Factor s x s blocks; for DMMA-supported sizes also emit the packed
+// triangular inverses used by lu_apply.
+static hodlr_status lu_factor(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides, double* out,
+                              int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, double* tinv,
+                              cudaStream_t st) {
+  return launch_getrf<double>(s, batch, mode, src, lds, strides, out, s, strideo, swaps, perm, info,
+                              tri_size_ok(s) ? tinv : nullptr, s, strideo, st);
+}
+
+// X_b = A_b^-1 B_b from the stored factors: two triangular DMMA GEMMs with the
+// packed inverses, or row substitution for other block sizes.
+static hodlr_status lu_apply(int s, int ncols, int batch, const double* LU, const double* tinv, const int32_t* perm,
+                             const double* B, int64_t ldb, int64_t sB, double* X, int64_t ldx, int64_t sX,
+                             cudaStream_t st) {
+  if (tri_size_ok(s))
+    return tri_apply_f64(s, ncols, batch, tinv, s, (int64_t)s * s, perm, B, ldb, sB, 0, X, ldx, sX, 0, 1, st);
+  return launch_getrs<double>(s, ncols, batch, LU, s, (int64_t)s * s, perm, B, ldb, sB, X, ldx, sX, 0, st);
 }
 
 // workspace layout (factorize): [split-K | TW | W | leaf tmp (m > 64 only)]
@@ -112,7 +134,8 @@ static FactWs fact_ws(const hodlr_desc* d) {
   w.split = kSplitBytes;
   w.tw = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * r * L);
   w.w = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * r * (L > 0 ? L - 1 : 0));
-  w.tmp = (d->m > 64) ? align_up(sizeof(double) * (size_t)n * r * L) : 0;
+  w.tmp = 0;
+  (void)n;
   w.total = w.split + w.tw + w.w + w.tmp;
   return w;
 }
@@ -123,8 +146,7 @@ extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
   if (!desc_ok(d) || nrhs < 0) return 0;
   // split-K | w | w2 | tmp (m > 64)
   const size_t wsz = align_up(sizeof(double) * (size_t)((int64_t)1 << d->L) * d->r * nrhs);
-  const size_t tmp = (d->m > 64) ? align_up(sizeof(double) * (size_t)d->n * nrhs) : 0;
-  return kSplitBytes + 2 * wsz + tmp;
+  return kSplitBytes + 2 * wsz;
 }
 
 #define TRY(x)                            \
@@ -132,23 +154,6 @@ extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
     hodlr_status s_ = (x);                \
     if (s_ != HODLR_OK) return s_;        \
   } while (0)
-
-// X_a <- Dinv_a X_a for all leaves (rows a*m.., ncols columns, ld ldx).
-static hodlr_status apply_leaf_inverse(const hodlr_desc* d, const double* Dinv, double* X, int64_t ldx, int ncols,
-                                       void* split, size_t split_bytes, double* tmp, cudaStream_t st) {
-  const int m = d->m;
-  const int64_t nleaf = (int64_t)1 << d->L;
-  if (m <= 64) {  // whole tile column per CTA: in place is safe
-    return gemm_f64(0, m, ncols, m, 1.0, Dinv, m, (int64_t)m * m, 0, X, ldx, m, 0, 0.0, X, ldx, m, 0, (int)nleaf, 1,
-                    split, split_bytes, st);
-  }
-  TRY(gemm_f64(0, m, ncols, m, 1.0, Dinv, m, (int64_t)m * m, 0, X, ldx, m, 0, 0.0, tmp, d->n, m, 0, (int)nleaf, 1,
-               split, split_bytes, st));
-  if (cudaMemcpy2DAsync(X, ldx * sizeof(double), tmp, d->n * sizeof(double), d->n * sizeof(double), ncols,
-                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-    return hodlr_set_cuda_error(cudaGetLastError());
-  return HODLR_OK;
-}
 
 extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* work, size_t work_bytes,
                                         void* stream) {
@@ -161,7 +166,6 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
   void* split = wp;
   double* TW = reinterpret_cast<double*>(wp + ws.split);
   double* W = reinterpret_cast<double*>(wp + ws.split + ws.tw);
-  double* tmp = ws.tmp ? reinterpret_cast<double*>(wp + ws.split + ws.tw + ws.w) : nullptr;
 
   const int64_t n = d->n;
   const int m = d->m, r = d->r, L = d->L;
@@ -173,14 +177,11 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
   double* K = (double*)f->K;
   double* Kinv = (double*)f->Kinv;
 
-  // (1) leaf getrf (bit-exact) + explicit inverse          Alg.3 l.2
-  TRY(launch_getrf<double>(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, m, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo,
-                           st));
-  TRY(launch_getrs<double>(m, m, (int)nleaf, D, m, (int64_t)m * m, f->dperm, nullptr, 0, 0, Dinv, m, (int64_t)m * m, 1,
-                           st));
+  // (1) leaf getrf (bit-exact) + packed triangular inverses     Alg.3 l.2
+  TRY(lu_factor(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo, Dinv, st));
   if (L == 0 || r == 0) return HODLR_OK;
   // (2) Y(I_a, :) <- D_a^-1 U(I_a, :) for all levels at once       Alg.3 l.3
-  TRY(apply_leaf_inverse(d, Dinv, Y, n, r * L, split, ws.split, tmp, st));
+  TRY(lu_apply(m, r * L, (int)nleaf, D, Dinv, f->dperm, Y, n, m, Y, n, m, st));
 
   // (3) levels                                                     Alg.3 l.4-10
   for (int lv = L - 1; lv >= 0; --lv) {
@@ -191,17 +192,15 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
     // [W|T]_c = V_c^T Y(I_c, 0:r(l+1)), paired per parent: 2r x ncol, ld 2r
     TRY(gemm_f64(1, r, ncol, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, Y, n, 2 * nc, nc, 0.0, TW, 2 * r,
                  (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
-    // K_p = [[T_2p, I], [I, T_2p+1]] assembled + factored (bit-exact) + inverted
-    TRY(launch_getrf<double>(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff, 2 * r,
-                             (int64_t)4 * r * r, f->kswaps + ((int64_t)npar - 1) * 2 * r,
-                             f->kperm + ((int64_t)npar - 1) * 2 * r, f->kinfo + (npar - 1), st));
-    TRY(launch_getrs<double>(2 * r, 2 * r, npar, K + koff, 2 * r, (int64_t)4 * r * r,
-                             f->kperm + ((int64_t)npar - 1) * 2 * r, nullptr, 0, 0, Kinv + koff, 2 * r,
-                             (int64_t)4 * r * r, 1, st));
+    // K_p = [[T_2p, I], [I, T_2p+1]] assembled + factored (bit-exact) + packed inverses
+    int32_t* kperm = f->kperm + ((int64_t)npar - 1) * 2 * r;
+    TRY(lu_factor(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff,
+                  (int64_t)4 * r * r, f->kswaps + ((int64_t)npar - 1) * 2 * r, kperm, f->kinfo + (npar - 1),
+                  Kinv + koff, st));
     if (lv == 0) break;
     // W_p <- K_p^-1 [W_2p; W_2p+1]
-    TRY(gemm_f64(0, 2 * r, wc, 2 * r, 1.0, Kinv + koff, 2 * r, (int64_t)4 * r * r, 0, TW, 2 * r,
-                 (int64_t)2 * r * ncol, 0, 0.0, W, 2 * r, (int64_t)2 * r * wc, 0, npar, 1, split, ws.split, st));
+    TRY(lu_apply(2 * r, wc, npar, K + koff, Kinv + koff, kperm, TW, 2 * r, (int64_t)2 * r * ncol, W, 2 * r,
+                 (int64_t)2 * r * wc, st));
     // Y(I_c, 0:rl) -= Y_c^{l+1} W_c
     TRY(gemm_f64(0, (int)nc, wc, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, W, 2 * r, (int64_t)2 * r * wc, r,
                  1.0, Y, n, 2 * nc, nc, nch, 2, split, ws.split, st));
@@ -224,13 +223,13 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
   void* split = wp;
   double* w = reinterpret_cast<double*>(wp + kSplitBytes);
   double* w2 = reinterpret_cast<double*>(wp + kSplitBytes + wsz);
-  double* tmp = (m > 64) ? reinterpret_cast<double*>(wp + kSplitBytes + 2 * wsz) : nullptr;
   double* X = (double*)Xv;
   const double* Y = (const double*)f->Y;
   const double* V = (const double*)f->V;
   const double* Kinv = (const double*)f->Kinv;
 
-  TRY(apply_leaf_inverse(d, (const double*)f->Dinv, X, ldx, nrhs, split, kSplitBytes, tmp, st));
+  TRY(lu_apply(m, nrhs, (int)((int64_t)1 << L), (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m, X,
+               ldx, m, st));
   if (r == 0) return HODLR_OK;
   for (int lv = L - 1; lv >= 0; --lv) {
     const int nch = 1 << (lv + 1), npar = 1 << lv;
@@ -240,8 +239,8 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
     TRY(gemm_f64(1, r, nrhs, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w, 2 * r,
                  (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
     // w_p <- K_p^-1 w_p
-    TRY(gemm_f64(0, 2 * r, nrhs, 2 * r, 1.0, Kinv + koff, 2 * r, (int64_t)4 * r * r, 0, w, 2 * r,
-                 (int64_t)2 * r * nrhs, 0, 0.0, w2, 2 * r, (int64_t)2 * r * nrhs, 0, npar, 1, split, kSplitBytes, st));
+    TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + koff, f->kperm + ((int64_t)npar - 1) * 2 * r,
+                 w, 2 * r, (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st));
     // x_c -= Y_c w_c
     TRY(gemm_f64(0, (int)nc, nrhs, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, w2, 2 * r, (int64_t)2 * r * nrhs,
                  r, 1.0, X, ldx, 2 * nc, nc, nch, 2, split, kSplitBytes, st));

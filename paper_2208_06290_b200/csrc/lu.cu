@@ -195,6 +195,226 @@ __global__ void __launch_bounds__(256) getrs_kernel(int s, int nrhs, int cw, con
     for (int i = lane; i < s; i += 32) gx[i + (int64_t)(c0 + c) * ldx] = x[c * s + i];
 }
 
+
+// ---------------------------------------------------------------------------
+// Register-resident batched LU for s = S in {16, 32, 64}: one CTA per block,
+// thread t owns row t of the block in registers (fully unrolled).  Row swaps
+// are logical: every thread tracks the logical position of its row; the
+// winner of step k takes position k and the row that held position k takes
+// the winner's old position -- exactly the reference's whole-row exchange.
+// The pivot row is broadcast through shared memory; ties in |a| go to the
+// smallest logical position and NaN wins (np.argmax).  Afterwards the packed
+// triangular inverses  Tinv = strict_lower(L^-1) + upper(U^-1)  are formed
+// (U^-1 and L^-1 rows, one per thread); applying them to a row-gathered right-
+// hand side reproduces getrs to substitution accuracy with DMMA GEMMs.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ bool beats(T v, int pv, T b, int pb) {
+  if (pv < 0) return false;
+  if (pb < 0) return true;
+  const bool vn = v != v, bn = b != b;
+  if (vn || bn) return (vn && bn) ? pv < pb : vn;
+  return v > b || (v == b && pv < pb);
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_rows_kernel(
+    int mode, const T* __restrict__ src, int64_t lds, int64_t strides, T* out, int64_t ldo, int64_t strideo,
+    int32_t* __restrict__ swaps, int32_t* __restrict__ perm, int32_t* __restrict__ info, T* __restrict__ tinv,
+    int64_t ldi, int64_t stridei) {
+  constexpr int NT = S < 32 ? 32 : S;
+  constexpr int NW = NT / 32;
+  constexpr int LP = S + 1;  // padded row pitch of the staged matrix
+  __shared__ __align__(16) T urow[2][S];
+  __shared__ T mat[S * LP];
+  __shared__ T cmax[S];
+  __shared__ T redv[2][NW];
+  __shared__ int redp[2][NW], redt[2][NW];
+  __shared__ int swk[S];
+  __shared__ int sflag;
+
+  const int64_t blk = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool live = t < S;
+  const T* g = src + blk * strides;
+  T a[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    T v = (T)0;
+    if (live) {
+      if (mode == 0) {
+        v = g[t + j * lds];
+      } else {
+        constexpr int R = S / 2;
+        if (t < R && j < R)
+          v = g[t + j * lds];
+        else if (t >= R && j >= R)
+          v = g[t + (j - R) * lds];
+        else
+          v = (t < R) ? (T)(t == j - R) : (T)(t - R == j);
+      }
+    }
+    a[j] = v;
+  }
+  // original column magnitudes (np.abs(a).max(axis=1), NaN-propagating)
+  if (live) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) mat[t * LP + j] = a[j];
+  }
+  if (t == 0) sflag = 0;
+  __syncthreads();
+  if (live) {
+    T m = (T)0;
+    for (int i = 0; i < S; ++i) m = nan_max(m, (T)fabs((double)mat[i * LP + t]));
+    cmax[t] = m;
+  }
+  const T thr_scale = mul_rn(Eps<T>::v, (T)S);
+
+  int pos = t;
+  bool active = live;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int buf = k & 1;
+    T v = active ? (T)fabs((double)a[k]) : (T)0;
+    int pv = active ? pos : -1;
+    int pt = t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int op = __shfl_xor_sync(0xffffffffu, pv, o);
+      const int ot = __shfl_xor_sync(0xffffffffu, pt, o);
+      if (beats(ov, op, v, pv)) {
+        v = ov;
+        pv = op;
+        pt = ot;
+      }
+    }
+    if (NW > 1) {
+      if (lane == 0) {
+        redv[buf][warp] = v;
+        redp[buf][warp] = pv;
+        redt[buf][warp] = pt;
+      }
+      __syncthreads();
+      v = redv[buf][0];
+      pv = redp[buf][0];
+      pt = redt[buf][0];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) {
+        if (beats(redv[buf][w], redp[buf][w], v, pv)) {
+          v = redv[buf][w];
+          pv = redp[buf][w];
+          pt = redt[buf][w];
+        }
+      }
+    }
+    if (t == pt) {
+#pragma unroll
+      for (int j = k; j < S; ++j) urow[buf][j] = a[j];
+    }
+    __syncthreads();
+    const T piv = urow[buf][k];
+    if (t == 0) {
+      swk[k] = pv;
+      if ((T)fabs((double)piv) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
+    }
+    if (pos == k) pos = pv;
+    if (t == pt) {
+      pos = k;
+      active = false;
+    }
+    if (active) {
+      const T d = (piv == (T)0) ? (T)1 : piv;
+      const T l = div_rn(a[k], d);
+      a[k] = l;
+#pragma unroll
+      for (int j = k + 1; j < S; ++j) a[j] = sub_rn(a[j], mul_rn(l, urow[buf][j]));
+    }
+  }
+  // factors out (row pos of the block), pivots, flag
+  if (live) {
+    T* o = out + blk * strideo;
+#pragma unroll
+    for (int j = 0; j < S; ++j) o[pos + j * ldo] = a[j];
+    perm[blk * S + pos] = t;
+    swaps[blk * S + t] = swk[t];
+  }
+  __syncthreads();
+  if (t == 0) info[blk] = sflag;
+  if (tinv == nullptr) return;
+  // stage LU row-major by logical row for the inverses
+  if (live) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) mat[pos * LP + j] = a[j];
+  }
+  __syncthreads();
+  if (!live) return;
+  T* ti = tinv + blk * stridei;
+  const int i = t;  // this thread forms row i of U^-1 and of L^-1
+  {
+    T x[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) x[j] = (T)(j == i);
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      x[k] = x[k] / mat[k * LP + k];
+#pragma unroll
+      for (int j = k + 1; j < S; ++j) x[j] = fma(-x[k], mat[k * LP + j], x[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (j >= i) ti[i + j * ldi] = x[j];
+  }
+  {
+    T x[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) x[j] = (T)(j == i);
+#pragma unroll
+    for (int k = S - 1; k > 0; --k) {
+#pragma unroll
+      for (int j = 0; j < k; ++j) x[j] = fma(-x[k], mat[k * LP + j], x[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (j < i) ti[i + j * ldi] = x[j];
+  }
+}
+
+// Packed triangular inverses from stored LU for sizes without a register
+// kernel: thread i forms row i of U^-1 (upper) and of L^-1 (strict lower).
+template <typename T>
+__global__ void __launch_bounds__(128) trtri_packed_kernel(int s, const T* __restrict__ LU, int64_t lda, int64_t strideA,
+                                                           T* __restrict__ tinv, int64_t ldi, int64_t stridei) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int LP = s + 1;
+  T* lu = reinterpret_cast<T*>(smem_raw);  // row-major, pitch LP
+  T* xs = lu + s * LP;                     // per-thread rows, pitch LP
+  const int64_t blk = blockIdx.x;
+  const T* g = LU + blk * strideA;
+  for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+    const int i = e % s, j = e / s;
+    lu[i * LP + j] = g[i + (int64_t)j * lda];
+  }
+  __syncthreads();
+  T* ti = tinv + blk * stridei;
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    T* x = xs + i * LP;
+    for (int j = 0; j < s; ++j) x[j] = (T)(j == i);
+    for (int k = i; k < s; ++k) {
+      const T xk = x[k] / lu[k * LP + k];
+      x[k] = xk;
+      for (int j = k + 1; j < s; ++j) x[j] = fma(-xk, lu[k * LP + j], x[j]);
+    }
+    for (int j = i; j < s; ++j) ti[i + (int64_t)j * ldi] = x[j];
+    for (int j = 0; j < s; ++j) x[j] = (T)(j == i);
+    for (int k = i; k > 0; --k) {
+      const T xk = x[k];
+      for (int j = 0; j < k; ++j) x[j] = fma(-xk, lu[k * LP + j], x[j]);
+    }
+    for (int j = 0; j < i; ++j) ti[i + (int64_t)j * ldi] = x[j];
+  }
+}
+
 template <typename T>
 static size_t getrf_smem(int s) {
   return (size_t)s * s * sizeof(T) + s * sizeof(T) + s * sizeof(int) + 16;
@@ -206,13 +426,34 @@ static size_t getrs_smem(int s, int cw) {
 
 template <typename T>
 hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
-                          int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, cudaStream_t st) {
+                          int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
+                          int64_t stridei, cudaStream_t st) {
   if (batch == 0 || s == 0) return HODLR_OK;
+  if (s == 64 || s == 32 || s == 16) {
+    if (s == 64)
+      getrf_rows_kernel<T, 64><<<batch, 64, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
+                                                     tinv, ldi, stridei);
+    else if (s == 32)
+      getrf_rows_kernel<T, 32><<<batch, 32, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
+                                                     tinv, ldi, stridei);
+    else
+      getrf_rows_kernel<T, 16><<<batch, 32, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
+                                                     tinv, ldi, stridei);
+    HODLR_CHECK_LAUNCH();
+    return HODLR_OK;
+  }
   size_t sm = getrf_smem<T>(s);
   if (sm > 227 * 1024) return HODLR_ERR_ARG;
   cudaFuncSetAttribute(getrf_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   getrf_kernel<T><<<batch, 256, sm, st>>>(s, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info);
   HODLR_CHECK_LAUNCH();
+  if (tinv) {
+    const size_t sm2 = (size_t)2 * s * (s + 1) * sizeof(T);
+    if (sm2 > 227 * 1024) return HODLR_ERR_ARG;
+    cudaFuncSetAttribute(trtri_packed_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    trtri_packed_kernel<T><<<batch, 128, sm2, st>>>(s, out, ldo, strideo, tinv, ldi, stridei);
+    HODLR_CHECK_LAUNCH();
+  }
   return HODLR_OK;
 }
 
@@ -238,9 +479,9 @@ hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, 
 }
 
 template hodlr_status launch_getrf<double>(int, int, int, const double*, int64_t, int64_t, double*, int64_t, int64_t,
-                                           int32_t*, int32_t*, int32_t*, cudaStream_t);
+                                           int32_t*, int32_t*, int32_t*, double*, int64_t, int64_t, cudaStream_t);
 template hodlr_status launch_getrf<float>(int, int, int, const float*, int64_t, int64_t, float*, int64_t, int64_t,
-                                          int32_t*, int32_t*, int32_t*, cudaStream_t);
+                                          int32_t*, int32_t*, int32_t*, float*, int64_t, int64_t, cudaStream_t);
 template hodlr_status launch_getrs<double>(int, int, int, const double*, int64_t, int64_t, const int32_t*,
                                            const double*, int64_t, int64_t, double*, int64_t, int64_t, int,
                                            cudaStream_t);
