@@ -18,7 +18,13 @@ hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds,
                           int64_t stridei, cudaStream_t st);
 hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int64_t ldi, int64_t strideT,
                            const int32_t* perm, const double* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double* X,
-                           int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st);
+                           int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st,
+                           const double* V = nullptr, int64_t ldv = 0, int64_t vstride = 0, int twr = 0,
+                           double* TW = nullptr, int64_t tw_stride = 0);
+hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc, const double* A1, const double* V,
+                              int64_t lda, const double* W, int64_t wstride, int ncols, double* TW, int64_t tw_stride,
+                              double* part, size_t part_bytes, cudaStream_t st);
+size_t level_partial_bytes(int64_t n, int m, int r, int L);
 template <typename T>
 hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
                           const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX, int identity,
@@ -124,9 +130,9 @@ static hodlr_status lu_apply(int s, int ncols, int batch, const double* LU, cons
   return launch_getrs<double>(s, ncols, batch, LU, s, (int64_t)s * s, perm, B, ldb, sB, X, ldx, sX, 0, st);
 }
 
-// workspace layout (factorize): [split-K | TW | W | leaf tmp (m > 64 only)]
+// workspace layout (factorize): [split-K | TW | W | level partial sums]
 struct FactWs {
-  size_t split, tw, w, tmp, total;
+  size_t split, tw, w, part, total;
 };
 static FactWs fact_ws(const hodlr_desc* d) {
   const int64_t n = d->n, r = d->r, L = d->L;
@@ -134,19 +140,22 @@ static FactWs fact_ws(const hodlr_desc* d) {
   w.split = kSplitBytes;
   w.tw = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * r * L);
   w.w = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * r * (L > 0 ? L - 1 : 0));
-  w.tmp = 0;
-  (void)n;
-  w.total = w.split + w.tw + w.w + w.tmp;
+  w.part = align_up(level_partial_bytes(n, d->m, (int)r, (int)L));
+  w.total = w.split + w.tw + w.w + w.part;
   return w;
 }
 
 extern "C" size_t hodlr_factorize_workspace(const hodlr_desc* d) { return desc_ok(d) ? fact_ws(d).total : 0; }
 
+static size_t solve_part_bytes(const hodlr_desc* d, int nrhs) {
+  return align_up(sizeof(double) * (size_t)4 * 148 * d->r * nrhs);
+}
+
 extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
   if (!desc_ok(d) || nrhs < 0) return 0;
-  // split-K | w | w2 | tmp (m > 64)
+  // split-K | w | w2 | level partial sums
   const size_t wsz = align_up(sizeof(double) * (size_t)((int64_t)1 << d->L) * d->r * nrhs);
-  return kSplitBytes + 2 * wsz;
+  return kSplitBytes + 2 * wsz + solve_part_bytes(d, nrhs);
 }
 
 #define TRY(x)                            \
@@ -166,6 +175,7 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
   void* split = wp;
   double* TW = reinterpret_cast<double*>(wp + ws.split);
   double* W = reinterpret_cast<double*>(wp + ws.split + ws.tw);
+  double* part = reinterpret_cast<double*>(wp + ws.split + ws.tw + ws.w);
 
   const int64_t n = d->n;
   const int m = d->m, r = d->r, L = d->L;
@@ -181,7 +191,15 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
   TRY(lu_factor(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo, Dinv, st));
   if (L == 0 || r == 0) return HODLR_OK;
   // (2) Y(I_a, :) <- D_a^-1 U(I_a, :) for all levels at once       Alg.3 l.3
-  TRY(lu_apply(m, r * L, (int)nleaf, D, Dinv, f->dperm, Y, n, m, Y, n, m, st));
+  //     fused with the level-(L-1) [W|T]_a = V_a^T Y(I_a, 0:rL)   Alg.3 l.5-6
+  bool tw_ready = false;
+  if (tri_size_ok(m)) {
+    hodlr_status s = tri_apply_f64(m, r * L, (int)nleaf, Dinv, m, (int64_t)m * m, f->dperm, Y, n, m, 0, Y, n, m, 0, 1,
+                                   st, V + (int64_t)(L - 1) * r * n, n, m, r, TW, (int64_t)2 * r * r * L);
+    if (s == HODLR_OK) tw_ready = true;
+    else if (s != HODLR_ERR_ARG) return s;
+  }
+  if (!tw_ready) TRY(lu_apply(m, r * L, (int)nleaf, D, Dinv, f->dperm, Y, n, m, Y, n, m, st));
 
   // (3) levels                                                     Alg.3 l.4-10
   for (int lv = L - 1; lv >= 0; --lv) {
@@ -189,9 +207,11 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
     const int64_t nc = n >> (lv + 1);
     const int ncol = r * (lv + 1), wc = r * lv;
     const int64_t koff = ((int64_t)npar - 1) * 4 * r * r;
-    // [W|T]_c = V_c^T Y(I_c, 0:r(l+1)), paired per parent: 2r x ncol, ld 2r
-    TRY(gemm_f64(1, r, ncol, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, Y, n, 2 * nc, nc, 0.0, TW, 2 * r,
-                 (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
+    if (!tw_ready) {
+      // [W|T]_c = V_c^T Y(I_c, 0:r(l+1)), paired per parent: 2r x ncol, ld 2r
+      TRY(gemm_f64(1, r, ncol, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, Y, n, 2 * nc, nc, 0.0, TW,
+                   2 * r, (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
+    }
     // K_p = [[T_2p, I], [I, T_2p+1]] assembled + factored (bit-exact) + packed inverses
     int32_t* kperm = f->kperm + ((int64_t)npar - 1) * 2 * r;
     TRY(lu_factor(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff,
@@ -201,7 +221,15 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
     // W_p <- K_p^-1 [W_2p; W_2p+1]
     TRY(lu_apply(2 * r, wc, npar, K + koff, Kinv + koff, kperm, TW, 2 * r, (int64_t)2 * r * ncol, W, 2 * r,
                  (int64_t)2 * r * wc, st));
-    // Y(I_c, 0:rl) -= Y_c^{l+1} W_c
+    // Y(I_c, 0:rl) -= Y_c^{l+1} W_c, fused with the next level's [W|T] (V^{(l)T} Y(I_q, 0:rl))
+    hodlr_status s = level_update_f64(r, n, (int)nc, Y, n, Y + (int64_t)lv * r * n, V + (int64_t)(lv - 1) * r * n, n,
+                                      W, (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st);
+    if (s == HODLR_OK) {
+      tw_ready = true;
+      continue;
+    }
+    if (s != HODLR_ERR_ARG) return s;
+    tw_ready = false;
     TRY(gemm_f64(0, (int)nc, wc, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, W, 2 * r, (int64_t)2 * r * wc, r,
                  1.0, Y, n, 2 * nc, nc, nch, 2, split, ws.split, st));
   }
@@ -223,25 +251,39 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
   void* split = wp;
   double* w = reinterpret_cast<double*>(wp + kSplitBytes);
   double* w2 = reinterpret_cast<double*>(wp + kSplitBytes + wsz);
+  double* part = reinterpret_cast<double*>(wp + kSplitBytes + 2 * wsz);
   double* X = (double*)Xv;
   const double* Y = (const double*)f->Y;
   const double* V = (const double*)f->V;
   const double* Kinv = (const double*)f->Kinv;
 
+  // x <- D^-1 x                                                   Alg.4 l.3
   TRY(lu_apply(m, nrhs, (int)((int64_t)1 << L), (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m, X,
                ldx, m, st));
   if (r == 0) return HODLR_OK;
+  bool w_ready = false;
   for (int lv = L - 1; lv >= 0; --lv) {
     const int nch = 1 << (lv + 1), npar = 1 << lv;
     const int64_t nc = n >> (lv + 1);
     const int64_t koff = ((int64_t)npar - 1) * 4 * r * r;
-    // w_c = V_c^T x_c  (paired per parent, 2r x nrhs, ld 2r)
-    TRY(gemm_f64(1, r, nrhs, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w, 2 * r,
-                 (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
-    // w_p <- K_p^-1 w_p
+    // w_c = V_c^T x_c  (paired per parent, 2r x nrhs, ld 2r)       Alg.4 l.5
+    if (!w_ready)
+      TRY(gemm_f64(1, r, nrhs, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w,
+                   2 * r, (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
+    // w_p <- K_p^-1 w_p                                              Alg.4 l.6
     TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + koff, f->kperm + ((int64_t)npar - 1) * 2 * r,
                  w, 2 * r, (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st));
-    // x_c -= Y_c w_c
+    // x_c -= Y_c w_c  fused with the next level's w = V^{(l)T} x    Alg.4 l.7 (+ l.5 of level l-1)
+    hodlr_status s = level_update_f64(r, n, (int)nc, X, ldx, Y + (int64_t)lv * r * n,
+                                      lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2,
+                                      (int64_t)2 * r * nrhs, nrhs, w, (int64_t)2 * r * nrhs, part,
+                                      solve_part_bytes(d, nrhs), st);
+    if (s == HODLR_OK) {
+      w_ready = true;
+      continue;
+    }
+    if (s != HODLR_ERR_ARG) return s;
+    w_ready = false;
     TRY(gemm_f64(0, (int)nc, nrhs, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, w2, 2 * r, (int64_t)2 * r * nrhs,
                  r, 1.0, X, ldx, 2 * nc, nc, nch, 2, split, kSplitBytes, st));
   }

@@ -1,0 +1,306 @@
+// Fused level step of the factorization (Alg. 3 lines 9-10 of level l
+// fused with lines 5-6 of level l-1) and of the solve (Alg. 4 lines 7 / 5).
+//
+// For every child c at level l+1 (n_c rows, parent p = c/2):
+//     C(I_c, :) -= Y_c^{l+1} W'_c                         (update, W' = half of K_p^-1 W_p)
+// and, with the freshly updated rows still in shared memory,
+//     TW_q(:, :) += V_q^{(l) T} C(I_q, :)                  (next level's [W|T], q = node at level l)
+//
+// C is the Y slab columns [0, r l) in the factorization (W' has r l columns) or
+// the solution block x (nrhs columns) in the solve.  One CTA owns a segment of
+// consecutive rows inside one level-l node q and walks (column tile, 64-row
+// sub-tile) pairs through a 2-stage cp.async pipeline; each 64 x BN update and
+// each r x BN reduction is a DMMA (FP64 tensor core) tile.  Y is therefore read
+// and written once per level, and V^T C never re-reads C from HBM.  Segments
+// shorter than the node write partial sums that a fixed-order reduction kernel
+// adds (deterministic).
+#include "common.cuh"
+
+namespace hodlr {
+
+struct LevelArgs {
+  double* C;  // rows [0, n) of the updated block, column-major
+  int64_t ldc;
+  const double* A1;  // Y^{l+1} panel: A1[row + k*lda], k < r
+  const double* V;   // V^{(l)} panel: V[row + k*lda], k < r  (may be null: no TW output)
+  int64_t lda;
+  const double* W;  // W_p (2r x ncols, ld 2r) at W + p * wstride
+  int64_t wstride;
+  double* TW;       // final: paired layout; partial: [seg][r x ncols] ld r
+  int64_t tw_stride;  // final: per next-parent stride (2r * ncols)
+  int partial;
+  int n_c;       // rows per child at level l+1
+  int seg_rows;  // rows per CTA segment (multiple of 64, divides 2 n_c)
+  int ncols;
+};
+
+template <int R, int BN>
+struct LevelCfg {
+  static constexpr int BM = 64;
+  static constexpr int P = BM + 4;  // pitch of row-contiguous tiles
+  static constexpr int PW = R + 4;  // pitch of W' tile (k contiguous)
+  static constexpr int C_SZ = BN * P;
+  static constexpr int A_SZ = R * P;
+  static constexpr int W_SZ = BN * PW;
+  static constexpr int STAGE = C_SZ + 2 * A_SZ + W_SZ;
+  static constexpr size_t SMEM = (size_t)2 * STAGE * sizeof(double);
+};
+
+template <int R, int BN>
+__global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
+  using Cfg = LevelCfg<R, BN>;
+  constexpr int BM = Cfg::BM, P = Cfg::P, PW = Cfg::PW;
+  // update GEMM: 64 x BN output on 8 warps
+  constexpr int UWM = (BN >= 64) ? 2 : 8, UWN = 8 / UWM;
+  constexpr int UTM = BM / UWM, UTN = BN / UWN;
+  constexpr int UMI = UTM / 8, UNI = UTN / 8;
+  // TW GEMM: R x BN output on 8 warps
+  constexpr int TWN = (BN / 8 >= 8) ? 8 : BN / 8;  // warps along N
+  constexpr int TWM = (8 / TWN) <= R / 8 ? 8 / TWN : R / 8;
+  constexpr int TTM = R / TWM, TTN = BN / TWN;
+  constexpr int TMI = TTM / 8, TNI = TTN / 8;
+  static_assert(UMI >= 1 && UNI >= 1 && TMI >= 1 && TNI >= 1, "tile config");
+
+  extern __shared__ __align__(16) double sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int64_t seg0 = (int64_t)blockIdx.x * g.seg_rows;
+  const int nsub = g.seg_rows / BM;
+  const int ntile = (g.ncols + BN - 1) / BN;
+  const int niter = nsub * ntile;
+  const bool want_tw = g.V != nullptr;
+
+  auto stage_ptr = [&](int s) { return sm + s * Cfg::STAGE; };
+
+  auto load = [&](int it, int s) {
+    const int ct = it / nsub, st = it % nsub;
+    const int64_t row0 = seg0 + (int64_t)st * BM;
+    const int c = (int)(row0 / g.n_c);
+    const int n0 = ct * BN;
+    double* Cs = stage_ptr(s);
+    double* As = Cs + Cfg::C_SZ;
+    double* Vs = As + Cfg::A_SZ;
+    double* Ws = Vs + Cfg::A_SZ;
+    // C tile [n][m]: 16B copies along rows
+    for (int idx = t; idx < BN * (BM / 2); idx += 256) {
+      const int n = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
+      const bool ok = n0 + n < g.ncols;
+      cp_async_16(Cs + n * P + m, ok ? g.C + row0 + m + (int64_t)(n0 + n) * g.ldc : g.C, ok ? 16 : 0);
+    }
+    // A1 tile [k][m] and V tile [k][m] (both rows-contiguous per rank column)
+    for (int idx = t; idx < R * (BM / 2); idx += 256) {
+      const int k = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
+      cp_async_16(As + k * P + m, g.A1 + row0 + m + (int64_t)k * g.lda, 16);
+      if (want_tw) cp_async_16(Vs + k * P + m, g.V + row0 + m + (int64_t)k * g.lda, 16);
+    }
+    // W' tile [n][k]: rows (c%2)*R.. of W_p, k contiguous
+    const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
+    for (int idx = t; idx < BN * (R / 2); idx += 256) {
+      const int n = idx / (R / 2), k = (idx % (R / 2)) * 2;
+      const bool ok = n0 + n < g.ncols;
+      cp_async_16(Ws + n * PW + k, ok ? Wp + k + (int64_t)(n0 + n) * (2 * R) : g.W, ok ? 16 : 0);
+    }
+  };
+
+  double tw[TMI][TNI][2];
+  if (niter > 0) load(0, 0);
+  cp_async_commit();
+  for (int it = 0; it < niter; ++it) {
+    const int s = it & 1;
+    const int ct = it / nsub, st = it % nsub;
+    if (it + 1 < niter) load(it + 1, s ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double* Cs = stage_ptr(s);
+    const double* As = Cs + Cfg::C_SZ;
+    const double* Vs = As + Cfg::A_SZ;
+    const double* Ws = Vs + Cfg::A_SZ;
+    if (st == 0) {
+#pragma unroll
+      for (int i = 0; i < TMI; ++i)
+#pragma unroll
+        for (int j = 0; j < TNI; ++j) tw[i][j][0] = tw[i][j][1] = 0.0;
+    }
+    // ---- update: upd = A1 W' (rounded product), C = C - upd ----
+    {
+      const int wm = warp / UWN, wn = warp % UWN;
+      double acc[UMI][UNI][2];
+#pragma unroll
+      for (int i = 0; i < UMI; ++i)
+#pragma unroll
+        for (int j = 0; j < UNI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < R; k0 += 4) {
+        double af[UMI], bf[UNI];
+#pragma unroll
+        for (int i = 0; i < UMI; ++i) af[i] = As[(k0 + ac) * P + wm * UTM + i * 8 + ar];
+#pragma unroll
+        for (int j = 0; j < UNI; ++j) bf[j] = Ws[(wn * UTN + j * 8 + ar) * PW + k0 + ac];
+#pragma unroll
+        for (int i = 0; i < UMI; ++i)
+#pragma unroll
+          for (int j = 0; j < UNI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < UMI; ++i)
+#pragma unroll
+        for (int j = 0; j < UNI; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int m = wm * UTM + i * 8 + ar, n = wn * UTN + j * 8 + ac * 2 + h;
+            Cs[n * P + m] = __dsub_rn(Cs[n * P + m], acc[i][j][h]);
+          }
+    }
+    __syncthreads();
+    // ---- store the updated tile (coalesced 16B) ----
+    {
+      const int64_t row0 = seg0 + (int64_t)st * BM;
+      const int n0 = ct * BN;
+      for (int idx = t; idx < BN * (BM / 2); idx += 256) {
+        const int n = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
+        if (n0 + n < g.ncols) {
+          double2 v = make_double2(Cs[n * P + m], Cs[n * P + m + 1]);
+          *reinterpret_cast<double2*>(g.C + row0 + m + (int64_t)(n0 + n) * g.ldc) = v;
+        }
+      }
+    }
+    // ---- next level's [W|T]: tw += V^T C_new ----
+    if (want_tw) {
+      const int wm = warp / TWN, wn = warp % TWN;
+      if (wm < TWM) {
+#pragma unroll 4
+        for (int k0 = 0; k0 < BM; k0 += 4) {
+          double af[TMI], bf[TNI];
+#pragma unroll
+          for (int i = 0; i < TMI; ++i) af[i] = Vs[(wm * TTM + i * 8 + ar) * P + k0 + ac];
+#pragma unroll
+          for (int j = 0; j < TNI; ++j) bf[j] = Cs[(wn * TTN + j * 8 + ar) * P + k0 + ac];
+#pragma unroll
+          for (int i = 0; i < TMI; ++i)
+#pragma unroll
+            for (int j = 0; j < TNI; ++j) dmma_8x8x4(tw[i][j][0], tw[i][j][1], af[i], bf[j]);
+        }
+      }
+      if (st == nsub - 1 && wm < TWM) {
+        const int n0 = ct * BN;
+        const int64_t q = seg0 / (2 * (int64_t)g.n_c);  // level-l node of this segment
+        double* out;
+        int64_t ld;
+        if (g.partial) {
+          out = g.TW + (int64_t)blockIdx.x * R * g.ncols;
+          ld = R;
+        } else {
+          out = g.TW + (q >> 1) * g.tw_stride + (q & 1) * R;
+          ld = 2 * R;
+        }
+#pragma unroll
+        for (int i = 0; i < TMI; ++i)
+#pragma unroll
+          for (int j = 0; j < TNI; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int m = wm * TTM + i * 8 + ar, n = n0 + wn * TTN + j * 8 + ac * 2 + h;
+              if (n < g.ncols) out[m + (int64_t)n * ld] = tw[i][j][h];
+            }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// TW_q = sum over the q's segments of the partials, fixed order; paired output.
+__global__ void level_reduce_kernel(const double* part, double* TW, int R, int ncols, int segs_per_node, int nnodes,
+                                    int64_t tw_stride) {
+  const int64_t per = (int64_t)R * ncols;
+  const int64_t total = per * nnodes;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / per, mn = e % per;
+    const int m = (int)(mn % R), n = (int)(mn / R);
+    double s = 0.0;
+    for (int k = 0; k < segs_per_node; ++k) s += part[(q * segs_per_node + k) * per + mn];
+    TW[(q >> 1) * tw_stride + (q & 1) * R + m + (int64_t)n * 2 * R] = s;
+  }
+}
+
+template <int R, int BN>
+static hodlr_status run_level(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
+  using Cfg = LevelCfg<R, BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(level_update_kernel<R, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    attr = true;
+  }
+  level_update_kernel<R, BN><<<(unsigned)nseg, 256, Cfg::SMEM, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// rows per CTA segment for a level whose nodes have `node` rows: the whole node
+// when that already gives >= 2 CTAs per SM, else split (partial sums), and never
+// more than 4096 rows of serial work per CTA.
+int64_t level_segment_rows(int64_t n, int64_t node, int sms) {
+  int64_t seg = node;
+  const int64_t want = 2 * (int64_t)sms;
+  while (seg > 64 && n / seg < want && seg % 128 == 0) seg >>= 1;
+  while (seg > 4096 && seg % 128 == 0) seg >>= 1;
+  return seg;
+}
+
+// partial-sum bytes the factorization's level steps need (max over levels)
+size_t level_partial_bytes(int64_t n, int m, int r, int L) {
+  size_t best = 0;
+  for (int lv = 1; lv < L; ++lv) {
+    const int64_t node = n >> lv;
+    const int64_t seg = level_segment_rows(n, node, 148);
+    if (seg < node) best = std::max(best, (size_t)(n / seg) * r * r * lv * sizeof(double));
+  }
+  (void)m;
+  return best;
+}
+
+// One fused level step over all n rows.  Returns ERR_ARG when the shape is not
+// supported (caller falls back to the generic batched GEMM path).
+hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc, const double* A1, const double* V,
+                              int64_t lda, const double* W, int64_t wstride, int ncols, double* TW, int64_t tw_stride,
+                              double* part, size_t part_bytes, cudaStream_t st) {
+  if (ncols == 0) return HODLR_OK;
+  if (n_c % 64 || (r != 16 && r != 32 && r != 64)) return HODLR_ERR_ARG;
+  if ((ldc & 1) || (lda & 1) || (reinterpret_cast<uintptr_t>(C) & 15) || (reinterpret_cast<uintptr_t>(A1) & 15) ||
+      (V && (reinterpret_cast<uintptr_t>(V) & 15)) || (reinterpret_cast<uintptr_t>(W) & 15) || (wstride & 1))
+    return HODLR_ERR_ARG;
+  const int64_t node = 2 * (int64_t)n_c;  // rows of a level-l node
+  const int64_t seg = level_segment_rows(n, node, sm_count());
+  const int64_t nseg = n / seg;
+  if (nseg > 2147483647LL) return HODLR_ERR_ARG;
+  const bool split = seg < node && V != nullptr;
+  if (split && (size_t)nseg * r * ncols * sizeof(double) > part_bytes) return HODLR_ERR_ARG;
+  LevelArgs g{C, ldc, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, n_c, (int)seg, ncols};
+  const bool small = ncols <= 8;
+  hodlr_status s;
+  switch (r) {
+    case 16: s = small ? run_level<16, 8>(g, nseg, st) : run_level<16, 64>(g, nseg, st); break;
+    case 32: s = small ? run_level<32, 8>(g, nseg, st) : run_level<32, 64>(g, nseg, st); break;
+    default: s = small ? run_level<64, 8>(g, nseg, st) : run_level<64, 64>(g, nseg, st); break;
+  }
+  if (s != HODLR_OK || !split) return s;
+  const int nnodes = (int)(n / node);
+  const int64_t total = (int64_t)r * ncols * nnodes;
+  const int64_t blocks = std::min<int64_t>(ceil_div(total, 256), 8 * (int64_t)sm_count());
+  level_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, TW, r, ncols, (int)(node / seg), nnodes, tw_stride);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+}  // namespace hodlr

@@ -198,15 +198,19 @@ __global__ void __launch_bounds__(256) getrs_kernel(int s, int nrhs, int cw, con
 
 // ---------------------------------------------------------------------------
 // Register-resident batched LU for s = S in {16, 32, 64}: one CTA per block,
-// thread t owns row t of the block in registers (fully unrolled).  Row swaps
-// are logical: every thread tracks the logical position of its row; the
-// winner of step k takes position k and the row that held position k takes
-// the winner's old position -- exactly the reference's whole-row exchange.
-// The pivot row is broadcast through shared memory; ties in |a| go to the
-// smallest logical position and NaN wins (np.argmax).  Afterwards the packed
-// triangular inverses  Tinv = strict_lower(L^-1) + upper(U^-1)  are formed
-// (U^-1 and L^-1 rows, one per thread); applying them to a row-gathered right-
-// hand side reproduces getrs to substitution accuracy with DMMA GEMMs.
+// thread t owns row t in registers.  The step loop is NOT unrolled (code stays
+// small enough for the instruction cache): column k of the own row is read /
+// written through a chunked select (chunk k/8 by a uniform switch, then 8
+// selects), and the trailing update walks 8-column chunks guarded by a uniform
+// branch so finished chunks are skipped.  Row swaps are logical: every thread
+// tracks the logical position of its row; the winner of step k takes position
+// k and the row that held position k takes the winner's old position --
+// exactly the reference's whole-row exchange.  The pivot row is broadcast
+// through shared memory; ties in |a| go to the smallest logical position and
+// NaN wins (np.argmax).  Afterwards the packed triangular inverses
+// Tinv = strict_lower(L^-1) + upper(U^-1) are formed (one row per thread);
+// applying them to a row-gathered right-hand side reproduces getrs to
+// substitution accuracy with DMMA GEMMs (apply.cu).
 // ---------------------------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ bool beats(T v, int pv, T b, int pb) {
@@ -217,17 +221,63 @@ __device__ __forceinline__ bool beats(T v, int pv, T b, int pb) {
   return v > b || (v == b && pv < pb);
 }
 
+// opaque select: keeps the optimizer from folding select chains over the row
+// into a dynamically indexed (local-memory) array access
+__device__ __forceinline__ double osel(int p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(r)
+      : "d"(a), "d"(b), "r"(p));
+  return r;
+}
+__device__ __forceinline__ float osel(int p, float a, float b) {
+  float r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f32 %0, %1, %2, q;\n\t}"
+      : "=f"(r)
+      : "f"(a), "f"(b), "r"(p));
+  return r;
+}
+
+// a[k] for a runtime k: uniform branch on the 8-wide chunk, then 8 selects
+template <typename T, int S>
+__device__ __forceinline__ T row_get(const T (&a)[S], int k) {
+  T v = a[0];
+  const int kk = k & 7;
+#pragma unroll
+  for (int c = 0; c < S / 8; ++c) {
+    if ((k >> 3) == c) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v = osel(kk == e, a[8 * c + e], v);
+    }
+  }
+  return v;
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void row_set(T (&a)[S], int k, T v) {
+  const int kk = k & 7;
+#pragma unroll
+  for (int c = 0; c < S / 8; ++c) {
+    if ((k >> 3) == c) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[8 * c + e] = osel(kk == e, v, a[8 * c + e]);
+    }
+  }
+}
+
 template <typename T, int S>
 __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_rows_kernel(
     int mode, const T* __restrict__ src, int64_t lds, int64_t strides, T* out, int64_t ldo, int64_t strideo,
     int32_t* __restrict__ swaps, int32_t* __restrict__ perm, int32_t* __restrict__ info, T* __restrict__ tinv,
     int64_t ldi, int64_t stridei) {
+  static_assert(S % 8 == 0, "S must be a multiple of 8");
   constexpr int NT = S < 32 ? 32 : S;
   constexpr int NW = NT / 32;
   constexpr int LP = S + 1;  // padded row pitch of the staged matrix
   __shared__ __align__(16) T urow[2][S];
   __shared__ T mat[S * LP];
   __shared__ T cmax[S];
+  __shared__ T dinv[S];
   __shared__ T redv[2][NW];
   __shared__ int redp[2][NW], redt[2][NW];
   __shared__ int swk[S];
@@ -272,10 +322,10 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_rows_kernel(
 
   int pos = t;
   bool active = live;
-#pragma unroll
   for (int k = 0; k < S; ++k) {
-    const int buf = k & 1;
-    T v = active ? (T)fabs((double)a[k]) : (T)0;
+    const int buf = k & 1, kc = k >> 3;
+    const T ak = row_get<T, S>(a, k);
+    T v = active ? (T)fabs((double)ak) : (T)0;
     int pv = active ? pos : -1;
     int pt = t;
 #pragma unroll
@@ -310,7 +360,12 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_rows_kernel(
     }
     if (t == pt) {
 #pragma unroll
-      for (int j = k; j < S; ++j) urow[buf][j] = a[j];
+      for (int c = 0; c < S / 8; ++c) {
+        if (c >= kc) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) urow[buf][8 * c + e] = a[8 * c + e];
+        }
+      }
     }
     __syncthreads();
     const T piv = urow[buf][k];
@@ -325,10 +380,18 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_rows_kernel(
     }
     if (active) {
       const T d = (piv == (T)0) ? (T)1 : piv;
-      const T l = div_rn(a[k], d);
-      a[k] = l;
+      const T l = div_rn(ak, d);
+      row_set<T, S>(a, k, l);
 #pragma unroll
-      for (int j = k + 1; j < S; ++j) a[j] = sub_rn(a[j], mul_rn(l, urow[buf][j]));
+      for (int c = 0; c < S / 8; ++c) {
+        if (c >= kc) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int j = 8 * c + e;
+            if (j > k) a[j] = sub_rn(a[j], mul_rn(l, urow[buf][j]));
+          }
+        }
+      }
     }
   }
   // factors out (row pos of the block), pivots, flag
@@ -348,36 +411,53 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_rows_kernel(
     for (int j = 0; j < S; ++j) mat[pos * LP + j] = a[j];
   }
   __syncthreads();
+  if (live) dinv[t] = (T)1 / mat[t * LP + t];
+  __syncthreads();
   if (!live) return;
   T* ti = tinv + blk * stridei;
   const int i = t;  // this thread forms row i of U^-1 and of L^-1
-  {
-    T x[S];
+  const int wlo = warp * 32, whi = min(S - 1, warp * 32 + 31);
+  // U^-1 row i: x U = e_i, right-looking over k >= (first row of this warp)
 #pragma unroll
-    for (int j = 0; j < S; ++j) x[j] = (T)(j == i);
+  for (int j = 0; j < S; ++j) a[j] = (T)(j == i);
+  for (int k = wlo; k < S; ++k) {
+    const int kc = k >> 3;
+    const T xk = row_get<T, S>(a, k) * dinv[k];
+    row_set<T, S>(a, k, xk);
 #pragma unroll
-    for (int k = 0; k < S; ++k) {
-      x[k] = x[k] / mat[k * LP + k];
+    for (int c = 0; c < S / 8; ++c) {
+      if (c >= kc) {
 #pragma unroll
-      for (int j = k + 1; j < S; ++j) x[j] = fma(-x[k], mat[k * LP + j], x[j]);
+        for (int e = 0; e < 8; ++e) {
+          const int j = 8 * c + e;
+          if (j > k) a[j] = fma(-xk, mat[k * LP + j], a[j]);
+        }
+      }
     }
-#pragma unroll
-    for (int j = 0; j < S; ++j)
-      if (j >= i) ti[i + j * ldi] = x[j];
   }
-  {
-    T x[S];
 #pragma unroll
-    for (int j = 0; j < S; ++j) x[j] = (T)(j == i);
+  for (int j = 0; j < S; ++j)
+    if (j >= i) ti[i + j * ldi] = a[j];
+  // L^-1 row i: x L = e_i (unit diagonal), left-looking from the last row of this warp
 #pragma unroll
-    for (int k = S - 1; k > 0; --k) {
+  for (int j = 0; j < S; ++j) a[j] = (T)(j == i);
+  for (int k = whi; k > 0; --k) {
+    const int kc = k >> 3;
+    const T xk = row_get<T, S>(a, k);
 #pragma unroll
-      for (int j = 0; j < k; ++j) x[j] = fma(-x[k], mat[k * LP + j], x[j]);
+    for (int c = 0; c < S / 8; ++c) {
+      if (c <= kc) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = 8 * c + e;
+          if (j < k) a[j] = fma(-xk, mat[k * LP + j], a[j]);
+        }
+      }
     }
-#pragma unroll
-    for (int j = 0; j < S; ++j)
-      if (j < i) ti[i + j * ldi] = x[j];
   }
+#pragma unroll
+  for (int j = 0; j < S; ++j)
+    if (j < i) ti[i + j * ldi] = a[j];
 }
 
 // Packed triangular inverses from stored LU for sizes without a register
