@@ -71,6 +71,9 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
   const bool want_tw = g.V != nullptr;
 
   auto stage_ptr = [&](int s) { return sm + s * Cfg::STAGE; };
+  // the A1 / V / W' panels are re-read for every column tile: keep them in L2;
+  // the C stream is touched once per level
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
 
   auto load = [&](int it, int s) {
     const int ct = it / nsub, st = it % nsub;
@@ -85,20 +88,20 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
     for (int idx = t; idx < BN * (BM / 2); idx += 256) {
       const int n = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
       const bool ok = n0 + n < g.ncols;
-      cp_async_16(Cs + n * P + m, ok ? g.C + row0 + m + (int64_t)(n0 + n) * g.ldc : g.C, ok ? 16 : 0);
+      cp_async_16_pol(Cs + n * P + m, ok ? g.C + row0 + m + (int64_t)(n0 + n) * g.ldc : g.C, ok ? 16 : 0, stream);
     }
     // A1 tile [k][m] and V tile [k][m] (both rows-contiguous per rank column)
     for (int idx = t; idx < R * (BM / 2); idx += 256) {
       const int k = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
-      cp_async_16(As + k * P + m, g.A1 + row0 + m + (int64_t)k * g.lda, 16);
-      if (want_tw) cp_async_16(Vs + k * P + m, g.V + row0 + m + (int64_t)k * g.lda, 16);
+      cp_async_16_pol(As + k * P + m, g.A1 + row0 + m + (int64_t)k * g.lda, 16, keep);
+      if (want_tw) cp_async_16_pol(Vs + k * P + m, g.V + row0 + m + (int64_t)k * g.lda, 16, keep);
     }
     // W' tile [n][k]: rows (c%2)*R.. of W_p, k contiguous
     const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
     for (int idx = t; idx < BN * (R / 2); idx += 256) {
       const int n = idx / (R / 2), k = (idx % (R / 2)) * 2;
       const bool ok = n0 + n < g.ncols;
-      cp_async_16(Ws + n * PW + k, ok ? Wp + k + (int64_t)(n0 + n) * (2 * R) : g.W, ok ? 16 : 0);
+      cp_async_16_pol(Ws + n * PW + k, ok ? Wp + k + (int64_t)(n0 + n) * (2 * R) : g.W, ok ? 16 : 0, keep);
     }
   };
 

@@ -496,6 +496,11 @@ __global__ void __launch_bounds__(128) trtri_packed_kernel(int s, const T* __res
 }
 
 template <typename T>
+hodlr_status launch_getrf_cyclic(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out,
+                                 int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv,
+                                 int64_t ldi, int64_t stridei, cudaStream_t st);
+
+template <typename T>
 static size_t getrf_smem(int s) {
   return (size_t)s * s * sizeof(T) + s * sizeof(T) + s * sizeof(int) + 16;
 }
@@ -509,19 +514,9 @@ hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds,
                           int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
                           int64_t stridei, cudaStream_t st) {
   if (batch == 0 || s == 0) return HODLR_OK;
-  if (s == 64 || s == 32 || s == 16) {
-    if (s == 64)
-      getrf_rows_kernel<T, 64><<<batch, 64, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
-                                                     tinv, ldi, stridei);
-    else if (s == 32)
-      getrf_rows_kernel<T, 32><<<batch, 32, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
-                                                     tinv, ldi, stridei);
-    else
-      getrf_rows_kernel<T, 16><<<batch, 32, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
-                                                     tinv, ldi, stridei);
-    HODLR_CHECK_LAUNCH();
-    return HODLR_OK;
-  }
+  if (s == 64 || s == 32 || s == 16)
+    return launch_getrf_cyclic<T>(s, batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi,
+                                  stridei, st);
   size_t sm = getrf_smem<T>(s);
   if (sm > 227 * 1024) return HODLR_ERR_ARG;
   cudaFuncSetAttribute(getrf_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -1,0 +1,363 @@
+// Batched bit-exact LU on a 2-D cyclic thread grid + DMMA triangular inversion.
+//
+// Replays backend.py:444-478 (_lu_factor_stack) exactly: right-looking,
+// first-max pivot over |a[k:, k]| (NaN wins, smallest logical index on ties),
+// whole-row exchange, singular guard |piv| <= eps*s*max|orig col k|, true
+// division by the pivot (0 -> 1), trailing update a - (l*u) with the product
+// rounded before the subtraction (__dmul_rn / __dsub_rn, no FMA).
+//
+// One CTA (256 threads) per block.  Thread (tr, tc) = (t % 16, t / 16) owns rows
+// {tr + 16a} x columns {tc + 16b} (a, b < S/16) in registers, so every step's
+// rank-1 update is spread over all threads and each thread loads only its S/16
+// multipliers and S/16 pivot-row entries from shared memory.  Row exchanges are
+// logical (each row carries its logical position), which is the reference's
+// physical swap with the same per-element operation sequence.
+//
+// The packed triangular inverses Tinv = strict_lower(L^-1) + upper(U^-1) that
+// the DMMA solves consume (apply.cu) are then formed in shared memory by
+// recursive doubling: 8x8 diagonal blocks are inverted per thread-row, and each
+// doubling step X = -A^-1 U_AB B^-1 (resp. X = -B^-1 C A^-1) is two small DMMA
+// GEMMs.
+#include "common.cuh"
+
+namespace hodlr {
+
+template <typename T>
+__device__ __forceinline__ bool cyc_beats(T v, int pv, T b, int pb) {
+  if (pv < 0) return false;
+  if (pb < 0) return true;
+  const bool vn = v != v, bn = b != b;
+  if (vn || bn) return (vn && bn) ? pv < pb : vn;
+  return v > b || (v == b && pv < pb);
+}
+
+template <typename T>
+__device__ __forceinline__ T cyc_nanmax(T a, T b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a > b ? a : b;
+}
+
+// opaque select (keeps register arrays in registers)
+__device__ __forceinline__ double csel(int p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}" : "=d"(r) : "d"(a), "d"(b), "r"(p));
+  return r;
+}
+__device__ __forceinline__ float csel(int p, float a, float b) {
+  float r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f32 %0, %1, %2, q;\n\t}" : "=f"(r) : "f"(a), "f"(b), "r"(p));
+  return r;
+}
+
+// C(8x8 tiles) = fa * fb over K, tiles spread over the CTA's warps; fo(i, j, v)
+// consumes the result.  DMMA for double, scalar FMA for float.
+template <typename T, class FA, class FB, class FO>
+__device__ __forceinline__ void tile_gemm(int M, int N, int K, FA fa, FB fb, FO fo) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ntile = (M / 8) * (N / 8);
+  for (int tile = warp; tile < ntile; tile += nw) {
+    const int tm = (tile % (M / 8)) * 8, tn = (tile / (M / 8)) * 8;
+    if constexpr (sizeof(T) == 8) {
+      double c0 = 0.0, c1 = 0.0;
+      const int ar = lane >> 2, ac = lane & 3;
+      for (int k0 = 0; k0 < K; k0 += 4) dmma_8x8x4(c0, c1, fa(tm + ar, k0 + ac), fb(k0 + ac, tn + ar));
+      fo(tm + ar, tn + 2 * ac, (T)c0);
+      fo(tm + ar, tn + 2 * ac + 1, (T)c1);
+    } else {
+      for (int e = lane; e < 64; e += 32) {
+        const int i = tm + (e & 7), j = tn + (e >> 3);
+        T s = 0;
+        for (int k = 0; k < K; ++k) s = fma(fa(i, k), fb(k, j), s);
+        fo(i, j, s);
+      }
+    }
+  }
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __restrict__ src, int64_t lds,
+                                                           int64_t strides, T* out, int64_t ldo, int64_t strideo,
+                                                           int32_t* __restrict__ swaps, int32_t* __restrict__ perm,
+                                                           int32_t* __restrict__ info, T* __restrict__ tinv,
+                                                           int64_t ldi, int64_t stridei) {
+  constexpr int LOC = S / 16;  // rows / columns per thread
+  constexpr int P = S + 4;     // pitch of the staged matrices
+  __shared__ T lbuf[S], ubuf[S], cmax[S];
+  __shared__ int piv_pos, piv_row, swk[S], sflag;
+  __shared__ T piv_val;
+  __shared__ __align__(16) T Tm[S * P];  // packed LU -> packed inverses, column-major
+  __shared__ __align__(16) T Tt[(S / 2) * (S / 2 + 4)];
+
+  const int64_t blk = blockIdx.x;
+  const int t = threadIdx.x, tr = t & 15, tc = t >> 4;
+  const T* g = src + blk * strides;
+
+  T e[LOC][LOC];
+#pragma unroll
+  for (int a = 0; a < LOC; ++a)
+#pragma unroll
+    for (int b = 0; b < LOC; ++b) {
+      const int i = tr + 16 * a, j = tc + 16 * b;
+      T v;
+      if (mode == 0) {
+        v = g[i + j * lds];
+      } else {
+        constexpr int R = S / 2;
+        if (i < R && j < R)
+          v = g[i + j * lds];
+        else if (i >= R && j >= R)
+          v = g[i + (j - R) * lds];
+        else
+          v = (i < R) ? (T)(i == j - R) : (T)(i - R == j);
+      }
+      e[a][b] = v;
+    }
+  // original column magnitudes: reduce over the 16 row-owners of each column
+#pragma unroll
+  for (int b = 0; b < LOC; ++b) {
+    T m = (T)0;
+#pragma unroll
+    for (int a = 0; a < LOC; ++a) m = cyc_nanmax(m, (T)fabs((double)e[a][b]));
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) m = cyc_nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tr == 0) cmax[tc + 16 * b] = m;
+  }
+  if (t == 0) sflag = 0;
+  int pos[LOC];
+  bool act[LOC];
+#pragma unroll
+  for (int a = 0; a < LOC; ++a) {
+    pos[a] = tr + 16 * a;
+    act[a] = true;
+  }
+  __syncthreads();
+  const T thr_scale = mul_rn(Eps<T>::v, (T)S);
+
+  for (int k = 0; k < S; ++k) {
+    const int kc = k & 15, kb = k >> 4;
+    // ---- pivot search by the 16 owners of column k (one half-warp) ----
+    if (tc == kc) {
+      T bv = (T)0, bs = (T)0;
+      int bp = -1, br = 0;
+#pragma unroll
+      for (int a = 0; a < LOC; ++a) {
+        T x = e[a][0];
+#pragma unroll
+        for (int b = 1; b < LOC; ++b) x = csel(kb == b, e[a][b], x);
+        const T v = (T)fabs((double)x);
+        const int pv = act[a] ? pos[a] : -1;
+        if (cyc_beats(v, pv, bv, bp)) {
+          bv = v;
+          bp = pv;
+          br = tr + 16 * a;
+          bs = x;
+        }
+      }
+      const unsigned half = (tc & 1) ? 0xffff0000u : 0x0000ffffu;  // this column group's lanes
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        const T ov = __shfl_xor_sync(half, bv, o);
+        const int op = __shfl_xor_sync(half, bp, o);
+        const int orr = __shfl_xor_sync(half, br, o);
+        const T os = __shfl_xor_sync(half, bs, o);
+        if (cyc_beats(ov, op, bv, bp)) {
+          bv = ov;
+          bp = op;
+          br = orr;
+          bs = os;
+        }
+      }
+      if (tr == 0) {
+        piv_pos = bp;
+        piv_row = br;
+        piv_val = bs;  // signed pivot value
+        swk[k] = bp;
+        if ((T)fabs((double)bs) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
+      }
+    }
+    __syncthreads();
+    const int prow = piv_row, ppos = piv_pos;
+    const T piv = piv_val;
+    // pivot-row owners publish u_kj; rows exchange logical positions
+    if ((prow & 15) == tr) {
+      const int ap = prow >> 4;
+#pragma unroll
+      for (int b = 0; b < LOC; ++b) {
+        T x = e[0][b];
+#pragma unroll
+        for (int a = 1; a < LOC; ++a) x = csel(ap == a, e[a][b], x);
+        const int j = tc + 16 * b;
+        if (j > k) ubuf[j] = x;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < LOC; ++a) {
+      if (pos[a] == k) pos[a] = ppos;
+      if (tr + 16 * a == prow) {
+        pos[a] = k;
+        act[a] = false;
+      }
+    }
+    // column-k owners form the multipliers l = a_ik / piv
+    const T d = (piv == (T)0) ? (T)1 : piv;
+    if (tc == kc) {
+#pragma unroll
+      for (int a = 0; a < LOC; ++a) {
+        if (act[a]) {
+          T x = e[a][0];
+#pragma unroll
+          for (int b = 1; b < LOC; ++b) x = csel(kb == b, e[a][b], x);
+          const T l = div_rn(x, d);
+#pragma unroll
+          for (int b = 0; b < LOC; ++b) e[a][b] = csel(kb == b, l, e[a][b]);
+          lbuf[tr + 16 * a] = l;
+        }
+      }
+    }
+    __syncthreads();
+    // trailing update: a_ij - (l_i * u_j) for active rows, columns j > k
+#pragma unroll
+    for (int a = 0; a < LOC; ++a) {
+      if (act[a]) {
+        const T l = lbuf[tr + 16 * a];
+#pragma unroll
+        for (int b = 0; b < LOC; ++b) {
+          const int j = tc + 16 * b;
+          if (b >= kb && j > k) e[a][b] = sub_rn(e[a][b], mul_rn(l, ubuf[j]));
+        }
+      }
+    }
+  }
+  // ---- outputs: LU rows at their logical positions, pivots, flag ----
+  T* o = out + blk * strideo;
+#pragma unroll
+  for (int a = 0; a < LOC; ++a)
+#pragma unroll
+    for (int b = 0; b < LOC; ++b) {
+      const int j = tc + 16 * b;
+      o[pos[a] + j * ldo] = e[a][b];
+      Tm[pos[a] + j * P] = e[a][b];
+    }
+  if (tc == 0) {
+#pragma unroll
+    for (int a = 0; a < LOC; ++a) perm[blk * S + pos[a]] = tr + 16 * a;
+  }
+  __syncthreads();
+  if (t < S) swaps[blk * S + t] = swk[t];
+  if (t == 0) info[blk] = sflag;
+  if (tinv == nullptr) return;
+
+  // ---- packed inverses, level 0: 8x8 diagonal blocks (thread = (block, row, U/L)) ----
+  {
+    const int q = (t >> 3) & (S / 8 - 1), i = t & 7, which = t / S;  // which: 0 = U, 1 = L (t < 2S)
+    T x[8];
+    if (t < 2 * S) {
+      const int o0 = 8 * q;
+      if (which == 0) {  // row i of inv(U_qq)
+        const T dii = (T)1 / Tm[(o0 + i) + (o0 + i) * P];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (j == i) ? dii : (T)0;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+          if (j > i) {
+            T s = (T)0;
+#pragma unroll
+            for (int kk = 0; kk < j; ++kk)
+              if (kk >= i) s = fma(x[kk], Tm[(o0 + kk) + (o0 + j) * P], s);
+            x[j] = -s / Tm[(o0 + j) + (o0 + j) * P];
+          }
+        }
+      } else {  // row i of inv(L_qq), unit diagonal
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (T)(j == i);
+#pragma unroll
+        for (int j = 6; j >= 0; --j) {
+          if (j < i) {
+            T s = (T)0;
+#pragma unroll
+            for (int kk = 1; kk < 8; ++kk)
+              if (kk > j && kk <= i) s = fma(x[kk], Tm[(o0 + kk) + (o0 + j) * P], s);
+            x[j] = -s;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (t < 2 * S) {
+      const int o0 = 8 * q;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (which == 0 ? (j >= i) : (j < i)) Tm[(o0 + i) + (o0 + j) * P] = x[j];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- doubling: h = 8, 16, ..., S/2 ----
+  constexpr int PT = S / 2 + 4;
+  for (int h = 8; h < S; h *= 2) {
+    for (int o0 = 0; o0 < S; o0 += 2 * h) {
+      const int a0 = o0, b0 = o0 + h;
+      // U: Tt = U_AB * inv(B) (inv(B) upper: k <= n)
+      tile_gemm<T>(
+          h, h, h, [&](int i, int k) { return Tm[(a0 + i) + (b0 + k) * P]; },
+          [&](int k, int n) { return k <= n ? Tm[(b0 + k) + (b0 + n) * P] : (T)0; },
+          [&](int i, int n, T v) { Tt[i + n * PT] = v; });
+      __syncthreads();
+      // U: X = -inv(A) * Tt (inv(A) upper: k >= i)
+      tile_gemm<T>(
+          h, h, h, [&](int i, int k) { return k >= i ? Tm[(a0 + i) + (a0 + k) * P] : (T)0; },
+          [&](int k, int n) { return Tt[k + n * PT]; }, [&](int i, int n, T v) { Tm[(a0 + i) + (b0 + n) * P] = -v; });
+      __syncthreads();
+      // L: Tt = C * inv(A) (inv(A) unit lower: strict part k > n, plus identity)
+      tile_gemm<T>(
+          h, h, h, [&](int i, int k) { return Tm[(b0 + i) + (a0 + k) * P]; },
+          [&](int k, int n) { return k > n ? Tm[(a0 + k) + (a0 + n) * P] : (T)(k == n); },
+          [&](int i, int n, T v) { Tt[i + n * PT] = v; });
+      __syncthreads();
+      // L: X = -inv(B) * Tt (inv(B) unit lower)
+      tile_gemm<T>(
+          h, h, h, [&](int i, int k) { return k < i ? Tm[(b0 + i) + (b0 + k) * P] : (T)(k == i); },
+          [&](int k, int n) { return Tt[k + n * PT]; }, [&](int i, int n, T v) { Tm[(b0 + i) + (a0 + n) * P] = -v; });
+      __syncthreads();
+    }
+  }
+  T* ti = tinv + blk * stridei;
+  for (int idx = t; idx < S * S; idx += 256) {
+    const int i = idx % S, j = idx / S;
+    ti[i + (int64_t)j * ldi] = Tm[i + j * P];
+  }
+}
+
+template <typename T>
+hodlr_status launch_getrf_cyclic(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out,
+                                 int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv,
+                                 int64_t ldi, int64_t stridei, cudaStream_t st) {
+  switch (s) {
+    case 16:
+      getrf_cyclic_kernel<T, 16><<<batch, 256, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
+                                                        tinv, ldi, stridei);
+      break;
+    case 32:
+      getrf_cyclic_kernel<T, 32><<<batch, 256, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
+                                                        tinv, ldi, stridei);
+      break;
+    case 64:
+      getrf_cyclic_kernel<T, 64><<<batch, 256, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
+                                                        tinv, ldi, stridei);
+      break;
+    default:
+      return HODLR_ERR_ARG;
+  }
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+template hodlr_status launch_getrf_cyclic<double>(int, int, int, const double*, int64_t, int64_t, double*, int64_t,
+                                                  int64_t, int32_t*, int32_t*, int32_t*, double*, int64_t, int64_t,
+                                                  cudaStream_t);
+template hodlr_status launch_getrf_cyclic<float>(int, int, int, const float*, int64_t, int64_t, float*, int64_t,
+                                                 int64_t, int32_t*, int32_t*, int32_t*, float*, int64_t, int64_t,
+                                                 cudaStream_t);
+
+}  // namespace hodlr
