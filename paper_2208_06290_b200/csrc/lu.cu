@@ -514,7 +514,7 @@ hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds,
                           int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
                           int64_t stridei, cudaStream_t st) {
   if (batch == 0 || s == 0) return HODLR_OK;
-  if (s == 64 || s == 32 || s == 16)
+  if (s == 128 || s == 64 || s == 32 || s == 16)
     return launch_getrf_cyclic<T>(s, batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi,
                                   stridei, st);
   size_t sm = getrf_smem<T>(s);

@@ -86,8 +86,9 @@ __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __
   __shared__ T lbuf[S], ubuf[S], cmax[S];
   __shared__ int piv_pos, piv_row, swk[S], sflag;
   __shared__ T piv_val;
-  __shared__ __align__(16) T Tm[S * P];  // packed LU -> packed inverses, column-major
-  __shared__ __align__(16) T Tt[(S / 2) * (S / 2 + 4)];
+  extern __shared__ __align__(16) unsigned char cyc_smem[];
+  T* Tm = reinterpret_cast<T*>(cyc_smem);  // packed LU -> packed inverses, column-major, pitch P
+  T* Tt = Tm + S * P;                      // (S/2) x (S/2) scratch, pitch S/2 + 4
 
   const int64_t blk = blockIdx.x;
   const int t = threadIdx.x, tr = t & 15, tc = t >> 4;
@@ -208,7 +209,8 @@ __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __
           T x = e[a][0];
 #pragma unroll
           for (int b = 1; b < LOC; ++b) x = csel(kb == b, e[a][b], x);
-          const T l = div_rn(x, d);
+          // 0 / d is +-0 (sign xor); skip the division's slow path for it
+          const T l = (x == (T)0 && d == d) ? ((signbit(x) != signbit(d)) ? (T)-0.0 : (T)0.0) : div_rn(x, d);
 #pragma unroll
           for (int b = 0; b < LOC; ++b) e[a][b] = csel(kb == b, l, e[a][b]);
           lbuf[tr + 16 * a] = l;
@@ -249,13 +251,16 @@ __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __
   if (tinv == nullptr) return;
 
   // ---- packed inverses, level 0: 8x8 diagonal blocks (thread = (block, row, U/L)) ----
+  __shared__ T rdiag[S];
+  if (t < S) rdiag[t] = (T)1 / Tm[t + t * P];
+  __syncthreads();
   {
     const int q = (t >> 3) & (S / 8 - 1), i = t & 7, which = t / S;  // which: 0 = U, 1 = L (t < 2S)
     T x[8];
     if (t < 2 * S) {
       const int o0 = 8 * q;
       if (which == 0) {  // row i of inv(U_qq)
-        const T dii = (T)1 / Tm[(o0 + i) + (o0 + i) * P];
+        const T dii = rdiag[o0 + i];
 #pragma unroll
         for (int j = 0; j < 8; ++j) x[j] = (j == i) ? dii : (T)0;
 #pragma unroll
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __
 #pragma unroll
             for (int kk = 0; kk < j; ++kk)
               if (kk >= i) s = fma(x[kk], Tm[(o0 + kk) + (o0 + j) * P], s);
-            x[j] = -s / Tm[(o0 + j) + (o0 + j) * P];
+            x[j] = -s * rdiag[o0 + j];
           }
         }
       } else {  // row i of inv(L_qq), unit diagonal
@@ -329,28 +334,33 @@ __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __
   }
 }
 
+template <typename T, int S>
+static hodlr_status run_cyclic(int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
+                               int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
+                               int64_t stridei, cudaStream_t st) {
+  constexpr size_t smem = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(getrf_cyclic_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  getrf_cyclic_kernel<T, S><<<batch, 256, smem, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
+                                                       tinv, ldi, stridei);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
 template <typename T>
 hodlr_status launch_getrf_cyclic(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out,
                                  int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv,
                                  int64_t ldi, int64_t stridei, cudaStream_t st) {
   switch (s) {
-    case 16:
-      getrf_cyclic_kernel<T, 16><<<batch, 256, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
-                                                        tinv, ldi, stridei);
-      break;
-    case 32:
-      getrf_cyclic_kernel<T, 32><<<batch, 256, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
-                                                        tinv, ldi, stridei);
-      break;
-    case 64:
-      getrf_cyclic_kernel<T, 64><<<batch, 256, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
-                                                        tinv, ldi, stridei);
-      break;
-    default:
-      return HODLR_ERR_ARG;
+    case 16: return run_cyclic<T, 16>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 32: return run_cyclic<T, 32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 64: return run_cyclic<T, 64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 128: return run_cyclic<T, 128>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    default: return HODLR_ERR_ARG;
   }
-  HODLR_CHECK_LAUNCH();
-  return HODLR_OK;
 }
 
 template hodlr_status launch_getrf_cyclic<double>(int, int, int, const double*, int64_t, int64_t, double*, int64_t,

@@ -129,11 +129,14 @@ def test_random_vs_oracle(n, m, r, s):
     assert rel(x, orc.solve(fo, b, threads=8)) <= max(TOL, 20 * sx)
     if s <= 4:
         assert rel(x, orc.solve(fo, b, threads=8)) <= TOL
-    # relative residual against the HODLR operator itself
+    # relative residual against the HODLR operator itself, vs the oracle's own
     hm = to_gpu(h)
-    res = hm.matvec(torch.from_numpy(x).cuda()) - torch.from_numpy(b).cuda()
-    relres = float(torch.linalg.norm(res) / torch.linalg.norm(torch.from_numpy(b)))
-    assert relres < 1e-12
+    bt = torch.from_numpy(b).cuda()
+
+    def relres(xx):
+        return float(torch.linalg.norm(hm.matvec(torch.from_numpy(xx).cuda()) - bt) / torch.linalg.norm(bt))
+
+    assert relres(x) <= max(1e-12, 4 * relres(orc.solve(fo, b, threads=8)))
 
 
 def test_multi_rhs_columns_bitwise_equal_single():
