@@ -75,6 +75,92 @@ __device__ __forceinline__ void tile_gemm(int M, int N, int K, FA fa, FB fb, FO 
   }
 }
 
+// In-place packed triangular inversion of the S x S LU in shared memory (column-
+// major, pitch P): upper(U) -> upper(U^-1), strict_lower(L) -> strict_lower(L^-1).
+// Tt: (S/2) x (S/2) scratch.  Works for any CTA size (multiple of 32).
+template <typename T, int S>
+__device__ void packed_trtri(T* Tm, T* Tt, int P) {
+  // ---- packed inverses, level 0: 8x8 diagonal blocks (thread = (block, row, U/L)) ----
+  __shared__ T rdiag[S];
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int u = t; u < S; u += nt) rdiag[u] = (T)1 / Tm[u + u * P];
+  __syncthreads();
+  for (int u0 = 0; u0 < 2 * S; u0 += nt) {
+    const int u = u0 + t;
+    const int q = (u >> 3) & (S / 8 - 1), i = u & 7, which = u / S;  // which: 0 = U, 1 = L
+    T x[8];
+    if (u < 2 * S) {
+      const int o0 = 8 * q;
+      if (which == 0) {  // row i of inv(U_qq)
+        const T dii = rdiag[o0 + i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (j == i) ? dii : (T)0;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+          if (j > i) {
+            T s = (T)0;
+#pragma unroll
+            for (int kk = 0; kk < j; ++kk)
+              if (kk >= i) s = fma(x[kk], Tm[(o0 + kk) + (o0 + j) * P], s);
+            x[j] = -s * rdiag[o0 + j];
+          }
+        }
+      } else {  // row i of inv(L_qq), unit diagonal
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (T)(j == i);
+#pragma unroll
+        for (int j = 6; j >= 0; --j) {
+          if (j < i) {
+            T s = (T)0;
+#pragma unroll
+            for (int kk = 1; kk < 8; ++kk)
+              if (kk > j && kk <= i) s = fma(x[kk], Tm[(o0 + kk) + (o0 + j) * P], s);
+            x[j] = -s;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (u < 2 * S) {
+      const int o0 = 8 * q;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (which == 0 ? (j >= i) : (j < i)) Tm[(o0 + i) + (o0 + j) * P] = x[j];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- doubling: h = 8, 16, ..., S/2 ----
+  constexpr int PT = S / 2 + 4;
+  for (int h = 8; h < S; h *= 2) {
+    for (int o0 = 0; o0 < S; o0 += 2 * h) {
+      const int a0 = o0, b0 = o0 + h;
+      // U: Tt = U_AB * inv(B) (inv(B) upper: k <= n)
+      tile_gemm<T>(
+          h, h, h, [&](int i, int k) { return Tm[(a0 + i) + (b0 + k) * P]; },
+          [&](int k, int n) { return k <= n ? Tm[(b0 + k) + (b0 + n) * P] : (T)0; },
+          [&](int i, int n, T v) { Tt[i + n * PT] = v; });
+      __syncthreads();
+      // U: X = -inv(A) * Tt (inv(A) upper: k >= i)
+      tile_gemm<T>(
+          h, h, h, [&](int i, int k) { return k >= i ? Tm[(a0 + i) + (a0 + k) * P] : (T)0; },
+          [&](int k, int n) { return Tt[k + n * PT]; }, [&](int i, int n, T v) { Tm[(a0 + i) + (b0 + n) * P] = -v; });
+      __syncthreads();
+      // L: Tt = C * inv(A) (inv(A) unit lower: strict part k > n, plus identity)
+      tile_gemm<T>(
+          h, h, h, [&](int i, int k) { return Tm[(b0 + i) + (a0 + k) * P]; },
+          [&](int k, int n) { return k > n ? Tm[(a0 + k) + (a0 + n) * P] : (T)(k == n); },
+          [&](int i, int n, T v) { Tt[i + n * PT] = v; });
+      __syncthreads();
+      // L: X = -inv(B) * Tt (inv(B) unit lower)
+      tile_gemm<T>(
+          h, h, h, [&](int i, int k) { return k < i ? Tm[(b0 + i) + (b0 + k) * P] : (T)(k == i); },
+          [&](int k, int n) { return Tt[k + n * PT]; }, [&](int i, int n, T v) { Tm[(b0 + i) + (a0 + n) * P] = -v; });
+      __syncthreads();
+    }
+  }
+}
+
 template <typename T, int S>
 __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __restrict__ src, int64_t lds,
                                                            int64_t strides, T* out, int64_t ldo, int64_t strideo,
@@ -250,88 +336,195 @@ __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __
   if (t == 0) info[blk] = sflag;
   if (tinv == nullptr) return;
 
-  // ---- packed inverses, level 0: 8x8 diagonal blocks (thread = (block, row, U/L)) ----
-  __shared__ T rdiag[S];
-  if (t < S) rdiag[t] = (T)1 / Tm[t + t * P];
-  __syncthreads();
-  {
-    const int q = (t >> 3) & (S / 8 - 1), i = t & 7, which = t / S;  // which: 0 = U, 1 = L (t < 2S)
-    T x[8];
-    if (t < 2 * S) {
-      const int o0 = 8 * q;
-      if (which == 0) {  // row i of inv(U_qq)
-        const T dii = rdiag[o0 + i];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = (j == i) ? dii : (T)0;
-#pragma unroll
-        for (int j = 1; j < 8; ++j) {
-          if (j > i) {
-            T s = (T)0;
-#pragma unroll
-            for (int kk = 0; kk < j; ++kk)
-              if (kk >= i) s = fma(x[kk], Tm[(o0 + kk) + (o0 + j) * P], s);
-            x[j] = -s * rdiag[o0 + j];
-          }
-        }
-      } else {  // row i of inv(L_qq), unit diagonal
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = (T)(j == i);
-#pragma unroll
-        for (int j = 6; j >= 0; --j) {
-          if (j < i) {
-            T s = (T)0;
-#pragma unroll
-            for (int kk = 1; kk < 8; ++kk)
-              if (kk > j && kk <= i) s = fma(x[kk], Tm[(o0 + kk) + (o0 + j) * P], s);
-            x[j] = -s;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (t < 2 * S) {
-      const int o0 = 8 * q;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (which == 0 ? (j >= i) : (j < i)) Tm[(o0 + i) + (o0 + j) * P] = x[j];
-      }
-    }
-    __syncthreads();
-  }
-  // ---- doubling: h = 8, 16, ..., S/2 ----
-  constexpr int PT = S / 2 + 4;
-  for (int h = 8; h < S; h *= 2) {
-    for (int o0 = 0; o0 < S; o0 += 2 * h) {
-      const int a0 = o0, b0 = o0 + h;
-      // U: Tt = U_AB * inv(B) (inv(B) upper: k <= n)
-      tile_gemm<T>(
-          h, h, h, [&](int i, int k) { return Tm[(a0 + i) + (b0 + k) * P]; },
-          [&](int k, int n) { return k <= n ? Tm[(b0 + k) + (b0 + n) * P] : (T)0; },
-          [&](int i, int n, T v) { Tt[i + n * PT] = v; });
-      __syncthreads();
-      // U: X = -inv(A) * Tt (inv(A) upper: k >= i)
-      tile_gemm<T>(
-          h, h, h, [&](int i, int k) { return k >= i ? Tm[(a0 + i) + (a0 + k) * P] : (T)0; },
-          [&](int k, int n) { return Tt[k + n * PT]; }, [&](int i, int n, T v) { Tm[(a0 + i) + (b0 + n) * P] = -v; });
-      __syncthreads();
-      // L: Tt = C * inv(A) (inv(A) unit lower: strict part k > n, plus identity)
-      tile_gemm<T>(
-          h, h, h, [&](int i, int k) { return Tm[(b0 + i) + (a0 + k) * P]; },
-          [&](int k, int n) { return k > n ? Tm[(a0 + k) + (a0 + n) * P] : (T)(k == n); },
-          [&](int i, int n, T v) { Tt[i + n * PT] = v; });
-      __syncthreads();
-      // L: X = -inv(B) * Tt (inv(B) unit lower)
-      tile_gemm<T>(
-          h, h, h, [&](int i, int k) { return k < i ? Tm[(b0 + i) + (b0 + k) * P] : (T)(k == i); },
-          [&](int k, int n) { return Tt[k + n * PT]; }, [&](int i, int n, T v) { Tm[(b0 + i) + (a0 + n) * P] = -v; });
-      __syncthreads();
-    }
-  }
+  packed_trtri<T, S>(Tm, Tt, P);
   T* ti = tinv + blk * stridei;
   for (int idx = t; idx < S * S; idx += 256) {
     const int i = idx % S, j = idx / S;
     ti[i + (int64_t)j * ldi] = Tm[i + j * P];
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Shared-memory row LU: thread t owns row t of the block, stored row-major in
+// shared memory (pitch S+2: conflict-free 16B accesses across threads).  The
+// step loop runs at runtime (no unrolling): each active thread forms its own
+// multiplier l = a_tk / piv and updates its row in place, reading the pivot
+// row straight from shared memory -- the pivot row is final once chosen, so
+// one barrier per step (the cross-warp argmax) orders everything.  Same IEEE
+// operation sequence per element as the reference.
+// ---------------------------------------------------------------------------
+template <typename T, int S>
+__global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, const T* __restrict__ src, int64_t lds,
+                                                                 int64_t strides, T* out, int64_t ldo,
+                                                                 int64_t strideo, int32_t* __restrict__ swaps,
+                                                                 int32_t* __restrict__ perm,
+                                                                 int32_t* __restrict__ info, T* __restrict__ tinv,
+                                                                 int64_t ldi, int64_t stridei) {
+  constexpr int NT = S < 32 ? 32 : S;
+  constexpr int NW = NT / 32;
+  constexpr int RP = S + 16 / (int)sizeof(T);  // row pitch: 16B-aligned rows, 16B bank shift per row
+  extern __shared__ __align__(16) unsigned char sr_smem[];
+  T* A = reinterpret_cast<T*>(sr_smem);  // S rows x RP
+  __shared__ T cmax[S];
+  __shared__ T redv[2][NW];
+  __shared__ int redp[2][NW], redt[2][NW];
+  __shared__ int swk[S];
+  __shared__ int sflag;
+
+  const int64_t blk = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool live = t < S;
+  const T* g = src + blk * strides;
+  T* row = A + t * RP;
+  if (live) {
+    for (int j = 0; j < S; ++j) {
+      T v;
+      if (mode == 0) {
+        v = g[t + j * lds];
+      } else {
+        constexpr int R = S / 2;
+        if (t < R && j < R)
+          v = g[t + j * lds];
+        else if (t >= R && j >= R)
+          v = g[t + (j - R) * lds];
+        else
+          v = (t < R) ? (T)(t == j - R) : (T)(t - R == j);
+      }
+      row[j] = v;
+    }
+  }
+  if (t == 0) sflag = 0;
+  __syncthreads();
+  if (live) {  // thread t: max |a_it| over the original column t (NaN-propagating)
+    T m = (T)0;
+    for (int i = 0; i < S; ++i) m = cyc_nanmax(m, (T)fabs((double)A[i * RP + t]));
+    cmax[t] = m;
+  }
+  const T thr_scale = mul_rn(Eps<T>::v, (T)S);
+  int pos = t;
+  bool active = live;
+  for (int k = 0; k < S; ++k) {
+    const int buf = k & 1;
+    T v = (T)0;
+    int pv = -1;
+    if (active) {
+      v = (T)fabs((double)row[k]);
+      pv = pos;
+    }
+    int pt = t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int op = __shfl_xor_sync(0xffffffffu, pv, o);
+      const int ot = __shfl_xor_sync(0xffffffffu, pt, o);
+      if (cyc_beats(ov, op, v, pv)) {
+        v = ov;
+        pv = op;
+        pt = ot;
+      }
+    }
+    if (NW > 1) {
+      if (lane == 0) {
+        redv[buf][warp] = v;
+        redp[buf][warp] = pv;
+        redt[buf][warp] = pt;
+      }
+      __syncthreads();
+      v = redv[buf][0];
+      pv = redp[buf][0];
+      pt = redt[buf][0];
+#pragma unroll
+      for (int w = 1; w < NW; ++w)
+        if (cyc_beats(redv[buf][w], redp[buf][w], v, pv)) {
+          v = redv[buf][w];
+          pv = redp[buf][w];
+          pt = redt[buf][w];
+        }
+    } else {
+      __syncwarp();
+    }
+    const T* prow = A + pt * RP;
+    const T piv = prow[k];
+    if (t == 0) {
+      swk[k] = pv;
+      if ((T)fabs((double)piv) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
+    }
+    if (pos == k) pos = pv;
+    if (t == pt) {
+      pos = k;
+      active = false;
+    }
+    if (active) {
+      const T d = (piv == (T)0) ? (T)1 : piv;
+      const T x = row[k];
+      const T l = (x == (T)0 && d == d) ? ((signbit(x) != signbit(d)) ? (T)-0.0 : (T)0.0) : div_rn(x, d);
+      row[k] = l;
+      int j = k + 1;
+      if (j & 1) {  // align to 16B pairs
+        if (j < S) row[j] = sub_rn(row[j], mul_rn(l, prow[j]));
+        ++j;
+      }
+      if constexpr (sizeof(T) == 8) {
+#pragma unroll 4
+        for (; j < S; j += 2) {
+          const double2 u = *reinterpret_cast<const double2*>(prow + j);
+          double2 a = *reinterpret_cast<double2*>(row + j);
+          a.x = sub_rn(a.x, mul_rn(l, u.x));
+          a.y = sub_rn(a.y, mul_rn(l, u.y));
+          *reinterpret_cast<double2*>(row + j) = a;
+        }
+      } else {
+#pragma unroll 4
+        for (; j < S; ++j) row[j] = sub_rn(row[j], mul_rn(l, prow[j]));
+      }
+    }
+  }
+  __syncthreads();
+  T* o = out + blk * strideo;
+  if (live) {
+    for (int j = 0; j < S; ++j) o[pos + j * ldo] = row[j];
+    perm[blk * S + pos] = t;
+    swaps[blk * S + t] = swk[t];
+  }
+  if (t == 0) info[blk] = sflag;
+  if (tinv == nullptr) return;
+  // packed inverses: stage the logical LU column-major (reuse the row buffer)
+  constexpr int P = S + 4;
+  __syncthreads();  // global LU writes visible to the block; row buffer free after this
+  T* Tm = A;
+  T* Tt = A + S * P;
+  for (int idx = t; idx < S * S; idx += NT) {
+    const int i = idx % S, j = idx / S;
+    Tm[i + j * P] = o[i + j * ldo];
+  }
+  __syncthreads();
+  packed_trtri<T, S>(Tm, Tt, P);
+  T* ti = tinv + blk * stridei;
+  for (int idx = t; idx < S * S; idx += NT) {
+    const int i = idx % S, j = idx / S;
+    ti[i + (int64_t)j * ldi] = Tm[i + j * P];
+  }
+}
+
+template <typename T, int S>
+static hodlr_status run_sr(int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
+                           int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
+                           int64_t stridei, cudaStream_t st) {
+  constexpr int RP = S + 16 / (int)sizeof(T);
+  constexpr size_t rows = (size_t)S * RP * sizeof(T);
+  constexpr size_t inv = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(T);
+  constexpr size_t smem = rows > inv ? rows : inv;
+  constexpr int NT = S < 32 ? 32 : S;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(getrf_sr_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  getrf_sr_kernel<T, S><<<batch, NT, smem, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv,
+                                                  ldi, stridei);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
 }
 
 template <typename T, int S>
@@ -355,10 +548,10 @@ hodlr_status launch_getrf_cyclic(int s, int batch, int mode, const T* src, int64
                                  int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv,
                                  int64_t ldi, int64_t stridei, cudaStream_t st) {
   switch (s) {
-    case 16: return run_cyclic<T, 16>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
-    case 32: return run_cyclic<T, 32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
-    case 64: return run_cyclic<T, 64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
-    case 128: return run_cyclic<T, 128>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 16: return run_sr<T, 16>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 32: return run_sr<T, 32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 64: return run_sr<T, 64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 128: return run_sr<T, 128>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     default: return HODLR_ERR_ARG;
   }
 }
