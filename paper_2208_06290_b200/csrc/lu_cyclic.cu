@@ -38,6 +38,31 @@ __device__ __forceinline__ T cyc_nanmax(T a, T b) {
   return a > b ? a : b;
 }
 
+
+// np.argmax key of |v|: the IEEE bit pattern of a non-negative number orders
+// like its value, NaN (canonicalised) sorts above +inf, and ties are broken
+// by the smallest logical position -- so the pivot search is two integer
+// max-reductions plus one min-reduction (REDUX), no float compares.
+__device__ __forceinline__ void abs_key(double v, unsigned& hi, unsigned& lo) {
+  unsigned long long b = (v != v) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(fabs(v));
+  hi = (unsigned)(b >> 32);
+  lo = (unsigned)b;
+}
+__device__ __forceinline__ void abs_key(float v, unsigned& hi, unsigned& lo) {
+  hi = (v != v) ? 0x7fc00000u : (unsigned)__float_as_uint(fabsf(v));
+  lo = 0u;
+}
+// warp argmax over (key, pos) with key descending, pos ascending; returns the
+// winning (hi, lo, pos) in every lane (inactive lanes: key 0, pos INT_MAX)
+__device__ __forceinline__ void warp_argmax(unsigned& hi, unsigned& lo, int& pos) {
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const int mp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? pos : 0x7fffffff);
+  hi = mh;
+  lo = ml;
+  pos = mp;
+}
+
 // opaque select (keeps register arrays in registers)
 __device__ __forceinline__ double csel(int p, double a, double b) {
   double r;
@@ -367,8 +392,8 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
   extern __shared__ __align__(16) unsigned char sr_smem[];
   T* A = reinterpret_cast<T*>(sr_smem);  // S rows x RP
   __shared__ T cmax[S];
-  __shared__ T redv[2][NW];
-  __shared__ int redp[2][NW], redt[2][NW];
+  __shared__ unsigned redh[2][NW], redl[2][NW];
+  __shared__ int redp[2][NW];
   __shared__ int swk[S];
   __shared__ int sflag;
 
@@ -397,53 +422,53 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
   if (t == 0) sflag = 0;
   __syncthreads();
   if (live) {  // thread t: max |a_it| over the original column t (NaN-propagating)
-    T m = (T)0;
-    for (int i = 0; i < S; ++i) m = cyc_nanmax(m, (T)fabs((double)A[i * RP + t]));
-    cmax[t] = m;
+    T m0 = (T)0, m1 = (T)0, m2 = (T)0, m3 = (T)0;
+#pragma unroll 4
+    for (int i = 0; i < S; i += 4) {
+      m0 = cyc_nanmax(m0, (T)fabs((double)A[i * RP + t]));
+      m1 = cyc_nanmax(m1, (T)fabs((double)A[(i + 1) * RP + t]));
+      m2 = cyc_nanmax(m2, (T)fabs((double)A[(i + 2) * RP + t]));
+      m3 = cyc_nanmax(m3, (T)fabs((double)A[(i + 3) * RP + t]));
+    }
+    cmax[t] = cyc_nanmax(cyc_nanmax(m0, m1), cyc_nanmax(m2, m3));
   }
   const T thr_scale = mul_rn(Eps<T>::v, (T)S);
   int pos = t;
   bool active = live;
   for (int k = 0; k < S; ++k) {
     const int buf = k & 1;
-    T v = (T)0;
-    int pv = -1;
+    unsigned kh = 0u, kl = 0u;
+    int pv = 0x7fffffff;  // (logical position << 8) | thread: unique, orders by position
     if (active) {
-      v = (T)fabs((double)row[k]);
-      pv = pos;
+      abs_key(row[k], kh, kl);
+      pv = (pos << 8) | t;
     }
-    int pt = t;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const T ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const int op = __shfl_xor_sync(0xffffffffu, pv, o);
-      const int ot = __shfl_xor_sync(0xffffffffu, pt, o);
-      if (cyc_beats(ov, op, v, pv)) {
-        v = ov;
-        pv = op;
-        pt = ot;
-      }
-    }
+    warp_argmax(kh, kl, pv);
     if (NW > 1) {
       if (lane == 0) {
-        redv[buf][warp] = v;
+        redh[buf][warp] = kh;
+        redl[buf][warp] = kl;
         redp[buf][warp] = pv;
-        redt[buf][warp] = pt;
       }
       __syncthreads();
-      v = redv[buf][0];
+      kh = redh[buf][0];
+      kl = redl[buf][0];
       pv = redp[buf][0];
-      pt = redt[buf][0];
 #pragma unroll
-      for (int w = 1; w < NW; ++w)
-        if (cyc_beats(redv[buf][w], redp[buf][w], v, pv)) {
-          v = redv[buf][w];
-          pv = redp[buf][w];
-          pt = redt[buf][w];
+      for (int w = 1; w < NW; ++w) {
+        const unsigned h2 = redh[buf][w], l2 = redl[buf][w];
+        const int p2 = redp[buf][w];
+        if (h2 > kh || (h2 == kh && (l2 > kl || (l2 == kl && p2 < pv)))) {
+          kh = h2;
+          kl = l2;
+          pv = p2;
         }
+      }
     } else {
       __syncwarp();
     }
+    const int pt = pv & 255;
+    pv >>= 8;
     const T* prow = A + pt * RP;
     const T piv = prow[k];
     if (t == 0) {
