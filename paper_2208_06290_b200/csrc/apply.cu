@@ -40,17 +40,20 @@ __device__ __forceinline__ int64_t aoff(int b, int bdiv, int64_t hi, int64_t lo)
   return (int64_t)(b / bdiv) * hi + (int64_t)(b % bdiv) * lo;
 }
 
+constexpr int AP_THREADS = 256;
+
 template <int S, int BN>
 struct ApplyCfg {
-  static constexpr int WM = (BN >= 32) ? ((S >= 32) ? ((S / 32) < 4 ? S / 32 : 4) : 1) : 4;
-  static constexpr int WN = 4 / WM;
+  // 8 warps: BN >= 32 -> (S/32) x (8/(S/32)) grid of 32-row warp tiles; BN = 8 -> warps along M
+  static constexpr int WM = (BN >= 32) ? ((S >= 32) ? S / 32 : 1) : (S / 8 < 8 ? S / 8 : 8);
+  static constexpr int WN = (BN >= 32) ? 8 / WM : 1;
   static constexpr int WTM = S / WM, WTN = BN / WN;
   static constexpr int MI = WTM / 8, NI = WTN / 8;
   static constexpr int P = S + 4;
 };
 
 template <int S, int BN, int TWR>
-__global__ void __launch_bounds__(128) tri_apply_kernel(ApplyArgs g) {
+__global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
   using Cfg = ApplyCfg<S, BN>;
   constexpr int WN = Cfg::WN, WTM = Cfg::WTM, WTN = Cfg::WTN, MI = Cfg::MI, NI = Cfg::NI, P = Cfg::P;
   static_assert(MI >= 1 && NI >= 1, "tile config");
@@ -65,16 +68,17 @@ __global__ void __launch_bounds__(128) tri_apply_kernel(ApplyArgs g) {
   const int ntiles = (g.ncols + BN - 1) / BN;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wm = warp / WN, wn = warp % WN;
+  const bool mma_warp = warp < Cfg::WM * WN;
   const int ar = lane >> 2, ac = lane & 3;
 
   const double* ti = g.tinv + (int64_t)b * g.strideT;
-  for (int idx = t; idx < S * (S / 2); idx += 128) {
+  for (int idx = t; idx < S * (S / 2); idx += AP_THREADS) {
     const int k = idx / (S / 2), m = (idx % (S / 2)) * 2;
     cp_async_16(At + k * P + m, ti + m + (int64_t)k * g.ldi, 16);
   }
   if constexpr (TWR > 0) {
     const double* vb = g.V + (int64_t)b * g.vstride;
-    for (int idx = t; idx < TWR * (S / 2); idx += 128) {
+    for (int idx = t; idx < TWR * (S / 2); idx += AP_THREADS) {
       const int j = idx / (S / 2), k = (idx % (S / 2)) * 2;
       cp_async_16(Vs + j * P + k, vb + k + (int64_t)j * g.ldv, 16);
     }
@@ -86,7 +90,7 @@ __global__ void __launch_bounds__(128) tri_apply_kernel(ApplyArgs g) {
 
   auto load_tile = [&](int tile, double* Bs) {
     const int n0 = tile * BN;
-    for (int idx = t; idx < BN * S; idx += 128) {
+    for (int idx = t; idx < BN * S; idx += AP_THREADS) {
       const int n = idx / S, k = idx % S;
       const bool ok = n0 + n < g.ncols;
       cp_async_8(Bs + n * P + k, ok ? Bb + pm[k] + (int64_t)(n0 + n) * g.ldb : g.B, ok ? 8 : 0);
@@ -105,6 +109,7 @@ __global__ void __launch_bounds__(128) tri_apply_kernel(ApplyArgs g) {
 
     double acc[MI][NI][2];
     // stage 1: T = P B + strict_lower(L^-1) P B
+    if (mma_warp) {
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -129,7 +134,9 @@ __global__ void __launch_bounds__(128) tri_apply_kernel(ApplyArgs g) {
 #pragma unroll
         for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
+    }
     __syncthreads();
+    if (mma_warp) {
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -140,8 +147,10 @@ __global__ void __launch_bounds__(128) tri_apply_kernel(ApplyArgs g) {
           Bs[n * P + m] = acc[i][j][h];
           acc[i][j][h] = 0.0;
         }
+    }
     __syncthreads();
     // stage 2: X = upper(U^-1) T
+    if (mma_warp) {
     for (int k0 = wm * WTM; k0 < S; k0 += 4) {
       const int k = k0 + ac;
       double af[MI], bf[NI];
@@ -157,7 +166,9 @@ __global__ void __launch_bounds__(128) tri_apply_kernel(ApplyArgs g) {
 #pragma unroll
         for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
+    }
     __syncthreads();
+    if (mma_warp) {
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -167,15 +178,16 @@ __global__ void __launch_bounds__(128) tri_apply_kernel(ApplyArgs g) {
           const int m = wm * WTM + i * 8 + ar, n = wn * WTN + j * 8 + ac * 2 + h;
           Bs[n * P + m] = acc[i][j][h];
         }
+    }
     __syncthreads();
     const int n0 = tile * BN;
-    for (int idx = t; idx < BN * S; idx += 128) {
+    for (int idx = t; idx < BN * S; idx += AP_THREADS) {
       const int n = idx / S, m = idx % S;
       if (n0 + n < g.ncols) Xb[m + (int64_t)(n0 + n) * g.ldx] = Bs[n * P + m];
     }
     if constexpr (TWR > 0) {
       // TW_b(:, tile) = V_b^T X_b(:, tile): TWR x BN, K = S, 4 warps along N
-      constexpr int TMI = TWR / 8, TNI = (BN / 4) / 8 >= 1 ? (BN / 4) / 8 : 1;
+      constexpr int TMI = TWR / 8, TNI = (BN / 8) / 8 >= 1 ? (BN / 8) / 8 : 1;
       constexpr int TWN = BN / (8 * TNI);
       if (warp < TWN) {
         double tw[TMI][TNI][2];
@@ -226,7 +238,7 @@ static hodlr_status run_apply(ApplyArgs g, cudaStream_t st) {
   if ((int64_t)g.batch * g.groups < 296) g.groups = ntiles;
   const int64_t grid = (int64_t)g.batch * g.groups;
   if (grid > 2147483647LL) return HODLR_ERR_ARG;
-  tri_apply_kernel<S, BN, TWR><<<(unsigned)grid, 128, smem, st>>>(g);
+  tri_apply_kernel<S, BN, TWR><<<(unsigned)grid, AP_THREADS, smem, st>>>(g);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }

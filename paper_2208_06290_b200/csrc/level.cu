@@ -34,6 +34,8 @@ struct LevelArgs {
   int ncols;
 };
 
+constexpr int LV_THREADS = 512;  // 16 warps: two per scheduler slot of each SMSP pair
+
 template <int R, int BN>
 struct LevelCfg {
   static constexpr int BM = 64;
@@ -43,25 +45,30 @@ struct LevelCfg {
   static constexpr int A_SZ = R * P;
   static constexpr int W_SZ = BN * PW;
   static constexpr int STAGE = C_SZ + 2 * A_SZ + W_SZ;
-  static constexpr size_t SMEM = (size_t)2 * STAGE * sizeof(double);
+  // [W|T] GEMM: BN/8 n-tiles x TK k-splits = 16 warps; partials combined in smem
+  static constexpr int TWN = BN / 8;
+  static constexpr int TK = 16 / TWN;
+  static constexpr int RED = TK * R * BN;
+  static constexpr size_t SMEM = ((size_t)2 * STAGE + RED) * sizeof(double);
 };
 
 template <int R, int BN>
-__global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
+__global__ void __launch_bounds__(LV_THREADS) level_update_kernel(LevelArgs g) {
   using Cfg = LevelCfg<R, BN>;
+  constexpr int NT = LV_THREADS, NWARP = NT / 32;
   constexpr int BM = Cfg::BM, P = Cfg::P, PW = Cfg::PW;
-  // update GEMM: 64 x BN output on 8 warps
-  constexpr int UWM = (BN >= 64) ? 2 : 8, UWN = 8 / UWM;
+  // update GEMM: 64 x BN output
+  constexpr int UWN = (BN >= 64) ? 4 : 1;      // warps along N
+  constexpr int UWM = (BN >= 64) ? 4 : 8;      // warps along M (BN = 8: 8 active warps)
   constexpr int UTM = BM / UWM, UTN = BN / UWN;
   constexpr int UMI = UTM / 8, UNI = UTN / 8;
-  // TW GEMM: R x BN output on 8 warps
-  constexpr int TWN = (BN / 8 >= 8) ? 8 : BN / 8;  // warps along N
-  constexpr int TWM = (8 / TWN) <= R / 8 ? 8 / TWN : R / 8;
-  constexpr int TTM = R / TWM, TTN = BN / TWN;
-  constexpr int TMI = TTM / 8, TNI = TTN / 8;
-  static_assert(UMI >= 1 && UNI >= 1 && TMI >= 1 && TNI >= 1, "tile config");
+  // [W|T] GEMM: R x BN, each warp owns one 8-column n-tile and one k-range
+  constexpr int TWN = Cfg::TWN, TK = Cfg::TK, KR = BM / TK;
+  constexpr int TMI = R / 8;
+  static_assert(UMI >= 1 && UNI >= 1 && KR % 4 == 0, "tile config");
 
   extern __shared__ __align__(16) double sm[];
+  double* red = sm + 2 * Cfg::STAGE;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ar = lane >> 2, ac = lane & 3;
   const int64_t seg0 = (int64_t)blockIdx.x * g.seg_rows;
@@ -84,28 +91,26 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
     double* As = Cs + Cfg::C_SZ;
     double* Vs = As + Cfg::A_SZ;
     double* Ws = Vs + Cfg::A_SZ;
-    // C tile [n][m]: 16B copies along rows
-    for (int idx = t; idx < BN * (BM / 2); idx += 256) {
+    for (int idx = t; idx < BN * (BM / 2); idx += NT) {
       const int n = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
       const bool ok = n0 + n < g.ncols;
       cp_async_16_pol(Cs + n * P + m, ok ? g.C + row0 + m + (int64_t)(n0 + n) * g.ldc : g.C, ok ? 16 : 0, stream);
     }
-    // A1 tile [k][m] and V tile [k][m] (both rows-contiguous per rank column)
-    for (int idx = t; idx < R * (BM / 2); idx += 256) {
+    for (int idx = t; idx < R * (BM / 2); idx += NT) {
       const int k = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
       cp_async_16_pol(As + k * P + m, g.A1 + row0 + m + (int64_t)k * g.lda, 16, keep);
       if (want_tw) cp_async_16_pol(Vs + k * P + m, g.V + row0 + m + (int64_t)k * g.lda, 16, keep);
     }
-    // W' tile [n][k]: rows (c%2)*R.. of W_p, k contiguous
     const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
-    for (int idx = t; idx < BN * (R / 2); idx += 256) {
+    for (int idx = t; idx < BN * (R / 2); idx += NT) {
       const int n = idx / (R / 2), k = (idx % (R / 2)) * 2;
       const bool ok = n0 + n < g.ncols;
       cp_async_16_pol(Ws + n * PW + k, ok ? Wp + k + (int64_t)(n0 + n) * (2 * R) : g.W, ok ? 16 : 0, keep);
     }
   };
 
-  double tw[TMI][TNI][2];
+  const int tn = warp % TWN, tk = warp / TWN;  // [W|T] role of this warp
+  double tw[TMI][2];
   if (niter > 0) load(0, 0);
   cp_async_commit();
   for (int it = 0; it < niter; ++it) {
@@ -121,12 +126,10 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
     const double* Ws = Vs + Cfg::A_SZ;
     if (st == 0) {
 #pragma unroll
-      for (int i = 0; i < TMI; ++i)
-#pragma unroll
-        for (int j = 0; j < TNI; ++j) tw[i][j][0] = tw[i][j][1] = 0.0;
+      for (int i = 0; i < TMI; ++i) tw[i][0] = tw[i][1] = 0.0;
     }
     // ---- update: upd = A1 W' (rounded product), C = C - upd ----
-    {
+    if (warp < UWM * UWN) {
       const int wm = warp / UWN, wn = warp % UWN;
       double acc[UMI][UNI][2];
 #pragma unroll
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
     {
       const int64_t row0 = seg0 + (int64_t)st * BM;
       const int n0 = ct * BN;
-      for (int idx = t; idx < BN * (BM / 2); idx += 256) {
+      for (int idx = t; idx < BN * (BM / 2); idx += NT) {
         const int n = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
         if (n0 + n < g.ncols) {
           double2 v = make_double2(Cs[n * P + m], Cs[n * P + m + 1]);
@@ -168,24 +171,24 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
         }
       }
     }
-    // ---- next level's [W|T]: tw += V^T C_new ----
+    // ---- next level's [W|T]: tw += V^T C_new over this warp's k-range ----
     if (want_tw) {
-      const int wm = warp / TWN, wn = warp % TWN;
-      if (wm < TWM) {
-#pragma unroll 4
-        for (int k0 = 0; k0 < BM; k0 += 4) {
-          double af[TMI], bf[TNI];
 #pragma unroll
-          for (int i = 0; i < TMI; ++i) af[i] = Vs[(wm * TTM + i * 8 + ar) * P + k0 + ac];
+      for (int k0 = tk * KR; k0 < (tk + 1) * KR; k0 += 4) {
+        double af[TMI];
 #pragma unroll
-          for (int j = 0; j < TNI; ++j) bf[j] = Cs[(wn * TTN + j * 8 + ar) * P + k0 + ac];
+        for (int i = 0; i < TMI; ++i) af[i] = Vs[(i * 8 + ar) * P + k0 + ac];
+        const double bf = Cs[(tn * 8 + ar) * P + k0 + ac];
 #pragma unroll
-          for (int i = 0; i < TMI; ++i)
-#pragma unroll
-            for (int j = 0; j < TNI; ++j) dmma_8x8x4(tw[i][j][0], tw[i][j][1], af[i], bf[j]);
-        }
+        for (int i = 0; i < TMI; ++i) dmma_8x8x4(tw[i][0], tw[i][1], af[i], bf);
       }
-      if (st == nsub - 1 && wm < TWM) {
+      if (st == nsub - 1) {
+        // combine the TK k-split partials in a fixed order, then write
+#pragma unroll
+        for (int i = 0; i < TMI; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) red[(tk * R + i * 8 + ar) * BN + tn * 8 + ac * 2 + h] = tw[i][h];
+        __syncthreads();
         const int n0 = ct * BN;
         const int64_t q = seg0 / (2 * (int64_t)g.n_c);  // level-l node of this segment
         double* out;
@@ -197,15 +200,13 @@ __global__ void __launch_bounds__(256) level_update_kernel(LevelArgs g) {
           out = g.TW + (q >> 1) * g.tw_stride + (q & 1) * R;
           ld = 2 * R;
         }
+        for (int idx = t; idx < R * BN; idx += NT) {
+          const int m = idx % R, n = idx / R;
+          double v = red[m * BN + n];
 #pragma unroll
-        for (int i = 0; i < TMI; ++i)
-#pragma unroll
-          for (int j = 0; j < TNI; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int m = wm * TTM + i * 8 + ar, n = n0 + wn * TTN + j * 8 + ac * 2 + h;
-              if (n < g.ncols) out[m + (int64_t)n * ld] = tw[i][j][h];
-            }
+          for (int kk = 1; kk < TK; ++kk) v += red[(kk * R + m) * BN + n];
+          if (n0 + n < g.ncols) out[m + (int64_t)(n0 + n) * ld] = v;
+        }
       }
     }
     __syncthreads();
@@ -234,7 +235,7 @@ static hodlr_status run_level(const LevelArgs& g, int64_t nseg, cudaStream_t st)
     cudaFuncSetAttribute(level_update_kernel<R, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     attr = true;
   }
-  level_update_kernel<R, BN><<<(unsigned)nseg, 256, Cfg::SMEM, st>>>(g);
+  level_update_kernel<R, BN><<<(unsigned)nseg, LV_THREADS, Cfg::SMEM, st>>>(g);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
@@ -279,7 +280,7 @@ hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc,
                               int64_t lda, const double* W, int64_t wstride, int ncols, double* TW, int64_t tw_stride,
                               double* part, size_t part_bytes, cudaStream_t st) {
   if (ncols == 0) return HODLR_OK;
-  if (n_c % 64 || (r != 16 && r != 32 && r != 64)) return HODLR_ERR_ARG;
+  if (n_c % 64 || (r != 16 && r != 32)) return HODLR_ERR_ARG;
   if ((ldc & 1) || (lda & 1) || (reinterpret_cast<uintptr_t>(C) & 15) || (reinterpret_cast<uintptr_t>(A1) & 15) ||
       (V && (reinterpret_cast<uintptr_t>(V) & 15)) || (reinterpret_cast<uintptr_t>(W) & 15) || (wstride & 1))
     return HODLR_ERR_ARG;
@@ -295,7 +296,7 @@ hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc,
   switch (r) {
     case 16: s = small ? run_level<16, 8>(g, nseg, st) : run_level<16, 64>(g, nseg, st); break;
     case 32: s = small ? run_level<32, 8>(g, nseg, st) : run_level<32, 64>(g, nseg, st); break;
-    default: s = small ? run_level<64, 8>(g, nseg, st) : run_level<64, 64>(g, nseg, st); break;
+    default: return HODLR_ERR_ARG;  // r = 64: generic path (fused tiles exceed shared memory)
   }
   if (s != HODLR_OK || !split) return s;
   const int nnodes = (int)(n / node);

@@ -402,21 +402,27 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
   const bool live = t < S;
   const T* g = src + blk * strides;
   T* row = A + t * RP;
-  if (live) {
-    for (int j = 0; j < S; ++j) {
-      T v;
-      if (mode == 0) {
-        v = g[t + j * lds];
-      } else {
-        constexpr int R = S / 2;
-        if (t < R && j < R)
-          v = g[t + j * lds];
-        else if (t >= R && j >= R)
-          v = g[t + (j - R) * lds];
-        else
-          v = (t < R) ? (T)(t == j - R) : (T)(t - R == j);
+  if (live) {  // 16 independent loads in flight per thread
+    constexpr int CH = S < 16 ? S : 16;
+    for (int j0 = 0; j0 < S; j0 += CH) {
+      T v[CH];
+#pragma unroll
+      for (int jj = 0; jj < CH; ++jj) {
+        const int j = j0 + jj;
+        if (mode == 0) {
+          v[jj] = g[t + j * lds];
+        } else {
+          constexpr int R = S / 2;
+          if (t < R && j < R)
+            v[jj] = g[t + j * lds];
+          else if (t >= R && j >= R)
+            v[jj] = g[t + (j - R) * lds];
+          else
+            v[jj] = (t < R) ? (T)(t == j - R) : (T)(t - R == j);
+        }
       }
-      row[j] = v;
+#pragma unroll
+      for (int jj = 0; jj < CH; ++jj) row[j0 + jj] = v[jj];
     }
   }
   if (t == 0) sflag = 0;
@@ -483,21 +489,46 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
     if (active) {
       const T d = (piv == (T)0) ? (T)1 : piv;
       const T x = row[k];
+#ifdef HODLR_PROBE_NODIV
+      const T l = x * d;
+#else
       const T l = (x == (T)0 && d == d) ? ((signbit(x) != signbit(d)) ? (T)-0.0 : (T)0.0) : div_rn(x, d);
+#endif
       row[k] = l;
       int j = k + 1;
+#ifdef HODLR_PROBE_NOUPD
+      j = S;
+#endif
       if (j & 1) {  // align to 16B pairs
         if (j < S) row[j] = sub_rn(row[j], mul_rn(l, prow[j]));
         ++j;
       }
       if constexpr (sizeof(T) == 8) {
-#pragma unroll 4
-        for (; j < S; j += 2) {
-          const double2 u = *reinterpret_cast<const double2*>(prow + j);
-          double2 a = *reinterpret_cast<double2*>(row + j);
+        // the pivot row is never this thread's row: load 8-wide chunks of both
+        // before storing so the loads are not serialised behind the stores
+        const double2* __restrict__ pu = reinterpret_cast<const double2*>(prow);
+        double2* __restrict__ pa = reinterpret_cast<double2*>(row);
+        int jj = j >> 1;
+        for (; jj + 4 <= S / 2; jj += 4) {
+          double2 u[4], a[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            u[q] = pu[jj + q];
+            a[q] = pa[jj + q];
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            a[q].x = sub_rn(a[q].x, mul_rn(l, u[q].x));
+            a[q].y = sub_rn(a[q].y, mul_rn(l, u[q].y));
+            pa[jj + q] = a[q];
+          }
+        }
+        for (; jj < S / 2; ++jj) {
+          const double2 u = pu[jj];
+          double2 a = pa[jj];
           a.x = sub_rn(a.x, mul_rn(l, u.x));
           a.y = sub_rn(a.y, mul_rn(l, u.y));
-          *reinterpret_cast<double2*>(row + j) = a;
+          pa[jj] = a;
         }
       } else {
 #pragma unroll 4
@@ -519,9 +550,18 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
   __syncthreads();  // global LU writes visible to the block; row buffer free after this
   T* Tm = A;
   T* Tt = A + S * P;
-  for (int idx = t; idx < S * S; idx += NT) {
-    const int i = idx % S, j = idx / S;
-    Tm[i + j * P] = o[i + j * ldo];
+  for (int idx0 = 0; idx0 < S * S; idx0 += 8 * NT) {  // 8 loads in flight (L2-resident)
+    T v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = idx0 + q * NT + t;
+      v[q] = idx < S * S ? o[idx % S + (idx / S) * ldo] : (T)0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = idx0 + q * NT + t;
+      if (idx < S * S) Tm[idx % S + (idx / S) * P] = v[q];
+    }
   }
   __syncthreads();
   packed_trtri<T, S>(Tm, Tt, P);
