@@ -1,0 +1,369 @@
+"""HODLR factor+solve benchmark (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1] shape): N = 2^20, leaf m = 64, uniform rank
+r = 32, L = 14, fp64, 1 RHS.  Data: seeded exact-HODLR stand-in generated in
+HBM -- the 2-D Laplace BIE compression at this N needs the GPU
+builder, which is a "next" row.  A step = one factorize (PAPER
+Alg. 3) + one solve (Alg. 4) of a freshly restored copy of the matrix; the
+restore copy is outside the timed events.  Inputs (8 GB) exceed L2 (126 MB),
+so no explicit flush is needed.
+
+Multi-GPU: one process per GPU (torchrun); round 1 runs independent replicas
+(every rank factors its own N = 2^20 matrix, scaling "weak"); subtree sharding
+with NCCL is DESIGN.md §Multi-GPU.  Rank 0 prints one JSON line.
+
+--impl reference: the reference's CPU path (oracle restatement of the
+reference kernels, oracle/hodlr_oracle.py, all host threads) on a bounded
+sample of the same workload (one 2^16-row subtree, m = 64, r = 32), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_DEFAULT, M_LEAF, RANK = 1 << 20, 64, 32
+SEED, SCALE = 1234, 1.0
+METRIC = "hodlr_factor_solve_tflops"
+CPU_SAMPLE_N = 1 << 16
+
+
+def factor_flops(n, m, r):
+    from oracle import hodlr_oracle as orc  # closed form only (no oracle compute)
+
+    return orc.factor_flops(n, m, r)
+
+
+def solve_flops(n, m, r, nrhs=1):
+    L = int(round(math.log2(n // m)))
+    return nrhs * (2 * m * n + 4 * r * n * L + 8 * r * r * ((1 << L) - 1))
+
+
+def level_flops(n, m, r):
+    """Algorithmic flops of the fused level-step launches (update + next [W|T])."""
+    L = int(round(math.log2(n // m)))
+    return sum(4 * r * r * n * lv for lv in range(1, L))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index=0):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world, backend):
+    import torch.distributed as dist
+
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return dist
+
+
+def measure_dgemm_peak(torch):
+    """cuBLAS DGEMM 8192^3 (burst): the FP64 tensor roofline denominator
+    (MEASURED_PEAKS.json carries bf16 only)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * n**3 / (best * 1e-3) / 1e12
+
+
+def read_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return {}
+
+
+def traffic_from_profiles():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        return d.get("level_update_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+def cpu_reference(n, threads):
+    """Oracle factor+solve (reference kernels restated) on a bounded sample."""
+    import numpy as np
+
+    from oracle import hodlr_oracle as orc
+
+    h = orc.make_exact_hodlr(n, M_LEAF, RANK, seed=SEED, s=SCALE)
+    b = np.random.default_rng(SEED + 1).standard_normal(n)
+    t0 = time.perf_counter()
+    f = orc.factorize(h, threads=threads)
+    t1 = time.perf_counter()
+    orc.solve(f, b, threads=threads)
+    t2 = time.perf_counter()
+    fl = orc.factor_flops(n, M_LEAF, RANK) + orc.solve_flops(n, M_LEAF, RANK)
+    return fl, t1 - t0, t2 - t1
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    n = CPU_SAMPLE_N
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_reference(1 << 12, threads)
+    vals, tfs, tss = [], [], []
+    for _ in range(args.steps):
+        fl, tf, ts = cpu_reference(n, threads)
+        vals.append(fl / (tf + ts) / 1e12)
+        tfs.append(tf)
+        tss.append(ts)
+    v = statistics.mean(vals)
+    sample = (f"oracle (reference batched kernels restated, numpy/OpenBLAS) factor+solve of one 2^16-row "
+              f"subtree of the cfg2 workload (m=64, r=32, fp64), {args.steps} step(s)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean([a + b for a, b in zip(tfs, tss)]),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "HODLR factor+solve, exact-HODLR stand-in", "N": n, "leaf": M_LEAF, "rank": RANK,
+                   "L": int(math.log2(n // M_LEAF)), "nrhs": 1, "device": "cpu"},
+        "t_factor_s": statistics.mean(tfs), "t_solve_s": statistics.mean(tss),
+        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import ctypes as C
+
+    import torch
+
+    import paper_2208_06290_b200 as hb
+    from paper_2208_06290_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = init_dist(world, "nccl")
+    lib = _lib.load()
+    n, m, r = args.n, M_LEAF, RANK
+    L = int(round(math.log2(n // m)))
+    f_flops, s_flops = factor_flops(n, m, r), solve_flops(n, m, r)
+
+    # resident input (HBM) and a pristine copy for restores
+    h0 = hb.random_hodlr(n, m, r, seed=SEED + rank, s=SCALE)
+    hw = h0.clone()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(SEED + 7 + rank)
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+
+    def restore():
+        hw.D.copy_(h0.D)
+        hw.U.copy_(h0.U)
+
+    def step():
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        f = hb.factorize(hw, check=False)
+        e1.record()
+        x = hb.solve(f, b)
+        e2.record()
+        return f, x, (e0, e1, e2)
+
+    for _ in range(args.warmup):
+        restore()
+        step()
+    torch.cuda.synchronize()
+
+    # per-phase event profile + launch count of one step (outside the timed loop)
+    restore()
+    lib.hodlr_profile_enable(1)
+    c0 = lib.hodlr_launch_count()
+    f, x, _ = step()
+    torch.cuda.synchronize()
+    launches_per_step = lib.hodlr_launch_count() - c0
+    ph = (C.c_double * 9)()
+    lib.hodlr_profile_read(ph, 9)
+    lib.hodlr_profile_enable(0)
+    phases = {name: ph[i] for i, name in enumerate(_lib.PHASES)}
+    # accuracy of this step: relres against the HODLR operator
+    relres = float(torch.linalg.norm(h0.matvec(x) - b) / torch.linalg.norm(b))
+
+    # ---- timed region ----
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tf_ms, ts_ms = [], []
+    with ClockSampler(local) as clk:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            restore()
+            _, _, ev = step()
+            tf_ms.append(ev)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tf = sum(ev[0].elapsed_time(ev[1]) for ev in tf_ms) / args.steps
+    ts = sum(ev[1].elapsed_time(ev[2]) for ev in tf_ms) / args.steps
+    t_step = tf + ts
+    if world > 1:
+        tt = torch.tensor([t_step, tf, ts], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, tf, ts = tt.tolist()
+    value = world * (f_flops + s_flops) / (t_step * 1e-3) / 1e12
+
+    # ---- e2e through the public API with host buffers (pinned) ----
+    e2e = None
+    if rank == 0 and not args.no_e2e:
+        Dh = h0.D.cpu().pin_memory()
+        Uh = h0.U.cpu().pin_memory()
+        Vh = h0.V.cpu().pin_memory()
+        bh = b.cpu().pin_memory()
+        e2e_t = []
+        for it in range(2 + 2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hm = hb.HodlrMatrix.from_buffers(n, m, r, Dh, Uh, Vh)
+            fe = hb.factorize(hm)
+            xh = hb.solve(fe, bh)  # host rhs in, host solution out
+            torch.cuda.synchronize()
+            if it >= 2:
+                e2e_t.append(time.perf_counter() - t0)
+            del hm, fe, xh
+        te = statistics.mean(e2e_t)
+        h2d = (Dh.numel() + Uh.numel() + Vh.numel() + bh.numel()) * 8
+        e2e = {"value": (f_flops + s_flops) / te / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": n * 8 + ((1 << L) + (1 << L) - 1) * 4, "seconds_per_step": te}
+
+    # ---- roofline of the dominant kernel (fused level step) ----
+    peaks = read_peaks()
+    dgemm = measure_dgemm_peak(torch) if rank == 0 else None
+    lvl_ms = phases["level"]
+    lvl_achieved = level_flops(n, m, r) / (lvl_ms * 1e-3) / 1e12 if lvl_ms > 0 else None
+    level_launches = L - 1
+    traffic, _ = traffic_from_profiles()
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            threads = os.cpu_count() or 1
+            fl, ctf, cts = cpu_reference(CPU_SAMPLE_N, threads)
+            cpu = {"value": fl / (ctf + cts) / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                   "sample": "oracle factor+solve of one 2^16-row subtree of this workload (m=64, r=32, fp64), "
+                             f"{ctf:.1f} s factor + {cts:.2f} s solve"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "HODLR factor+solve, cfg2 shape (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
+                                   "seeded exact-HODLR stand-in", "N": n, "leaf": m, "rank": r, "L": L, "nrhs": 1,
+                       "parallelism": f"replicas{world}", "l2_flush": "inputs 8 GB > L2"},
+            "t_factor_ms": tf, "t_solve_ms": ts, "factor_tflops": f_flops / (tf * 1e-3) / 1e12,
+            "solve_gbps": (8 * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 16 * n) / (ts * 1e-3) / 1e9,
+            "relres": relres, "flops_factor": f_flops, "flops_solve": s_flops,
+            "phase_ms": phases, "gpu_launches": launches_per_step * args.steps,
+            "roofline": {"bound": "tensor", "kernel": "level_update_kernel (fused Y update + next-level [W|T])",
+                         "achieved": lvl_achieved, "peak": dgemm, "unit": "TFLOP/s",
+                         "frac": (lvl_achieved / dgemm) if (lvl_achieved and dgemm) else None,
+                         "peak_source": "measured cuBLAS DGEMM 8192^3 in this run (MEASURED_PEAKS.json has no fp64)",
+                         "traffic": traffic, "launches_per_step": level_launches,
+                         "flops_per_step": level_flops(n, m, r)},
+            "clocks": clk.summary(), "wall_s_timed": wall,
+            "hbm_peak_measured_gbps": peaks.get("hbm_gbs"),
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

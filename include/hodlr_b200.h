@@ -40,6 +40,26 @@ typedef enum {
 const char* hodlr_version(void);
 const char* hodlr_last_error(void);
 
+/* Instrumentation (no reference counterpart; the reference only returns flop
+ * counts, backend.py:18-20).  hodlr_launch_count: kernels launched by this
+ * library since load.  hodlr_profile_enable(1) brackets every factorize /
+ * solve phase with CUDA events on the caller's stream; hodlr_profile_read
+ * synchronises, writes the accumulated milliseconds per phase class
+ * (HODLR_PHASE_*) into ms[0..n) and resets.  Returns the number of classes. */
+#define HODLR_PHASE_LEAF_GETRF 0
+#define HODLR_PHASE_LEAF_APPLY 1
+#define HODLR_PHASE_K_GETRF 2
+#define HODLR_PHASE_K_APPLY 3
+#define HODLR_PHASE_LEVEL 4
+#define HODLR_PHASE_GEMM 5
+#define HODLR_PHASE_SOLVE_LEAF 6
+#define HODLR_PHASE_SOLVE_K 7
+#define HODLR_PHASE_SOLVE_LEVEL 8
+#define HODLR_NUM_PHASES 9
+long long hodlr_launch_count(void);
+void hodlr_profile_enable(int on);
+int hodlr_profile_read(double* ms, int n);
+
 /* ------------------------------------------------------------------------
  * Batched kernels (reference batched-kernel layer, backend.py)
  * --------------------------------------------------------------------- */
@@ -51,8 +71,10 @@ const char* hodlr_last_error(void);
  * A: batch blocks of s x s at A + b*strideA (ld lda).
  * swaps/perm: int32 [batch*s] (0-based, LAPACK-style swaps; P A = A[perm]).
  * info: int32 [batch], 1 = flagged singular.
- * Ainv (optional, may be NULL): explicit inverse A^-1 = U^-1 L^-1 P written at
- * Ainv + b*strideInv (ld ldinv) -- used by the DMMA solve GEMMs. */
+ * Ainv (optional, may be NULL; s in {16,32,64,128}): packed triangular inverses
+ * strict_lower(L^-1) + upper(U^-1) written at Ainv + b*strideInv (ld ldinv);
+ * X = U^-1 (L^-1 (P B)) is then two masked DMMA GEMMs (the solves of the
+ * factor and solve phases). */
 hodlr_status hodlr_getrf_batched(int dtype, int s, int batch, void* A, int64_t lda, int64_t strideA,
                                  int32_t* swaps, int32_t* perm, int32_t* info, void* Ainv,
                                  int64_t ldinv, int64_t strideInv, void* stream);
@@ -94,11 +116,11 @@ typedef struct {
 /* Device buffers of a factorization (all owned by the caller). */
 typedef struct {
   void* D;        /* in: leaf blocks; out: leaf LU                       */
-  void* Dinv;     /* out: leaf inverses (2^L m^2)                        */
+  void* Dinv;     /* out: packed L^-1 / U^-1 of the leaves (2^L m^2)     */
   void* Y;        /* in: U slab; out: Y slab                             */
   void* V;        /* in: V slab                                          */
   void* K;        /* out: K LU per level ((2^L - 1) (2r)^2)              */
-  void* Kinv;     /* out: K inverses, same layout                        */
+  void* Kinv;     /* out: packed L^-1 / U^-1 of the K blocks, K layout   */
   int32_t* dswaps; /* out: 2^L m                                          */
   int32_t* dperm;  /* out: 2^L m                                          */
   int32_t* dinfo;  /* out: 2^L                                            */

@@ -15,6 +15,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhodlr_b200.so"
 
 OK, ERR_ARG, ERR_SHAPE, ERR_SINGULAR, ERR_CUDA, ERR_NCCL = range(6)
+PHASES = ("leaf_getrf", "leaf_apply", "k_getrf", "k_apply", "level", "gemm", "solve_leaf", "solve_k", "solve_level")
 F64, F32 = 0, 1
 
 _STATUS = {
@@ -54,6 +55,9 @@ SIGNATURES = {
         _i,
         [_i, _i, _i, _i, _i, _d, _p, _i64, _i64, _i64, _p, _i64, _i64, _i64, _d, _p, _i64, _i64, _i64, _i, _i, _p, _sz, _p],
     ),
+    "hodlr_launch_count": (C.c_longlong, []),
+    "hodlr_profile_enable": (None, [_i]),
+    "hodlr_profile_read": (_i, [C.POINTER(C.c_double), _i]),
     "hodlr_factorize_workspace": (_sz, [C.POINTER(Desc)]),
     "hodlr_solve_workspace": (_sz, [C.POINTER(Desc), _i]),
     "hodlr_factorize": (_i, [C.POINTER(Desc), C.POINTER(Factors), _p, _sz, _p]),

@@ -9,6 +9,7 @@
 
 #define HODLR_CHECK_LAUNCH()                                   \
   do {                                                         \
+    hodlr_count_launch();                                      \
     cudaError_t e_ = cudaGetLastError();                       \
     if (e_ != cudaSuccess) return hodlr_set_cuda_error(e_);    \
   } while (0)
@@ -79,3 +80,5 @@ __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + 
 
 // records the CUDA error string for hodlr_last_error(); defined in hodlr.cu
 hodlr_status hodlr_set_cuda_error(cudaError_t e);
+// counts kernel launches issued by this library (hodlr_launch_count)
+void hodlr_count_launch();

@@ -7,6 +7,7 @@
 // of every leaf and K block, so every triangular solve of the factor and solve
 // phases becomes a pair of batched DMMA GEMMs (apply.cu).
 #include <cstdio>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -46,6 +47,71 @@ hodlr_status hodlr_set_cuda_error(cudaError_t e) {
 
 extern "C" const char* hodlr_version(void) { return "hodlr_b200 0.1 (sm_100a, fp64 DMMA)"; }
 extern "C" const char* hodlr_last_error(void) { return g_last_error.c_str(); }
+
+// ---- instrumentation ----
+#include <atomic>
+#include <vector>
+static std::atomic<long long> g_launches{0};
+void hodlr_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" long long hodlr_launch_count(void) { return g_launches.load(); }
+
+namespace {
+struct PhaseProfiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+PhaseProfiler g_prof;
+std::mutex g_prof_mu;
+
+// RAII bracket: records start/stop events on `st` around one phase
+struct Phase {
+  cudaStream_t st;
+  int cls;
+  cudaEvent_t a = nullptr;
+  Phase(int c, cudaStream_t s) : st(s), cls(c) {
+    if (g_prof.on) {
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      a = g_prof.get();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~Phase() {
+    if (a) {
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      cudaEvent_t b = g_prof.get();
+      cudaEventRecord(b, st);
+      g_prof.recs.push_back({cls, a, b});
+    }
+  }
+};
+}  // namespace
+
+extern "C" void hodlr_profile_enable(int on) { g_prof.on = on != 0; }
+
+extern "C" int hodlr_profile_read(double* ms, int n) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int i = 0; i < n; ++i) ms[i] = 0.0;
+  for (auto& r : g_prof.recs) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.cls < n) ms[r.cls] += t;
+  }
+  g_prof.recs.clear();
+  g_prof.used = 0;
+  return HODLR_NUM_PHASES;
+}
 
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
@@ -188,11 +254,16 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
   double* Kinv = (double*)f->Kinv;
 
   // (1) leaf getrf (bit-exact) + packed triangular inverses     Alg.3 l.2
-  TRY(lu_factor(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo, Dinv, st));
+  {
+    Phase ph(HODLR_PHASE_LEAF_GETRF, st);
+    TRY(lu_factor(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo, Dinv, st));
+  }
   if (L == 0 || r == 0) return HODLR_OK;
   // (2) Y(I_a, :) <- D_a^-1 U(I_a, :) for all levels at once       Alg.3 l.3
   //     fused with the level-(L-1) [W|T]_a = V_a^T Y(I_a, 0:rL)   Alg.3 l.5-6
   bool tw_ready = false;
+  {
+  Phase ph(HODLR_PHASE_LEAF_APPLY, st);
   if (tri_size_ok(m)) {
     hodlr_status s = tri_apply_f64(m, r * L, (int)nleaf, Dinv, m, (int64_t)m * m, f->dperm, Y, n, m, 0, Y, n, m, 0, 1,
                                    st, V + (int64_t)(L - 1) * r * n, n, m, r, TW, (int64_t)2 * r * r * L);
@@ -200,6 +271,7 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
     else if (s != HODLR_ERR_ARG) return s;
   }
   if (!tw_ready) TRY(lu_apply(m, r * L, (int)nleaf, D, Dinv, f->dperm, Y, n, m, Y, n, m, st));
+  }
 
   // (3) levels                                                     Alg.3 l.4-10
   for (int lv = L - 1; lv >= 0; --lv) {
@@ -208,28 +280,40 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
     const int ncol = r * (lv + 1), wc = r * lv;
     const int64_t koff = ((int64_t)npar - 1) * 4 * r * r;
     if (!tw_ready) {
+      Phase ph(HODLR_PHASE_GEMM, st);
       // [W|T]_c = V_c^T Y(I_c, 0:r(l+1)), paired per parent: 2r x ncol, ld 2r
       TRY(gemm_f64(1, r, ncol, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, Y, n, 2 * nc, nc, 0.0, TW,
                    2 * r, (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
     }
     // K_p = [[T_2p, I], [I, T_2p+1]] assembled + factored (bit-exact) + packed inverses
     int32_t* kperm = f->kperm + ((int64_t)npar - 1) * 2 * r;
+    {
+    Phase ph(HODLR_PHASE_K_GETRF, st);
     TRY(lu_factor(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff,
                   (int64_t)4 * r * r, f->kswaps + ((int64_t)npar - 1) * 2 * r, kperm, f->kinfo + (npar - 1),
                   Kinv + koff, st));
+    }
     if (lv == 0) break;
     // W_p <- K_p^-1 [W_2p; W_2p+1]
+    {
+    Phase ph(HODLR_PHASE_K_APPLY, st);
     TRY(lu_apply(2 * r, wc, npar, K + koff, Kinv + koff, kperm, TW, 2 * r, (int64_t)2 * r * ncol, W, 2 * r,
                  (int64_t)2 * r * wc, st));
+    }
     // Y(I_c, 0:rl) -= Y_c^{l+1} W_c, fused with the next level's [W|T] (V^{(l)T} Y(I_q, 0:rl))
-    hodlr_status s = level_update_f64(r, n, (int)nc, Y, n, Y + (int64_t)lv * r * n, V + (int64_t)(lv - 1) * r * n, n,
+    hodlr_status s;
+    {
+    Phase ph(HODLR_PHASE_LEVEL, st);
+    s = level_update_f64(r, n, (int)nc, Y, n, Y + (int64_t)lv * r * n, V + (int64_t)(lv - 1) * r * n, n,
                                       W, (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st);
+    }
     if (s == HODLR_OK) {
       tw_ready = true;
       continue;
     }
     if (s != HODLR_ERR_ARG) return s;
     tw_ready = false;
+    Phase ph(HODLR_PHASE_GEMM, st);
     TRY(gemm_f64(0, (int)nc, wc, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, W, 2 * r, (int64_t)2 * r * wc, r,
                  1.0, Y, n, 2 * nc, nc, nch, 2, split, ws.split, st));
   }
@@ -258,8 +342,11 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
   const double* Kinv = (const double*)f->Kinv;
 
   // x <- D^-1 x                                                   Alg.4 l.3
+  {
+  Phase ph(HODLR_PHASE_SOLVE_LEAF, st);
   TRY(lu_apply(m, nrhs, (int)((int64_t)1 << L), (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m, X,
                ldx, m, st));
+  }
   if (r == 0) return HODLR_OK;
   bool w_ready = false;
   for (int lv = L - 1; lv >= 0; --lv) {
@@ -267,23 +354,33 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
     const int64_t nc = n >> (lv + 1);
     const int64_t koff = ((int64_t)npar - 1) * 4 * r * r;
     // w_c = V_c^T x_c  (paired per parent, 2r x nrhs, ld 2r)       Alg.4 l.5
-    if (!w_ready)
+    if (!w_ready) {
+      Phase ph(HODLR_PHASE_GEMM, st);
       TRY(gemm_f64(1, r, nrhs, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w,
                    2 * r, (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
+    }
     // w_p <- K_p^-1 w_p                                              Alg.4 l.6
+    {
+    Phase ph(HODLR_PHASE_SOLVE_K, st);
     TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + koff, f->kperm + ((int64_t)npar - 1) * 2 * r,
                  w, 2 * r, (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st));
+    }
     // x_c -= Y_c w_c  fused with the next level's w = V^{(l)T} x    Alg.4 l.7 (+ l.5 of level l-1)
-    hodlr_status s = level_update_f64(r, n, (int)nc, X, ldx, Y + (int64_t)lv * r * n,
+    hodlr_status s;
+    {
+    Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
+    s = level_update_f64(r, n, (int)nc, X, ldx, Y + (int64_t)lv * r * n,
                                       lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2,
                                       (int64_t)2 * r * nrhs, nrhs, w, (int64_t)2 * r * nrhs, part,
                                       solve_part_bytes(d, nrhs), st);
+    }
     if (s == HODLR_OK) {
       w_ready = true;
       continue;
     }
     if (s != HODLR_ERR_ARG) return s;
     w_ready = false;
+    Phase ph(HODLR_PHASE_GEMM, st);
     TRY(gemm_f64(0, (int)nc, nrhs, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, w2, 2 * r, (int64_t)2 * r * nrhs,
                  r, 1.0, X, ldx, 2 * nc, nc, nch, 2, split, kSplitBytes, st));
   }
