@@ -1,0 +1,137 @@
+"""Alg. 3/4 driven through the REFERENCE's own batched kernels -- TEST / BASELINE
+INFRASTRUCTURE ONLY (tests/, bench.py --impl reference / cpu_baseline).
+
+The reference package implements the batched kernel layer
+(pkg/src/hodlr/backend.py) but not factorize/solve, so this
+module is the SPEC recipe (SURVEY.md
+Appendix B) issuing only the reference's public kernels:
+``BlockRef`` (backend.py:48), ``batched_gemm`` (:320),
+``batched_lu_factor_inplace`` (:481), ``batched_lu_solve_inplace`` (:570),
+with its executors (:175-232).  ``scratch`` is always None (the reference's
+shared-scratch race).
+
+The reference is imported read-only from ``baseline/_ref`` (pip-installed
+copy, travels to the GPU box) or ``/root/reference/pkg/src``.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+_ROOT = Path(__file__).resolve().parent.parent
+for cand in (_ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+    if (cand / "hodlr" / "backend.py").exists():
+        if str(cand) not in sys.path:
+            sys.path.insert(0, str(cand))
+        break
+
+try:  # noqa: E402
+    from hodlr.backend import (  # type: ignore
+        SERIAL,
+        BlockRef,
+        ThreadedExecutor,
+        batched_gemm,
+        batched_lu_factor_inplace,
+        batched_lu_solve_inplace,
+    )
+
+    AVAILABLE = True
+except Exception:  # pragma: no cover - reference not present
+    AVAILABLE = False
+
+
+def executor(threads: int):
+    return SERIAL if threads <= 1 else ThreadedExecutor(threads)
+
+
+def ref_factorize(D, Y, V, n, m, r, L, ex=None):
+    """Appendix-B recipe through the reference kernels; returns pivots + K."""
+    ex = ex or SERIAL
+    nleaf = 1 << L
+    drefs = [BlockRef(D, a * m * m, m, m, m) for a in range(nleaf)]
+    dpiv, _ = batched_lu_factor_inplace(drefs, executor=ex)
+    assert not dpiv.singular
+    if L > 0:
+        batched_lu_solve_inplace(drefs, dpiv, [BlockRef(Y, a * m, m, r * L, n) for a in range(nleaf)], executor=ex)
+    Ks, kpivs = [None] * L, [None] * L
+    for lv in range(L - 1, -1, -1):
+        nch, npar, nc, ncol = 1 << (lv + 1), 1 << lv, n >> (lv + 1), r * (lv + 1)
+        tw = np.zeros(nch * r * ncol)
+        batched_gemm(
+            [
+                (
+                    BlockRef(V, lv * r * n + c * nc, nc, r, n),
+                    BlockRef(Y, c * nc, nc, ncol, n),
+                    BlockRef(tw, c * r * ncol, r, ncol, r),
+                )
+                for c in range(nch)
+            ],
+            transpose_a="conj_transpose",
+            executor=ex,
+        )
+        K = np.zeros(npar * 4 * r * r)
+        for p in range(npar):
+            kb = BlockRef(K, p * 4 * r * r, 2 * r, 2 * r, 2 * r).view()
+            kb[:r, :r] = BlockRef(tw, 2 * p * r * ncol + lv * r * r, r, r, r).view()
+            kb[r:, r:] = BlockRef(tw, (2 * p + 1) * r * ncol + lv * r * r, r, r, r).view()
+            kb[:r, r:] = np.eye(r)
+            kb[r:, :r] = np.eye(r)
+        krefs = [BlockRef(K, p * 4 * r * r, 2 * r, 2 * r, 2 * r) for p in range(npar)]
+        kpiv, _ = batched_lu_factor_inplace(krefs, executor=ex)
+        assert not kpiv.singular
+        Ks[lv], kpivs[lv] = K, kpiv
+        if lv == 0:
+            continue
+        wc = r * lv
+        W = np.zeros(npar * 2 * r * wc)
+        for c in range(nch):
+            BlockRef(W, (c // 2) * 2 * r * wc + (c % 2) * r, r, wc, 2 * r).view()[...] = BlockRef(
+                tw, c * r * ncol, r, wc, r
+            ).view()
+        batched_lu_solve_inplace(krefs, kpiv, [BlockRef(W, p * 2 * r * wc, 2 * r, wc, 2 * r) for p in range(npar)], executor=ex)
+        batched_gemm(
+            [
+                (
+                    BlockRef(Y, lv * r * n + c * nc, nc, r, n),
+                    BlockRef(W, (c // 2) * 2 * r * wc + (c % 2) * r, r, wc, 2 * r),
+                    BlockRef(Y, c * nc, nc, wc, n),
+                )
+                for c in range(nch)
+            ],
+            alpha=-1.0,
+            beta=1.0,
+            executor=ex,
+        )
+    return dpiv, Ks, kpivs
+
+
+def ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L, ex=None):
+    ex = ex or SERIAL
+    nrhs = b.shape[1]
+    x = np.asfortranarray(b).ravel(order="F").copy()
+    nleaf = 1 << L
+    drefs = [BlockRef(D, a * m * m, m, m, m) for a in range(nleaf)]
+    batched_lu_solve_inplace(drefs, dpiv, [BlockRef(x, a * m, m, nrhs, n) for a in range(nleaf)], executor=ex)
+    for lv in range(L - 1, -1, -1):
+        nch, npar, nc = 1 << (lv + 1), 1 << lv, n >> (lv + 1)
+        w = np.zeros(npar * 2 * r * nrhs)
+        wref = lambda c: BlockRef(w, (c // 2) * 2 * r * nrhs + (c % 2) * r, r, nrhs, 2 * r)  # noqa: E731
+        batched_gemm(
+            [(BlockRef(V, lv * r * n + c * nc, nc, r, n), BlockRef(x, c * nc, nc, nrhs, n), wref(c)) for c in range(nch)],
+            transpose_a="conj_transpose",
+            executor=ex,
+        )
+        krefs = [BlockRef(Ks[lv], p * 4 * r * r, 2 * r, 2 * r, 2 * r) for p in range(npar)]
+        batched_lu_solve_inplace(krefs, kpivs[lv], [BlockRef(w, p * 2 * r * nrhs, 2 * r, nrhs, 2 * r) for p in range(npar)], executor=ex)
+        batched_gemm(
+            [(BlockRef(Y, lv * r * n + c * nc, nc, r, n), wref(c), BlockRef(x, c * nc, nc, nrhs, n)) for c in range(nch)],
+            alpha=-1.0,
+            beta=1.0,
+            executor=ex,
+        )
+    return x.reshape(nrhs, n).T.copy()
+
+

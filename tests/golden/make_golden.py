@@ -28,14 +28,8 @@ REPO = HERE.parent.parent
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, str(REPO))
 
-from hodlr.backend import (  # noqa: E402  (reference, read-only)
-    BlockRef,
-    batched_gemm,
-    batched_lu_factor_inplace,
-    batched_lu_solve_inplace,
-)
-
 from oracle import hodlr_oracle as orc  # noqa: E402
+from oracle.ref_driver import BlockRef, ref_factorize, ref_solve  # noqa: E402  (reference kernels)
 
 CASES = [
     # name, N, m, r, s(U scale), seed, nrhs
@@ -44,88 +38,6 @@ CASES = [
     ("n1024_m64_r16_s16", 1024, 64, 16, 16.0, 13, 1),
     ("n512_m16_r32_s16", 512, 16, 32, 16.0, 14, 2),
 ]
-
-
-def ref_factorize(D, Y, V, n, m, r, L):
-    """Appendix-B recipe through the reference kernels; returns pivots + K."""
-    nleaf = 1 << L
-    drefs = [BlockRef(D, a * m * m, m, m, m) for a in range(nleaf)]
-    dpiv, _ = batched_lu_factor_inplace(drefs)
-    assert not dpiv.singular
-    if L > 0:
-        batched_lu_solve_inplace(drefs, dpiv, [BlockRef(Y, a * m, m, r * L, n) for a in range(nleaf)])
-    Ks, kpivs = [None] * L, [None] * L
-    for lv in range(L - 1, -1, -1):
-        nch, npar, nc, ncol = 1 << (lv + 1), 1 << lv, n >> (lv + 1), r * (lv + 1)
-        tw = np.zeros(nch * r * ncol)
-        batched_gemm(
-            [
-                (
-                    BlockRef(V, lv * r * n + c * nc, nc, r, n),
-                    BlockRef(Y, c * nc, nc, ncol, n),
-                    BlockRef(tw, c * r * ncol, r, ncol, r),
-                )
-                for c in range(nch)
-            ],
-            transpose_a="conj_transpose",
-        )
-        K = np.zeros(npar * 4 * r * r)
-        for p in range(npar):
-            kb = BlockRef(K, p * 4 * r * r, 2 * r, 2 * r, 2 * r).view()
-            kb[:r, :r] = BlockRef(tw, 2 * p * r * ncol + lv * r * r, r, r, r).view()
-            kb[r:, r:] = BlockRef(tw, (2 * p + 1) * r * ncol + lv * r * r, r, r, r).view()
-            kb[:r, r:] = np.eye(r)
-            kb[r:, :r] = np.eye(r)
-        krefs = [BlockRef(K, p * 4 * r * r, 2 * r, 2 * r, 2 * r) for p in range(npar)]
-        kpiv, _ = batched_lu_factor_inplace(krefs)
-        assert not kpiv.singular
-        Ks[lv], kpivs[lv] = K, kpiv
-        if lv == 0:
-            continue
-        wc = r * lv
-        W = np.zeros(npar * 2 * r * wc)
-        for c in range(nch):
-            BlockRef(W, (c // 2) * 2 * r * wc + (c % 2) * r, r, wc, 2 * r).view()[...] = BlockRef(
-                tw, c * r * ncol, r, wc, r
-            ).view()
-        batched_lu_solve_inplace(krefs, kpiv, [BlockRef(W, p * 2 * r * wc, 2 * r, wc, 2 * r) for p in range(npar)])
-        batched_gemm(
-            [
-                (
-                    BlockRef(Y, lv * r * n + c * nc, nc, r, n),
-                    BlockRef(W, (c // 2) * 2 * r * wc + (c % 2) * r, r, wc, 2 * r),
-                    BlockRef(Y, c * nc, nc, wc, n),
-                )
-                for c in range(nch)
-            ],
-            alpha=-1.0,
-            beta=1.0,
-        )
-    return dpiv, Ks, kpivs
-
-
-def ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L):
-    nrhs = b.shape[1]
-    x = np.asfortranarray(b).ravel(order="F").copy()
-    nleaf = 1 << L
-    drefs = [BlockRef(D, a * m * m, m, m, m) for a in range(nleaf)]
-    batched_lu_solve_inplace(drefs, dpiv, [BlockRef(x, a * m, m, nrhs, n) for a in range(nleaf)])
-    for lv in range(L - 1, -1, -1):
-        nch, npar, nc = 1 << (lv + 1), 1 << lv, n >> (lv + 1)
-        w = np.zeros(npar * 2 * r * nrhs)
-        wref = lambda c: BlockRef(w, (c // 2) * 2 * r * nrhs + (c % 2) * r, r, nrhs, 2 * r)  # noqa: E731
-        batched_gemm(
-            [(BlockRef(V, lv * r * n + c * nc, nc, r, n), BlockRef(x, c * nc, nc, nrhs, n), wref(c)) for c in range(nch)],
-            transpose_a="conj_transpose",
-        )
-        krefs = [BlockRef(Ks[lv], p * 4 * r * r, 2 * r, 2 * r, 2 * r) for p in range(npar)]
-        batched_lu_solve_inplace(krefs, kpivs[lv], [BlockRef(w, p * 2 * r * nrhs, 2 * r, nrhs, 2 * r) for p in range(npar)])
-        batched_gemm(
-            [(BlockRef(Y, lv * r * n + c * nc, nc, r, n), wref(c), BlockRef(x, c * nc, nc, nrhs, n)) for c in range(nch)],
-            alpha=-1.0,
-            beta=1.0,
-        )
-    return x.reshape(nrhs, n).T.copy()
 
 
 def digest(*arrays) -> str:

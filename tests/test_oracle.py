@@ -129,3 +129,21 @@ def test_identity_and_singular_leaf():
     h2.D[:m * m] = 0.0
     with pytest.raises(orc.SingularError, match="level 3"):
         orc.factorize(h2)
+
+
+def test_reference_driver_matches_oracle_bitwise_threaded():
+    """The reference's own kernels (threads executor) through the SPEC recipe
+    reproduce the oracle bit for bit (bench.py --impl reference uses this)."""
+    from oracle import ref_driver as rd
+
+    if not rd.AVAILABLE:
+        pytest.skip("reference package not installed (baseline/_ref)")
+    n, m, r = 2048, 64, 16
+    h = orc.make_exact_hodlr(n, m, r, seed=21, s=16.0)
+    D, Y, V = h.D.copy(), h.U.copy(), h.V.copy()
+    dpiv, Ks, kp = rd.ref_factorize(D, Y, V, n, m, r, h.lay.L, rd.executor(4))
+    fo = orc.factorize(h.copy(), threads=4)
+    assert Y.tobytes() == fo.Y.tobytes() and D.tobytes() == fo.D.tobytes()
+    b = np.random.default_rng(2).standard_normal((n, 1))
+    x = rd.ref_solve(D, dpiv, Y, V, Ks, kp, b, n, m, r, h.lay.L, rd.executor(4))
+    assert x.tobytes() == orc.solve(fo, b, threads=4).tobytes()
