@@ -24,7 +24,7 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int6
                            double* TW = nullptr, int64_t tw_stride = 0);
 hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc, const double* A1, const double* V,
                               int64_t lda, const double* W, int64_t wstride, int ncols, double* TW, int64_t tw_stride,
-                              double* part, size_t part_bytes, cudaStream_t st);
+                              double* part, size_t part_bytes, cudaStream_t st, bool reg_resident);
 size_t level_partial_bytes(int64_t n, int m, int r, int L);
 template <typename T>
 hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
@@ -305,7 +305,7 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
     {
     Phase ph(HODLR_PHASE_LEVEL, st);
     s = level_update_f64(r, n, (int)nc, Y, n, Y + (int64_t)lv * r * n, V + (int64_t)(lv - 1) * r * n, n,
-                                      W, (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st);
+                                      W, (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st, true);
     }
     if (s == HODLR_OK) {
       tw_ready = true;
@@ -372,7 +372,7 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
     s = level_update_f64(r, n, (int)nc, X, ldx, Y + (int64_t)lv * r * n,
                                       lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2,
                                       (int64_t)2 * r * nrhs, nrhs, w, (int64_t)2 * r * nrhs, part,
-                                      solve_part_bytes(d, nrhs), st);
+                                      solve_part_bytes(d, nrhs), st, false);
     }
     if (s == HODLR_OK) {
       w_ready = true;

@@ -227,6 +227,178 @@ __global__ void level_reduce_kernel(const double* part, double* TW, int R, int n
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Register-resident variant for the factorization (BN = 64 columns per tile).
+// Each of the 8 warps owns 8 columns x 64 rows of the C tile in DMMA
+// accumulator registers: C is loaded straight from HBM into the accumulators
+// (prefetched one iteration ahead), the update is accumulated into it
+// (C + (-A1) W', FP64 tensor core), stored back, and the next level's
+// [W|T]^T = C^T V is formed from the same registers (the accumulator tile is
+// re-laid-out as A fragments with two shuffles per k-step).  No shared-memory
+// C tile, no cross-warp reduction: shared memory only stages the A1, V and W'
+// panels (2-stage cp.async), so 2 CTAs (16 warps) fit per SM.
+// ---------------------------------------------------------------------------
+template <int R>
+struct Level2Cfg {
+  static constexpr int BM = 64, BN = 64;
+  static constexpr int P = BM + 4;  // [k][m] / [rank][row] pitch
+  static constexpr int PW = R + 4;  // W' [n][k] pitch
+  static constexpr int A_SZ = R * P;
+  static constexpr int W_SZ = BN * PW;
+  static constexpr int STAGE = 2 * A_SZ + W_SZ;
+  static constexpr size_t SMEM = (size_t)2 * STAGE * sizeof(double);
+};
+
+template <int R>
+__global__ void __launch_bounds__(256, 2) level_update2_kernel(LevelArgs g) {
+  using Cfg = Level2Cfg<R>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, P = Cfg::P, PW = Cfg::PW;
+  constexpr int NT = 256;
+  extern __shared__ __align__(16) double sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int64_t seg0 = (int64_t)blockIdx.x * g.seg_rows;
+  const int nsub = g.seg_rows / BM;
+  const int ntile = (g.ncols + BN - 1) / BN;
+  const int niter = nsub * ntile;
+  const uint64_t keep = l2_evict_last();
+
+  auto stage_ptr = [&](int s) { return sm + s * Cfg::STAGE; };
+  auto load_panels = [&](int it, int s) {
+    const int ct = it / nsub, st = it % nsub;
+    const int64_t row0 = seg0 + (int64_t)st * BM;
+    const int c = (int)(row0 / g.n_c);
+    const int n0 = ct * BN;
+    double* As = stage_ptr(s);
+    double* Vs = As + Cfg::A_SZ;
+    double* Ws = Vs + Cfg::A_SZ;
+    for (int idx = t; idx < R * (BM / 2); idx += NT) {
+      const int k = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
+      cp_async_16_pol(As + k * P + m, g.A1 + row0 + m + (int64_t)k * g.lda, 16, keep);
+      cp_async_16_pol(Vs + k * P + m, g.V + row0 + m + (int64_t)k * g.lda, 16, keep);
+    }
+    const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
+    for (int idx = t; idx < BN * (R / 2); idx += NT) {
+      const int n = idx / (R / 2), k = (idx % (R / 2)) * 2;
+      const bool ok = n0 + n < g.ncols;
+      cp_async_16_pol(Ws + n * PW + k, ok ? Wp + k + (int64_t)(n0 + n) * (2 * R) : g.W, ok ? 16 : 0, keep);
+    }
+  };
+  // this lane's C elements of iteration `it`: rows row0 + 8i + ar, columns col, col + 1
+  auto load_c = [&](int it, double (&v)[8][2]) {
+    const int ct = it / nsub, st = it % nsub;
+    const int64_t row0 = seg0 + (int64_t)st * BM;
+    const int col = ct * BN + warp * 8 + 2 * ac;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        v[i][h] = (col + h < g.ncols) ? __ldcs(g.C + row0 + 8 * i + ar + (int64_t)(col + h) * g.ldc) : 0.0;
+  };
+
+  double cn[8][2], tw[R / 8][2];
+  if (niter > 0) {
+    load_panels(0, 0);
+    load_c(0, cn);
+  }
+  cp_async_commit();
+  for (int it = 0; it < niter; ++it) {
+    const int s = it & 1;
+    const int ct = it / nsub, st = it % nsub;
+    double acc[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = cn[i][0], acc[i][1] = cn[i][1];
+    if (it + 1 < niter) {
+      load_panels(it + 1, s ^ 1);
+      load_c(it + 1, cn);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* As = stage_ptr(s);
+    const double* Vs = As + Cfg::A_SZ;
+    const double* Ws = Vs + Cfg::A_SZ;
+    if (st == 0) {
+#pragma unroll
+      for (int j = 0; j < R / 8; ++j) tw[j][0] = tw[j][1] = 0.0;
+    }
+    // ---- C <- C - A1 W' on this warp's 8 columns (accumulated on the tensor core) ----
+#pragma unroll
+    for (int k0 = 0; k0 < R; k0 += 4) {
+      const double bf = Ws[(warp * 8 + ar) * PW + k0 + ac];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double af = -As[(k0 + ac) * P + 8 * i + ar];
+        dmma_8x8x4(acc[i][0], acc[i][1], af, bf);
+      }
+    }
+    // ---- store the updated 64 x 8 slice ----
+    {
+      const int64_t row0 = seg0 + (int64_t)st * BM;
+      const int col = ct * BN + warp * 8 + 2 * ac;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (col + h < g.ncols) __stcs(g.C + row0 + 8 * i + ar + (int64_t)(col + h) * g.ldc, acc[i][h]);
+    }
+    // ---- [W|T]^T += C_new^T V: A fragments re-laid-out from the accumulators ----
+    {
+      const int cl = ar;                  // this lane's C column within the warp's 8
+      const int src_h = cl & 1;
+#pragma unroll
+      for (int ks = 0; ks < BM / 4; ++ks) {
+        const int rr = 4 * (ks & 1) + ac;  // row within 8-row tile ks/2
+        const int src = rr * 4 + (cl >> 1);
+        const double v0 = __shfl_sync(0xffffffffu, acc[ks >> 1][0], src);
+        const double v1 = __shfl_sync(0xffffffffu, acc[ks >> 1][1], src);
+        const double af = src_h ? v1 : v0;
+#pragma unroll
+        for (int j = 0; j < R / 8; ++j) {
+          const double bf = Vs[(8 * j + ar) * P + 4 * ks + ac];
+          dmma_8x8x4(tw[j][0], tw[j][1], af, bf);
+        }
+      }
+    }
+    if (st == nsub - 1) {
+      // tw[j][h] = TW^T[col = ar][rank = 8j + 2ac + h]
+      const int n0 = ct * BN;
+      const int64_t q = seg0 / (2 * (int64_t)g.n_c);
+      double* out;
+      int64_t ld;
+      if (g.partial) {
+        out = g.TW + (int64_t)blockIdx.x * R * g.ncols;
+        ld = R;
+      } else {
+        out = g.TW + (q >> 1) * g.tw_stride + (q & 1) * R;
+        ld = 2 * R;
+      }
+      const int col = n0 + warp * 8 + ar;
+      if (col < g.ncols) {
+#pragma unroll
+        for (int j = 0; j < R / 8; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) out[8 * j + 2 * ac + h + (int64_t)col * ld] = tw[j][h];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int R>
+static hodlr_status run_level2(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
+  using Cfg = Level2Cfg<R>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(level_update2_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    attr = true;
+  }
+  level_update2_kernel<R><<<(unsigned)nseg, 256, Cfg::SMEM, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
 template <int R, int BN>
 static hodlr_status run_level(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
   using Cfg = LevelCfg<R, BN>;
@@ -276,9 +448,13 @@ size_t level_partial_bytes(int64_t n, int m, int r, int L) {
 
 // One fused level step over all n rows.  Returns ERR_ARG when the shape is not
 // supported (caller falls back to the generic batched GEMM path).
+// reg_resident selects the register-resident kernel, which accumulates the
+// update into C on the tensor core (factorization); the solve keeps the
+// product-then-subtract kernel so every right-hand-side column is computed
+// identically whatever nrhs is (multi-RHS bitwise contract).
 hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc, const double* A1, const double* V,
                               int64_t lda, const double* W, int64_t wstride, int ncols, double* TW, int64_t tw_stride,
-                              double* part, size_t part_bytes, cudaStream_t st) {
+                              double* part, size_t part_bytes, cudaStream_t st, bool reg_resident) {
   if (ncols == 0) return HODLR_OK;
   if (n_c % 64 || (r != 16 && r != 32)) return HODLR_ERR_ARG;
   if ((ldc & 1) || (lda & 1) || (reinterpret_cast<uintptr_t>(C) & 15) || (reinterpret_cast<uintptr_t>(A1) & 15) ||
@@ -294,8 +470,8 @@ hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc,
   const bool small = ncols <= 8;
   hodlr_status s;
   switch (r) {
-    case 16: s = small ? run_level<16, 8>(g, nseg, st) : run_level<16, 64>(g, nseg, st); break;
-    case 32: s = small ? run_level<32, 8>(g, nseg, st) : run_level<32, 64>(g, nseg, st); break;
+    case 16: s = small ? run_level<16, 8>(g, nseg, st) : (V && reg_resident ? run_level2<16>(g, nseg, st) : run_level<16, 64>(g, nseg, st)); break;
+    case 32: s = small ? run_level<32, 8>(g, nseg, st) : (V && reg_resident ? run_level2<32>(g, nseg, st) : run_level<32, 64>(g, nseg, st)); break;
     default: return HODLR_ERR_ARG;  // r = 64: generic path (fused tiles exceed shared memory)
   }
   if (s != HODLR_OK || !split) return s;
