@@ -59,8 +59,11 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
   static_assert(MI >= 1 && NI >= 1, "tile config");
   extern __shared__ __align__(16) double sm[];
   double* At = sm;                 // [k][m] packed inverses
-  double* Bbuf = sm + S * P;       // 2 x [n][k] tiles
-  double* Vs = Bbuf + 2 * BN * P;  // [j][k] (TWR x S, k contiguous)
+  // with the fused reduction the V panel takes the second tile buffer's place,
+  // so 2 CTAs still fit per SM (the co-resident CTA hides the tile load)
+  constexpr int NBUF = TWR > 0 ? 1 : 2;
+  double* Bbuf = sm + S * P;          // NBUF x [n][k] tiles
+  double* Vs = Bbuf + NBUF * BN * P;  // [j][k] (TWR x S, k contiguous)
   __shared__ int pm[S];
 
   const int b = blockIdx.x / g.groups;
@@ -102,82 +105,101 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
   cp_async_commit();
   for (int tile = grp; tile < ntiles; tile += g.groups) {
     double* Bs = Bbuf + cur * BN * P;
-    if (tile + g.groups < ntiles) load_tile(tile + g.groups, Bbuf + (cur ^ 1) * BN * P);
-    cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (NBUF == 2) {
+      if (tile + g.groups < ntiles) load_tile(tile + g.groups, Bbuf + (cur ^ 1) * BN * P);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      if (tile != grp) {
+        load_tile(tile, Bs);
+        cp_async_commit();
+      }
+      cp_async_wait<0>();
+    }
     __syncthreads();
 
     double acc[MI][NI][2];
+    // Row tiles are dealt to warps in balanced pairs (tile q with tile S/8-1-q), so
+    // every warp does the same triangular work in both stages.
+    int mrow[MI];
+    int kmax = 0, kmin = S;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      constexpr int H = MI / 2;
+      mrow[i] = (MI == 1) ? 8 * wm : (i < H ? 8 * (wm * H + i) : 8 * (S / 8 - 1 - (wm * H + (i - H))));
+      kmax = max(kmax, mrow[i] + 8);
+      kmin = min(kmin, mrow[i]);
+    }
     // stage 1: T = P B + strict_lower(L^-1) P B
     if (mma_warp) {
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < NI; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int m = wm * WTM + i * 8 + ar, n = wn * WTN + j * 8 + ac * 2 + h;
-          acc[i][j][h] = Bs[n * P + m];
-        }
-    for (int k0 = 0; k0 < (wm + 1) * WTM; k0 += 4) {
-      const int k = k0 + ac;
-      double af[MI], bf[NI];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        const int m = wm * WTM + i * 8 + ar;
-        af[i] = (k < m) ? At[k * P + m] : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < NI; ++j) bf[j] = Bs[(wn * WTN + j * 8 + ar) * P + k];
-#pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int m = mrow[i] + ar, n = wn * WTN + j * 8 + ac * 2 + h;
+            acc[i][j][h] = Bs[n * P + m];
+          }
+      for (int k0 = 0; k0 < kmax; k0 += 4) {
+        const int k = k0 + ac;
+        double bf[NI];
+#pragma unroll
+        for (int j = 0; j < NI; ++j) bf[j] = Bs[(wn * WTN + j * 8 + ar) * P + k];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          if (k0 < mrow[i] + 8) {
+            const int m = mrow[i] + ar;
+            const double af = (k < m) ? At[k * P + m] : 0.0;
+#pragma unroll
+            for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af, bf[j]);
+          }
+        }
+      }
     }
     __syncthreads();
     if (mma_warp) {
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < NI; ++j)
+        for (int j = 0; j < NI; ++j)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int m = wm * WTM + i * 8 + ar, n = wn * WTN + j * 8 + ac * 2 + h;
-          Bs[n * P + m] = acc[i][j][h];
-          acc[i][j][h] = 0.0;
-        }
+          for (int h = 0; h < 2; ++h) {
+            const int m = mrow[i] + ar, n = wn * WTN + j * 8 + ac * 2 + h;
+            Bs[n * P + m] = acc[i][j][h];
+            acc[i][j][h] = 0.0;
+          }
     }
     __syncthreads();
     // stage 2: X = upper(U^-1) T
     if (mma_warp) {
-    for (int k0 = wm * WTM; k0 < S; k0 += 4) {
-      const int k = k0 + ac;
-      double af[MI], bf[NI];
+      for (int k0 = kmin; k0 < S; k0 += 4) {
+        const int k = k0 + ac;
+        double bf[NI];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        const int m = wm * WTM + i * 8 + ar;
-        af[i] = (k >= m) ? At[k * P + m] : 0.0;
+        for (int j = 0; j < NI; ++j) bf[j] = Bs[(wn * WTN + j * 8 + ar) * P + k];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          if (k0 + 3 >= mrow[i]) {
+            const int m = mrow[i] + ar;
+            const double af = (k >= m) ? At[k * P + m] : 0.0;
+#pragma unroll
+            for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af, bf[j]);
+          }
+        }
       }
-#pragma unroll
-      for (int j = 0; j < NI; ++j) bf[j] = Bs[(wn * WTN + j * 8 + ar) * P + k];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
     }
     __syncthreads();
     if (mma_warp) {
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < NI; ++j)
+        for (int j = 0; j < NI; ++j)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int m = wm * WTM + i * 8 + ar, n = wn * WTN + j * 8 + ac * 2 + h;
-          Bs[n * P + m] = acc[i][j][h];
-        }
+          for (int h = 0; h < 2; ++h) {
+            const int m = mrow[i] + ar, n = wn * WTN + j * 8 + ac * 2 + h;
+            Bs[n * P + m] = acc[i][j][h];
+          }
     }
     __syncthreads();
     const int n0 = tile * BN;
@@ -220,13 +242,13 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
       }
     }
     __syncthreads();
-    cur ^= 1;
+    if constexpr (NBUF == 2) cur ^= 1;
   }
 }
 
 template <int S, int BN, int TWR>
 static hodlr_status run_apply(ApplyArgs g, cudaStream_t st) {
-  constexpr size_t smem = (size_t)(S + 2 * BN + TWR) * (S + 4) * sizeof(double);
+  constexpr size_t smem = (size_t)(S + (TWR > 0 ? 1 : 2) * BN + TWR) * (S + 4) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tri_apply_kernel<S, BN, TWR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
