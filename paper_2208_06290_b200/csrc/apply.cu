@@ -91,12 +91,23 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
   const double* Bb = g.B + aoff(b, g.bdiv, g.sB_hi, g.sB_lo);
   double* Xb = g.X + aoff(b, g.bdiv, g.sX_hi, g.sX_lo);
 
+  // the tile is staged in natural row order with 16-byte copies; the row
+  // permutation P is applied when stage 1 reads it (pm[] lookups)
+  const bool vec16 = !((reinterpret_cast<uintptr_t>(Bb) | (uintptr_t)(g.ldb * 8)) & 15);
   auto load_tile = [&](int tile, double* Bs) {
     const int n0 = tile * BN;
-    for (int idx = t; idx < BN * S; idx += AP_THREADS) {
-      const int n = idx / S, k = idx % S;
-      const bool ok = n0 + n < g.ncols;
-      cp_async_8(Bs + n * P + k, ok ? Bb + pm[k] + (int64_t)(n0 + n) * g.ldb : g.B, ok ? 8 : 0);
+    if (vec16) {
+      for (int idx = t; idx < BN * (S / 2); idx += AP_THREADS) {
+        const int n = idx / (S / 2), k = (idx % (S / 2)) * 2;
+        const bool ok = n0 + n < g.ncols;
+        cp_async_16(Bs + n * P + k, ok ? Bb + k + (int64_t)(n0 + n) * g.ldb : g.B, ok ? 16 : 0);
+      }
+    } else {
+      for (int idx = t; idx < BN * S; idx += AP_THREADS) {
+        const int n = idx / S, k = idx % S;
+        const bool ok = n0 + n < g.ncols;
+        cp_async_8(Bs + n * P + k, ok ? Bb + k + (int64_t)(n0 + n) * g.ldb : g.B, ok ? 8 : 0);
+      }
     }
   };
 
@@ -139,13 +150,14 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int m = mrow[i] + ar, n = wn * WTN + j * 8 + ac * 2 + h;
-            acc[i][j][h] = Bs[n * P + m];
+            acc[i][j][h] = Bs[n * P + pm[m]];
           }
       for (int k0 = 0; k0 < kmax; k0 += 4) {
         const int k = k0 + ac;
+        const int pk = pm[k];
         double bf[NI];
 #pragma unroll
-        for (int j = 0; j < NI; ++j) bf[j] = Bs[(wn * WTN + j * 8 + ar) * P + k];
+        for (int j = 0; j < NI; ++j) bf[j] = Bs[(wn * WTN + j * 8 + ar) * P + pk];
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
           if (k0 < mrow[i] + 8) {
@@ -208,37 +220,34 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
       if (n0 + n < g.ncols) Xb[m + (int64_t)(n0 + n) * g.ldx] = Bs[n * P + m];
     }
     if constexpr (TWR > 0) {
-      // TW_b(:, tile) = V_b^T X_b(:, tile): TWR x BN, K = S, 4 warps along N
-      constexpr int TMI = TWR / 8, TNI = (BN / 8) / 8 >= 1 ? (BN / 8) / 8 : 1;
-      constexpr int TWN = BN / (8 * TNI);
-      if (warp < TWN) {
-        double tw[TMI][TNI][2];
+      // TW_b(:, tile) = V_b^T X_b(:, tile): TWR x BN, K = S.  BN = 64: one n-tile per
+      // warp, all TWR/8 m-tiles; BN = 8: one m-tile per warp.
+      constexpr int TWN = BN / 8;
+      constexpr int TMI = TWN >= 8 ? TWR / 8 : 1;
+      constexpr int NTW = TWN >= 8 ? 8 : (TWR / 8) * TWN;
+      if (warp < NTW) {
+        const int tn = TWN >= 8 ? warp : warp / (TWR / 8);
+        const int tm0 = TWN >= 8 ? 0 : warp % (TWR / 8);
+        double tw[TMI][2];
 #pragma unroll
-        for (int i = 0; i < TMI; ++i)
-#pragma unroll
-          for (int j = 0; j < TNI; ++j) tw[i][j][0] = tw[i][j][1] = 0.0;
+        for (int i = 0; i < TMI; ++i) tw[i][0] = tw[i][1] = 0.0;
 #pragma unroll 4
         for (int k0 = 0; k0 < S; k0 += 4) {
-          double af[TMI], bf[TNI];
+          const double bf = Bs[(tn * 8 + ar) * P + k0 + ac];
 #pragma unroll
-          for (int i = 0; i < TMI; ++i) af[i] = Vs[(i * 8 + ar) * P + k0 + ac];
-#pragma unroll
-          for (int j = 0; j < TNI; ++j) bf[j] = Bs[(warp * TNI * 8 + j * 8 + ar) * P + k0 + ac];
-#pragma unroll
-          for (int i = 0; i < TMI; ++i)
-#pragma unroll
-            for (int j = 0; j < TNI; ++j) dmma_8x8x4(tw[i][j][0], tw[i][j][1], af[i], bf[j]);
+          for (int i = 0; i < TMI; ++i) {
+            const double af = Vs[((tm0 + i) * 8 + ar) * P + k0 + ac];
+            dmma_8x8x4(tw[i][0], tw[i][1], af, bf);
+          }
         }
         double* out = g.TW + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR;
 #pragma unroll
         for (int i = 0; i < TMI; ++i)
 #pragma unroll
-          for (int j = 0; j < TNI; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int mm = i * 8 + ar, nn = n0 + warp * TNI * 8 + j * 8 + ac * 2 + h;
-              if (nn < g.ncols) out[mm + (int64_t)nn * 2 * TWR] = tw[i][j][h];
-            }
+          for (int h = 0; h < 2; ++h) {
+            const int mm = (tm0 + i) * 8 + ar, nn = n0 + tn * 8 + ac * 2 + h;
+            if (nn < g.ncols) out[mm + (int64_t)nn * 2 * TWR] = tw[i][h];
+          }
       }
     }
     __syncthreads();
@@ -279,8 +288,9 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int6
               V, ldv, vstride, TW, tw_stride};
   if (V) {
     if ((ldv & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15)) return HODLR_ERR_ARG;
-    if (s == 64 && twr == 32) return run_apply<64, 64, 32>(g, st);
-    if (s == 64 && twr == 16) return run_apply<64, 64, 16>(g, st);
+    const bool nw = ncols <= 8;
+    if (s == 64 && twr == 32) return nw ? run_apply<64, 8, 32>(g, st) : run_apply<64, 64, 32>(g, st);
+    if (s == 64 && twr == 16) return nw ? run_apply<64, 8, 16>(g, st) : run_apply<64, 64, 16>(g, st);
     if (s == 32 && twr == 16) return run_apply<32, 64, 16>(g, st);
     if (s == 32 && twr == 32) return run_apply<32, 64, 32>(g, st);
     return HODLR_ERR_ARG;

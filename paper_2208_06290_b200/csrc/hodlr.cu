@@ -341,14 +341,22 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
   const double* V = (const double*)f->V;
   const double* Kinv = (const double*)f->Kinv;
 
-  // x <- D^-1 x                                                   Alg.4 l.3
+  // x <- D^-1 x, fused with the level-(L-1) w_a = V_a^T x_a        Alg.4 l.3 (+ l.5)
+  bool w_ready = false;
   {
-  Phase ph(HODLR_PHASE_SOLVE_LEAF, st);
-  TRY(lu_apply(m, nrhs, (int)((int64_t)1 << L), (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m, X,
-               ldx, m, st));
+    Phase ph(HODLR_PHASE_SOLVE_LEAF, st);
+    if (r > 0 && L > 0 && tri_size_ok(m)) {
+      hodlr_status s = tri_apply_f64(m, nrhs, (int)((int64_t)1 << L), (const double*)f->Dinv, m, (int64_t)m * m,
+                                     f->dperm, X, ldx, m, 0, X, ldx, m, 0, 1, st, V + (int64_t)(L - 1) * r * n, n, m,
+                                     r, w, (int64_t)2 * r * nrhs);
+      if (s == HODLR_OK) w_ready = true;
+      else if (s != HODLR_ERR_ARG) return s;
+    }
+    if (!w_ready)
+      TRY(lu_apply(m, nrhs, (int)((int64_t)1 << L), (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m,
+                   X, ldx, m, st));
   }
   if (r == 0) return HODLR_OK;
-  bool w_ready = false;
   for (int lv = L - 1; lv >= 0; --lv) {
     const int nch = 1 << (lv + 1), npar = 1 << lv;
     const int64_t nc = n >> (lv + 1);
