@@ -143,6 +143,31 @@ hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* 
 hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f, void* X, int64_t ldx, int nrhs,
                          void* work, size_t work_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Row-sharded (multi-GPU) schedule, SURVEY.md §8e.  The caller holds the rows
+ * [row0, row0 + n_loc) of one level-p node (n_loc = N / 2^p): its leaves' D
+ * (local arrays), its rows of the Y / V slabs (ld n_loc) and the full K /
+ * K-pivot arrays in the global level layout.  Levels >= p are local
+ * (hodlr_factorize_local); each level lv < p is one sum all-reduce of the
+ * packed [W|T] of the 2^(lv+1) children (paired per parent: 2r x r(lv+1), ld
+ * 2r, parent stride 2r*r(lv+1)) followed by hodlr_factorize_top.  Outputs
+ * tw_out / w_out are the caller's contribution for its own node, r x ncols,
+ * ld r.  The solve mirrors it with w (2r x nrhs per parent).  With n_loc = N
+ * these reduce to hodlr_factorize / hodlr_solve.
+ * --------------------------------------------------------------------- */
+size_t hodlr_factorize_local_workspace(const hodlr_desc* d, int64_t n_loc);
+hodlr_status hodlr_factorize_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
+                                   int lv_stop, double* tw_out, void* work, size_t work_bytes, void* stream);
+hodlr_status hodlr_factorize_top(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0, int lv,
+                                 const double* tw_all, double* tw_out, void* work, size_t work_bytes,
+                                 void* stream);
+hodlr_status hodlr_solve_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
+                               int lv_stop, void* X, int64_t ldx, int nrhs, double* w_out, void* work,
+                               size_t work_bytes, void* stream);
+hodlr_status hodlr_solve_top(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0, int lv,
+                             const double* w_all, double* w_out, void* X, int64_t ldx, int nrhs, void* work,
+                             size_t work_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

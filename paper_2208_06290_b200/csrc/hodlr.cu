@@ -22,10 +22,12 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int6
                            int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st,
                            const double* V = nullptr, int64_t ldv = 0, int64_t vstride = 0, int twr = 0,
                            double* TW = nullptr, int64_t tw_stride = 0);
-hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc, const double* A1, const double* V,
-                              int64_t lda, const double* W, int64_t wstride, int ncols, double* TW, int64_t tw_stride,
-                              double* part, size_t part_bytes, cudaStream_t st, bool reg_resident);
+hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, double* C, int64_t ldc,
+                              const double* A1, const double* V, int64_t lda, const double* W, int64_t wstride,
+                              int ncols, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
+                              cudaStream_t st, bool reg_resident);
 size_t level_partial_bytes(int64_t n, int m, int r, int L);
+int64_t level_segment_rows(int64_t n, int64_t node, int sms);
 template <typename T>
 hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
                           const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX, int identity,
@@ -196,22 +198,47 @@ static hodlr_status lu_apply(int s, int ncols, int batch, const double* LU, cons
   return launch_getrs<double>(s, ncols, batch, LU, s, (int64_t)s * s, perm, B, ldb, sB, X, ldx, sX, 0, st);
 }
 
+// ---------------------------------------------------------------------------
+// Row-sharded schedule.  A caller may hold only the rows [row0, row0 + n_loc)
+// of a level-p node (n_loc = N / 2^p): its leaves' D, its rows of the Y / V
+// slabs (ld n_loc), and the full K / K-pivot arrays (global level layout; the
+// deep levels are filled for its own parents only, the top levels redundantly).
+// Levels l >= p are then entirely local; for l < p the partial [W|T] / w of
+// the caller's rows is exchanged (sum all-reduce) and hodlr_*_top finishes
+// level l.  Single GPU: n_loc = N, row0 = 0, p = 0.
+// ---------------------------------------------------------------------------
+
 // workspace layout (factorize): [split-K | TW | W | level partial sums]
 struct FactWs {
   size_t split, tw, w, part, total;
 };
-static FactWs fact_ws(const hodlr_desc* d) {
-  const int64_t n = d->n, r = d->r, L = d->L;
+static FactWs fact_ws_local(const hodlr_desc* d, int64_t n_loc) {
+  const int64_t r = d->r, L = d->L;
+  const int64_t nleaf = n_loc / d->m;
   FactWs w{};
   w.split = kSplitBytes;
-  w.tw = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * r * L);
-  w.w = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * r * (L > 0 ? L - 1 : 0));
-  w.part = align_up(level_partial_bytes(n, d->m, (int)r, (int)L));
+  w.tw = align_up(sizeof(double) * (size_t)std::max<int64_t>(nleaf, 2) * r * r * std::max<int64_t>(L, 1));
+  w.w = align_up(sizeof(double) * (size_t)std::max<int64_t>(nleaf, 2) * r * r * std::max<int64_t>(L, 1));
+  size_t part = level_partial_bytes(n_loc, d->m, (int)r, (int)L);
+  // top levels: the caller's rows form one output node
+  const int64_t seg = level_segment_rows(n_loc, n_loc, 148);
+  part = std::max(part, (size_t)(n_loc / std::max<int64_t>(seg, 1)) * r * r * L * sizeof(double));
+  w.part = align_up(part);
   w.total = w.split + w.tw + w.w + w.part;
   return w;
 }
+static FactWs fact_ws(const hodlr_desc* d) { return fact_ws_local(d, d->n); }
+
+static bool local_ok(const hodlr_desc* d, int64_t n_loc, int64_t row0) {
+  if (n_loc <= 0 || row0 < 0 || row0 + n_loc > d->n || n_loc % d->m) return false;
+  if (d->n % n_loc || row0 % n_loc) return false;  // a whole level-p node
+  return ((d->n / n_loc) & (d->n / n_loc - 1)) == 0;
+}
 
 extern "C" size_t hodlr_factorize_workspace(const hodlr_desc* d) { return desc_ok(d) ? fact_ws(d).total : 0; }
+extern "C" size_t hodlr_factorize_local_workspace(const hodlr_desc* d, int64_t n_loc) {
+  return desc_ok(d) && n_loc > 0 ? fact_ws_local(d, n_loc).total : 0;
+}
 
 static size_t solve_part_bytes(const hodlr_desc* d, int nrhs) {
   return align_up(sizeof(double) * (size_t)4 * 148 * d->r * nrhs);
@@ -220,7 +247,7 @@ static size_t solve_part_bytes(const hodlr_desc* d, int nrhs) {
 extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
   if (!desc_ok(d) || nrhs < 0) return 0;
   // split-K | w | w2 | level partial sums
-  const size_t wsz = align_up(sizeof(double) * (size_t)((int64_t)1 << d->L) * d->r * nrhs);
+  const size_t wsz = align_up(sizeof(double) * (size_t)std::max<int64_t>((int64_t)1 << d->L, 2) * d->r * nrhs);
   return kSplitBytes + 2 * wsz + solve_part_bytes(d, nrhs);
 }
 
@@ -230,22 +257,19 @@ extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
     if (s_ != HODLR_OK) return s_;        \
   } while (0)
 
-extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* work, size_t work_bytes,
-                                        void* stream) {
-  if (!desc_ok(d) || !f) return HODLR_ERR_ARG;
-  if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
-  const FactWs ws = fact_ws(d);
-  if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
-  cudaStream_t st = S(stream);
-  char* wp = static_cast<char*>(work);
+// Leaf phase + levels L-1 .. lv_stop over the local rows.  On return the
+// workspace TW region holds [W|T] of the local level-lv_stop node(s) (paired
+// layout, local node 0 first) unless lv_stop == 0.
+static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0, int lv_stop,
+                                 char* wp, const FactWs& ws, cudaStream_t st) {
   void* split = wp;
   double* TW = reinterpret_cast<double*>(wp + ws.split);
   double* W = reinterpret_cast<double*>(wp + ws.split + ws.tw);
   double* part = reinterpret_cast<double*>(wp + ws.split + ws.tw + ws.w);
 
-  const int64_t n = d->n;
+  const int64_t N = d->n, n = n_loc;
   const int m = d->m, r = d->r, L = d->L;
-  const int64_t nleaf = (int64_t)1 << L;
+  const int64_t nleaf = n / m;
   double* D = (double*)f->D;
   double* Dinv = (double*)f->Dinv;
   double* Y = (double*)f->Y;
@@ -263,22 +287,24 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
   //     fused with the level-(L-1) [W|T]_a = V_a^T Y(I_a, 0:rL)   Alg.3 l.5-6
   bool tw_ready = false;
   {
-  Phase ph(HODLR_PHASE_LEAF_APPLY, st);
-  if (tri_size_ok(m)) {
-    hodlr_status s = tri_apply_f64(m, r * L, (int)nleaf, Dinv, m, (int64_t)m * m, f->dperm, Y, n, m, 0, Y, n, m, 0, 1,
-                                   st, V + (int64_t)(L - 1) * r * n, n, m, r, TW, (int64_t)2 * r * r * L);
-    if (s == HODLR_OK) tw_ready = true;
-    else if (s != HODLR_ERR_ARG) return s;
-  }
-  if (!tw_ready) TRY(lu_apply(m, r * L, (int)nleaf, D, Dinv, f->dperm, Y, n, m, Y, n, m, st));
+    Phase ph(HODLR_PHASE_LEAF_APPLY, st);
+    if (tri_size_ok(m)) {
+      hodlr_status s = tri_apply_f64(m, r * L, (int)nleaf, Dinv, m, (int64_t)m * m, f->dperm, Y, n, m, 0, Y, n, m, 0,
+                                     1, st, V + (int64_t)(L - 1) * r * n, n, m, r, TW, (int64_t)2 * r * r * L);
+      if (s == HODLR_OK) tw_ready = true;
+      else if (s != HODLR_ERR_ARG) return s;
+    }
+    if (!tw_ready) TRY(lu_apply(m, r * L, (int)nleaf, D, Dinv, f->dperm, Y, n, m, Y, n, m, st));
   }
 
   // (3) levels                                                     Alg.3 l.4-10
-  for (int lv = L - 1; lv >= 0; --lv) {
-    const int nch = 1 << (lv + 1), npar = 1 << lv;
-    const int64_t nc = n >> (lv + 1);
+  for (int lv = L - 1; lv >= lv_stop; --lv) {
+    const int64_t nc = N >> (lv + 1);
+    const int nch = (int)(n / nc), npar = nch / 2;
+    const int64_t p0 = row0 / (2 * nc);  // global index of the first local parent
     const int ncol = r * (lv + 1), wc = r * lv;
-    const int64_t koff = ((int64_t)npar - 1) * 4 * r * r;
+    const int64_t kblk = ((int64_t)1 << lv) - 1 + p0;  // first local K block (global layout)
+    const int64_t koff = kblk * 4 * r * r;
     if (!tw_ready) {
       Phase ph(HODLR_PHASE_GEMM, st);
       // [W|T]_c = V_c^T Y(I_c, 0:r(l+1)), paired per parent: 2r x ncol, ld 2r
@@ -286,26 +312,25 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
                    2 * r, (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
     }
     // K_p = [[T_2p, I], [I, T_2p+1]] assembled + factored (bit-exact) + packed inverses
-    int32_t* kperm = f->kperm + ((int64_t)npar - 1) * 2 * r;
+    int32_t* kperm = f->kperm + kblk * 2 * r;
     {
-    Phase ph(HODLR_PHASE_K_GETRF, st);
-    TRY(lu_factor(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff,
-                  (int64_t)4 * r * r, f->kswaps + ((int64_t)npar - 1) * 2 * r, kperm, f->kinfo + (npar - 1),
-                  Kinv + koff, st));
+      Phase ph(HODLR_PHASE_K_GETRF, st);
+      TRY(lu_factor(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff,
+                    (int64_t)4 * r * r, f->kswaps + kblk * 2 * r, kperm, f->kinfo + kblk, Kinv + koff, st));
     }
     if (lv == 0) break;
     // W_p <- K_p^-1 [W_2p; W_2p+1]
     {
-    Phase ph(HODLR_PHASE_K_APPLY, st);
-    TRY(lu_apply(2 * r, wc, npar, K + koff, Kinv + koff, kperm, TW, 2 * r, (int64_t)2 * r * ncol, W, 2 * r,
-                 (int64_t)2 * r * wc, st));
+      Phase ph(HODLR_PHASE_K_APPLY, st);
+      TRY(lu_apply(2 * r, wc, npar, K + koff, Kinv + koff, kperm, TW, 2 * r, (int64_t)2 * r * ncol, W, 2 * r,
+                   (int64_t)2 * r * wc, st));
     }
     // Y(I_c, 0:rl) -= Y_c^{l+1} W_c, fused with the next level's [W|T] (V^{(l)T} Y(I_q, 0:rl))
     hodlr_status s;
     {
-    Phase ph(HODLR_PHASE_LEVEL, st);
-    s = level_update_f64(r, n, (int)nc, Y, n, Y + (int64_t)lv * r * n, V + (int64_t)(lv - 1) * r * n, n,
-                                      W, (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st, true);
+      Phase ph(HODLR_PHASE_LEVEL, st);
+      s = level_update_f64(r, n, nc, 2 * nc, Y, n, Y + (int64_t)lv * r * n, V + (int64_t)(lv - 1) * r * n, n, W,
+                           (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st, true);
     }
     if (s == HODLR_OK) {
       tw_ready = true;
@@ -317,50 +342,147 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
     TRY(gemm_f64(0, (int)nc, wc, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, W, 2 * r, (int64_t)2 * r * wc, r,
                  1.0, Y, n, 2 * nc, nc, nch, 2, split, ws.split, st));
   }
+  if (!tw_ready && lv_stop > 0) {
+    // the caller wants the level-lv_stop [W|T] in the workspace
+    const int lv = lv_stop - 1;
+    const int64_t nc = N >> (lv + 1);
+    const int nch = (int)(n / nc);
+    if (nch >= 1 && nc <= n) {
+      Phase ph(HODLR_PHASE_GEMM, st);
+      const int ncol = r * (lv + 1);
+      TRY(gemm_f64(1, r, ncol, (int)std::min<int64_t>(nc, n), 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, Y, n,
+                   2 * nc, nc, 0.0, TW, 2 * r, (int64_t)2 * r * ncol, r, std::max(nch, 1), 2, split, ws.split, st));
+    }
+  }
   return HODLR_OK;
 }
 
-extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f, void* Xv, int64_t ldx, int nrhs,
-                                    void* work, size_t work_bytes, void* stream) {
-  if (!desc_ok(d) || !f || nrhs < 0 || ldx < d->n) return HODLR_ERR_ARG;
+extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* work, size_t work_bytes,
+                                        void* stream) {
+  if (!desc_ok(d) || !f) return HODLR_ERR_ARG;
   if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
-  if (nrhs == 0) return HODLR_OK;
-  const size_t need = hodlr_solve_workspace(d, nrhs);
-  if (work_bytes < need || !work) return HODLR_ERR_ARG;
+  const FactWs ws = fact_ws(d);
+  if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
+  return factor_local(d, f, d->n, 0, 0, static_cast<char*>(work), ws, S(stream));
+}
+
+extern "C" hodlr_status hodlr_factorize_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
+                                              int lv_stop, double* tw_out, void* work, size_t work_bytes,
+                                              void* stream) {
+  if (!desc_ok(d) || !f || !local_ok(d, n_loc, row0)) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64 || lv_stop < 0 || lv_stop > d->L) return HODLR_ERR_ARG;
+  if ((d->n >> lv_stop) > n_loc) return HODLR_ERR_ARG;  // levels >= lv_stop must be local
+  const FactWs ws = fact_ws_local(d, n_loc);
+  if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
   cudaStream_t st = S(stream);
-  const int64_t n = d->n;
-  const int m = d->m, r = d->r, L = d->L;
-  const size_t wsz = align_up(sizeof(double) * (size_t)((int64_t)1 << L) * r * nrhs);
+  TRY(factor_local(d, f, n_loc, row0, lv_stop, static_cast<char*>(work), ws, st));
+  if (tw_out && lv_stop > 0 && d->r > 0) {
+    // [W|T] of the caller's level-lv_stop node: r x r*lv_stop, ld r
+    const double* TW = reinterpret_cast<const double*>(static_cast<char*>(work) + ws.split);
+    const int r = d->r, nc = r * lv_stop;
+    if (cudaMemcpy2DAsync(tw_out, sizeof(double) * r, TW, sizeof(double) * 2 * r, sizeof(double) * r, nc,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return hodlr_set_cuda_error(cudaGetLastError());
+  }
+  return HODLR_OK;
+}
+
+// Finish level lv < p for the caller's rows.  tw_all: complete [W|T] of all
+// 2^(lv+1) children at level lv+1 (paired per parent: 2r x r(lv+1), ld 2r,
+// parent stride 2r*r(lv+1)) after the all-reduce.  Factors all 2^lv K blocks
+// (redundant on every rank), applies K_p^-1 for the caller's parent, updates
+// its rows of Y(:, 0:r lv) and writes the caller's partial [W|T] of its
+// level-lv node (r x r lv, ld r) to tw_out (lv > 0).
+extern "C" hodlr_status hodlr_factorize_top(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
+                                            int lv, const double* tw_all, double* tw_out, void* work,
+                                            size_t work_bytes, void* stream) {
+  if (!desc_ok(d) || !f || !local_ok(d, n_loc, row0) || !tw_all) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64 || lv < 0 || lv >= d->L || (d->n >> (lv + 1)) < n_loc) return HODLR_ERR_ARG;
+  const FactWs ws = fact_ws_local(d, n_loc);
+  if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
+  cudaStream_t st = S(stream);
   char* wp = static_cast<char*>(work);
+  double* W = reinterpret_cast<double*>(wp + ws.split + ws.tw);
+  double* part = reinterpret_cast<double*>(wp + ws.split + ws.tw + ws.w);
+  const int64_t N = d->n, n = n_loc;
+  const int r = d->r;
+  const int npar = 1 << lv, ncol = r * (lv + 1), wc = r * lv;
+  const int64_t kblk = (int64_t)npar - 1;
+  double* K = (double*)f->K + kblk * 4 * r * r;
+  double* Kinv = (double*)f->Kinv + kblk * 4 * r * r;
+  int32_t* kperm = f->kperm + kblk * 2 * r;
+  {
+    Phase ph(HODLR_PHASE_K_GETRF, st);
+    TRY(lu_factor(2 * r, npar, 1, tw_all + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K, (int64_t)4 * r * r,
+                  f->kswaps + kblk * 2 * r, kperm, f->kinfo + kblk, Kinv, st));
+  }
+  if (lv == 0) return HODLR_OK;
+  const int64_t nc = N >> (lv + 1);
+  const int64_t p = row0 / (2 * nc), half = (row0 / nc) & 1;
+  {
+    Phase ph(HODLR_PHASE_K_APPLY, st);
+    TRY(lu_apply(2 * r, wc, 1, K + p * 4 * r * r, Kinv + p * 4 * r * r, kperm + p * 2 * r,
+                 tw_all + p * 2 * r * ncol, 2 * r, 0, W, 2 * r, 0, st));
+  }
+  double* Y = (double*)f->Y;
+  const double* V = (const double*)f->V;
+  Phase ph(HODLR_PHASE_LEVEL, st);
+  double* TWws = reinterpret_cast<double*>(wp + ws.split);
+  hodlr_status s = level_update_f64(r, n, nc, n, Y, n, Y + (int64_t)lv * r * n, V + (int64_t)(lv - 1) * r * n, n,
+                                    W + half * r, 0, wc, TWws, 0, part, ws.part, st, true);
+  if (s == HODLR_OK) {
+    if (cudaMemcpy2DAsync(tw_out, sizeof(double) * r, TWws, sizeof(double) * 2 * r, sizeof(double) * r, wc,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return hodlr_set_cuda_error(cudaGetLastError());
+    return HODLR_OK;
+  }
+  if (s != HODLR_ERR_ARG) return s;
+  // generic path: update, then the partial [W|T] over all local rows
+  TRY(gemm_f64(0, (int)n, wc, r, -1.0, Y + (int64_t)lv * r * n, n, 0, 0, W + half * r, 2 * r, 0, 0, 1.0, Y, n, 0, 0,
+               1, 1, wp, ws.split, st));
+  return gemm_f64(1, r, wc, (int)n, 1.0, V + (int64_t)(lv - 1) * r * n, n, 0, 0, Y, n, 0, 0, 0.0, tw_out, r, 0, 0, 1,
+                  1, wp, ws.split, st);
+}
+
+// Leaf solve + levels L-1 .. lv_stop over the caller's rows of X (ld ldx).
+// On return the workspace w region holds w of the local level-lv_stop node
+// (paired layout, local node 0) when lv_stop > 0.
+static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0, int lv_stop,
+                                double* X, int64_t ldx, int nrhs, char* wp, cudaStream_t st) {
+  const int64_t N = d->n, n = n_loc;
+  const int m = d->m, r = d->r, L = d->L;
+  const size_t wsz = align_up(sizeof(double) * (size_t)std::max<int64_t>((int64_t)1 << L, 2) * r * nrhs);
   void* split = wp;
   double* w = reinterpret_cast<double*>(wp + kSplitBytes);
   double* w2 = reinterpret_cast<double*>(wp + kSplitBytes + wsz);
   double* part = reinterpret_cast<double*>(wp + kSplitBytes + 2 * wsz);
-  double* X = (double*)Xv;
   const double* Y = (const double*)f->Y;
   const double* V = (const double*)f->V;
   const double* Kinv = (const double*)f->Kinv;
+  const int64_t nleaf = n / m;
 
   // x <- D^-1 x, fused with the level-(L-1) w_a = V_a^T x_a        Alg.4 l.3 (+ l.5)
   bool w_ready = false;
   {
     Phase ph(HODLR_PHASE_SOLVE_LEAF, st);
     if (r > 0 && L > 0 && tri_size_ok(m)) {
-      hodlr_status s = tri_apply_f64(m, nrhs, (int)((int64_t)1 << L), (const double*)f->Dinv, m, (int64_t)m * m,
-                                     f->dperm, X, ldx, m, 0, X, ldx, m, 0, 1, st, V + (int64_t)(L - 1) * r * n, n, m,
-                                     r, w, (int64_t)2 * r * nrhs);
+      hodlr_status s = tri_apply_f64(m, nrhs, (int)nleaf, (const double*)f->Dinv, m, (int64_t)m * m, f->dperm, X, ldx,
+                                     m, 0, X, ldx, m, 0, 1, st, V + (int64_t)(L - 1) * r * n, n, m, r, w,
+                                     (int64_t)2 * r * nrhs);
       if (s == HODLR_OK) w_ready = true;
       else if (s != HODLR_ERR_ARG) return s;
     }
     if (!w_ready)
-      TRY(lu_apply(m, nrhs, (int)((int64_t)1 << L), (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m,
-                   X, ldx, m, st));
+      TRY(lu_apply(m, nrhs, (int)nleaf, (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m, X, ldx, m,
+                   st));
   }
-  if (r == 0) return HODLR_OK;
-  for (int lv = L - 1; lv >= 0; --lv) {
-    const int nch = 1 << (lv + 1), npar = 1 << lv;
-    const int64_t nc = n >> (lv + 1);
-    const int64_t koff = ((int64_t)npar - 1) * 4 * r * r;
+  if (r == 0 || L == 0) return HODLR_OK;
+  for (int lv = L - 1; lv >= lv_stop; --lv) {
+    const int64_t nc = N >> (lv + 1);
+    const int nch = (int)(n / nc), npar = nch / 2;
+    const int64_t p0 = row0 / (2 * nc);
+    const int64_t kblk = ((int64_t)1 << lv) - 1 + p0;
+    const int64_t koff = kblk * 4 * r * r;
     // w_c = V_c^T x_c  (paired per parent, 2r x nrhs, ld 2r)       Alg.4 l.5
     if (!w_ready) {
       Phase ph(HODLR_PHASE_GEMM, st);
@@ -369,21 +491,20 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
     }
     // w_p <- K_p^-1 w_p                                              Alg.4 l.6
     {
-    Phase ph(HODLR_PHASE_SOLVE_K, st);
-    TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + koff, f->kperm + ((int64_t)npar - 1) * 2 * r,
-                 w, 2 * r, (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st));
+      Phase ph(HODLR_PHASE_SOLVE_K, st);
+      TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + koff, f->kperm + kblk * 2 * r, w, 2 * r,
+                   (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st));
     }
     // x_c -= Y_c w_c  fused with the next level's w = V^{(l)T} x    Alg.4 l.7 (+ l.5 of level l-1)
     hodlr_status s;
     {
-    Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
-    s = level_update_f64(r, n, (int)nc, X, ldx, Y + (int64_t)lv * r * n,
-                                      lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2,
-                                      (int64_t)2 * r * nrhs, nrhs, w, (int64_t)2 * r * nrhs, part,
-                                      solve_part_bytes(d, nrhs), st, false);
+      Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
+      s = level_update_f64(r, n, nc, 2 * nc, X, ldx, Y + (int64_t)lv * r * n,
+                           lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
+                           (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st, false);
     }
     if (s == HODLR_OK) {
-      w_ready = true;
+      w_ready = lv > 0;
       continue;
     }
     if (s != HODLR_ERR_ARG) return s;
@@ -392,5 +513,90 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
     TRY(gemm_f64(0, (int)nc, nrhs, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, w2, 2 * r, (int64_t)2 * r * nrhs,
                  r, 1.0, X, ldx, 2 * nc, nc, nch, 2, split, kSplitBytes, st));
   }
+  if (!w_ready && lv_stop > 0) {
+    const int lv = lv_stop - 1;
+    const int64_t nc = N >> (lv + 1);
+    Phase ph(HODLR_PHASE_GEMM, st);
+    TRY(gemm_f64(1, r, nrhs, (int)std::min<int64_t>(nc, n), 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, X, ldx,
+                 2 * nc, nc, 0.0, w, 2 * r, (int64_t)2 * r * nrhs, r, std::max<int>((int)(n / nc), 1), 2, split,
+                 kSplitBytes, st));
+  }
+  return HODLR_OK;
+}
+
+extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f, void* Xv, int64_t ldx, int nrhs,
+                                    void* work, size_t work_bytes, void* stream) {
+  if (!desc_ok(d) || !f || nrhs < 0 || ldx < d->n) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
+  if (nrhs == 0) return HODLR_OK;
+  if (work_bytes < hodlr_solve_workspace(d, nrhs) || !work) return HODLR_ERR_ARG;
+  return solve_local(d, f, d->n, 0, 0, (double*)Xv, ldx, nrhs, static_cast<char*>(work), S(stream));
+}
+
+extern "C" hodlr_status hodlr_solve_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
+                                          int lv_stop, void* Xv, int64_t ldx, int nrhs, double* w_out, void* work,
+                                          size_t work_bytes, void* stream) {
+  if (!desc_ok(d) || !f || !local_ok(d, n_loc, row0) || nrhs < 0 || ldx < n_loc) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64 || lv_stop < 0 || lv_stop > d->L || (d->n >> lv_stop) > n_loc) return HODLR_ERR_ARG;
+  if (nrhs == 0) return HODLR_OK;
+  if (work_bytes < hodlr_solve_workspace(d, nrhs) || !work) return HODLR_ERR_ARG;
+  cudaStream_t st = S(stream);
+  TRY(solve_local(d, f, n_loc, row0, lv_stop, (double*)Xv, ldx, nrhs, static_cast<char*>(work), st));
+  if (w_out && lv_stop > 0 && d->r > 0) {
+    const double* w = reinterpret_cast<const double*>(static_cast<char*>(work) + kSplitBytes);
+    const int r = d->r;
+    if (cudaMemcpy2DAsync(w_out, sizeof(double) * r, w, sizeof(double) * 2 * r, sizeof(double) * r, nrhs,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return hodlr_set_cuda_error(cudaGetLastError());
+  }
+  return HODLR_OK;
+}
+
+// Finish solve level lv < p for the caller's rows: w_all = complete w of all
+// 2^(lv+1) children (paired per parent, 2r x nrhs, ld 2r, parent stride
+// 2r*nrhs); applies K_p^-1 for the caller's parent, updates its rows of X and
+// writes its partial w of its level-lv node (r x nrhs, ld r) to w_out (lv > 0).
+extern "C" hodlr_status hodlr_solve_top(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
+                                        int lv, const double* w_all, double* w_out, void* Xv, int64_t ldx, int nrhs,
+                                        void* work, size_t work_bytes, void* stream) {
+  if (!desc_ok(d) || !f || !local_ok(d, n_loc, row0) || !w_all || nrhs <= 0 || ldx < n_loc) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64 || lv < 0 || lv >= d->L || (d->n >> (lv + 1)) < n_loc) return HODLR_ERR_ARG;
+  if (work_bytes < hodlr_solve_workspace(d, nrhs) || !work) return HODLR_ERR_ARG;
+  cudaStream_t st = S(stream);
+  char* wp = static_cast<char*>(work);
+  const int64_t N = d->n, n = n_loc;
+  const int r = d->r, L = d->L;
+  const size_t wsz = align_up(sizeof(double) * (size_t)std::max<int64_t>((int64_t)1 << L, 2) * r * nrhs);
+  double* w = reinterpret_cast<double*>(wp + kSplitBytes);
+  double* w2 = reinterpret_cast<double*>(wp + kSplitBytes + wsz);
+  double* part = reinterpret_cast<double*>(wp + kSplitBytes + 2 * wsz);
+  const int64_t nc = N >> (lv + 1);
+  const int64_t p = row0 / (2 * nc), half = (row0 / nc) & 1;
+  const int64_t kblk = ((int64_t)1 << lv) - 1 + p;
+  {
+    Phase ph(HODLR_PHASE_SOLVE_K, st);
+    TRY(lu_apply(2 * r, nrhs, 1, (const double*)f->K + kblk * 4 * r * r, (const double*)f->Kinv + kblk * 4 * r * r,
+                 f->kperm + kblk * 2 * r, w_all + p * 2 * r * nrhs, 2 * r, 0, w2, 2 * r, 0, st));
+  }
+  const double* Y = (const double*)f->Y;
+  const double* V = (const double*)f->V;
+  double* X = (double*)Xv;
+  Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
+  hodlr_status s = level_update_f64(r, n, nc, n, X, ldx, Y + (int64_t)lv * r * n,
+                                    lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2 + half * r, 0, nrhs, w, 0,
+                                    part, solve_part_bytes(d, nrhs), st, false);
+  if (s == HODLR_OK) {
+    if (lv > 0 && w_out &&
+        cudaMemcpy2DAsync(w_out, sizeof(double) * r, w, sizeof(double) * 2 * r, sizeof(double) * r, nrhs,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return hodlr_set_cuda_error(cudaGetLastError());
+    return HODLR_OK;
+  }
+  if (s != HODLR_ERR_ARG) return s;
+  TRY(gemm_f64(0, (int)n, nrhs, r, -1.0, Y + (int64_t)lv * r * n, n, 0, 0, w2 + half * r, 2 * r, 0, 0, 1.0, X, ldx, 0,
+               0, 1, 1, wp, kSplitBytes, st));
+  if (lv > 0 && w_out)
+    TRY(gemm_f64(1, r, nrhs, (int)n, 1.0, V + (int64_t)(lv - 1) * r * n, n, 0, 0, X, ldx, 0, 0, 0.0, w_out, r, 0, 0, 1,
+                 1, wp, kSplitBytes, st));
   return HODLR_OK;
 }

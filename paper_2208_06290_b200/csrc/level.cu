@@ -29,8 +29,9 @@ struct LevelArgs {
   double* TW;       // final: paired layout; partial: [seg][r x ncols] ld r
   int64_t tw_stride;  // final: per next-parent stride (2r * ncols)
   int partial;
-  int n_c;       // rows per child at level l+1
-  int seg_rows;  // rows per CTA segment (multiple of 64, divides 2 n_c)
+  int n_c;       // rows per child at level l+1 (selects the W' half)
+  int seg_rows;  // rows per CTA segment (multiple of 64, divides node_rows)
+  int64_t node_rows;  // rows of one [W|T] output node (2 n_c, or a rank's share)
   int ncols;
 };
 
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(LV_THREADS) level_update_kernel(LevelArgs g) {
           for (int h = 0; h < 2; ++h) red[(tk * R + i * 8 + ar) * BN + tn * 8 + ac * 2 + h] = tw[i][h];
         __syncthreads();
         const int n0 = ct * BN;
-        const int64_t q = seg0 / (2 * (int64_t)g.n_c);  // level-l node of this segment
+        const int64_t q = seg0 / g.node_rows;  // level-l node of this segment
         double* out;
         int64_t ld;
         if (g.partial) {
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(256, 2) level_update2_kernel(LevelArgs g) {
     if (st == nsub - 1) {
       // tw[j][h] = TW^T[col = ar][rank = 8j + 2ac + h]
       const int n0 = ct * BN;
-      const int64_t q = seg0 / (2 * (int64_t)g.n_c);
+      const int64_t q = seg0 / g.node_rows;
       double* out;
       int64_t ld;
       if (g.partial) {
@@ -452,21 +453,24 @@ size_t level_partial_bytes(int64_t n, int m, int r, int L) {
 // update into C on the tensor core (factorization); the solve keeps the
 // product-then-subtract kernel so every right-hand-side column is computed
 // identically whatever nrhs is (multi-RHS bitwise contract).
-hodlr_status level_update_f64(int r, int64_t n, int n_c, double* C, int64_t ldc, const double* A1, const double* V,
-                              int64_t lda, const double* W, int64_t wstride, int ncols, double* TW, int64_t tw_stride,
-                              double* part, size_t part_bytes, cudaStream_t st, bool reg_resident) {
+hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, double* C, int64_t ldc,
+                              const double* A1, const double* V, int64_t lda, const double* W, int64_t wstride,
+                              int ncols, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
+                              cudaStream_t st, bool reg_resident) {
   if (ncols == 0) return HODLR_OK;
-  if (n_c % 64 || (r != 16 && r != 32)) return HODLR_ERR_ARG;
+  if ((n_c % 64 && n_c < n) || n % 64 || node_rows % 64 || (r != 16 && r != 32)) return HODLR_ERR_ARG;
+  if (n_c > 2147483647LL) n_c = 2147483647LL;  // a child larger than the local rows: W' half is pre-selected
   if ((ldc & 1) || (lda & 1) || (reinterpret_cast<uintptr_t>(C) & 15) || (reinterpret_cast<uintptr_t>(A1) & 15) ||
       (V && (reinterpret_cast<uintptr_t>(V) & 15)) || (reinterpret_cast<uintptr_t>(W) & 15) || (wstride & 1))
     return HODLR_ERR_ARG;
-  const int64_t node = 2 * (int64_t)n_c;  // rows of a level-l node
+  const int64_t node = node_rows;  // rows of one output node
   const int64_t seg = level_segment_rows(n, node, sm_count());
   const int64_t nseg = n / seg;
   if (nseg > 2147483647LL) return HODLR_ERR_ARG;
   const bool split = seg < node && V != nullptr;
   if (split && (size_t)nseg * r * ncols * sizeof(double) > part_bytes) return HODLR_ERR_ARG;
-  LevelArgs g{C, ldc, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, n_c, (int)seg, ncols};
+  LevelArgs g{C, ldc, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)seg, node,
+              ncols};
   const bool small = ncols <= 8;
   hodlr_status s;
   switch (r) {
