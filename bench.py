@@ -70,6 +70,7 @@ class ClockSampler:
     def __init__(self, index=0):
         self.index, self.samples, self.reasons, self._stop = index, [], set(), threading.Event()
         self.max_mhz = None
+        self._ready = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
@@ -81,6 +82,7 @@ class ClockSampler:
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(hd, nv.NVML_CLOCK_SM)
             while not self._stop.is_set():
                 self.samples.append(nv.nvmlDeviceGetClockInfo(hd, nv.NVML_CLOCK_SM))
+                self._ready.set()
                 mask = nv.nvmlDeviceGetCurrentClocksEventReasons(hd)
                 for name, attr in self.REASONS:
                     if mask & getattr(nv, attr):
@@ -88,9 +90,14 @@ class ClockSampler:
                 self._stop.wait(0.01)
         except Exception as e:  # pragma: no cover - diagnostics only
             self.reasons.add(f"nvml unavailable: {e}")
+        finally:
+            self._ready.set()
 
     def __enter__(self):
+        # NVML import/init runs before the timed region starts: an import holding
+        # the GIL inside the region would stall the launching thread
         self._t.start()
+        self._ready.wait(timeout=30)
         return self
 
     def __exit__(self, *a):
@@ -263,20 +270,6 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
 
-    # per-phase event profile + launch count of one step (outside the timed loop)
-    restore()
-    lib.hodlr_profile_enable(1)
-    c0 = lib.hodlr_launch_count()
-    f, x, _ = step()
-    torch.cuda.synchronize()
-    launches_per_step = lib.hodlr_launch_count() - c0
-    ph = (C.c_double * 9)()
-    lib.hodlr_profile_read(ph, 9)
-    lib.hodlr_profile_enable(0)
-    phases = {name: ph[i] for i, name in enumerate(_lib.PHASES)}
-    # accuracy of this step: relres against the HODLR operator
-    relres = float(torch.linalg.norm(h0.matvec(x) - b) / torch.linalg.norm(b))
-
     # ---- timed region ----
     if world > 1:
         dist.barrier()
@@ -293,9 +286,25 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    step_ms = [ev[0].elapsed_time(ev[2]) for ev in tf_ms]
     tf = sum(ev[0].elapsed_time(ev[1]) for ev in tf_ms) / args.steps
     ts = sum(ev[1].elapsed_time(ev[2]) for ev in tf_ms) / args.steps
     t_step = tf + ts
+
+    # per-phase event profile + launch count of one step (after the timed loop)
+    restore()
+    lib.hodlr_profile_enable(1)
+    c0 = lib.hodlr_launch_count()
+    f, x, _ = step()
+    torch.cuda.synchronize()
+    launches_per_step = lib.hodlr_launch_count() - c0
+    ph = (C.c_double * 9)()
+    lib.hodlr_profile_read(ph, 9)
+    lib.hodlr_profile_enable(0)
+    phases = {name: ph[i] for i, name in enumerate(_lib.PHASES)}
+    # accuracy of this step: relres against the HODLR operator
+    relres = float(torch.linalg.norm(h0.matvec(x) - b) / torch.linalg.norm(b))
+    del f, x
     if world > 1:
         tt = torch.tensor([t_step, tf, ts], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -350,6 +359,7 @@ def run_ours(args):
                                    "seeded exact-HODLR stand-in", "N": n, "leaf": m, "rank": r, "L": L, "nrhs": 1,
                        "parallelism": f"replicas{world}", "l2_flush": "inputs 8 GB > L2"},
             "t_factor_ms": tf, "t_solve_ms": ts, "factor_tflops": f_flops / (tf * 1e-3) / 1e12,
+            "step_ms_min_med_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
             "solve_gbps": (8 * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 16 * n) / (ts * 1e-3) / 1e9,
             "relres": relres, "flops_factor": f_flops, "flops_solve": s_flops,
             "phase_ms": phases, "gpu_launches": launches_per_step * args.steps,

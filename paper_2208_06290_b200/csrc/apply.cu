@@ -17,6 +17,8 @@
 // line 3 and the level-(L-1) [W|T] GEMM of lines 5-6 into one HBM pass.
 //
 // Used for the leaf solve of Y, K_p^-1 W (Alg.3 l.9) and the solve phase.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hodlr {
@@ -255,6 +257,185 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Column-group variant (S in {32, 64}): every warp owns 8 columns of B at a
+// time and runs the whole chain for them in registers, transposed so that no
+// operand ever changes lanes:
+//
+//   T^T = (P B)^T L^-T     A = gathered rows of B (lane: column, 2 rows)
+//   X^T = T^T U^-T         A = the stage-1 accumulators, as they are
+//   TW^T = X^T V           A = the stage-2 accumulators, as they are
+//
+// The k index of every product runs over rows in the order (tile j, pair
+// 2c + h), which is exactly the order in which an m8n8k4 accumulator holds a
+// lane's row entries -- so accumulators feed the next product directly.  The
+// triangular factors are read as [row][k] LDS.128 pairs (pitch 8 mod 16:
+// conflict-free) and only their non-zero 8x8 tiles are multiplied.  No CTA
+// barrier after the one-time staging of Tinv / V: warps stream their column
+// groups independently, B of the next group prefetched into registers.
+// ---------------------------------------------------------------------------
+template <int S>
+struct Apply2Cfg {
+  static constexpr int PT = S + 8;  // Tinv [row][k] and V [rank][row] pitch (8 mod 16)
+};
+
+template <int S, int TWR>
+__global__ void __launch_bounds__(AP_THREADS, 2) tri_apply2_kernel(ApplyArgs g) {
+  constexpr int NJ = S / 8, PT = Apply2Cfg<S>::PT, RT = TWR / 8;
+  extern __shared__ __align__(16) double sm[];
+  double* Tm = sm;            // [row][k]
+  double* Vs = sm + S * PT;   // [rank][row]
+  __shared__ __align__(8) int pm[S];
+  const int b = blockIdx.x / g.groups, part = blockIdx.x % g.groups;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+
+  // ---- one-time staging: Tinv transposed to [row][k] (k pairs per thread) ----
+  const double* ti = g.tinv + (int64_t)b * g.strideT;
+  for (int idx = t; idx < S * (S / 2); idx += AP_THREADS) {
+    const int m = idx % S, k = (idx / S) * 2;
+    const double x0 = ti[m + (int64_t)k * g.ldi], x1 = ti[m + (int64_t)(k + 1) * g.ldi];
+    *reinterpret_cast<double2*>(Tm + m * PT + k) = make_double2(x0, x1);
+  }
+  if constexpr (TWR > 0) {
+    const double* vb = g.V + (int64_t)b * g.vstride;
+    for (int idx = t; idx < TWR * (S / 2); idx += AP_THREADS) {
+      const int j = idx / (S / 2), k = (idx % (S / 2)) * 2;
+      cp_async_16(Vs + j * PT + k, vb + k + (int64_t)j * g.ldv, 16);
+    }
+    cp_async_commit();
+  }
+  if (t < S) pm[t] = g.perm[(int64_t)b * S + t];
+  cp_async_wait<0>();
+  __syncthreads();
+
+  const double* Bb = g.B + aoff(b, g.bdiv, g.sB_hi, g.sB_lo);
+  double* Xb = g.X + aoff(b, g.bdiv, g.sX_hi, g.sX_lo);
+
+  const int G = (g.ncols + 7) >> 3;
+  const int gpc = (G + g.groups - 1) / g.groups;
+  const int g0 = part * gpc, g1 = min(G, g0 + gpc);
+  auto load_b = [&](int grp, double (&v)[NJ][2]) {
+    const int col = grp * 8 + ar;
+    const bool ok = col < g.ncols;
+    const double* bc = Bb + (int64_t)(ok ? col : 0) * g.ldb;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {  // this lane's gathered rows: P rows 8j + 2ac + {0, 1}
+      const int2 p = *reinterpret_cast<const int2*>(pm + 8 * j + 2 * ac);
+      v[j][0] = ok ? bc[p.x] : 0.0;
+      v[j][1] = ok ? bc[p.y] : 0.0;
+    }
+  };
+
+  double bn[NJ][2];
+  int grp = g0 + warp;
+  if (grp < g1) load_b(grp, bn);
+  for (; grp < g1; grp += 8) {
+    double bv[NJ][2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) bv[j][0] = bn[j][0], bv[j][1] = bn[j][1];
+    if (grp + 8 < g1) load_b(grp + 8, bn);
+    // ---- stage 1: T^T = (P B)^T L^-T   (L unit lower: k <= n) ----
+    double a1[NJ][2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) a1[j][0] = a1[j][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int jn = j; jn < NJ; ++jn) {
+        double2 l = *reinterpret_cast<const double2*>(Tm + (8 * jn + ar) * PT + 8 * j + 2 * ac);
+        if (jn == j) {  // diagonal tile: strict lower part, unit diagonal
+          const int k0 = 2 * ac;
+          l.x = k0 < ar ? l.x : (k0 == ar ? 1.0 : 0.0);
+          l.y = k0 + 1 < ar ? l.y : (k0 + 1 == ar ? 1.0 : 0.0);
+        }
+        dmma_8x8x4(a1[jn][0], a1[jn][1], bv[j][0], l.x);
+        dmma_8x8x4(a1[jn][0], a1[jn][1], bv[j][1], l.y);
+      }
+    }
+    // ---- stage 2: X^T = T^T U^-T   (U upper: k >= n) ----
+    double a2[NJ][2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) a2[j][0] = a2[j][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int jn = 0; jn <= j; ++jn) {
+        double2 u = *reinterpret_cast<const double2*>(Tm + (8 * jn + ar) * PT + 8 * j + 2 * ac);
+        if (jn == j) {
+          const int k0 = 2 * ac;
+          u.x = k0 >= ar ? u.x : 0.0;
+          u.y = k0 + 1 >= ar ? u.y : 0.0;
+        }
+        dmma_8x8x4(a2[jn][0], a2[jn][1], a1[j][0], u.x);
+        dmma_8x8x4(a2[jn][0], a2[jn][1], a1[j][1], u.y);
+      }
+    }
+    const int col = grp * 8 + ar;
+    if (col < g.ncols) {
+      double* xc = Xb + (int64_t)col * g.ldx + 2 * ac;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) *reinterpret_cast<double2*>(xc + 8 * j) = make_double2(a2[j][0], a2[j][1]);
+    }
+    if constexpr (TWR > 0) {
+      // ---- TW^T = X^T V ----
+      double tw[RT][2];
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr) tw[jr][0] = tw[jr][1] = 0.0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int jr = 0; jr < RT; ++jr) {
+          const double2 v = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * PT + 8 * j + 2 * ac);
+          dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][0], v.x);
+          dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][1], v.y);
+        }
+      if (col < g.ncols) {
+        double* out = g.TW + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR + (int64_t)col * 2 * TWR + 2 * ac;
+#pragma unroll
+        for (int jr = 0; jr < RT; ++jr) *reinterpret_cast<double2*>(out + 8 * jr) = make_double2(tw[jr][0], tw[jr][1]);
+      }
+    }
+  }
+}
+
+template <int S, int TWR>
+static hodlr_status run_apply2(ApplyArgs g, cudaStream_t st) {
+  constexpr int PT = Apply2Cfg<S>::PT;
+  constexpr size_t smem = (size_t)(S + TWR) * PT * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tri_apply2_kernel<S, TWR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  // CTAs per block: one (8 warps over the block's column groups) unless the
+  // batch is too small to fill 2 CTAs per SM
+  const int G = (int)ceil_div(g.ncols, 8);
+  int cpb = 1;
+  while ((int64_t)g.batch * cpb < 2 * 148 && cpb * 8 < G) cpb *= 2;
+  g.groups = cpb;
+  const int64_t grid = (int64_t)g.batch * cpb;
+  if (grid > 2147483647LL) return HODLR_ERR_ARG;
+  tri_apply2_kernel<S, TWR><<<(unsigned)grid, AP_THREADS, smem, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+static bool apply2_ok(const ApplyArgs& g) {
+  // 16-byte X stores and 16-byte TW stores need even strides and aligned bases
+  return !(g.ldx & 1) && !(g.sX_hi & 1) && !(g.sX_lo & 1) && !(reinterpret_cast<uintptr_t>(g.X) & 15) &&
+         (g.TW == nullptr || (!(g.tw_stride & 1) && !(reinterpret_cast<uintptr_t>(g.TW) & 15)));
+}
+
+static int apply_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HODLR_APPLY_V1");
+    v = (e && atoi(e)) ? 1 : 2;
+  }
+  return v;
+}
+
 template <int S, int BN, int TWR>
 static hodlr_status run_apply(ApplyArgs g, cudaStream_t st) {
   constexpr size_t smem = (size_t)(S + (TWR > 0 ? 1 : 2) * BN + TWR) * (S + 4) * sizeof(double);
@@ -289,6 +470,12 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int6
   if (V) {
     if ((ldv & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15)) return HODLR_ERR_ARG;
     const bool nw = ncols <= 8;
+    if (apply_variant() == 2 && apply2_ok(g) && ncols > 8) {
+      if (s == 64 && twr == 32) return run_apply2<64, 32>(g, st);
+      if (s == 64 && twr == 16) return run_apply2<64, 16>(g, st);
+      if (s == 32 && twr == 16) return run_apply2<32, 16>(g, st);
+      if (s == 32 && twr == 32) return run_apply2<32, 32>(g, st);
+    }
     if (s == 64 && twr == 32) return nw ? run_apply<64, 8, 32>(g, st) : run_apply<64, 64, 32>(g, st);
     if (s == 64 && twr == 16) return nw ? run_apply<64, 8, 16>(g, st) : run_apply<64, 64, 16>(g, st);
     if (s == 32 && twr == 16) return run_apply<32, 64, 16>(g, st);
@@ -296,6 +483,10 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int6
     return HODLR_ERR_ARG;
   }
   const bool narrow = ncols <= 8;
+  if (apply_variant() == 2 && apply2_ok(g) && !narrow) {
+    if (s == 64) return run_apply2<64, 0>(g, st);
+    if (s == 32) return run_apply2<32, 0>(g, st);
+  }
   switch (s) {
     case 16: return run_apply<16, 64, 0>(g, st);
     case 32: return narrow ? run_apply<32, 8, 0>(g, st) : run_apply<32, 64, 0>(g, st);
