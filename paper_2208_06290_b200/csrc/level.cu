@@ -39,6 +39,12 @@ struct LevelArgs {
   int tpc;  // 64-column tiles per group
 };
 
+constexpr int64_t kMaxSegs = 1184;
+struct FactSched {
+  int64_t seg;
+  int ncg, tpc;
+};
+
 constexpr int LV_THREADS = 512;  // 16 warps: two per scheduler slot of each SMSP pair
 
 template <int R, int BN>
@@ -454,6 +460,214 @@ __global__ void __launch_bounds__(256, 2) level_update3_kernel(LevelArgs g) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Column-group variant for the factorization (no per-tile CTA barrier).
+// The CTA stages the A1 / V panels of a 64-row chunk (2-stage cp.async ring,
+// one barrier per chunk); every warp then streams its own column groups of 8
+// through the chunk, transposed so that no operand changes lanes:
+//
+//   C^T  += (-W'^T) A1^T   A: W' column entries (registers, from L2),
+//                          B: A1 panel (LDS.128 row pairs)
+//   TW^T +=  C^T V         A: the updated C^T accumulators themselves
+//
+// An m8n8k4 accumulator row of lane (ar, ac) holds n = 2ac + {0,1}; rows are
+// mapped as sigma(jn, n) = 16 (jn/2) + 2n + (jn%2), so a lane's 8 accumulator
+// values of a 16-row band are 4 consecutive rows of one column (one 32-byte
+// load / store per band) and every panel read is a conflict-free LDS.128.
+// [W|T] partial sums stay in registers (GPW groups per warp) for the whole
+// segment.
+// ---------------------------------------------------------------------------
+template <int R>
+struct Level4Cfg {
+  static constexpr int CH = 64;     // rows per chunk
+  static constexpr int P = CH + 2;  // [rank][row] pitch: 2P = 4 (mod 16) doubles
+  static constexpr int PANEL = R * P;
+  static constexpr int STAGE = 2 * PANEL;
+  static constexpr size_t SMEM = (size_t)2 * STAGE * sizeof(double);
+};
+
+__device__ __forceinline__ void ldg_v4(const double* p, double& x, double& y, double& z, double& w) {
+  asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];\n"
+               : "=d"(x), "=d"(y), "=d"(z), "=d"(w)
+               : "l"(p));
+}
+__device__ __forceinline__ void stg_v4(double* p, double x, double y, double z, double w) {
+  asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w)
+               : "memory");
+}
+
+template <int R, int GPW>
+__global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
+  using Cfg = Level4Cfg<R>;
+  constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8;
+  extern __shared__ __align__(16) double sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int seg = blockIdx.x / g.ncg, cg = blockIdx.x % g.ncg;
+  const int64_t seg0 = (int64_t)seg * g.seg_rows;
+  const int nch = g.seg_rows / CH;
+  const int G = g.ncols >> 3;
+  const int gb = cg * g.tpc, ge = min(G, gb + g.tpc);
+
+  auto stage = [&](int ch, int s) {
+    double* As = sm + s * Cfg::STAGE;
+    double* Vs = As + Cfg::PANEL;
+    const double* a1 = g.A1 + seg0 + (int64_t)ch * CH;
+    const double* v1 = g.V + seg0 + (int64_t)ch * CH;
+    static_assert((R * (CH / 2)) % 256 == 0, "panel split");
+#pragma unroll
+    for (int q = 0; q < R * (CH / 2) / 256; ++q) {
+      const int idx = t + q * 256;
+      const int k = idx / (CH / 2), m = (idx % (CH / 2)) * 2;
+      cp_async_16(As + k * P + m, a1 + m + (int64_t)k * g.lda, 16);
+      cp_async_16(Vs + k * P + m, v1 + m + (int64_t)k * g.lda, 16);
+    }
+  };
+
+  double tw[GPW][RT][2];
+#pragma unroll
+  for (int q = 0; q < GPW; ++q)
+#pragma unroll
+    for (int jr = 0; jr < RT; ++jr) tw[q][jr][0] = tw[q][jr][1] = 0.0;
+
+  if (nch > 0) stage(0, 0);
+  cp_async_commit();
+  for (int ch = 0; ch < nch; ++ch) {
+    const int s = ch & 1;
+    if (ch + 1 < nch) stage(ch + 1, s ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* As = sm + s * Cfg::STAGE;
+    const double* Vs = As + Cfg::PANEL;
+    const int64_t row0 = seg0 + (int64_t)ch * CH;
+    const int c = (int)(row0 / g.n_c);
+    const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
+#pragma unroll
+    for (int q = 0; q < GPW; ++q) {
+      const int grp = gb + warp + 8 * q;
+      if (grp < ge) {
+        const int col = grp * 8 + ar;
+        double* cptr = g.C + row0 + (int64_t)col * g.ldc + 4 * ac;
+        double acc[8][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+        const double* wc = Wp + (int64_t)col * (2 * R) + 2 * ac;
+        // ---- C^T += (-W'^T) A1^T ----
+#pragma unroll
+        for (int kt = 0; kt < R / 8; ++kt) {
+          const double2 w2 = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const double a = -(u ? w2.y : w2.x);
+            const double* ak = As + (8 * kt + 2 * ac + u) * P + 2 * ar;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const double2 b2 = *reinterpret_cast<const double2*>(ak + 16 * i);
+              dmma_8x8x4(acc[2 * i][0], acc[2 * i][1], a, b2.x);
+              dmma_8x8x4(acc[2 * i + 1][0], acc[2 * i + 1][1], a, b2.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+        // ---- TW^T += C^T V ----
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int jr = 0; jr < RT; ++jr) {
+              const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
+              dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i][h], v2.x);
+              dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i + 1][h], v2.y);
+            }
+      }
+    }
+    __syncthreads();
+  }
+  // tw[q][jr][h] = TW^T[col][rank 8 jr + 2 ac + h]
+  const int64_t qn = seg0 / g.node_rows;
+  double* out;
+  int64_t ld;
+  if (g.partial) {
+    out = g.TW + (int64_t)seg * R * g.ncols;
+    ld = R;
+  } else {
+    out = g.TW + (qn >> 1) * g.tw_stride + (qn & 1) * R;
+    ld = 2 * R;
+  }
+#pragma unroll
+  for (int q = 0; q < GPW; ++q) {
+    const int grp = gb + warp + 8 * q;
+    if (grp < ge) {
+      const int col = grp * 8 + ar;
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr)
+        *reinterpret_cast<double2*>(out + 8 * jr + 2 * ac + (int64_t)col * ld) = make_double2(tw[q][jr][0], tw[q][jr][1]);
+    }
+  }
+}
+
+template <int R, int GPW>
+static hodlr_status launch_level4(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
+  using Cfg = Level4Cfg<R>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(level_update4_kernel<R, GPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    attr = true;
+  }
+  level_update4_kernel<R, GPW><<<(unsigned)(nseg * g.ncg), 256, Cfg::SMEM, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+template <int R>
+static hodlr_status run_level4(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
+  const int gpw = (g.tpc + 7) / 8;
+  if (gpw <= 1) return launch_level4<R, 1>(g, nseg, st);
+  if (gpw <= 2) return launch_level4<R, 2>(g, nseg, st);
+  if (gpw <= 4) return launch_level4<R, 4>(g, nseg, st);
+  if constexpr (R <= 16) {
+    if (gpw <= 7) return launch_level4<R, 7>(g, nseg, st);
+  }
+  return HODLR_ERR_ARG;
+}
+
+// Schedule for level_update4: work item = (row segment, range of column
+// groups of 8); at most maxg groups per CTA (the [W|T] partials live in registers).
+static FactSched level4_schedule(int64_t n, int64_t node, int G, int sms, int maxg) {
+  const int64_t slots = 2 * (int64_t)sms;
+  FactSched best{node, 0, 0};
+  double best_cost = 1e300;
+  for (int64_t seg = node; seg >= 64; seg >>= 1) {
+    const int64_t nseg = n / seg;
+    if (seg < node && nseg > kMaxSegs) break;
+    for (int ncg = 1; ncg <= G; ++ncg) {
+      const int gpc = (G + ncg - 1) / ncg;
+      if ((ncg - 1) * gpc >= G || gpc > maxg) continue;
+      const double waves = (double)ceil_div(nseg * ncg, slots);
+      double cost = waves * ((double)(seg / 64) * ((gpc + 7) / 8) + 0.5);
+      if (seg < node) cost *= 1.05;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = {seg, ncg, gpc};
+      }
+    }
+    if (seg % 128) break;
+  }
+  return best;
+}
+
+static int level_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HODLR_LEVEL_V");
+    v = e ? atoi(e) : 4;
+  }
+  return v;
+}
+
 static int level_pf() {
   static int v = -1;
   if (v < 0) {
@@ -519,11 +733,6 @@ int64_t level_segment_rows(int64_t n, int64_t node, int sms) {
 // Minimises (waves of 2 CTAs/SM) x (64x64 tiles per CTA + pipeline fill),
 // splitting a node's rows (partial [W|T] sums) only when that wins by > 5%,
 // and never into more than kMaxSegs segments (bounds the partial workspace).
-constexpr int64_t kMaxSegs = 1184;
-struct FactSched {
-  int64_t seg;
-  int ncg, tpc;
-};
 static FactSched level_fact_schedule(int64_t n, int64_t node, int ntile, int sms) {
   const int64_t slots = 2 * (int64_t)sms;
   FactSched best{node, 1, ntile};
@@ -580,7 +789,11 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   const bool fact = V != nullptr && reg_resident && ncols > 8;
   const int ntile = (int)ceil_div(ncols, 64);
   FactSched fs{level_segment_rows(n, node, sm_count()), 1, ntile};
-  if (fact) fs = level_fact_schedule(n, node, ntile, sm_count());
+  // column-group kernel: 16 or more groups of 8, 32-byte aligned C columns
+  const bool v4 = fact && level_variant() == 4 && ncols % 8 == 0 && ncols / 8 >= 16 && !(ldc & 3) &&
+                  !(reinterpret_cast<uintptr_t>(C) & 31);
+  if (v4) fs = level4_schedule(n, node, ncols / 8, sm_count(), r <= 16 ? 56 : 32);
+  else if (fact) fs = level_fact_schedule(n, node, ntile, sm_count());
   const int64_t seg = fs.seg;
   const int64_t nseg = n / seg;
   if (nseg * fs.ncg > 2147483647LL) return HODLR_ERR_ARG;
@@ -591,8 +804,8 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   const bool small = ncols <= 8;
   hodlr_status s;
   switch (r) {
-    case 16: s = small ? run_level<16, 8>(g, nseg, st) : (fact ? run_level3<16>(g, nseg, st) : run_level<16, 64>(g, nseg, st)); break;
-    case 32: s = small ? run_level<32, 8>(g, nseg, st) : (fact ? run_level3<32>(g, nseg, st) : run_level<32, 64>(g, nseg, st)); break;
+    case 16: s = small ? run_level<16, 8>(g, nseg, st) : v4 ? run_level4<16>(g, nseg, st) : (fact ? run_level3<16>(g, nseg, st) : run_level<16, 64>(g, nseg, st)); break;
+    case 32: s = small ? run_level<32, 8>(g, nseg, st) : v4 ? run_level4<32>(g, nseg, st) : (fact ? run_level3<32>(g, nseg, st) : run_level<32, 64>(g, nseg, st)); break;
     default: return HODLR_ERR_ARG;  // r = 64: generic path (fused tiles exceed shared memory)
   }
   if (s != HODLR_OK || !split) return s;
