@@ -496,7 +496,7 @@ __device__ __forceinline__ void stg_v4(double* p, double x, double y, double z, 
                : "memory");
 }
 
-template <int R, int GPW>
+template <int R, int GPW, bool LATE>
 __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
   using Cfg = Level4Cfg<R>;
   constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8;
@@ -549,9 +549,17 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
       if (grp < ge) {
         const int col = grp * 8 + ar;
         double* cptr = g.C + row0 + (int64_t)col * g.ldc + 4 * ac;
-        double acc[8][2];
+        double acc[8][2], cin[8][2];
+        if constexpr (LATE) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+          for (int i = 0; i < 4; ++i) {
+            ldg_v4(cptr + 16 * i, cin[2 * i][0], cin[2 * i + 1][0], cin[2 * i][1], cin[2 * i + 1][1]);
+            acc[2 * i][0] = acc[2 * i][1] = acc[2 * i + 1][0] = acc[2 * i + 1][1] = 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+        }
         const double* wc = Wp + (int64_t)col * (2 * R) + 2 * ac;
         // ---- C^T += (-W'^T) A1^T ----
 #pragma unroll
@@ -568,6 +576,10 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
               dmma_8x8x4(acc[2 * i + 1][0], acc[2 * i + 1][1], a, b2.y);
             }
           }
+        }
+        if constexpr (LATE) {  // C - (A1 W'): the load latency hides behind the update products
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i][0] = cin[i][0] + acc[i][0], acc[i][1] = cin[i][1] + acc[i][1];
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
@@ -612,12 +624,13 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
 template <int R, int GPW>
 static hodlr_status launch_level4(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
   using Cfg = Level4Cfg<R>;
+  constexpr bool LATE = GPW <= 2;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(level_update4_kernel<R, GPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaFuncSetAttribute(level_update4_kernel<R, GPW, LATE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     attr = true;
   }
-  level_update4_kernel<R, GPW><<<(unsigned)(nseg * g.ncg), 256, Cfg::SMEM, st>>>(g);
+  level_update4_kernel<R, GPW, LATE><<<(unsigned)(nseg * g.ncg), 256, Cfg::SMEM, st>>>(g);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
@@ -666,6 +679,15 @@ static int level_variant() {
     v = e ? atoi(e) : 4;
   }
   return v;
+}
+
+static int level4_maxg(int r) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HODLR_LEVEL4_MAXG");
+    v = e ? atoi(e) : 0;
+  }
+  return v > 0 ? v : (r <= 16 ? 56 : 32);
 }
 
 static int level_pf() {
@@ -792,7 +814,7 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   // column-group kernel: 16 or more groups of 8, 32-byte aligned C columns
   const bool v4 = fact && level_variant() == 4 && ncols % 8 == 0 && ncols / 8 >= 16 && !(ldc & 3) &&
                   !(reinterpret_cast<uintptr_t>(C) & 31);
-  if (v4) fs = level4_schedule(n, node, ncols / 8, sm_count(), r <= 16 ? 56 : 32);
+  if (v4) fs = level4_schedule(n, node, ncols / 8, sm_count(), level4_maxg(r));
   else if (fact) fs = level_fact_schedule(n, node, ntile, sm_count());
   const int64_t seg = fs.seg;
   const int64_t nseg = n / seg;
