@@ -812,7 +812,7 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   const int ntile = (int)ceil_div(ncols, 64);
   FactSched fs{level_segment_rows(n, node, sm_count()), 1, ntile};
   // column-group kernel: 16 or more groups of 8, 32-byte aligned C columns
-  const bool v4 = fact && level_variant() == 4 && ncols % 8 == 0 && ncols / 8 >= 16 && !(ldc & 3) &&
+  const bool v4 = fact && level_variant() == 4 && ncols % 8 == 0 && ncols / 8 >= 8 && !(ldc & 3) &&
                   !(reinterpret_cast<uintptr_t>(C) & 31);
   if (v4) fs = level4_schedule(n, node, ncols / 8, sm_count(), level4_maxg(r));
   else if (fact) fs = level_fact_schedule(n, node, ntile, sm_count());
