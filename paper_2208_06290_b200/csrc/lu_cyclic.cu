@@ -18,6 +18,8 @@
 // recursive doubling: 8x8 diagonal blocks are inverted per thread-row, and each
 // doubling step X = -A^-1 U_AB B^-1 (resp. X = -B^-1 C A^-1) is two small DMMA
 // GEMMs.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hodlr {
@@ -572,6 +574,222 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-row LU (fp64, S in {32, 64}): thread t owns row t of the block in
+// registers for the whole factorization (the trailing update never touches
+// shared memory for its own operands).  Same IEEE operation sequence per
+// element as backend.py:444-478 (see getrf_sr_kernel).  One barrier per step:
+// every warp publishes the row of its own argmax winner (parity-buffered)
+// together with its key, so after the barrier each thread reads the global
+// pivot row straight from the winning warp's slot.  Steps run in chunks of 8
+// (unrolled), so register columns are compile-time indices; column blocks left
+// of the current chunk are skipped with warp-uniform branches.  The packed
+// triangular inverses are formed by a separate kernel (trtri_sm_kernel).
+// ---------------------------------------------------------------------------
+template <int S>
+__global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode, const double* __restrict__ src,
+                                                                      int64_t lds, int64_t strides, double* out,
+                                                                      int64_t ldo, int64_t strideo,
+                                                                      int32_t* __restrict__ swaps,
+                                                                      int32_t* __restrict__ perm,
+                                                                      int32_t* __restrict__ info) {
+  constexpr int NW = S / 32, NB = S / 8, RP = S + 1;
+  __shared__ double A[S * RP];                     // staging (row-major, odd pitch)
+  __shared__ __align__(16) double urow[2][NW][S];  // per-warp candidate pivot rows
+  __shared__ double cmax[S];
+  __shared__ unsigned redh[2][NW], redl[2][NW];
+  __shared__ int redp[2][NW];
+  __shared__ int swk[S];
+  __shared__ int sflag;
+
+  const int64_t blk = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const double* g = src + blk * strides;
+  // ---- stage: coalesced column reads -> row-major smem ----
+  for (int idx = t; idx < S * S; idx += S) {
+    const int i = idx % S, j = idx / S;
+    double v;
+    if (mode == 0) {
+      v = g[i + (int64_t)j * lds];
+    } else {
+      constexpr int R = S / 2;
+      if (i < R && j < R)
+        v = g[i + (int64_t)j * lds];
+      else if (i >= R && j >= R)
+        v = g[i + (int64_t)(j - R) * lds];
+      else
+        v = (i < R) ? (double)(i == j - R) : (double)(i - R == j);
+    }
+    A[i * RP + j] = v;
+  }
+  if (t == 0) sflag = 0;
+  __syncthreads();
+  {  // thread t: max |a_it| over the original column t (NaN-propagating)
+    double m0 = 0.0, m1 = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < S; i += 2) {
+      m0 = cyc_nanmax(m0, fabs(A[i * RP + t]));
+      m1 = cyc_nanmax(m1, fabs(A[(i + 1) * RP + t]));
+    }
+    cmax[t] = cyc_nanmax(m0, m1);
+  }
+  double a[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) a[j] = A[t * RP + j];
+  __syncthreads();  // cmax visible
+
+  const double thr_scale = mul_rn(Eps<double>::v, (double)S);
+  int pos = t;
+  bool active = true;
+  for (int kb = 0; kb < NB; ++kb) {
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k = 8 * kb + kk;
+      const int par = k & 1;
+      // a[k] with k = 8 kb + kk (kb runtime): select over the column blocks
+      double ak = a[kk];
+#pragma unroll
+      for (int jb = 1; jb < NB; ++jb) ak = csel(kb == jb, a[8 * jb + kk], ak);
+      unsigned kh = 0u, kl = 0u;
+      int pv = 0x7fffffff;  // (position << 8) | thread: unique, orders by position
+      if (active) {
+        abs_key(ak, kh, kl);
+        pv = (pos << 8) | t;
+      }
+      warp_argmax(kh, kl, pv);
+      // the warp's winner publishes its row (columns >= the current block)
+      if (pv != 0x7fffffff && (pv & 255) == t) {
+        double* ur = urow[par][warp];
+#pragma unroll
+        for (int jb = 0; jb < NB; ++jb)
+          if (jb >= kb) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              *reinterpret_cast<double2*>(ur + 8 * jb + 2 * q) = make_double2(a[8 * jb + 2 * q], a[8 * jb + 2 * q + 1]);
+          }
+      }
+      if (lane == 0) {
+        redh[par][warp] = kh;
+        redl[par][warp] = kl;
+        redp[par][warp] = pv;
+      }
+      __syncthreads();
+      int ww = 0;
+      if (NW > 1) {
+        kh = redh[par][0];
+        kl = redl[par][0];
+        pv = redp[par][0];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+          const unsigned h2 = redh[par][w], l2 = redl[par][w];
+          const int p2 = redp[par][w];
+          if (h2 > kh || (h2 == kh && (l2 > kl || (l2 == kl && p2 < pv)))) {
+            kh = h2;
+            kl = l2;
+            pv = p2;
+            ww = w;
+          }
+        }
+      }
+      const int pt = pv & 255;
+      pv >>= 8;
+      const double* u = urow[par][ww];
+      const double piv = u[k];
+      if (t == 0) {
+        swk[k] = pv;
+        if (fabs(piv) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
+      }
+      if (pos == k) pos = pv;
+      if (t == pt) {
+        pos = k;
+        active = false;
+      }
+      if (active) {
+        const double d = (piv == 0.0) ? 1.0 : piv;
+        const double l = (ak == 0.0 && d == d) ? ((signbit(ak) != signbit(d)) ? -0.0 : 0.0) : div_rn(ak, d);
+#pragma unroll
+        for (int jb = 0; jb < NB; ++jb) {
+          if (jb == kb) {
+            a[8 * jb + kk] = l;
+#pragma unroll
+            for (int jj = kk + 1; jj < 8; ++jj) a[8 * jb + jj] = sub_rn(a[8 * jb + jj], mul_rn(l, u[8 * jb + jj]));
+          } else if (jb > kb) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double2 uu = *reinterpret_cast<const double2*>(u + 8 * jb + 2 * q);
+              a[8 * jb + 2 * q] = sub_rn(a[8 * jb + 2 * q], mul_rn(l, uu.x));
+              a[8 * jb + 2 * q + 1] = sub_rn(a[8 * jb + 2 * q + 1], mul_rn(l, uu.y));
+            }
+          }
+        }
+      }
+    }
+  }
+  // ---- outputs: rows to their logical positions (through smem), pivots, flag ----
+#pragma unroll
+  for (int j = 0; j < S; ++j) A[pos * RP + j] = a[j];
+  perm[blk * S + pos] = t;
+  __syncthreads();
+  double* o = out + blk * strideo;
+  for (int idx = t; idx < S * S; idx += S) {
+    const int i = idx % S, j = idx / S;
+    o[i + (int64_t)j * ldo] = A[i * RP + j];
+  }
+  swaps[blk * S + t] = swk[t];
+  if (t == 0) info[blk] = sflag;
+}
+
+// Packed triangular inverses of already-factored blocks (L2-hot right after
+// getrf_reg_kernel): stage column-major, packed_trtri, store.
+template <int S>
+__global__ void __launch_bounds__(128) trtri_sm_kernel(const double* __restrict__ LU, int64_t ldl, int64_t stridel,
+                                                       double* __restrict__ tinv, int64_t ldi, int64_t stridei) {
+  constexpr int P = S + 4;
+  extern __shared__ __align__(16) unsigned char tr_smem[];
+  double* Tm = reinterpret_cast<double*>(tr_smem);
+  double* Tt = Tm + S * P;
+  const int64_t blk = blockIdx.x;
+  const double* l = LU + blk * stridel;
+  for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) {
+    const int i = idx % S, j = idx / S;
+    Tm[i + j * P] = l[i + (int64_t)j * ldl];
+  }
+  __syncthreads();
+  packed_trtri<double, S>(Tm, Tt, P);
+  double* ti = tinv + blk * stridei;
+  for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) {
+    const int i = idx % S, j = idx / S;
+    ti[i + (int64_t)j * ldi] = Tm[i + j * P];
+  }
+}
+
+template <int S>
+static hodlr_status run_reg(int batch, int mode, const double* src, int64_t lds, int64_t strides, double* out,
+                            int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, double* tinv,
+                            int64_t ldi, int64_t stridei, cudaStream_t st) {
+  getrf_reg_kernel<S><<<batch, S, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info);
+  HODLR_CHECK_LAUNCH();
+  if (tinv == nullptr) return HODLR_OK;
+  constexpr size_t smem = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(trtri_sm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  trtri_sm_kernel<S><<<batch, 128, smem, st>>>(out, ldo, strideo, tinv, ldi, stridei);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+static int lu_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HODLR_LU_SR");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v;
+}
+
 template <typename T, int S>
 static hodlr_status run_sr(int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
                            int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
@@ -614,8 +832,14 @@ hodlr_status launch_getrf_cyclic(int s, int batch, int mode, const T* src, int64
                                  int64_t ldi, int64_t stridei, cudaStream_t st) {
   switch (s) {
     case 16: return run_sr<T, 16>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
-    case 32: return run_sr<T, 32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
-    case 64: return run_sr<T, 64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 32:
+      if constexpr (sizeof(T) == 8)
+        if (lu_variant() && batch >= 2048) return run_reg<32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+      return run_sr<T, 32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+    case 64:
+      if constexpr (sizeof(T) == 8)
+        if (lu_variant() && batch >= 2048) return run_reg<64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+      return run_sr<T, 64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     case 128: return run_sr<T, 128>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     default: return HODLR_ERR_ARG;
   }
