@@ -399,6 +399,127 @@ __global__ void __launch_bounds__(AP_THREADS, 2) tri_apply2_kernel(ApplyArgs g) 
   }
 }
 
+static bool apply2_ok(const ApplyArgs& g) {
+  // 16-byte X stores and 16-byte TW stores need even strides and aligned bases
+  return !(g.ldx & 1) && !(g.sX_hi & 1) && !(g.sX_lo & 1) && !(reinterpret_cast<uintptr_t>(g.X) & 15) &&
+         (g.TW == nullptr || (!(g.tw_stride & 1) && !(reinterpret_cast<uintptr_t>(g.TW) & 15)));
+}
+
+static int apply_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HODLR_APPLY_V1");
+    v = (e && atoi(e)) ? 1 : 2;
+  }
+  return v;
+}
+
+// Narrow variant (ncols <= 8, the solve phase): one warp per block, the same
+// DMMA instruction sequence per column as tri_apply2_kernel (so a column of a
+// multi-RHS solve is bit-identical to the single-vector solve), with the
+// packed inverses, the permutation and the V panel read straight from global
+// memory into fragments -- the phase is a single HBM pass over Tinv / V.
+template <int S, int TWR>
+__global__ void __launch_bounds__(AP_THREADS) tri_apply_narrow_kernel(ApplyArgs g) {
+  constexpr int NJ = S / 8, RT = TWR / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x * (AP_THREADS / 32) + warp;
+  if (b >= g.batch) return;
+  const int ar = lane >> 2, ac = lane & 3;
+  const double* ti = g.tinv + (int64_t)b * g.strideT;
+  const int32_t* pmb = g.perm + (int64_t)b * S;
+  const double* Bb = g.B + aoff(b, g.bdiv, g.sB_hi, g.sB_lo);
+  double* Xb = g.X + aoff(b, g.bdiv, g.sX_hi, g.sX_lo);
+  const int col = ar;
+  const bool ok = col < g.ncols;
+  double bv[NJ][2];
+  {
+    const double* bc = Bb + (int64_t)(ok ? col : 0) * g.ldb;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int2 p = __ldg(reinterpret_cast<const int2*>(pmb + 8 * j + 2 * ac));
+      bv[j][0] = ok ? bc[p.x] : 0.0;
+      bv[j][1] = ok ? bc[p.y] : 0.0;
+    }
+  }
+  // Tinv[row][k] = ti[row + k * ldi]
+  auto tl = [&](int jn, int j) {
+    const double* q = ti + (8 * jn + ar) + (int64_t)(8 * j + 2 * ac) * g.ldi;
+    return make_double2(__ldg(q), __ldg(q + g.ldi));
+  };
+  double a1[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) a1[j][0] = a1[j][1] = 0.0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+    for (int jn = j; jn < NJ; ++jn) {
+      double2 l = tl(jn, j);
+      if (jn == j) {
+        const int k0 = 2 * ac;
+        l.x = k0 < ar ? l.x : (k0 == ar ? 1.0 : 0.0);
+        l.y = k0 + 1 < ar ? l.y : (k0 + 1 == ar ? 1.0 : 0.0);
+      }
+      dmma_8x8x4(a1[jn][0], a1[jn][1], bv[j][0], l.x);
+      dmma_8x8x4(a1[jn][0], a1[jn][1], bv[j][1], l.y);
+    }
+  }
+  double a2[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) a2[j][0] = a2[j][1] = 0.0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+    for (int jn = 0; jn <= j; ++jn) {
+      double2 u = tl(jn, j);
+      if (jn == j) {
+        const int k0 = 2 * ac;
+        u.x = k0 >= ar ? u.x : 0.0;
+        u.y = k0 + 1 >= ar ? u.y : 0.0;
+      }
+      dmma_8x8x4(a2[jn][0], a2[jn][1], a1[j][0], u.x);
+      dmma_8x8x4(a2[jn][0], a2[jn][1], a1[j][1], u.y);
+    }
+  }
+  if (ok) {
+    double* xc = Xb + (int64_t)col * g.ldx + 2 * ac;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) *reinterpret_cast<double2*>(xc + 8 * j) = make_double2(a2[j][0], a2[j][1]);
+  }
+  if constexpr (TWR > 0) {
+    const double* vb = g.V + (int64_t)b * g.vstride;
+    double tw[RT][2];
+#pragma unroll
+    for (int jr = 0; jr < RT; ++jr) tw[jr][0] = tw[jr][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(vb + (int64_t)(8 * jr + ar) * g.ldv + 8 * j + 2 * ac));
+        dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][0], v.x);
+        dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][1], v.y);
+      }
+    if (ok) {
+      double* out = g.TW + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR + (int64_t)col * 2 * TWR + 2 * ac;
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr) *reinterpret_cast<double2*>(out + 8 * jr) = make_double2(tw[jr][0], tw[jr][1]);
+    }
+  }
+}
+
+template <int S, int TWR>
+static hodlr_status run_apply_narrow(ApplyArgs g, cudaStream_t st) {
+  const int64_t grid = ceil_div(g.batch, AP_THREADS / 32);
+  tri_apply_narrow_kernel<S, TWR><<<(unsigned)grid, AP_THREADS, 0, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+static bool apply_narrow_ok(const ApplyArgs& g) {
+  // 16-byte B/X/V/TW accesses of the narrow kernel
+  return apply2_ok(g) && !(g.ldi & 1) && (g.V == nullptr || (!(g.ldv & 1) && !(g.vstride & 1)));
+}
+
 template <int S, int TWR>
 static hodlr_status run_apply2(ApplyArgs g, cudaStream_t st) {
   constexpr int PT = Apply2Cfg<S>::PT;
@@ -421,20 +542,6 @@ static hodlr_status run_apply2(ApplyArgs g, cudaStream_t st) {
   return HODLR_OK;
 }
 
-static bool apply2_ok(const ApplyArgs& g) {
-  // 16-byte X stores and 16-byte TW stores need even strides and aligned bases
-  return !(g.ldx & 1) && !(g.sX_hi & 1) && !(g.sX_lo & 1) && !(reinterpret_cast<uintptr_t>(g.X) & 15) &&
-         (g.TW == nullptr || (!(g.tw_stride & 1) && !(reinterpret_cast<uintptr_t>(g.TW) & 15)));
-}
-
-static int apply_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_APPLY_V1");
-    v = (e && atoi(e)) ? 1 : 2;
-  }
-  return v;
-}
 
 template <int S, int BN, int TWR>
 static hodlr_status run_apply(ApplyArgs g, cudaStream_t st) {
@@ -470,6 +577,12 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int6
   if (V) {
     if ((ldv & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15)) return HODLR_ERR_ARG;
     const bool nw = ncols <= 8;
+    if (apply_variant() == 2 && nw && apply_narrow_ok(g)) {
+      if (s == 64 && twr == 32) return run_apply_narrow<64, 32>(g, st);
+      if (s == 64 && twr == 16) return run_apply_narrow<64, 16>(g, st);
+      if (s == 32 && twr == 16) return run_apply_narrow<32, 16>(g, st);
+      if (s == 32 && twr == 32) return run_apply_narrow<32, 32>(g, st);
+    }
     if (apply_variant() == 2 && apply2_ok(g) && ncols > 8) {
       if (s == 64 && twr == 32) return run_apply2<64, 32>(g, st);
       if (s == 64 && twr == 16) return run_apply2<64, 16>(g, st);
@@ -483,6 +596,10 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int6
     return HODLR_ERR_ARG;
   }
   const bool narrow = ncols <= 8;
+  if (apply_variant() == 2 && narrow && apply_narrow_ok(g)) {
+    if (s == 64) return run_apply_narrow<64, 0>(g, st);
+    if (s == 32) return run_apply_narrow<32, 0>(g, st);
+  }
   if (apply_variant() == 2 && apply2_ok(g) && !narrow) {
     if (s == 64) return run_apply2<64, 0>(g, st);
     if (s == 32) return run_apply2<32, 0>(g, st);

@@ -27,6 +27,11 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
                               int ncols, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
                               cudaStream_t st, bool reg_resident);
 size_t level_partial_bytes(int64_t n, int m, int r, int L);
+size_t solve_level_partial_bytes(int64_t n, int r, int nrhs);
+hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, double* X, int64_t ldx,
+                             const double* A1, const double* V, int64_t lda, const double* W, int64_t wstride,
+                             int nrhs, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
+                             cudaStream_t st);
 int64_t level_segment_rows(int64_t n, int64_t node, int sms);
 template <typename T>
 hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
@@ -241,7 +246,7 @@ extern "C" size_t hodlr_factorize_local_workspace(const hodlr_desc* d, int64_t n
 }
 
 static size_t solve_part_bytes(const hodlr_desc* d, int nrhs) {
-  return align_up(sizeof(double) * (size_t)4 * 148 * d->r * nrhs);
+  return align_up(std::max(sizeof(double) * (size_t)4 * 148 * d->r * nrhs, solve_level_partial_bytes(d->n, d->r, nrhs)));
 }
 
 extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
@@ -499,9 +504,13 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
     hodlr_status s;
     {
       Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
-      s = level_update_f64(r, n, nc, 2 * nc, X, ldx, Y + (int64_t)lv * r * n,
-                           lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
-                           (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st, false);
+      s = solve_level_f64(r, n, nc, 2 * nc, X, ldx, Y + (int64_t)lv * r * n,
+                          lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
+                          (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st);
+      if (s == HODLR_ERR_ARG)
+        s = level_update_f64(r, n, nc, 2 * nc, X, ldx, Y + (int64_t)lv * r * n,
+                             lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
+                             (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st, false);
     }
     if (s == HODLR_OK) {
       w_ready = lv > 0;
@@ -582,9 +591,13 @@ extern "C" hodlr_status hodlr_solve_top(const hodlr_desc* d, const hodlr_factors
   const double* V = (const double*)f->V;
   double* X = (double*)Xv;
   Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
-  hodlr_status s = level_update_f64(r, n, nc, n, X, ldx, Y + (int64_t)lv * r * n,
-                                    lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2 + half * r, 0, nrhs, w, 0,
-                                    part, solve_part_bytes(d, nrhs), st, false);
+  hodlr_status s = solve_level_f64(r, n, nc, n, X, ldx, Y + (int64_t)lv * r * n,
+                                   lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2 + half * r, 0, nrhs, w, 0,
+                                   part, solve_part_bytes(d, nrhs), st);
+  if (s == HODLR_ERR_ARG)
+    s = level_update_f64(r, n, nc, n, X, ldx, Y + (int64_t)lv * r * n,
+                         lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2 + half * r, 0, nrhs, w, 0, part,
+                         solve_part_bytes(d, nrhs), st, false);
   if (s == HODLR_OK) {
     if (lv > 0 && w_out &&
         cudaMemcpy2DAsync(w_out, sizeof(double) * r, w, sizeof(double) * 2 * r, sizeof(double) * r, nrhs,

@@ -45,6 +45,17 @@ struct FactSched {
   int ncg, tpc;
 };
 
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 constexpr int LV_THREADS = 512;  // 16 warps: two per scheduler slot of each SMSP pair
 
 template <int R, int BN>
@@ -225,16 +236,33 @@ __global__ void __launch_bounds__(LV_THREADS) level_update_kernel(LevelArgs g) {
 }
 
 // TW_q = sum over the q's segments of the partials, fixed order; paired output.
+// Few segments: one thread per output, sequential.  Many segments (top
+// levels): one warp per output, lane l sums segments l, l+32, ... in order,
+// then a fixed xor-butterfly.  The order depends only on the segment count.
 __global__ void level_reduce_kernel(const double* part, double* TW, int R, int ncols, int segs_per_node, int nnodes,
                                     int64_t tw_stride) {
   const int64_t per = (int64_t)R * ncols;
   const int64_t total = per * nnodes;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+  if (segs_per_node <= 32) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t q = e / per, mn = e % per;
+      const int m = (int)(mn % R), n = (int)(mn / R);
+      double s = 0.0;
+      for (int k = 0; k < segs_per_node; ++k) s += part[(q * segs_per_node + k) * per + mn];
+      TW[(q >> 1) * tw_stride + (q & 1) * R + m + (int64_t)n * 2 * R] = s;
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t e = blockIdx.x * wpb + (threadIdx.x >> 5); e < total; e += (int64_t)gridDim.x * wpb) {
     const int64_t q = e / per, mn = e % per;
     const int m = (int)(mn % R), n = (int)(mn / R);
     double s = 0.0;
-    for (int k = 0; k < segs_per_node; ++k) s += part[(q * segs_per_node + k) * per + mn];
-    TW[(q >> 1) * tw_stride + (q & 1) * R + m + (int64_t)n * 2 * R] = s;
+    for (int k = lane; k < segs_per_node; k += 32) s += part[(q * segs_per_node + k) * per + mn];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) TW[(q >> 1) * tw_stride + (q & 1) * R + m + (int64_t)n * 2 * R] = s;
   }
 }
 
@@ -672,6 +700,162 @@ static FactSched level4_schedule(int64_t n, int64_t node, int G, int sms, int ma
   return best;
 }
 
+// ---------------------------------------------------------------------------
+// Solve level step (PAPER Alg. 4 l.7 fused with l.5 of the next level), any
+// nrhs: x(I_c, :) -= Y_c^{l+1} w'_c, then the chunk's contribution to the next
+// level's w = V^{(l)T} x.  One warp per 64-row chunk, 8 chunks (512 rows) per
+// CTA; the HBM-bound panels (Y^{l+1}, V^{(l)}) are read straight from global
+// memory into DMMA fragments (16-byte loads, no shared-memory staging), and
+// the right-hand sides are swept in groups of 8 columns.  Every column is
+// computed by the same instruction sequence whatever nrhs is, and the w
+// reduction order is fixed (chunk partials summed in row order inside a CTA,
+// CTA partials summed in row order by level_reduce_kernel), so a column of a
+// multi-RHS solve is bit-identical to the single-vector solve.
+// Fragment / row mapping as in level_update4_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kSolveCtaRows = 512;
+
+template <int R>
+__global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
+  constexpr int RT = R / 8;
+  __shared__ double ps[8][R * 8];  // chunk partials of the current column group: [chunk][rank + 8? ]
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int64_t cta0 = (int64_t)blockIdx.x * g.seg_rows;
+  const int nchunk = g.seg_rows / 64;
+  const int64_t row0 = cta0 + 64 * warp;
+  const bool has_chunk = warp < nchunk;
+  const int c = has_chunk ? (int)(row0 / g.n_c) : 0;
+  const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
+  const bool want_w = g.V != nullptr;
+  const int G = (g.ncols + 7) >> 3;
+  for (int grp = 0; grp < G; ++grp) {
+    const int col = grp * 8 + ar;
+    const bool ok = col < g.ncols;
+    if (has_chunk) {
+      double acc[8][2];
+      double* xp = g.C + row0 + (int64_t)(ok ? col : 0) * g.ldc + 4 * ac;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (ok) {
+          ldg_v4(xp + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+        } else {
+          acc[2 * i][0] = acc[2 * i + 1][0] = acc[2 * i][1] = acc[2 * i + 1][1] = 0.0;
+        }
+      }
+      const double* wc = Wp + (int64_t)(ok ? col : 0) * (2 * R) + 2 * ac;
+      const double* a1 = g.A1 + row0 + 2 * ar;
+      // ---- x^T += (-w'^T) Y^T ----
+#pragma unroll
+      for (int kt = 0; kt < R / 8; ++kt) {
+        double2 w2 = make_double2(0.0, 0.0);
+        if (ok) w2 = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const double a = -(u ? w2.y : w2.x);
+          const double* ak = a1 + (int64_t)(8 * kt + 2 * ac + u) * g.lda;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double2 b2 = __ldcs(reinterpret_cast<const double2*>(ak + 16 * i));
+            dmma_8x8x4(acc[2 * i][0], acc[2 * i][1], a, b2.x);
+            dmma_8x8x4(acc[2 * i + 1][0], acc[2 * i + 1][1], a, b2.y);
+          }
+        }
+      }
+      if (ok) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) stg_v4(xp + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+      }
+      if (want_w) {
+        // ---- chunk partial p^T = x_new^T V (from zero) ----
+        double p[RT][2];
+#pragma unroll
+        for (int jr = 0; jr < RT; ++jr) p[jr][0] = p[jr][1] = 0.0;
+        const double* vb = g.V + row0 + 4 * ac;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int jr = 0; jr < RT; ++jr) {
+              const double2 v2 = __ldcs(reinterpret_cast<const double2*>(vb + (int64_t)(8 * jr + ar) * g.lda + 16 * i + 2 * h));
+              dmma_8x8x4(p[jr][0], p[jr][1], acc[2 * i][h], v2.x);
+              dmma_8x8x4(p[jr][0], p[jr][1], acc[2 * i + 1][h], v2.y);
+            }
+        // ps[chunk][col_local * R + rank]
+#pragma unroll
+        for (int jr = 0; jr < RT; ++jr)
+          *reinterpret_cast<double2*>(&ps[warp][ar * R + 8 * jr + 2 * ac]) = make_double2(p[jr][0], p[jr][1]);
+      }
+    }
+    if (!want_w) continue;
+    __syncthreads();
+    // ---- fixed-order sums of the chunk partials per output node / CTA segment ----
+    const int cpn = (int)(g.node_rows / 64 < nchunk ? g.node_rows / 64 : nchunk);  // chunks per output unit
+    const int units = nchunk / cpn;
+    for (int e = t; e < units * 8 * R; e += 256) {
+      const int uidx = e / (8 * R), mn = e % (8 * R);
+      const int cl = mn / R, rank = mn % R;
+      const int colg = grp * 8 + cl;
+      double sacc = 0.0;
+      for (int k = 0; k < cpn; ++k) sacc += ps[uidx * cpn + k][mn];
+      if (colg < g.ncols) {
+        if (g.partial) {
+          g.TW[(int64_t)blockIdx.x * R * g.ncols + rank + (int64_t)colg * R] = sacc;
+        } else {
+          const int64_t q = (cta0 + (int64_t)uidx * cpn * 64) / g.node_rows;
+          g.TW[(q >> 1) * g.tw_stride + (q & 1) * R + rank + (int64_t)colg * 2 * R] = sacc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int R>
+static hodlr_status run_solve_level(const LevelArgs& g, int64_t nblk, cudaStream_t st) {
+  solve_level_kernel<R><<<(unsigned)nblk, 256, 0, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+// partial-sum bytes of the solve level steps (one R x nrhs partial per CTA)
+size_t solve_level_partial_bytes(int64_t n, int r, int nrhs) {
+  return (size_t)(n / kSolveCtaRows + 1) * r * nrhs * sizeof(double);
+}
+
+// One solve level step over n rows of X (see solve_level_kernel).  Returns
+// ERR_ARG for unsupported shapes (caller falls back).
+hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, double* X, int64_t ldx,
+                             const double* A1, const double* V, int64_t lda, const double* W, int64_t wstride,
+                             int nrhs, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
+                             cudaStream_t st) {
+  if (nrhs == 0) return HODLR_OK;
+  if (r != 16 && r != 32) return HODLR_ERR_ARG;
+  if ((n_c % 64 && n_c < n) || n % 64 || node_rows % 64) return HODLR_ERR_ARG;
+  if (n_c > 2147483647LL) n_c = 2147483647LL;
+  if ((ldx & 3) || (reinterpret_cast<uintptr_t>(X) & 31) || (lda & 1) || (reinterpret_cast<uintptr_t>(A1) & 15) ||
+      (V && (reinterpret_cast<uintptr_t>(V) & 15)) || (reinterpret_cast<uintptr_t>(W) & 15) || (wstride & 1))
+    return HODLR_ERR_ARG;
+  const int64_t cta_rows = std::min<int64_t>(kSolveCtaRows, n);
+  if (n % cta_rows || (node_rows < cta_rows && cta_rows % node_rows) || (node_rows > cta_rows && node_rows % cta_rows))
+    return HODLR_ERR_ARG;
+  const int64_t nblk = n / cta_rows;
+  const bool split = node_rows > cta_rows && V != nullptr;
+  if (split && (size_t)nblk * r * nrhs * sizeof(double) > part_bytes) return HODLR_ERR_ARG;
+  LevelArgs g{X, ldx, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)cta_rows,
+              node_rows, nrhs, 1, 1};
+  hodlr_status s = r == 16 ? run_solve_level<16>(g, nblk, st) : run_solve_level<32>(g, nblk, st);
+  if (s != HODLR_OK || !split) return s;
+  const int nnodes = (int)(n / node_rows);
+  const int64_t total = (int64_t)r * nrhs * nnodes;
+  const int segs = (int)(node_rows / cta_rows);
+  const int64_t blocks = std::min<int64_t>(ceil_div(segs > 32 ? total * 32 : total, 256), 8 * (int64_t)sm_count());
+  level_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, TW, r, nrhs, segs, nnodes, tw_stride);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
 static int level_variant() {
   static int v = -1;
   if (v < 0) {
@@ -729,16 +913,6 @@ static hodlr_status run_level(const LevelArgs& g, int64_t nseg, cudaStream_t st)
   return HODLR_OK;
 }
 
-static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
 
 // rows per CTA segment for a level whose nodes have `node` rows: the whole node
 // when that already gives >= 2 CTAs per SM, else split (partial sums), and never
@@ -833,8 +1007,9 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   if (s != HODLR_OK || !split) return s;
   const int nnodes = (int)(n / node);
   const int64_t total = (int64_t)r * ncols * nnodes;
-  const int64_t blocks = std::min<int64_t>(ceil_div(total, 256), 8 * (int64_t)sm_count());
-  level_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, TW, r, ncols, (int)(node / seg), nnodes, tw_stride);
+  const int segs = (int)(node / seg);
+  const int64_t blocks = std::min<int64_t>(ceil_div(segs > 32 ? total * 32 : total, 256), 8 * (int64_t)sm_count());
+  level_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, TW, r, ncols, segs, nnodes, tw_stride);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
