@@ -581,11 +581,13 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
 // element as backend.py:444-478 (see getrf_sr_kernel).  One barrier per step:
 // every warp publishes the row of its own argmax winner (parity-buffered)
 // together with its key, so after the barrier each thread reads the global
-// pivot row straight from the winning warp's slot.  Steps run in chunks of 8
-// (unrolled), so register columns are compile-time indices; column blocks left
-// of the current chunk are skipped with warp-uniform branches.  The packed
-// triangular inverses are formed by a separate kernel (trtri_sm_kernel).
+// pivot row straight from the winning warp's slot.  The step loop is fully
+// unrolled: every register column index and every "j > k" test is a
+// compile-time constant, so a step is the argmax, the exchange, one division
+// and exactly (S-1-k) multiply/subtract pairs.  The packed triangular
+// inverses are formed by a separate kernel (trtri_sm_kernel).
 // ---------------------------------------------------------------------------
+
 template <int S>
 __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode, const double* __restrict__ src,
                                                                       int64_t lds, int64_t strides, double* out,
@@ -641,87 +643,68 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
   const double thr_scale = mul_rn(Eps<double>::v, (double)S);
   int pos = t;
   bool active = true;
-  for (int kb = 0; kb < NB; ++kb) {
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int k = 8 * kb + kk;
-      const int par = k & 1;
-      // a[k] with k = 8 kb + kk (kb runtime): select over the column blocks
-      double ak = a[kk];
+  for (int k = 0; k < S; ++k) {
+    const int par = k & 1;
+    const double ak = a[k];
+    unsigned kh = 0u, kl = 0u;
+    int pv = 0x7fffffff;
+    if (active) {
+      abs_key(ak, kh, kl);
+      pv = (pos << 8) | t;
+    }
+    warp_argmax(kh, kl, pv);
+    if (pv != 0x7fffffff && (pv & 255) == t) {
+      double* ur = urow[par][warp];
 #pragma unroll
-      for (int jb = 1; jb < NB; ++jb) ak = csel(kb == jb, a[8 * jb + kk], ak);
-      unsigned kh = 0u, kl = 0u;
-      int pv = 0x7fffffff;  // (position << 8) | thread: unique, orders by position
-      if (active) {
-        abs_key(ak, kh, kl);
-        pv = (pos << 8) | t;
-      }
-      warp_argmax(kh, kl, pv);
-      // the warp's winner publishes its row (columns >= the current block)
-      if (pv != 0x7fffffff && (pv & 255) == t) {
-        double* ur = urow[par][warp];
+      for (int j = k & ~1; j < S; j += 2) *reinterpret_cast<double2*>(ur + j) = make_double2(a[j], a[j + 1]);
+    }
+    if (lane == 0) {
+      redh[par][warp] = kh;
+      redl[par][warp] = kl;
+      redp[par][warp] = pv;
+    }
+    __syncthreads();
+    int ww = 0;
+    if (NW > 1) {
+      kh = redh[par][0];
+      kl = redl[par][0];
+      pv = redp[par][0];
 #pragma unroll
-        for (int jb = 0; jb < NB; ++jb)
-          if (jb >= kb) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              *reinterpret_cast<double2*>(ur + 8 * jb + 2 * q) = make_double2(a[8 * jb + 2 * q], a[8 * jb + 2 * q + 1]);
-          }
-      }
-      if (lane == 0) {
-        redh[par][warp] = kh;
-        redl[par][warp] = kl;
-        redp[par][warp] = pv;
-      }
-      __syncthreads();
-      int ww = 0;
-      if (NW > 1) {
-        kh = redh[par][0];
-        kl = redl[par][0];
-        pv = redp[par][0];
-#pragma unroll
-        for (int w = 1; w < NW; ++w) {
-          const unsigned h2 = redh[par][w], l2 = redl[par][w];
-          const int p2 = redp[par][w];
-          if (h2 > kh || (h2 == kh && (l2 > kl || (l2 == kl && p2 < pv)))) {
-            kh = h2;
-            kl = l2;
-            pv = p2;
-            ww = w;
-          }
+      for (int w = 1; w < NW; ++w) {
+        const unsigned h2 = redh[par][w], l2 = redl[par][w];
+        const int p2 = redp[par][w];
+        if (h2 > kh || (h2 == kh && (l2 > kl || (l2 == kl && p2 < pv)))) {
+          kh = h2;
+          kl = l2;
+          pv = p2;
+          ww = w;
         }
       }
-      const int pt = pv & 255;
-      pv >>= 8;
-      const double* u = urow[par][ww];
-      const double piv = u[k];
-      if (t == 0) {
-        swk[k] = pv;
-        if (fabs(piv) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
-      }
-      if (pos == k) pos = pv;
-      if (t == pt) {
-        pos = k;
-        active = false;
-      }
-      if (active) {
-        const double d = (piv == 0.0) ? 1.0 : piv;
-        const double l = (ak == 0.0 && d == d) ? ((signbit(ak) != signbit(d)) ? -0.0 : 0.0) : div_rn(ak, d);
+    }
+    const int pt = pv & 255;
+    pv >>= 8;
+    const double* u = urow[par][ww];
+    const double piv = u[k];
+    if (t == 0) {
+      swk[k] = pv;
+      if (fabs(piv) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
+    }
+    if (pos == k) pos = pv;
+    if (t == pt) {
+      pos = k;
+      active = false;
+    }
+    if (active) {
+      const double d = (piv == 0.0) ? 1.0 : piv;
+      const double l = (ak == 0.0 && d == d) ? ((signbit(ak) != signbit(d)) ? -0.0 : 0.0) : div_rn(ak, d);
+      a[k] = l;
+      if ((k & 1) == 0 && k + 1 < S) a[k + 1] = sub_rn(a[k + 1], mul_rn(l, u[k + 1]));
 #pragma unroll
-        for (int jb = 0; jb < NB; ++jb) {
-          if (jb == kb) {
-            a[8 * jb + kk] = l;
-#pragma unroll
-            for (int jj = kk + 1; jj < 8; ++jj) a[8 * jb + jj] = sub_rn(a[8 * jb + jj], mul_rn(l, u[8 * jb + jj]));
-          } else if (jb > kb) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const double2 uu = *reinterpret_cast<const double2*>(u + 8 * jb + 2 * q);
-              a[8 * jb + 2 * q] = sub_rn(a[8 * jb + 2 * q], mul_rn(l, uu.x));
-              a[8 * jb + 2 * q + 1] = sub_rn(a[8 * jb + 2 * q + 1], mul_rn(l, uu.y));
-            }
-          }
-        }
+      for (int j = (k + 2) & ~1; j < S; j += 2) {
+        const double2 uu = *reinterpret_cast<const double2*>(u + j);
+        a[j] = sub_rn(a[j], mul_rn(l, uu.x));
+        a[j + 1] = sub_rn(a[j + 1], mul_rn(l, uu.y));
       }
     }
   }
@@ -834,11 +817,11 @@ hodlr_status launch_getrf_cyclic(int s, int batch, int mode, const T* src, int64
     case 16: return run_sr<T, 16>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     case 32:
       if constexpr (sizeof(T) == 8)
-        if (lu_variant() && batch >= 2048) return run_reg<32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+        if (lu_variant()) return run_reg<32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
       return run_sr<T, 32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     case 64:
       if constexpr (sizeof(T) == 8)
-        if (lu_variant() && batch >= 2048) return run_reg<64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+        if (lu_variant()) return run_reg<64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
       return run_sr<T, 64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     case 128: return run_sr<T, 128>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     default: return HODLR_ERR_ARG;
