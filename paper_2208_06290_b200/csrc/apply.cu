@@ -24,7 +24,8 @@
 namespace hodlr {
 
 struct ApplyArgs {
-  const double* tinv;
+  const double* tinv;  // packed full inverses (S in {16, 128}) or diagonal-block inverses (S in {32, 64})
+  const double* lu;    // the LU factors (same layout as tinv); used with the diagonal-block format
   int64_t ldi, strideT;
   const int32_t* perm;
   const double* B;
@@ -290,12 +291,18 @@ __global__ void __launch_bounds__(AP_THREADS, 2) tri_apply2_kernel(ApplyArgs g) 
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ar = lane >> 2, ac = lane & 3;
 
-  // ---- one-time staging: Tinv transposed to [row][k] (k pairs per thread) ----
-  const double* ti = g.tinv + (int64_t)b * g.strideT;
+  // ---- one-time staging, [row][k] (k pairs per thread): the LU factors off the
+  // diagonal 8x8 tiles, the diagonal-block inverses P_q on them ----
+  const double* lb = g.lu + (int64_t)b * g.strideT;
+  const double* di = g.tinv + (int64_t)b * g.strideT;
   for (int idx = t; idx < S * (S / 2); idx += AP_THREADS) {
     const int m = idx % S, k = (idx / S) * 2;
-    const double x0 = ti[m + (int64_t)k * g.ldi], x1 = ti[m + (int64_t)(k + 1) * g.ldi];
-    *reinterpret_cast<double2*>(Tm + m * PT + k) = make_double2(x0, x1);
+    double2 x;
+    if ((m >> 3) == (k >> 3))
+      x = *reinterpret_cast<const double2*>(di + 64 * (m >> 3) + 8 * (m & 7) + (k & 7));
+    else
+      x = make_double2(lb[m + (int64_t)k * g.ldi], lb[m + (int64_t)(k + 1) * g.ldi]);
+    *reinterpret_cast<double2*>(Tm + m * PT + k) = x;
   }
   if constexpr (TWR > 0) {
     const double* vb = g.V + (int64_t)b * g.vstride;
@@ -335,41 +342,43 @@ __global__ void __launch_bounds__(AP_THREADS, 2) tri_apply2_kernel(ApplyArgs g) 
 #pragma unroll
     for (int j = 0; j < NJ; ++j) bv[j][0] = bn[j][0], bv[j][1] = bn[j][1];
     if (grp + 8 < g1) load_b(grp + 8, bn);
-    // ---- stage 1: T^T = (P B)^T L^-T   (L unit lower: k <= n) ----
+    // ---- stage 1: blocked forward substitution, T_j = L_jj^-1 ((P B)_j - sum_{i<j} L_ji T_i) ----
     double a1[NJ][2];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) a1[j][0] = a1[j][1] = 0.0;
-#pragma unroll
     for (int j = 0; j < NJ; ++j) {
+      double c0 = bv[j][0], c1 = bv[j][1];
 #pragma unroll
-      for (int jn = j; jn < NJ; ++jn) {
-        double2 l = *reinterpret_cast<const double2*>(Tm + (8 * jn + ar) * PT + 8 * j + 2 * ac);
-        if (jn == j) {  // diagonal tile: strict lower part, unit diagonal
-          const int k0 = 2 * ac;
-          l.x = k0 < ar ? l.x : (k0 == ar ? 1.0 : 0.0);
-          l.y = k0 + 1 < ar ? l.y : (k0 + 1 == ar ? 1.0 : 0.0);
-        }
-        dmma_8x8x4(a1[jn][0], a1[jn][1], bv[j][0], l.x);
-        dmma_8x8x4(a1[jn][0], a1[jn][1], bv[j][1], l.y);
+      for (int i = 0; i < j; ++i) {
+        const double2 l = *reinterpret_cast<const double2*>(Tm + (8 * j + ar) * PT + 8 * i + 2 * ac);
+        dmma_8x8x4(c0, c1, a1[i][0], -l.x);
+        dmma_8x8x4(c0, c1, a1[i][1], -l.y);
       }
+      const double2 p = *reinterpret_cast<const double2*>(Tm + (8 * j + ar) * PT + 8 * j + 2 * ac);
+      const int k0 = 2 * ac;
+      const double lx = k0 < ar ? p.x : (k0 == ar ? 1.0 : 0.0);
+      const double ly = k0 + 1 < ar ? p.y : (k0 + 1 == ar ? 1.0 : 0.0);
+      a1[j][0] = a1[j][1] = 0.0;
+      dmma_8x8x4(a1[j][0], a1[j][1], c0, lx);
+      dmma_8x8x4(a1[j][0], a1[j][1], c1, ly);
     }
-    // ---- stage 2: X^T = T^T U^-T   (U upper: k >= n) ----
+    // ---- stage 2: blocked backward substitution, X_j = U_jj^-1 (T_j - sum_{i>j} U_ji X_i) ----
     double a2[NJ][2];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) a2[j][0] = a2[j][1] = 0.0;
+    for (int j = NJ - 1; j >= 0; --j) {
+      double c0 = a1[j][0], c1 = a1[j][1];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-#pragma unroll
-      for (int jn = 0; jn <= j; ++jn) {
-        double2 u = *reinterpret_cast<const double2*>(Tm + (8 * jn + ar) * PT + 8 * j + 2 * ac);
-        if (jn == j) {
-          const int k0 = 2 * ac;
-          u.x = k0 >= ar ? u.x : 0.0;
-          u.y = k0 + 1 >= ar ? u.y : 0.0;
-        }
-        dmma_8x8x4(a2[jn][0], a2[jn][1], a1[j][0], u.x);
-        dmma_8x8x4(a2[jn][0], a2[jn][1], a1[j][1], u.y);
+      for (int i = j + 1; i < NJ; ++i) {
+        const double2 u = *reinterpret_cast<const double2*>(Tm + (8 * j + ar) * PT + 8 * i + 2 * ac);
+        dmma_8x8x4(c0, c1, a2[i][0], -u.x);
+        dmma_8x8x4(c0, c1, a2[i][1], -u.y);
       }
+      const double2 p = *reinterpret_cast<const double2*>(Tm + (8 * j + ar) * PT + 8 * j + 2 * ac);
+      const int k0 = 2 * ac;
+      const double ux = k0 >= ar ? p.x : 0.0;
+      const double uy = k0 + 1 >= ar ? p.y : 0.0;
+      a2[j][0] = a2[j][1] = 0.0;
+      dmma_8x8x4(a2[j][0], a2[j][1], c0, ux);
+      dmma_8x8x4(a2[j][0], a2[j][1], c1, uy);
     }
     const int col = grp * 8 + ar;
     if (col < g.ncols) {
@@ -405,14 +414,6 @@ static bool apply2_ok(const ApplyArgs& g) {
          (g.TW == nullptr || (!(g.tw_stride & 1) && !(reinterpret_cast<uintptr_t>(g.TW) & 15)));
 }
 
-static int apply_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_APPLY_V1");
-    v = (e && atoi(e)) ? 1 : 2;
-  }
-  return v;
-}
 
 // Narrow variant (ncols <= 8, the solve phase): one warp per block, the same
 // DMMA instruction sequence per column as tri_apply2_kernel (so a column of a
@@ -442,44 +443,49 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_narrow_kernel(ApplyArgs 
       bv[j][1] = ok ? bc[p.y] : 0.0;
     }
   }
-  // Tinv[row][k] = ti[row + k * ldi]
+  // [row][k] pair of rows 8 jn + ar, columns 8 j + 2 ac + {0, 1}: LU off the
+  // diagonal tiles, the diagonal-block inverse on them
+  const double* lb = g.lu + (int64_t)b * g.strideT;
   auto tl = [&](int jn, int j) {
-    const double* q = ti + (8 * jn + ar) + (int64_t)(8 * j + 2 * ac) * g.ldi;
+    if (jn == j) return __ldg(reinterpret_cast<const double2*>(ti + 64 * j + 8 * ar + 2 * ac));
+    const double* q = lb + (8 * jn + ar) + (int64_t)(8 * j + 2 * ac) * g.ldi;
     return make_double2(__ldg(q), __ldg(q + g.ldi));
   };
   double a1[NJ][2];
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) a1[j][0] = a1[j][1] = 0.0;
-#pragma unroll
   for (int j = 0; j < NJ; ++j) {
+    double c0 = bv[j][0], c1 = bv[j][1];
 #pragma unroll
-    for (int jn = j; jn < NJ; ++jn) {
-      double2 l = tl(jn, j);
-      if (jn == j) {
-        const int k0 = 2 * ac;
-        l.x = k0 < ar ? l.x : (k0 == ar ? 1.0 : 0.0);
-        l.y = k0 + 1 < ar ? l.y : (k0 + 1 == ar ? 1.0 : 0.0);
-      }
-      dmma_8x8x4(a1[jn][0], a1[jn][1], bv[j][0], l.x);
-      dmma_8x8x4(a1[jn][0], a1[jn][1], bv[j][1], l.y);
+    for (int i = 0; i < j; ++i) {
+      const double2 l = tl(j, i);
+      dmma_8x8x4(c0, c1, a1[i][0], -l.x);
+      dmma_8x8x4(c0, c1, a1[i][1], -l.y);
     }
+    const double2 p = tl(j, j);
+    const int k0 = 2 * ac;
+    const double lx = k0 < ar ? p.x : (k0 == ar ? 1.0 : 0.0);
+    const double ly = k0 + 1 < ar ? p.y : (k0 + 1 == ar ? 1.0 : 0.0);
+    a1[j][0] = a1[j][1] = 0.0;
+    dmma_8x8x4(a1[j][0], a1[j][1], c0, lx);
+    dmma_8x8x4(a1[j][0], a1[j][1], c1, ly);
   }
   double a2[NJ][2];
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) a2[j][0] = a2[j][1] = 0.0;
+  for (int j = NJ - 1; j >= 0; --j) {
+    double c0 = a1[j][0], c1 = a1[j][1];
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-#pragma unroll
-    for (int jn = 0; jn <= j; ++jn) {
-      double2 u = tl(jn, j);
-      if (jn == j) {
-        const int k0 = 2 * ac;
-        u.x = k0 >= ar ? u.x : 0.0;
-        u.y = k0 + 1 >= ar ? u.y : 0.0;
-      }
-      dmma_8x8x4(a2[jn][0], a2[jn][1], a1[j][0], u.x);
-      dmma_8x8x4(a2[jn][0], a2[jn][1], a1[j][1], u.y);
+    for (int i = j + 1; i < NJ; ++i) {
+      const double2 u = tl(j, i);
+      dmma_8x8x4(c0, c1, a2[i][0], -u.x);
+      dmma_8x8x4(c0, c1, a2[i][1], -u.y);
     }
+    const double2 p = tl(j, j);
+    const int k0 = 2 * ac;
+    const double ux = k0 >= ar ? p.x : 0.0;
+    const double uy = k0 + 1 >= ar ? p.y : 0.0;
+    a2[j][0] = a2[j][1] = 0.0;
+    dmma_8x8x4(a2[j][0], a2[j][1], c0, ux);
+    dmma_8x8x4(a2[j][0], a2[j][1], c1, uy);
   }
   if (ok) {
     double* xc = Xb + (int64_t)col * g.ldx + 2 * ac;
@@ -565,49 +571,41 @@ static hodlr_status run_apply(ApplyArgs g, cudaStream_t st) {
 // X_b = Tinv-apply(P_b B_b) for s in {16, 32, 64, 128}; returns ERR_ARG otherwise.
 // With V != nullptr (s in {32, 64}, twr in {16, 32}) also writes the fused
 // TW_b = V_b^T X_b reduction.
-hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int64_t ldi, int64_t strideT,
+hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const double* tinv, int64_t ldi, int64_t strideT,
                            const int32_t* perm, const double* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double* X,
                            int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st,
                            const double* V = nullptr, int64_t ldv = 0, int64_t vstride = 0, int twr = 0,
                            double* TW = nullptr, int64_t tw_stride = 0) {
   if (batch == 0 || ncols == 0 || s == 0) return HODLR_OK;
   if ((ldi & 1) || (reinterpret_cast<uintptr_t>(tinv) & 15) || (strideT & 1)) return HODLR_ERR_ARG;
-  ApplyArgs g{tinv, ldi, strideT, perm, B, ldb, sB_hi, sB_lo, X, ldx, sX_hi, sX_lo, ncols, batch, bdiv, 1,
+  ApplyArgs g{tinv, lu, ldi, strideT, perm, B, ldb, sB_hi, sB_lo, X, ldx, sX_hi, sX_lo, ncols, batch, bdiv, 1,
               V, ldv, vstride, TW, tw_stride};
-  if (V) {
-    if ((ldv & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15)) return HODLR_ERR_ARG;
-    const bool nw = ncols <= 8;
-    if (apply_variant() == 2 && nw && apply_narrow_ok(g)) {
-      if (s == 64 && twr == 32) return run_apply_narrow<64, 32>(g, st);
-      if (s == 64 && twr == 16) return run_apply_narrow<64, 16>(g, st);
-      if (s == 32 && twr == 16) return run_apply_narrow<32, 16>(g, st);
-      if (s == 32 && twr == 32) return run_apply_narrow<32, 32>(g, st);
+  const bool narrow = ncols <= 8;
+  if (s == 32 || s == 64) {
+    // diagonal-block-inverse format: blocked substitutions only (the caller
+    // falls back to row substitution on ERR_ARG)
+    if (lu == nullptr || (reinterpret_cast<uintptr_t>(tinv) & 15)) return HODLR_ERR_ARG;
+    if (V) {
+      if ((ldv & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15) || (twr != 16 && twr != 32))
+        return HODLR_ERR_ARG;
+      if (narrow && apply_narrow_ok(g)) {
+        if (s == 64) return twr == 32 ? run_apply_narrow<64, 32>(g, st) : run_apply_narrow<64, 16>(g, st);
+        return twr == 32 ? run_apply_narrow<32, 32>(g, st) : run_apply_narrow<32, 16>(g, st);
+      }
+      if (!narrow && apply2_ok(g)) {
+        if (s == 64) return twr == 32 ? run_apply2<64, 32>(g, st) : run_apply2<64, 16>(g, st);
+        return twr == 32 ? run_apply2<32, 32>(g, st) : run_apply2<32, 16>(g, st);
+      }
+      return HODLR_ERR_ARG;
     }
-    if (apply_variant() == 2 && apply2_ok(g) && ncols > 8) {
-      if (s == 64 && twr == 32) return run_apply2<64, 32>(g, st);
-      if (s == 64 && twr == 16) return run_apply2<64, 16>(g, st);
-      if (s == 32 && twr == 16) return run_apply2<32, 16>(g, st);
-      if (s == 32 && twr == 32) return run_apply2<32, 32>(g, st);
-    }
-    if (s == 64 && twr == 32) return nw ? run_apply<64, 8, 32>(g, st) : run_apply<64, 64, 32>(g, st);
-    if (s == 64 && twr == 16) return nw ? run_apply<64, 8, 16>(g, st) : run_apply<64, 64, 16>(g, st);
-    if (s == 32 && twr == 16) return run_apply<32, 64, 16>(g, st);
-    if (s == 32 && twr == 32) return run_apply<32, 64, 32>(g, st);
+    if (narrow && apply_narrow_ok(g)) return s == 64 ? run_apply_narrow<64, 0>(g, st) : run_apply_narrow<32, 0>(g, st);
+    if (!narrow && apply2_ok(g)) return s == 64 ? run_apply2<64, 0>(g, st) : run_apply2<32, 0>(g, st);
     return HODLR_ERR_ARG;
   }
-  const bool narrow = ncols <= 8;
-  if (apply_variant() == 2 && narrow && apply_narrow_ok(g)) {
-    if (s == 64) return run_apply_narrow<64, 0>(g, st);
-    if (s == 32) return run_apply_narrow<32, 0>(g, st);
-  }
-  if (apply_variant() == 2 && apply2_ok(g) && !narrow) {
-    if (s == 64) return run_apply2<64, 0>(g, st);
-    if (s == 32) return run_apply2<32, 0>(g, st);
-  }
+  // packed full-inverse format (s in {16, 128})
+  if (V) return HODLR_ERR_ARG;
   switch (s) {
     case 16: return run_apply<16, 64, 0>(g, st);
-    case 32: return narrow ? run_apply<32, 8, 0>(g, st) : run_apply<32, 64, 0>(g, st);
-    case 64: return narrow ? run_apply<64, 8, 0>(g, st) : run_apply<64, 64, 0>(g, st);
     case 128: return narrow ? run_apply<128, 8, 0>(g, st) : run_apply<128, 32, 0>(g, st);
     default: return HODLR_ERR_ARG;
   }

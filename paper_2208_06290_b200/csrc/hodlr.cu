@@ -17,7 +17,7 @@ template <typename T>
 hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
                           int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
                           int64_t stridei, cudaStream_t st);
-hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* tinv, int64_t ldi, int64_t strideT,
+hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const double* tinv, int64_t ldi, int64_t strideT,
                            const int32_t* perm, const double* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double* X,
                            int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st,
                            const double* V = nullptr, int64_t ldv = 0, int64_t vstride = 0, int twr = 0,
@@ -27,6 +27,9 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
                               int ncols, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
                               cudaStream_t st, bool reg_resident);
 size_t level_partial_bytes(int64_t n, int m, int r, int L);
+hodlr_status launch_getrf_dbi_f64(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides,
+                                  double* out, int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm,
+                                  int32_t* info, double* dbi, int64_t stridedbi, cudaStream_t st);
 size_t solve_level_partial_bytes(int64_t n, int r, int nrhs);
 hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, double* X, int64_t ldx,
                              const double* A1, const double* V, int64_t lda, const double* W, int64_t wstride,
@@ -189,6 +192,9 @@ static bool desc_ok(const hodlr_desc* d) {
 static hodlr_status lu_factor(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides, double* out,
                               int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, double* tinv,
                               cudaStream_t st) {
+  if (s == 32 || s == 64)  // diagonal-block inverses for the blocked DMMA substitutions
+    return launch_getrf_dbi_f64(s, batch, mode, src, lds, strides, out, s, strideo, swaps, perm, info, tinv, strideo,
+                                st);
   return launch_getrf<double>(s, batch, mode, src, lds, strides, out, s, strideo, swaps, perm, info,
                               tri_size_ok(s) ? tinv : nullptr, s, strideo, st);
 }
@@ -198,8 +204,11 @@ static hodlr_status lu_factor(int s, int batch, int mode, const double* src, int
 static hodlr_status lu_apply(int s, int ncols, int batch, const double* LU, const double* tinv, const int32_t* perm,
                              const double* B, int64_t ldb, int64_t sB, double* X, int64_t ldx, int64_t sX,
                              cudaStream_t st) {
-  if (tri_size_ok(s))
-    return tri_apply_f64(s, ncols, batch, tinv, s, (int64_t)s * s, perm, B, ldb, sB, 0, X, ldx, sX, 0, 1, st);
+  if (tri_size_ok(s)) {
+    const hodlr_status r = tri_apply_f64(s, ncols, batch, LU, tinv, s, (int64_t)s * s, perm, B, ldb, sB, 0, X, ldx, sX,
+                                         0, 1, st);
+    if (r != HODLR_ERR_ARG) return r;
+  }
   return launch_getrs<double>(s, ncols, batch, LU, s, (int64_t)s * s, perm, B, ldb, sB, X, ldx, sX, 0, st);
 }
 
@@ -294,7 +303,7 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
   {
     Phase ph(HODLR_PHASE_LEAF_APPLY, st);
     if (tri_size_ok(m)) {
-      hodlr_status s = tri_apply_f64(m, r * L, (int)nleaf, Dinv, m, (int64_t)m * m, f->dperm, Y, n, m, 0, Y, n, m, 0,
+      hodlr_status s = tri_apply_f64(m, r * L, (int)nleaf, D, Dinv, m, (int64_t)m * m, f->dperm, Y, n, m, 0, Y, n, m, 0,
                                      1, st, V + (int64_t)(L - 1) * r * n, n, m, r, TW, (int64_t)2 * r * r * L);
       if (s == HODLR_OK) tw_ready = true;
       else if (s != HODLR_ERR_ARG) return s;
@@ -471,7 +480,7 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
   {
     Phase ph(HODLR_PHASE_SOLVE_LEAF, st);
     if (r > 0 && L > 0 && tri_size_ok(m)) {
-      hodlr_status s = tri_apply_f64(m, nrhs, (int)nleaf, (const double*)f->Dinv, m, (int64_t)m * m, f->dperm, X, ldx,
+      hodlr_status s = tri_apply_f64(m, nrhs, (int)nleaf, (const double*)f->D, (const double*)f->Dinv, m, (int64_t)m * m, f->dperm, X, ldx,
                                      m, 0, X, ldx, m, 0, 1, st, V + (int64_t)(L - 1) * r * n, n, m, r, w,
                                      (int64_t)2 * r * nrhs);
       if (s == HODLR_OK) w_ready = true;

@@ -594,7 +594,8 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
                                                                       int64_t ldo, int64_t strideo,
                                                                       int32_t* __restrict__ swaps,
                                                                       int32_t* __restrict__ perm,
-                                                                      int32_t* __restrict__ info) {
+                                                                      int32_t* __restrict__ info,
+                                                                      double* __restrict__ dbi, int64_t stridedbi) {
   constexpr int NW = S / 32, NB = S / 8, RP = S + 1;
   __shared__ double A[S * RP];                     // staging (row-major, odd pitch)
   __shared__ __align__(16) double urow[2][NW][S];  // per-warp candidate pivot rows
@@ -720,6 +721,50 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
   }
   swaps[blk * S + t] = swk[t];
   if (t == 0) info[blk] = sflag;
+  if (dbi == nullptr) return;
+  // ---- diagonal-block inverses (the blocked triangular solves' 8x8 pivots):
+  // P_q = strict_lower(L_qq^-1) + upper(U_qq^-1), row-major 8x8 at dbi + 64 q.
+  // Task u = (which, tile q, row i); A holds the logical LU rows.
+  double* di = dbi + blk * stridedbi;
+  for (int u = t; u < 2 * S; u += S) {
+    const int which = u / S, q = (u % S) >> 3, i = u & 7, o0 = 8 * q;
+    const double* T = A + o0 * RP + o0;  // T[r * RP + c] = LU(o0 + r, o0 + c)
+    double x[8];
+    if (which == 0) {  // row i of inv(U_qq)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = 0.0;
+      x[i] = 1.0 / T[i * RP + i];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) {
+        if (j > i) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < j; ++kk)
+            if (kk >= i) sacc = fma(x[kk], T[kk * RP + j], sacc);
+          x[j] = -sacc / T[j * RP + j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j >= i) di[64 * q + 8 * i + j] = x[j];
+    } else {  // row i of inv(L_qq), unit diagonal
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = (j == i) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 6; j >= 0; --j) {
+        if (j < i) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int kk = 1; kk < 8; ++kk)
+            if (kk > j && kk <= i) sacc = fma(x[kk], T[kk * RP + j], sacc);
+          x[j] = -sacc;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < i) di[64 * q + 8 * i + j] = x[j];
+    }
+  }
 }
 
 // Packed triangular inverses of already-factored blocks (L2-hot right after
@@ -750,7 +795,7 @@ template <int S>
 static hodlr_status run_reg(int batch, int mode, const double* src, int64_t lds, int64_t strides, double* out,
                             int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, double* tinv,
                             int64_t ldi, int64_t stridei, cudaStream_t st) {
-  getrf_reg_kernel<S><<<batch, S, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info);
+  getrf_reg_kernel<S><<<batch, S, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, nullptr, 0);
   HODLR_CHECK_LAUNCH();
   if (tinv == nullptr) return HODLR_OK;
   constexpr size_t smem = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(double);
@@ -760,6 +805,25 @@ static hodlr_status run_reg(int batch, int mode, const double* src, int64_t lds,
     attr = true;
   }
   trtri_sm_kernel<S><<<batch, 128, smem, st>>>(out, ldo, strideo, tinv, ldi, stridei);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+// Factorization-internal LU (fp64, s in {32, 64}): factors + diagonal-block
+// inverses (8 s doubles per block at dbi + b * stridedbi) instead of the
+// packed full inverses -- the apply kernels run blocked substitutions.
+hodlr_status launch_getrf_dbi_f64(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides,
+                                  double* out, int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm,
+                                  int32_t* info, double* dbi, int64_t stridedbi, cudaStream_t st) {
+  if (batch == 0) return HODLR_OK;
+  if (s == 64)
+    getrf_reg_kernel<64><<<batch, 64, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, dbi,
+                                              stridedbi);
+  else if (s == 32)
+    getrf_reg_kernel<32><<<batch, 32, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, dbi,
+                                              stridedbi);
+  else
+    return HODLR_ERR_ARG;
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
