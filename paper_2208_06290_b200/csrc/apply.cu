@@ -281,7 +281,7 @@ struct Apply2Cfg {
 };
 
 template <int S, int TWR>
-__global__ void __launch_bounds__(AP_THREADS, 2) tri_apply2_kernel(ApplyArgs g) {
+__global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply2_kernel(ApplyArgs g) {
   constexpr int NJ = S / 8, PT = Apply2Cfg<S>::PT, RT = TWR / 8;
   extern __shared__ __align__(16) double sm[];
   double* Tm = sm;            // [row][k]
@@ -387,22 +387,27 @@ __global__ void __launch_bounds__(AP_THREADS, 2) tri_apply2_kernel(ApplyArgs g) 
       for (int j = 0; j < NJ; ++j) *reinterpret_cast<double2*>(xc + 8 * j) = make_double2(a2[j][0], a2[j][1]);
     }
     if constexpr (TWR > 0) {
-      // ---- TW^T = X^T V ----
-      double tw[RT][2];
+      // ---- TW^T = X^T V, in passes of at most 32 ranks (bounded registers) ----
+      constexpr int RP = RT < 4 ? RT : 4;
 #pragma unroll
-      for (int jr = 0; jr < RT; ++jr) tw[jr][0] = tw[jr][1] = 0.0;
+      for (int r0 = 0; r0 < RT; r0 += RP) {
+        double tw[RP][2];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+        for (int jr = 0; jr < RP; ++jr) tw[jr][0] = tw[jr][1] = 0.0;
 #pragma unroll
-        for (int jr = 0; jr < RT; ++jr) {
-          const double2 v = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * PT + 8 * j + 2 * ac);
-          dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][0], v.x);
-          dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][1], v.y);
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int jr = 0; jr < RP; ++jr) {
+            const double2 v = *reinterpret_cast<const double2*>(Vs + (8 * (r0 + jr) + ar) * PT + 8 * j + 2 * ac);
+            dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][0], v.x);
+            dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][1], v.y);
+          }
+        if (col < g.ncols) {
+          double* out = g.TW + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR + (int64_t)col * 2 * TWR + 2 * ac;
+#pragma unroll
+          for (int jr = 0; jr < RP; ++jr)
+            *reinterpret_cast<double2*>(out + 8 * (r0 + jr)) = make_double2(tw[jr][0], tw[jr][1]);
         }
-      if (col < g.ncols) {
-        double* out = g.TW + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR + (int64_t)col * 2 * TWR + 2 * ac;
-#pragma unroll
-        for (int jr = 0; jr < RT; ++jr) *reinterpret_cast<double2*>(out + 8 * jr) = make_double2(tw[jr][0], tw[jr][1]);
       }
     }
   }
@@ -421,7 +426,7 @@ static bool apply2_ok(const ApplyArgs& g) {
 // packed inverses, the permutation and the V panel read straight from global
 // memory into fragments -- the phase is a single HBM pass over Tinv / V.
 template <int S, int TWR>
-__global__ void __launch_bounds__(AP_THREADS) tri_apply_narrow_kernel(ApplyArgs g) {
+__global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply_narrow_kernel(ApplyArgs g) {
   constexpr int NJ = S / 8, RT = TWR / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x * (AP_THREADS / 32) + warp;
@@ -494,21 +499,26 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_narrow_kernel(ApplyArgs 
   }
   if constexpr (TWR > 0) {
     const double* vb = g.V + (int64_t)b * g.vstride;
-    double tw[RT][2];
+    constexpr int RP = RT < 4 ? RT : 4;
 #pragma unroll
-    for (int jr = 0; jr < RT; ++jr) tw[jr][0] = tw[jr][1] = 0.0;
+    for (int r0 = 0; r0 < RT; r0 += RP) {
+      double tw[RP][2];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
+      for (int jr = 0; jr < RP; ++jr) tw[jr][0] = tw[jr][1] = 0.0;
 #pragma unroll
-      for (int jr = 0; jr < RT; ++jr) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(vb + (int64_t)(8 * jr + ar) * g.ldv + 8 * j + 2 * ac));
-        dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][0], v.x);
-        dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][1], v.y);
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int jr = 0; jr < RP; ++jr) {
+          const double2 v =
+              __ldg(reinterpret_cast<const double2*>(vb + (int64_t)(8 * (r0 + jr) + ar) * g.ldv + 8 * j + 2 * ac));
+          dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][0], v.x);
+          dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][1], v.y);
+        }
+      if (ok) {
+        double* out = g.TW + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR + (int64_t)col * 2 * TWR + 2 * ac;
+#pragma unroll
+        for (int jr = 0; jr < RP; ++jr) *reinterpret_cast<double2*>(out + 8 * (r0 + jr)) = make_double2(tw[jr][0], tw[jr][1]);
       }
-    if (ok) {
-      double* out = g.TW + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR + (int64_t)col * 2 * TWR + 2 * ac;
-#pragma unroll
-      for (int jr = 0; jr < RT; ++jr) *reinterpret_cast<double2*>(out + 8 * jr) = make_double2(tw[jr][0], tw[jr][1]);
     }
   }
 }
@@ -581,19 +591,30 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const 
   ApplyArgs g{tinv, lu, ldi, strideT, perm, B, ldb, sB_hi, sB_lo, X, ldx, sX_hi, sX_lo, ncols, batch, bdiv, 1,
               V, ldv, vstride, TW, tw_stride};
   const bool narrow = ncols <= 8;
+  if (s == 128) {  // diagonal-block-inverse format, no fused reduction
+    if (V || lu == nullptr || (reinterpret_cast<uintptr_t>(tinv) & 15)) return HODLR_ERR_ARG;
+    if (narrow && apply_narrow_ok(g)) return run_apply_narrow<128, 0>(g, st);
+    if (!narrow && apply2_ok(g)) return run_apply2<128, 0>(g, st);
+    return HODLR_ERR_ARG;
+  }
   if (s == 32 || s == 64) {
     // diagonal-block-inverse format: blocked substitutions only (the caller
     // falls back to row substitution on ERR_ARG)
     if (lu == nullptr || (reinterpret_cast<uintptr_t>(tinv) & 15)) return HODLR_ERR_ARG;
     if (V) {
-      if ((ldv & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15) || (twr != 16 && twr != 32))
+      if ((ldv & 1) || (vstride & 1) || (reinterpret_cast<uintptr_t>(V) & 15) || (twr != 16 && twr != 32 && twr != 64))
         return HODLR_ERR_ARG;
       if (narrow && apply_narrow_ok(g)) {
-        if (s == 64) return twr == 32 ? run_apply_narrow<64, 32>(g, st) : run_apply_narrow<64, 16>(g, st);
+        if (s == 64)
+          return twr == 64 ? run_apply_narrow<64, 64>(g, st)
+                           : twr == 32 ? run_apply_narrow<64, 32>(g, st) : run_apply_narrow<64, 16>(g, st);
+        if (twr == 64) return HODLR_ERR_ARG;
         return twr == 32 ? run_apply_narrow<32, 32>(g, st) : run_apply_narrow<32, 16>(g, st);
       }
       if (!narrow && apply2_ok(g)) {
-        if (s == 64) return twr == 32 ? run_apply2<64, 32>(g, st) : run_apply2<64, 16>(g, st);
+        if (s == 64)
+          return twr == 64 ? run_apply2<64, 64>(g, st) : twr == 32 ? run_apply2<64, 32>(g, st) : run_apply2<64, 16>(g, st);
+        if (twr == 64) return HODLR_ERR_ARG;
         return twr == 32 ? run_apply2<32, 32>(g, st) : run_apply2<32, 16>(g, st);
       }
       return HODLR_ERR_ARG;
@@ -602,13 +623,10 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const 
     if (!narrow && apply2_ok(g)) return s == 64 ? run_apply2<64, 0>(g, st) : run_apply2<32, 0>(g, st);
     return HODLR_ERR_ARG;
   }
-  // packed full-inverse format (s in {16, 128})
+  // packed full-inverse format (s = 16)
   if (V) return HODLR_ERR_ARG;
-  switch (s) {
-    case 16: return run_apply<16, 64, 0>(g, st);
-    case 128: return narrow ? run_apply<128, 8, 0>(g, st) : run_apply<128, 32, 0>(g, st);
-    default: return HODLR_ERR_ARG;
-  }
+  if (s == 16) return run_apply<16, 64, 0>(g, st);
+  return HODLR_ERR_ARG;
 }
 
 }  // namespace hodlr

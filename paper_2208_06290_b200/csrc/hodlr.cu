@@ -192,7 +192,7 @@ static bool desc_ok(const hodlr_desc* d) {
 static hodlr_status lu_factor(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides, double* out,
                               int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, double* tinv,
                               cudaStream_t st) {
-  if (s == 32 || s == 64)  // diagonal-block inverses for the blocked DMMA substitutions
+  if (s == 32 || s == 64 || s == 128)  // diagonal-block inverses for the blocked DMMA substitutions
     return launch_getrf_dbi_f64(s, batch, mode, src, lds, strides, out, s, strideo, swaps, perm, info, tinv, strideo,
                                 st);
   return launch_getrf<double>(s, batch, mode, src, lds, strides, out, s, strideo, swaps, perm, info,

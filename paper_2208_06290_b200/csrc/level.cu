@@ -507,8 +507,9 @@ __global__ void __launch_bounds__(256, 2) level_update3_kernel(LevelArgs g) {
 // ---------------------------------------------------------------------------
 template <int R>
 struct Level4Cfg {
-  static constexpr int CH = 64;     // rows per chunk
-  static constexpr int P = CH + 2;  // [rank][row] pitch: 2P = 4 (mod 16) doubles
+  static constexpr int CH = R >= 64 ? 32 : 64;  // rows per chunk (the warp's C^T tile height)
+  static constexpr int NI = CH / 16;            // 16-row bands per chunk
+  static constexpr int P = CH + 2;              // [rank][row] pitch: 2P = 4 (mod 16) doubles
   static constexpr int PANEL = R * P;
   static constexpr int STAGE = 2 * PANEL;
   static constexpr size_t SMEM = (size_t)2 * STAGE * sizeof(double);
@@ -527,7 +528,7 @@ __device__ __forceinline__ void stg_v4(double* p, double x, double y, double z, 
 template <int R, int GPW, bool LATE>
 __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
   using Cfg = Level4Cfg<R>;
-  constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8;
+  constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8, NI = Cfg::NI;
   extern __shared__ __align__(16) double sm[];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ar = lane >> 2, ac = lane & 3;
@@ -577,16 +578,16 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
       if (grp < ge) {
         const int col = grp * 8 + ar;
         double* cptr = g.C + row0 + (int64_t)col * g.ldc + 4 * ac;
-        double acc[8][2], cin[8][2];
+        double acc[2 * NI][2], cin[2 * NI][2];
         if constexpr (LATE) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < NI; ++i) {
             ldg_v4(cptr + 16 * i, cin[2 * i][0], cin[2 * i + 1][0], cin[2 * i][1], cin[2 * i + 1][1]);
             acc[2 * i][0] = acc[2 * i][1] = acc[2 * i + 1][0] = acc[2 * i + 1][1] = 0.0;
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+          for (int i = 0; i < NI; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
         }
         const double* wc = Wp + (int64_t)col * (2 * R) + 2 * ac;
         // ---- C^T += (-W'^T) A1^T ----
@@ -598,7 +599,7 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
             const double a = -(u ? w2.y : w2.x);
             const double* ak = As + (8 * kt + 2 * ac + u) * P + 2 * ar;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < NI; ++i) {
               const double2 b2 = *reinterpret_cast<const double2*>(ak + 16 * i);
               dmma_8x8x4(acc[2 * i][0], acc[2 * i][1], a, b2.x);
               dmma_8x8x4(acc[2 * i + 1][0], acc[2 * i + 1][1], a, b2.y);
@@ -607,13 +608,13 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
         }
         if constexpr (LATE) {  // C - (A1 W'): the load latency hides behind the update products
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i][0] = cin[i][0] + acc[i][0], acc[i][1] = cin[i][1] + acc[i][1];
+          for (int i = 0; i < 2 * NI; ++i) acc[i][0] = cin[i][0] + acc[i][0], acc[i][1] = cin[i][1] + acc[i][1];
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+        for (int i = 0; i < NI; ++i) stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
         // ---- TW^T += C^T V ----
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < NI; ++i)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -668,7 +669,9 @@ static hodlr_status run_level4(const LevelArgs& g, int64_t nseg, cudaStream_t st
   const int gpw = (g.tpc + 7) / 8;
   if (gpw <= 1) return launch_level4<R, 1>(g, nseg, st);
   if (gpw <= 2) return launch_level4<R, 2>(g, nseg, st);
-  if (gpw <= 4) return launch_level4<R, 4>(g, nseg, st);
+  if constexpr (R <= 32) {
+    if (gpw <= 4) return launch_level4<R, 4>(g, nseg, st);
+  }
   if constexpr (R <= 16) {
     if (gpw <= 7) return launch_level4<R, 7>(g, nseg, st);
   }
@@ -831,7 +834,7 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
                              int nrhs, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
                              cudaStream_t st) {
   if (nrhs == 0) return HODLR_OK;
-  if (r != 16 && r != 32) return HODLR_ERR_ARG;
+  if (r != 16 && r != 32 && r != 64) return HODLR_ERR_ARG;
   if ((n_c % 64 && n_c < n) || n % 64 || node_rows % 64) return HODLR_ERR_ARG;
   if (n_c > 2147483647LL) n_c = 2147483647LL;
   if ((ldx & 3) || (reinterpret_cast<uintptr_t>(X) & 31) || (lda & 1) || (reinterpret_cast<uintptr_t>(A1) & 15) ||
@@ -845,7 +848,9 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   if (split && (size_t)nblk * r * nrhs * sizeof(double) > part_bytes) return HODLR_ERR_ARG;
   LevelArgs g{X, ldx, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)cta_rows,
               node_rows, nrhs, 1, 1};
-  hodlr_status s = r == 16 ? run_solve_level<16>(g, nblk, st) : run_solve_level<32>(g, nblk, st);
+  hodlr_status s = r == 16 ? run_solve_level<16>(g, nblk, st)
+                   : r == 32 ? run_solve_level<32>(g, nblk, st)
+                             : run_solve_level<64>(g, nblk, st);
   if (s != HODLR_OK || !split) return s;
   const int nnodes = (int)(n / node_rows);
   const int64_t total = (int64_t)r * nrhs * nnodes;
@@ -871,7 +876,7 @@ static int level4_maxg(int r) {
     const char* e = getenv("HODLR_LEVEL4_MAXG");
     v = e ? atoi(e) : 0;
   }
-  return v > 0 ? v : (r <= 16 ? 56 : 32);
+  return v > 0 ? v : (r <= 16 ? 56 : r <= 32 ? 32 : 16);
 }
 
 static int level_pf() {
@@ -976,7 +981,7 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
                               int ncols, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
                               cudaStream_t st, bool reg_resident) {
   if (ncols == 0) return HODLR_OK;
-  if ((n_c % 64 && n_c < n) || n % 64 || node_rows % 64 || (r != 16 && r != 32)) return HODLR_ERR_ARG;
+  if ((n_c % 64 && n_c < n) || n % 64 || node_rows % 64 || (r != 16 && r != 32 && r != 64)) return HODLR_ERR_ARG;
   if (n_c > 2147483647LL) n_c = 2147483647LL;  // a child larger than the local rows: W' half is pre-selected
   if ((ldc & 1) || (lda & 1) || (reinterpret_cast<uintptr_t>(C) & 15) || (reinterpret_cast<uintptr_t>(A1) & 15) ||
       (V && (reinterpret_cast<uintptr_t>(V) & 15)) || (reinterpret_cast<uintptr_t>(W) & 15) || (wstride & 1))
@@ -1002,6 +1007,7 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   switch (r) {
     case 16: s = small ? run_level<16, 8>(g, nseg, st) : v4 ? run_level4<16>(g, nseg, st) : (fact ? run_level3<16>(g, nseg, st) : run_level<16, 64>(g, nseg, st)); break;
     case 32: s = small ? run_level<32, 8>(g, nseg, st) : v4 ? run_level4<32>(g, nseg, st) : (fact ? run_level3<32>(g, nseg, st) : run_level<32, 64>(g, nseg, st)); break;
+    case 64: if (!v4) return HODLR_ERR_ARG; s = run_level4<64>(g, nseg, st); break;
     default: return HODLR_ERR_ARG;  // r = 64: generic path (fused tiles exceed shared memory)
   }
   if (s != HODLR_OK || !split) return s;

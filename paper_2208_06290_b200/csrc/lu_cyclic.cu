@@ -372,6 +372,52 @@ __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __
 }
 
 
+// Diagonal-block inverses of an S x S LU held in shared memory (element (r, c)
+// at T[r * rs + c * cs]): P_q = strict_lower(L_qq^-1) + upper(U_qq^-1) for the
+// 8x8 diagonal tiles, row-major at di + 64 q.  Task = (which, tile, row).
+template <int S>
+__device__ __forceinline__ void diag_block_inverses(const double* T, int rs, int cs, double* di) {
+  for (int u = threadIdx.x; u < 2 * S; u += blockDim.x) {
+    const int which = u / S, q = (u % S) >> 3, i = u & 7, o0 = 8 * q;
+    auto e = [&](int rr, int cc) { return T[(o0 + rr) * rs + (o0 + cc) * cs]; };
+    double x[8];
+    if (which == 0) {  // row i of inv(U_qq)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = 0.0;
+      x[i] = 1.0 / e(i, i);
+#pragma unroll
+      for (int j = 1; j < 8; ++j) {
+        if (j > i) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < j; ++kk)
+            if (kk >= i) sacc = fma(x[kk], e(kk, j), sacc);
+          x[j] = -sacc / e(j, j);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j >= i) di[64 * q + 8 * i + j] = x[j];
+    } else {  // row i of inv(L_qq), unit diagonal
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = (j == i) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 6; j >= 0; --j) {
+        if (j < i) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int kk = 1; kk < 8; ++kk)
+            if (kk > j && kk <= i) sacc = fma(x[kk], e(kk, j), sacc);
+          x[j] = -sacc;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < i) di[64 * q + 8 * i + j] = x[j];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Shared-memory row LU: thread t owns row t of the block, stored row-major in
 // shared memory (pitch S+2: conflict-free 16B accesses across threads).  The
@@ -387,7 +433,7 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
                                                                  int64_t strideo, int32_t* __restrict__ swaps,
                                                                  int32_t* __restrict__ perm,
                                                                  int32_t* __restrict__ info, T* __restrict__ tinv,
-                                                                 int64_t ldi, int64_t stridei) {
+                                                                 int64_t ldi, int64_t stridei, int dbi = 0) {
   constexpr int NT = S < 32 ? 32 : S;
   constexpr int NW = NT / 32;
   constexpr int RP = S + 16 / (int)sizeof(T);  // row pitch: 16B-aligned rows, 16B bank shift per row
@@ -566,6 +612,12 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
     }
   }
   __syncthreads();
+  if constexpr (sizeof(T) == 8) {
+    if (dbi) {  // diagonal-block inverses (blocked DMMA substitutions) instead of full inverses
+      diag_block_inverses<S>(reinterpret_cast<const double*>(Tm), 1, P, reinterpret_cast<double*>(tinv) + blk * stridei);
+      return;
+    }
+  }
   packed_trtri<T, S>(Tm, Tt, P);
   T* ti = tinv + blk * stridei;
   for (int idx = t; idx < S * S; idx += NT) {
@@ -722,49 +774,8 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
   swaps[blk * S + t] = swk[t];
   if (t == 0) info[blk] = sflag;
   if (dbi == nullptr) return;
-  // ---- diagonal-block inverses (the blocked triangular solves' 8x8 pivots):
-  // P_q = strict_lower(L_qq^-1) + upper(U_qq^-1), row-major 8x8 at dbi + 64 q.
-  // Task u = (which, tile q, row i); A holds the logical LU rows.
-  double* di = dbi + blk * stridedbi;
-  for (int u = t; u < 2 * S; u += S) {
-    const int which = u / S, q = (u % S) >> 3, i = u & 7, o0 = 8 * q;
-    const double* T = A + o0 * RP + o0;  // T[r * RP + c] = LU(o0 + r, o0 + c)
-    double x[8];
-    if (which == 0) {  // row i of inv(U_qq)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = 0.0;
-      x[i] = 1.0 / T[i * RP + i];
-#pragma unroll
-      for (int j = 1; j < 8; ++j) {
-        if (j > i) {
-          double sacc = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < j; ++kk)
-            if (kk >= i) sacc = fma(x[kk], T[kk * RP + j], sacc);
-          x[j] = -sacc / T[j * RP + j];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j >= i) di[64 * q + 8 * i + j] = x[j];
-    } else {  // row i of inv(L_qq), unit diagonal
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = (j == i) ? 1.0 : 0.0;
-#pragma unroll
-      for (int j = 6; j >= 0; --j) {
-        if (j < i) {
-          double sacc = 0.0;
-#pragma unroll
-          for (int kk = 1; kk < 8; ++kk)
-            if (kk > j && kk <= i) sacc = fma(x[kk], T[kk * RP + j], sacc);
-          x[j] = -sacc;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < i) di[64 * q + 8 * i + j] = x[j];
-    }
-  }
+  // ---- diagonal-block inverses (the blocked triangular solves' 8x8 pivots) ----
+  diag_block_inverses<S>(A, RP, 1, dbi + blk * stridedbi);
 }
 
 // Packed triangular inverses of already-factored blocks (L2-hot right after
@@ -822,7 +833,19 @@ hodlr_status launch_getrf_dbi_f64(int s, int batch, int mode, const double* src,
   else if (s == 32)
     getrf_reg_kernel<32><<<batch, 32, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, dbi,
                                               stridedbi);
-  else
+  else if (s == 128) {
+    constexpr int S = 128, RP = S + 2;
+    constexpr size_t rows = (size_t)S * RP * sizeof(double);
+    constexpr size_t inv = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(double);
+    constexpr size_t smem = rows > inv ? rows : inv;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(getrf_sr_kernel<double, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    getrf_sr_kernel<double, S><<<batch, S, smem, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
+                                                         dbi, 0, stridedbi, 1);
+  } else
     return HODLR_ERR_ARG;
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
