@@ -363,7 +363,8 @@ def run_ours(args):
             "solve_gbps": (8 * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 16 * n) / (ts * 1e-3) / 1e9,
             "relres": relres, "flops_factor": f_flops, "flops_solve": s_flops,
             "phase_ms": phases, "gpu_launches": launches_per_step * args.steps,
-            "roofline": {"bound": "tensor", "kernel": "level_update_kernel (fused Y update + next-level [W|T])",
+            "roofline": {"bound": "tensor", "kernel": "level_update4_kernel (fused Y update + next-level [W|T]); traffic = "
+                                   "mean DRAM bytes per level_update4 launch (ncu, profiles/traffic.json)",
                          "achieved": lvl_achieved, "peak": dgemm, "unit": "TFLOP/s",
                          "frac": (lvl_achieved / dgemm) if (lvl_achieved and dgemm) else None,
                          "peak_source": "measured cuBLAS DGEMM 8192^3 in this run (MEASURED_PEAKS.json has no fp64)",

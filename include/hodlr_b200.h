@@ -116,11 +116,14 @@ typedef struct {
 /* Device buffers of a factorization (all owned by the caller). */
 typedef struct {
   void* D;        /* in: leaf blocks; out: leaf LU                       */
-  void* Dinv;     /* out: packed L^-1 / U^-1 of the leaves (2^L m^2)     */
+  void* Dinv;     /* out: leaf solve aids, 2^L m^2 slots: for m in {32,64,128}
+                     the 8x8 diagonal-block inverses P_q = strict_lower(L_qq^-1)
+                     + upper(U_qq^-1), row-major at slot + 64 q (blocked DMMA
+                     substitutions); m = 16: packed L^-1 / U^-1             */
   void* Y;        /* in: U slab; out: Y slab                             */
   void* V;        /* in: V slab                                          */
   void* K;        /* out: K LU per level ((2^L - 1) (2r)^2)              */
-  void* Kinv;     /* out: packed L^-1 / U^-1 of the K blocks, K layout   */
+  void* Kinv;     /* out: the same for the K blocks (2r), K layout        */
   int32_t* dswaps; /* out: 2^L m                                          */
   int32_t* dperm;  /* out: 2^L m                                          */
   int32_t* dinfo;  /* out: 2^L                                            */
