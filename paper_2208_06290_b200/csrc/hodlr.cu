@@ -36,6 +36,10 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
                              int nrhs, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
                              cudaStream_t st);
 int64_t level_segment_rows(int64_t n, int64_t node, int sms);
+hodlr_status gemm_f32(int transA, int M, int N, int K, float alpha, const float* A, int64_t lda, int64_t sA_hi,
+                      int64_t sA_lo, const float* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, float beta, float* C,
+                      int64_t ldc, int64_t sC_hi, int64_t sC_lo, int batch, int bdiv, void* work, size_t work_bytes,
+                      cudaStream_t st);
 template <typename T>
 hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
                           const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX, int identity,
@@ -169,6 +173,9 @@ extern "C" hodlr_status hodlr_gemm_batched(int dtype, int transA, int M, int N, 
                                            int64_t sB_hi, int64_t sB_lo, double beta, void* C, int64_t ldc,
                                            int64_t sC_hi, int64_t sC_lo, int batch, int bdiv, void* work,
                                            size_t work_bytes, void* stream) {
+  if (dtype == HODLR_F32)
+    return gemm_f32(transA, M, N, K, (float)alpha, (const float*)A, lda, sA_hi, sA_lo, (const float*)B, ldb, sB_hi,
+                    sB_lo, (float)beta, (float*)C, ldc, sC_hi, sC_lo, batch, bdiv, work, work_bytes, S(stream));
   if (dtype != HODLR_F64) return HODLR_ERR_ARG;
   return gemm_f64(transA, M, N, K, alpha, (const double*)A, lda, sA_hi, sA_lo, (const double*)B, ldb, sB_hi, sB_lo,
                   beta, (double*)C, ldc, sC_hi, sC_lo, batch, bdiv, work, work_bytes, S(stream));
@@ -371,12 +378,129 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
   return HODLR_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Generic-precision drivers (fp32: the low-accuracy preconditioner config).
+// The SPEC recipe issued as batched kernels only:
+// bit-exact getrf, substitution getrs, batched GEMMs.  No packed inverses, no
+// fused level kernels (those are the fp64 DMMA path).
+// ---------------------------------------------------------------------------
+static hodlr_status gemm_T(int transA, int M, int N, int K, double alpha, const float* A, int64_t lda, int64_t sAh,
+                           int64_t sAl, const float* B, int64_t ldb, int64_t sBh, int64_t sBl, double beta, float* C,
+                           int64_t ldc, int64_t sCh, int64_t sCl, int batch, int bdiv, void* w, size_t wb,
+                           cudaStream_t st) {
+  return gemm_f32(transA, M, N, K, (float)alpha, A, lda, sAh, sAl, B, ldb, sBh, sBl, (float)beta, C, ldc, sCh, sCl,
+                  batch, bdiv, w, wb, st);
+}
+static hodlr_status gemm_T(int transA, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sAh,
+                           int64_t sAl, const double* B, int64_t ldb, int64_t sBh, int64_t sBl, double beta, double* C,
+                           int64_t ldc, int64_t sCh, int64_t sCl, int batch, int bdiv, void* w, size_t wb,
+                           cudaStream_t st) {
+  return gemm_f64(transA, M, N, K, alpha, A, lda, sAh, sAl, B, ldb, sBh, sBl, beta, C, ldc, sCh, sCl, batch, bdiv, w,
+                  wb, st);
+}
+
+template <typename T>
+static hodlr_status factor_generic(const hodlr_desc* d, const hodlr_factors* f, char* wp, const FactWs& ws,
+                                   cudaStream_t st) {
+  void* split = wp;
+  T* TW = reinterpret_cast<T*>(wp + ws.split);
+  T* W = reinterpret_cast<T*>(wp + ws.split + ws.tw);
+  const int64_t N = d->n;
+  const int m = d->m, r = d->r, L = d->L;
+  const int64_t nleaf = N / m;
+  T* D = (T*)f->D;
+  T* Y = (T*)f->Y;
+  const T* V = (const T*)f->V;
+  T* K = (T*)f->K;
+  {
+    Phase ph(HODLR_PHASE_LEAF_GETRF, st);
+    TRY(launch_getrf<T>(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, m, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo,
+                        nullptr, 0, 0, st));
+  }
+  if (L == 0 || r == 0) return HODLR_OK;
+  {
+    Phase ph(HODLR_PHASE_LEAF_APPLY, st);
+    TRY(launch_getrs<T>(m, r * L, (int)nleaf, D, m, (int64_t)m * m, f->dperm, Y, N, m, Y, N, m, 0, st));
+  }
+  for (int lv = L - 1; lv >= 0; --lv) {
+    const int64_t nc = N >> (lv + 1);
+    const int nch = 2 << lv, npar = 1 << lv;
+    const int ncol = r * (lv + 1), wc = r * lv;
+    const int64_t kblk = (int64_t)npar - 1, koff = kblk * 4 * r * r;
+    {
+      Phase ph(HODLR_PHASE_GEMM, st);
+      TRY(gemm_T(1, r, ncol, (int)nc, 1.0, V + (int64_t)lv * r * N, N, 2 * nc, nc, Y, N, 2 * nc, nc, 0.0, TW, 2 * r,
+                 (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
+    }
+    {
+      Phase ph(HODLR_PHASE_K_GETRF, st);
+      TRY(launch_getrf<T>(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff, 2 * r,
+                          (int64_t)4 * r * r, f->kswaps + kblk * 2 * r, f->kperm + kblk * 2 * r, f->kinfo + kblk,
+                          nullptr, 0, 0, st));
+    }
+    if (lv == 0) break;
+    {
+      Phase ph(HODLR_PHASE_K_APPLY, st);
+      TRY(launch_getrs<T>(2 * r, wc, npar, K + koff, 2 * r, (int64_t)4 * r * r, f->kperm + kblk * 2 * r, TW, 2 * r,
+                          (int64_t)2 * r * ncol, W, 2 * r, (int64_t)2 * r * wc, 0, st));
+    }
+    {
+      Phase ph(HODLR_PHASE_GEMM, st);
+      TRY(gemm_T(0, (int)nc, wc, r, -1.0, Y + (int64_t)lv * r * N, N, 2 * nc, nc, W, 2 * r, (int64_t)2 * r * wc, r,
+                 1.0, Y, N, 2 * nc, nc, nch, 2, split, ws.split, st));
+    }
+  }
+  return HODLR_OK;
+}
+
+template <typename T>
+static hodlr_status solve_generic(const hodlr_desc* d, const hodlr_factors* f, T* X, int64_t ldx, int nrhs, char* wp,
+                                  cudaStream_t st) {
+  const int64_t N = d->n;
+  const int m = d->m, r = d->r, L = d->L;
+  const size_t wsz = align_up(sizeof(double) * (size_t)std::max<int64_t>((int64_t)1 << L, 2) * r * nrhs);
+  void* split = wp;
+  T* w = reinterpret_cast<T*>(wp + kSplitBytes);
+  T* w2 = reinterpret_cast<T*>(wp + kSplitBytes + wsz);
+  const T* D = (const T*)f->D;
+  const T* Y = (const T*)f->Y;
+  const T* V = (const T*)f->V;
+  const T* K = (const T*)f->K;
+  {
+    Phase ph(HODLR_PHASE_SOLVE_LEAF, st);
+    TRY(launch_getrs<T>(m, nrhs, (int)(N / m), D, m, (int64_t)m * m, f->dperm, X, ldx, m, X, ldx, m, 0, st));
+  }
+  if (r == 0 || L == 0) return HODLR_OK;
+  for (int lv = L - 1; lv >= 0; --lv) {
+    const int64_t nc = N >> (lv + 1);
+    const int nch = 2 << lv, npar = 1 << lv;
+    const int64_t kblk = (int64_t)npar - 1, koff = kblk * 4 * r * r;
+    {
+      Phase ph(HODLR_PHASE_GEMM, st);
+      TRY(gemm_T(1, r, nrhs, (int)nc, 1.0, V + (int64_t)lv * r * N, N, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w, 2 * r,
+                 (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
+    }
+    {
+      Phase ph(HODLR_PHASE_SOLVE_K, st);
+      TRY(launch_getrs<T>(2 * r, nrhs, npar, K + koff, 2 * r, (int64_t)4 * r * r, f->kperm + kblk * 2 * r, w, 2 * r,
+                          (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, 0, st));
+    }
+    {
+      Phase ph(HODLR_PHASE_GEMM, st);
+      TRY(gemm_T(0, (int)nc, nrhs, r, -1.0, Y + (int64_t)lv * r * N, N, 2 * nc, nc, w2, 2 * r, (int64_t)2 * r * nrhs,
+                 r, 1.0, X, ldx, 2 * nc, nc, nch, 2, split, kSplitBytes, st));
+    }
+  }
+  return HODLR_OK;
+}
+
 extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* work, size_t work_bytes,
                                         void* stream) {
   if (!desc_ok(d) || !f) return HODLR_ERR_ARG;
-  if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64 && d->dtype != HODLR_F32) return HODLR_ERR_ARG;
   const FactWs ws = fact_ws(d);
   if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
+  if (d->dtype == HODLR_F32) return factor_generic<float>(d, f, static_cast<char*>(work), ws, S(stream));
   return factor_local(d, f, d->n, 0, 0, static_cast<char*>(work), ws, S(stream));
 }
 
@@ -545,9 +669,11 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
 extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f, void* Xv, int64_t ldx, int nrhs,
                                     void* work, size_t work_bytes, void* stream) {
   if (!desc_ok(d) || !f || nrhs < 0 || ldx < d->n) return HODLR_ERR_ARG;
-  if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64 && d->dtype != HODLR_F32) return HODLR_ERR_ARG;
   if (nrhs == 0) return HODLR_OK;
   if (work_bytes < hodlr_solve_workspace(d, nrhs) || !work) return HODLR_ERR_ARG;
+  if (d->dtype == HODLR_F32)
+    return solve_generic<float>(d, f, (float*)Xv, ldx, nrhs, static_cast<char*>(work), S(stream));
   return solve_local(d, f, d->n, 0, 0, (double*)Xv, ldx, nrhs, static_cast<char*>(work), S(stream));
 }
 

@@ -256,8 +256,8 @@ def factorize(h: HodlrMatrix, variant: str = "pivoted_standard", check: bool = T
     torch = _torch()
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r} (supported: {VARIANTS})")
-    if h.D.dtype != torch.float64:
-        raise NotImplementedError("the factorization path is fp64 in this build")
+    if h.D.dtype not in (torch.float64, torch.float32):
+        raise TypeError(f"unsupported dtype {h.D.dtype} (float64: DMMA path; float32: preconditioner path)")
     lib = _lib.load()
     dev = h.D.device
     n, m, r, L = h.n, h.m, h.rank, h.L

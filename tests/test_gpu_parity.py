@@ -189,3 +189,21 @@ def test_singular_leaf_raises_with_level_and_node():
     h.D[3 * m * m : 4 * m * m] = 0.0  # leaf 3 is the zero matrix
     with pytest.raises(hb.HodlrSingularError, match=r"leaf block at level 3, node\(s\) \[3\]"):
         hb.factorize(to_gpu(h))
+
+
+@pytest.mark.parametrize("n,m,r", [(1 << 13, 64, 8), (1 << 12, 32, 16)])
+def test_fp32_preconditioner_path_vs_oracle(n, m, r):
+    # cfg4 path (rank-8 fp32 HODLR): bit-exact fp32 leaf LU + pivots, <= 1e-4 elsewhere (north star)
+    h = orc.make_exact_hodlr(n, m, r, seed=n + r, s=1.0, dtype=np.float32)
+    b = np.random.default_rng(2).standard_normal((n, 3)).astype(np.float32)
+    fo = orc.factorize(h.copy(), threads=8)
+    f = hb.factorize(to_gpu(h))
+    assert f.D.dtype == torch.float32
+    assert np.array_equal(f.D.cpu().numpy(), fo.D)
+    assert np.array_equal(f.dperm.cpu().numpy().reshape(-1, m), fo.dpiv.perm)
+    ks = f.kswaps.cpu().numpy().reshape(-1, 2 * r)
+    assert np.array_equal(ks, np.concatenate([kp.swaps for kp in fo.kpiv]))
+    assert rel(f.Y.cpu().numpy(), fo.Y) <= 1e-4
+    x = hb.solve(f, b)
+    assert x.dtype == np.float32
+    assert rel(x, orc.solve(fo, b, threads=8)) <= 1e-4
