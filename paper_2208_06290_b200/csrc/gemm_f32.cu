@@ -39,10 +39,11 @@ __device__ __forceinline__ float combine_f(float prod, const float* cptr, float 
   return __fadd_rn(c, __fmul_rn(prod, alpha));
 }
 
-constexpr int FBM = 64, FBN = 64, FBK = 16;
-
-template <bool TA>
+// BM x BN x BK tile, 16 x 16 threads, thread (ty, tx) owns rows ty + 16 i
+// (i < BM/16) and columns tx + 16 j (j < BN/16)
+template <bool TA, int FBM, int FBN, int FBK>
 __global__ void __launch_bounds__(256) gemm_f32_kernel(GemmArgsF g) {
+  constexpr int TM = FBM / 16, TN = FBN / 16;
   __shared__ float As[FBK][FBM + 4];
   __shared__ float Bs[FBK][FBN + 4];
   int64_t lin = blockIdx.x;
@@ -56,12 +57,12 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(GemmArgsF g) {
   const int kbeg = split * g.kchunk, kend = min(g.K, kbeg + g.kchunk);
   const float* Ab = g.A + boff_f(b, g.bdiv, g.sA_hi, g.sA_lo);
   const float* Bb = g.B + boff_f(b, g.bdiv, g.sB_hi, g.sB_lo);
-  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;  // 16 x 16 threads, 4 x 4 each
-  float acc[4][4];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  float acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
   for (int k0 = kbeg; k0 < kend; k0 += FBK) {
     for (int idx = t; idx < FBM * FBK; idx += 256) {
       int m, k;
@@ -85,24 +86,24 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(GemmArgsF g) {
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < FBK; ++k) {
-      float a[4], bb[4];
+      float a[TM], bb[TN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[k][ty + 16 * i];
+      for (int i = 0; i < TM; ++i) a[i] = As[k][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bb[j] = Bs[k][tx + 16 * j];
+      for (int j = 0; j < TN; ++j) bb[j] = Bs[k][tx + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < TM; ++i) {
     const int gm = m0 + ty + 16 * i;
     if (gm >= g.M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < TN; ++j) {
       const int gn = n0 + tx + 16 * j;
       if (gn >= g.N) continue;
       if (g.ksplit > 1) {
@@ -142,9 +143,16 @@ hodlr_status gemm_f32(int transA, int M, int N, int K, float alpha, const float*
   g.C = C; g.ldc = ldc; g.sC_hi = sC_hi; g.sC_lo = sC_lo;
   g.batch = batch; g.bdiv = bdiv;
   g.ksplit = 1;
+  // tile shapes: [W|T] / w reductions (M = rank <= 16), the solve's narrow
+  // x updates (N = nrhs <= 16), and the general 64 x 64 tile
+  const bool skinny = M <= 16;
+  const int cfg = skinny ? (N <= 16 ? 1 : 0) : (N <= 16 && !transA ? 2 : 3);
+  const int BMc = cfg <= 1 ? 16 : cfg == 2 ? 256 : 64;
+  const int BNc = cfg == 0 ? 128 : cfg == 3 ? 64 : 16;
+  const int FBK = cfg == 1 ? 128 : 16;
   g.kchunk = (int)std::max<int64_t>(FBK, ceil_div(K, FBK) * FBK);
-  g.tiles_m = (int)ceil_div(M, FBM);
-  g.tiles_n = (int)ceil_div(N, FBN);
+  g.tiles_m = (int)ceil_div(M, BMc);
+  g.tiles_n = (int)ceil_div(N, BNc);
   int sms = 148;
   {
     int dev = 0;
@@ -158,17 +166,29 @@ hodlr_status gemm_f32(int transA, int M, int N, int K, float alpha, const float*
     ks = std::min<int64_t>(ks, 128);
     while (ks > 1 && (size_t)ks * batch * M * N * sizeof(float) > work_bytes) --ks;
     if (ks > 1) {
-      g.kchunk = (int)(ceil_div(ceil_div(K, ks), FBK) * FBK);
+      // chunk boundaries on a 128 grid whatever the tile's BK: the split (and so
+      // every output's summation order) never depends on N
+      g.kchunk = (int)(ceil_div(ceil_div(K, ks), 128) * 128);
       g.ksplit = (int)ceil_div(K, g.kchunk);
       g.part = static_cast<float*>(work);
     }
   }
   const int64_t grid = (int64_t)g.tiles_m * g.tiles_n * g.batch * g.ksplit;
   if (grid > 2147483647LL) return HODLR_ERR_ARG;
-  if (transA)
-    gemm_f32_kernel<true><<<(unsigned)grid, 256, 0, st>>>(g);
-  else
-    gemm_f32_kernel<false><<<(unsigned)grid, 256, 0, st>>>(g);
+  switch (cfg) {
+    case 0:
+      if (transA) gemm_f32_kernel<true, 16, 128, 16><<<(unsigned)grid, 256, 0, st>>>(g);
+      else gemm_f32_kernel<false, 16, 128, 16><<<(unsigned)grid, 256, 0, st>>>(g);
+      break;
+    case 1:
+      if (transA) gemm_f32_kernel<true, 16, 16, 128><<<(unsigned)grid, 256, 0, st>>>(g);
+      else gemm_f32_kernel<false, 16, 16, 128><<<(unsigned)grid, 256, 0, st>>>(g);
+      break;
+    case 2: gemm_f32_kernel<false, 256, 16, 16><<<(unsigned)grid, 256, 0, st>>>(g); break;
+    default:
+      if (transA) gemm_f32_kernel<true, 64, 64, 16><<<(unsigned)grid, 256, 0, st>>>(g);
+      else gemm_f32_kernel<false, 64, 64, 16><<<(unsigned)grid, 256, 0, st>>>(g);
+  }
   HODLR_CHECK_LAUNCH();
   if (g.ksplit > 1) {
     const int64_t total = (int64_t)M * N * batch;

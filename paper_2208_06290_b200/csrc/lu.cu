@@ -532,11 +532,76 @@ hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds,
   return HODLR_OK;
 }
 
+// Thread-per-column substitution for S in {16, 32, 64}: the block's LU is
+// staged once in shared memory, every thread carries one right-hand-side column
+// in registers (fully unrolled, compile-time indices) and runs the
+// column-oriented (axpy) forward / backward sweeps -- after x_j is final the
+// S-1-j updates it feeds are independent, so each thread has S-way ILP and no
+// barrier is needed between steps.  L / U columns are read as broadcast
+// 16-byte shared loads.
+template <typename T, int S>
+__global__ void __launch_bounds__(128) getrs_col_kernel(int nrhs, int cpb, const T* __restrict__ LU, int64_t lda,
+                                                        int64_t strideA, const int32_t* __restrict__ perm, const T* B,
+                                                        int64_t ldb, int64_t strideB, T* X, int64_t ldx,
+                                                        int64_t strideX, int identity) {
+  __shared__ __align__(16) T lu[S * S];  // column-major, ld S
+  __shared__ int pm[S];
+  const int64_t blk = blockIdx.x / cpb;
+  const int c = (int)(blockIdx.x % cpb) * 128 + threadIdx.x;
+  const T* g = LU + blk * strideA;
+  for (int idx = threadIdx.x; idx < S * S; idx += 128) lu[idx] = g[(idx % S) + (int64_t)(idx / S) * lda];
+  if (threadIdx.x < S) pm[threadIdx.x] = perm[blk * S + threadIdx.x];
+  __syncthreads();
+  if (c >= nrhs) return;
+  T x[S];
+  const T* gb = B + blk * strideB + (int64_t)c * ldb;
+#pragma unroll
+  for (int i = 0; i < S; ++i) x[i] = identity ? (T)(pm[i] == c) : gb[pm[i]];
+  // forward: unit lower
+#pragma unroll
+  for (int j = 0; j < S - 1; ++j) {
+    const T xj = x[j];
+#pragma unroll
+    for (int i = j + 1; i < S; ++i) x[i] -= lu[i + j * S] * xj;
+  }
+  // backward: upper with true division
+#pragma unroll
+  for (int j = S - 1; j >= 0; --j) {
+    x[j] = x[j] / lu[j + j * S];
+    const T xj = x[j];
+#pragma unroll
+    for (int i = 0; i < j; ++i) x[i] -= lu[i + j * S] * xj;
+  }
+  T* gx = X + blk * strideX + (int64_t)c * ldx;
+#pragma unroll
+  for (int i = 0; i < S; ++i) gx[i] = x[i];
+}
+
+template <typename T, int S>
+static hodlr_status run_getrs_col(int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
+                                  const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX,
+                                  int identity, cudaStream_t st) {
+  const int cpb = (nrhs + 127) / 128;
+  const int64_t grid = (int64_t)batch * cpb;
+  if (grid > 2147483647LL) return HODLR_ERR_ARG;
+  getrs_col_kernel<T, S><<<(unsigned)grid, 128, 0, st>>>(nrhs, cpb, LU, lda, strideA, perm, B, ldb, strideB, X, ldx,
+                                                        strideX, identity);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
 template <typename T>
 hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
                           const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX, int identity,
                           cudaStream_t st) {
   if (batch == 0 || s == 0 || nrhs == 0) return HODLR_OK;
+  // thread-per-column substitution (each thread reads and writes only its own column, so X may alias B)
+  if (s == 16) return run_getrs_col<T, 16>(nrhs, batch, LU, lda, strideA, perm, B, ldb, strideB, X, ldx, strideX, identity, st);
+  if (s == 32) return run_getrs_col<T, 32>(nrhs, batch, LU, lda, strideA, perm, B, ldb, strideB, X, ldx, strideX, identity, st);
+  if constexpr (sizeof(T) == 4) {
+    if (s == 64)
+      return run_getrs_col<T, 64>(nrhs, batch, LU, lda, strideA, perm, B, ldb, strideB, X, ldx, strideX, identity, st);
+  }
   int cw = nrhs < 64 ? nrhs : 64;
   size_t sm = getrs_smem<T>(s, cw);
   while (sm > 227 * 1024 && cw > 8) {

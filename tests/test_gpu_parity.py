@@ -207,3 +207,13 @@ def test_fp32_preconditioner_path_vs_oracle(n, m, r):
     x = hb.solve(f, b)
     assert x.dtype == np.float32
     assert rel(x, orc.solve(fo, b, threads=8)) <= 1e-4
+
+
+def test_fp32_multi_rhs_columns_bitwise_equal_single():
+    n, m, r = 1 << 13, 64, 8
+    h = hb.random_hodlr(n, m, r, seed=5, s=1.0, dtype=torch.float32)
+    f = hb.factorize(h)
+    B = torch.randn(n, 20, dtype=torch.float32, device="cuda", generator=torch.Generator("cuda").manual_seed(4))
+    X = hb.solve(f, B)
+    for j in (0, 7, 19):
+        assert torch.equal(X[:, j], hb.solve(f, B[:, j].contiguous())), j
