@@ -1,0 +1,84 @@
+"""Timing of the other BASELINE.json configs on one B200 (the contract line is
+bench.py = cfg2).  Prints one JSON object per configuration:
+
+  cfg1  Gaussian-kernel-shaped exact HODLR, N = 2^14, leaf 64, rank 32, fp64
+  cfg3  rank-64 HODLR, N = 2^21 (the per-GPU share of 2^22 at P = 2), fp64
+  cfg4  rank-8 fp32 preconditioner, N = 2^21
+  cfg5  multi-RHS solve sweep (1..256) on the cfg2 factorization (N = 2^20, r = 32)
+
+Inputs: seeded exact-HODLR stand-ins generated in HBM.
+Timing: CUDA events, warm-up first, median of the timed repetitions.
+"""
+import json, math, statistics, sys
+sys.path.insert(0, ".")
+import torch
+import paper_2208_06290_b200 as hb
+
+
+def solve_flops(n, m, r, nrhs):
+    L = int(round(math.log2(n // m)))
+    return nrhs * (2 * m * n + 4 * r * n * L + 8 * r * r * ((1 << L) - 1))
+
+
+def solve_bytes(n, m, r, es, nrhs):
+    L = int(round(math.log2(n // m)))
+    return es * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 2 * n * nrhs * es
+
+
+def time_factor_solve(n, m, r, dtype, reps=5, nrhs=1):
+    h0 = hb.random_hodlr(n, m, r, seed=0, s=1.0, dtype=dtype)
+    b = torch.randn(n, nrhs, dtype=dtype, device="cuda").squeeze(1) if nrhs == 1 else torch.randn(n, nrhs, dtype=dtype, device="cuda")
+    tf, ts = [], []
+    for it in range(reps + 2):
+        h = h0.clone()
+        torch.cuda.synchronize()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(); f = hb.factorize(h, check=False); e[1].record(); x = hb.solve(f, b); e[2].record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            tf.append(e[0].elapsed_time(e[1])); ts.append(e[1].elapsed_time(e[2]))
+        del f
+    res = float(torch.linalg.norm(h0.matvec(x) - b) / torch.linalg.norm(b))
+    del h0, h
+    torch.cuda.empty_cache()
+    return statistics.median(tf), statistics.median(ts), res
+
+
+def line(cfg, n, m, r, dtype_name, tf, ts, res, extra=None):
+    fl_f = hb.flop_report(n, m, r)["total"]
+    es = 4 if dtype_name == "f32" else 8
+    d = {"config": cfg, "N": n, "leaf": m, "rank": r, "dtype": dtype_name, "t_factor_ms": round(tf, 3),
+         "t_solve_ms": round(ts, 3), "factor_tflops": round(fl_f / tf / 1e9, 3),
+         "solve_gbps": round(solve_bytes(n, m, r, es, 1) / ts / 1e6, 1), "relres": res}
+    if extra:
+        d.update(extra)
+    print(json.dumps(d), flush=True)
+
+
+which = sys.argv[1:] or ["cfg1", "cfg3", "cfg4", "cfg5"]
+if "cfg1" in which:
+    tf, ts, res = time_factor_solve(1 << 14, 64, 32, torch.float64)
+    line("cfg1", 1 << 14, 64, 32, "f64", tf, ts, res)
+if "cfg3" in which:
+    tf, ts, res = time_factor_solve(1 << 21, 64, 64, torch.float64, reps=3)
+    line("cfg3-shape (per-GPU share of N=2^22 at P=2)", 1 << 21, 64, 64, "f64", tf, ts, res)
+if "cfg4" in which:
+    tf, ts, res = time_factor_solve(1 << 21, 64, 8, torch.float32)
+    line("cfg4", 1 << 21, 64, 8, "f32", tf, ts, res)
+if "cfg5" in which:
+    n, m, r = 1 << 20, 64, 32
+    f = hb.factorize(hb.random_hodlr(n, m, r, seed=0, s=1.0), check=False)
+    for nrhs in (1, 2, 4, 8, 16, 32, 64, 128, 256):
+        B = torch.randn(n, nrhs, dtype=torch.float64, device="cuda")
+        ts = []
+        for it in range(5):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); X = hb.solve(f, B); e1.record(); torch.cuda.synchronize()
+            if it >= 2:
+                ts.append(e0.elapsed_time(e1))
+        t = statistics.median(ts)
+        print(json.dumps({"config": "cfg5 multi-RHS solve on the cfg2 factorization", "N": n, "rank": r, "nrhs": nrhs,
+                          "t_solve_ms": round(t, 3), "solve_tflops": round(solve_flops(n, m, r, nrhs) / t / 1e9, 3),
+                          "solve_gbps": round(solve_bytes(n, m, r, 8, nrhs) / t / 1e6, 1)}), flush=True)
+        del B, X
