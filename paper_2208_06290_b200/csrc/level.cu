@@ -525,7 +525,11 @@ __device__ __forceinline__ void stg_v4(double* p, double x, double y, double z, 
                : "memory");
 }
 
-template <int R, int GPW, bool LATE>
+// SOLVE: the multi-RHS solve step (columns = right-hand sides, ragged last
+// group masked) with the solve kernel's reduction order -- every 64-row
+// chunk's [W|T] contribution is a DMMA chain from zero, added to the running
+// sum in row order -- so the result is bit-identical to solve_level_kernel.
+template <int R, int GPW, bool LATE, bool SOLVE = false>
 __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
   using Cfg = Level4Cfg<R>;
   constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8, NI = Cfg::NI;
@@ -535,21 +539,21 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
   const int seg = blockIdx.x / g.ncg, cg = blockIdx.x % g.ncg;
   const int64_t seg0 = (int64_t)seg * g.seg_rows;
   const int nch = g.seg_rows / CH;
-  const int G = g.ncols >> 3;
+  const int G = SOLVE ? (g.ncols + 7) >> 3 : g.ncols >> 3;
   const int gb = cg * g.tpc, ge = min(G, gb + g.tpc);
 
   auto stage = [&](int ch, int s) {
     double* As = sm + s * Cfg::STAGE;
     double* Vs = As + Cfg::PANEL;
     const double* a1 = g.A1 + seg0 + (int64_t)ch * CH;
-    const double* v1 = g.V + seg0 + (int64_t)ch * CH;
+    const double* v1 = g.V ? g.V + seg0 + (int64_t)ch * CH : nullptr;
     static_assert((R * (CH / 2)) % 256 == 0, "panel split");
 #pragma unroll
     for (int q = 0; q < R * (CH / 2) / 256; ++q) {
       const int idx = t + q * 256;
       const int k = idx / (CH / 2), m = (idx % (CH / 2)) * 2;
       cp_async_16(As + k * P + m, a1 + m + (int64_t)k * g.lda, 16);
-      cp_async_16(Vs + k * P + m, v1 + m + (int64_t)k * g.lda, 16);
+      if (g.V) cp_async_16(Vs + k * P + m, v1 + m + (int64_t)k * g.lda, 16);
     }
   };
 
@@ -577,9 +581,19 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
       const int grp = gb + warp + 8 * q;
       if (grp < ge) {
         const int col = grp * 8 + ar;
-        double* cptr = g.C + row0 + (int64_t)col * g.ldc + 4 * ac;
+        const bool cok = !SOLVE || col < g.ncols;
+        double* cptr = g.C + row0 + (int64_t)(cok ? col : 0) * g.ldc + 4 * ac;
         double acc[2 * NI][2], cin[2 * NI][2];
-        if constexpr (LATE) {
+        if constexpr (SOLVE) {
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            if (cok) {
+              ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+            } else {
+              acc[2 * i][0] = acc[2 * i + 1][0] = acc[2 * i][1] = acc[2 * i + 1][1] = 0.0;
+            }
+          }
+        } else if constexpr (LATE) {
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
             ldg_v4(cptr + 16 * i, cin[2 * i][0], cin[2 * i + 1][0], cin[2 * i][1], cin[2 * i + 1][1]);
@@ -589,11 +603,12 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
 #pragma unroll
           for (int i = 0; i < NI; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
         }
-        const double* wc = Wp + (int64_t)col * (2 * R) + 2 * ac;
+        const double* wc = Wp + (int64_t)(cok ? col : 0) * (2 * R) + 2 * ac;
         // ---- C^T += (-W'^T) A1^T ----
 #pragma unroll
         for (int kt = 0; kt < R / 8; ++kt) {
-          const double2 w2 = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
+          double2 w2 = make_double2(0.0, 0.0);
+          if (cok) w2 = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const double a = -(u ? w2.y : w2.x);
@@ -606,28 +621,51 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
             }
           }
         }
-        if constexpr (LATE) {  // C - (A1 W'): the load latency hides behind the update products
+        if constexpr (LATE && !SOLVE) {  // C - (A1 W'): the load latency hides behind the update products
 #pragma unroll
           for (int i = 0; i < 2 * NI; ++i) acc[i][0] = cin[i][0] + acc[i][0], acc[i][1] = cin[i][1] + acc[i][1];
         }
+        if (cok) {
 #pragma unroll
-        for (int i = 0; i < NI; ++i) stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+          for (int i = 0; i < NI; ++i)
+            stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+        }
+        if (g.V == nullptr) continue;
         // ---- TW^T += C^T V ----
+        if constexpr (SOLVE) {
+          double p[RT][2];
 #pragma unroll
-        for (int i = 0; i < NI; ++i)
+          for (int jr = 0; jr < RT; ++jr) p[jr][0] = p[jr][1] = 0.0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+          for (int i = 0; i < NI; ++i)
 #pragma unroll
-            for (int jr = 0; jr < RT; ++jr) {
-              const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
-              dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i][h], v2.x);
-              dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i + 1][h], v2.y);
-            }
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int jr = 0; jr < RT; ++jr) {
+                const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
+                dmma_8x8x4(p[jr][0], p[jr][1], acc[2 * i][h], v2.x);
+                dmma_8x8x4(p[jr][0], p[jr][1], acc[2 * i + 1][h], v2.y);
+              }
+#pragma unroll
+          for (int jr = 0; jr < RT; ++jr) tw[q][jr][0] += p[jr][0], tw[q][jr][1] += p[jr][1];
+        } else {
+#pragma unroll
+          for (int i = 0; i < NI; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int jr = 0; jr < RT; ++jr) {
+                const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
+                dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i][h], v2.x);
+                dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i + 1][h], v2.y);
+              }
+        }
       }
     }
     __syncthreads();
   }
   // tw[q][jr][h] = TW^T[col][rank 8 jr + 2 ac + h]
+  if (g.V == nullptr) return;
   const int64_t qn = seg0 / g.node_rows;
   double* out;
   int64_t ld;
@@ -641,7 +679,7 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
 #pragma unroll
   for (int q = 0; q < GPW; ++q) {
     const int grp = gb + warp + 8 * q;
-    if (grp < ge) {
+    if (grp < ge && (!SOLVE || grp * 8 + ar < g.ncols)) {
       const int col = grp * 8 + ar;
 #pragma unroll
       for (int jr = 0; jr < RT; ++jr)
@@ -822,6 +860,30 @@ static hodlr_status run_solve_level(const LevelArgs& g, int64_t nblk, cudaStream
   return HODLR_OK;
 }
 
+template <int R>
+static hodlr_status run_level4_solve(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
+  using Cfg = Level4Cfg<R>;
+  const int gpw = (g.tpc + 7) / 8;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    kern<<<(unsigned)(nseg * g.ncg), 256, Cfg::SMEM, st>>>(g);
+  };
+  if (gpw <= 1) launch(level_update4_kernel<R, 1, false, true>);
+  else if (gpw <= 2) launch(level_update4_kernel<R, 2, false, true>);
+  else launch(level_update4_kernel<R, 4, false, true>);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+static int solve_wide() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HODLR_SOLVE_WIDE");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 // partial-sum bytes of the solve level steps (one R x nrhs partial per CTA)
 size_t solve_level_partial_bytes(int64_t n, int r, int nrhs) {
   return (size_t)(n / kSolveCtaRows + 1) * r * nrhs * sizeof(double);
@@ -848,9 +910,22 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   if (split && (size_t)nblk * r * nrhs * sizeof(double) > part_bytes) return HODLR_ERR_ARG;
   LevelArgs g{X, ldx, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)cta_rows,
               node_rows, nrhs, 1, 1};
-  hodlr_status s = r == 16 ? run_solve_level<16>(g, nblk, st)
-                   : r == 32 ? run_solve_level<32>(g, nblk, st)
-                             : run_solve_level<64>(g, nblk, st);
+  hodlr_status s;
+  if (nrhs >= 16 && r <= 32 && solve_wide()) {
+    // many right-hand sides: shared-memory panels reused by every column group
+    // (same segments and reduction order as solve_level_kernel)
+    const int G = (nrhs + 7) / 8;
+    const int gpc = std::min(G, 32);
+    g.seg_rows = (int)std::min<int64_t>(node_rows, cta_rows);
+    g.ncg = (G + gpc - 1) / gpc;
+    g.tpc = gpc;
+    const int64_t nseg = n / g.seg_rows;
+    s = r == 16 ? run_level4_solve<16>(g, nseg, st) : run_level4_solve<32>(g, nseg, st);
+  } else {
+    s = r == 16 ? run_solve_level<16>(g, nblk, st)
+        : r == 32 ? run_solve_level<32>(g, nblk, st)
+                  : run_solve_level<64>(g, nblk, st);
+  }
   if (s != HODLR_OK || !split) return s;
   const int nnodes = (int)(n / node_rows);
   const int64_t total = (int64_t)r * nrhs * nnodes;
