@@ -660,22 +660,31 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
   const int64_t blk = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const double* g = src + blk * strides;
-  // ---- stage: coalesced column reads -> row-major smem ----
-  for (int idx = t; idx < S * S; idx += S) {
-    const int i = idx % S, j = idx / S;
-    double v;
-    if (mode == 0) {
-      v = g[i + (int64_t)j * lds];
-    } else {
-      constexpr int R = S / 2;
-      if (i < R && j < R)
-        v = g[i + (int64_t)j * lds];
-      else if (i >= R && j >= R)
-        v = g[i + (int64_t)(j - R) * lds];
-      else
-        v = (i < R) ? (double)(i == j - R) : (double)(i - R == j);
+  // ---- stage: coalesced column reads -> row-major smem (16 loads in flight per
+  // thread: the top-level single-block factorizations are load-latency bound) ----
+  {
+    const int i = t;  // thread t stages row i = t of every column j
+#pragma unroll
+    for (int j0 = 0; j0 < S; j0 += 16) {
+      double v[16];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int j = j0 + jj;
+        if (mode == 0) {
+          v[jj] = g[i + (int64_t)j * lds];
+        } else {
+          constexpr int R = S / 2;
+          if (i < R && j < R)
+            v[jj] = g[i + (int64_t)j * lds];
+          else if (i >= R && j >= R)
+            v[jj] = g[i + (int64_t)(j - R) * lds];
+          else
+            v[jj] = (i < R) ? (double)(i == j - R) : (double)(i - R == j);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) A[i * RP + j0 + jj] = v[jj];
     }
-    A[i * RP + j] = v;
   }
   if (t == 0) sflag = 0;
   __syncthreads();
