@@ -37,17 +37,30 @@ def test_gemm_one_by_one():  # test_backend.py:73-76
     assert c.view()[0, 0] == 6.0
 
 
-@pytest.mark.parametrize("dtype", [np.float64])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_gemm_batch_matches_sequential(dtype):  # :87-98 (relaxed to rounding)
     rng = np.random.default_rng(7)
     items, refs = [], []
     for _ in range(8):
-        a, b = rng.standard_normal((16, 16)), rng.standard_normal((16, 16))
-        items.append((make_block(a), make_block(b), make_block(np.zeros((16, 16)))))
+        a, b = rng.standard_normal((16, 16)).astype(dtype), rng.standard_normal((16, 16)).astype(dtype)
+        items.append((make_block(a), make_block(b), make_block(np.zeros((16, 16), dtype=dtype))))
         refs.append(a @ b)
     batched_gemm(items)
+    tol = 1e-14 if dtype == np.float64 else 2e-5
     for (_, _, c), want in zip(items, refs):
-        np.testing.assert_allclose(c.view(), want, rtol=1e-14, atol=1e-14)
+        assert c.view().dtype == dtype
+        np.testing.assert_allclose(c.view(), want, rtol=tol, atol=tol)
+
+
+def test_gemm_fp32_conj_transpose_long_k_split():
+    # fp32 transA with a long reduction (the fixed-order split-K path)
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((4096, 8)).astype(np.float32)
+    b = rng.standard_normal((4096, 24)).astype(np.float32)
+    c = make_block(np.zeros((8, 24), dtype=np.float32))
+    batched_gemm([(make_block(a), make_block(b), c)], transpose_a="conj_transpose")
+    want = a.astype(np.float64).T @ b.astype(np.float64)
+    assert np.abs(c.view() - want).max() <= 1e-4 * np.abs(want).max()
 
 
 def test_gemm_accumulate_and_alpha_beta():  # :101-110
