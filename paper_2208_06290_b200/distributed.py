@@ -202,10 +202,12 @@ class GpuBackend:
         i32 = dict(dtype=torch.int32, device=dev)
         b = dict(
             D=sh.D, Dinv=torch.empty_like(sh.D), Y=sh.U, V=sh.V,
-            K=torch.zeros(max(nk, 1) * 4 * r * r, dtype=torch.float64, device=dev),
-            Kinv=torch.zeros(max(nk, 1) * 4 * r * r, dtype=torch.float64, device=dev),
+            # K blocks of other ranks' deep parents are never written nor read here:
+            # no zero-fill (it would be a 1 GB memset per factorization at cfg2)
+            K=torch.empty(max(nk, 1) * 4 * r * r, dtype=torch.float64, device=dev),
+            Kinv=torch.empty(max(nk, 1) * 4 * r * r, dtype=torch.float64, device=dev),
             dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
-            kswaps=torch.zeros(max(nk, 1) * 2 * r, **i32), kperm=torch.zeros(max(nk, 1) * 2 * r, **i32),
+            kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
             kinfo=torch.zeros(max(nk, 1), **i32),
         )
         p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
