@@ -220,8 +220,12 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean([a + b for a, b in zip(tfs, tss)]),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "HODLR factor+solve, exact-HODLR stand-in", "N": n, "leaf": M_LEAF, "rank": RANK,
-                   "L": int(math.log2(n // M_LEAF)), "nrhs": 1, "device": "cpu"},
+        # the arm's config is the GPU arm's (cfg2 shape); each step is a bounded
+        # sample of it (one 2^16-row subtree, stated in cpu_baseline.sample)
+        "config": {"workload": "HODLR factor+solve, cfg2 shape (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
+                               "seeded exact-HODLR stand-in", "N": N_DEFAULT, "leaf": M_LEAF, "rank": RANK,
+                   "L": int(math.log2(N_DEFAULT // M_LEAF)), "nrhs": 1, "parallelism": "cpu (reference)",
+                   "sample_rows": n, "device": "cpu"},
         "t_factor_s": statistics.mean(tfs), "t_solve_s": statistics.mean(tss),
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
