@@ -141,6 +141,15 @@ size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs);
 hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* work,
                              size_t work_bytes, void* stream);
 
+/* Alg. 3 from host memory: D / U / V (pinned host buffers in the reference
+ * layout) are uploaded on copy_stream in the order the factorization consumes
+ * them (D, U, V^(L), then V^(L-1) .. V^(1)) while the factorization runs on
+ * `stream`, each level waiting only for its own V panel.  f->D / f->Y / f->V are
+ * the device destinations (f->Y receives U).  fp64. */
+hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hodlr_factors* f, const void* D_host,
+                                       const void* U_host, const void* V_host, void* work, size_t work_bytes,
+                                       void* stream, void* copy_stream);
+
 /* Alg. 4: X (N x nrhs, ld ldx) is
  * overwritten with A^-1 X. */
 hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f, void* X, int64_t ldx, int nrhs,

@@ -27,6 +27,7 @@ from .hodlr import (  # noqa: F401
     HodlrMatrix,
     HodlrSingularError,
     factorize,
+    factorize_from_host,
     flop_report,
     logdet,
     random_hodlr,

@@ -61,6 +61,7 @@ SIGNATURES = {
     "hodlr_factorize_workspace": (_sz, [C.POINTER(Desc)]),
     "hodlr_solve_workspace": (_sz, [C.POINTER(Desc), _i]),
     "hodlr_factorize": (_i, [C.POINTER(Desc), C.POINTER(Factors), _p, _sz, _p]),
+    "hodlr_factorize_from_host": (_i, [C.POINTER(Desc), C.POINTER(Factors), _p, _p, _p, _p, _sz, _p, _p]),
     "hodlr_factorize_local_workspace": (_sz, [C.POINTER(Desc), _i64]),
     "hodlr_factorize_local": (_i, [C.POINTER(Desc), C.POINTER(Factors), _i64, _i64, _i, _p, _p, _sz, _p]),
     "hodlr_factorize_top": (_i, [C.POINTER(Desc), C.POINTER(Factors), _i64, _i64, _i, _p, _p, _p, _sz, _p]),

@@ -281,8 +281,11 @@ extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
 // Leaf phase + levels L-1 .. lv_stop over the local rows.  On return the
 // workspace TW region holds [W|T] of the local level-lv_stop node(s) (paired
 // layout, local node 0 first) unless lv_stop == 0.
+// vready (optional): vready[l'] is recorded once the level-l' V panel
+// (columns (l'-1) r .. l' r) is resident; the leaf phase needs vready[L],
+// level l's update kernel vready[l] (streamed host upload, hodlr_factorize_from_host).
 static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0, int lv_stop,
-                                 char* wp, const FactWs& ws, cudaStream_t st) {
+                                 char* wp, const FactWs& ws, cudaStream_t st, const cudaEvent_t* vready = nullptr) {
   void* split = wp;
   double* TW = reinterpret_cast<double*>(wp + ws.split);
   double* W = reinterpret_cast<double*>(wp + ws.split + ws.tw);
@@ -299,6 +302,7 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
   double* Kinv = (double*)f->Kinv;
 
   // (1) leaf getrf (bit-exact) + packed triangular inverses     Alg.3 l.2
+  if (vready && L > 0) cudaStreamWaitEvent(st, vready[L], 0);  // D, U and V^(L) resident
   {
     Phase ph(HODLR_PHASE_LEAF_GETRF, st);
     TRY(lu_factor(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo, Dinv, st));
@@ -347,6 +351,7 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
                    (int64_t)2 * r * wc, st));
     }
     // Y(I_c, 0:rl) -= Y_c^{l+1} W_c, fused with the next level's [W|T] (V^{(l)T} Y(I_q, 0:rl))
+    if (vready) cudaStreamWaitEvent(st, vready[lv], 0);  // V^(lv) resident (streamed upload)
     hodlr_status s;
     {
       Phase ph(HODLR_PHASE_LEVEL, st);
@@ -502,6 +507,51 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
   if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
   if (d->dtype == HODLR_F32) return factor_generic<float>(d, f, static_cast<char*>(work), ws, S(stream));
   return factor_local(d, f, d->n, 0, 0, static_cast<char*>(work), ws, S(stream));
+}
+
+// Factorization from host (pinned) buffers with the upload overlapped: D, U and
+// V^(L) are copied first on copy_stream, then the V panels in the order the
+// levels consume them (V^(L-1) ... V^(1)); the compute on `stream` waits per
+// level, so all but the first 4.6 GB (cfg2) of the transfer hide behind the
+// factorization.  f's D / Y / V are the device destinations (Y receives U).
+static std::mutex g_up_mu;
+static std::vector<cudaEvent_t> g_up_ev;
+extern "C" hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hodlr_factors* f, const void* D_host,
+                                                  const void* U_host, const void* V_host, void* work,
+                                                  size_t work_bytes, void* stream, void* copy_stream) {
+  if (!desc_ok(d) || !f || !D_host || !U_host || !V_host) return HODLR_ERR_ARG;
+  if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
+  const FactWs ws = fact_ws(d);
+  if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
+  cudaStream_t st = S(stream), cs = S(copy_stream);
+  const int64_t n = d->n;
+  const int m = d->m, r = d->r, L = d->L;
+  const size_t es = sizeof(double);
+  std::lock_guard<std::mutex> lk(g_up_mu);
+  while ((int)g_up_ev.size() < L + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return hodlr_set_cuda_error(cudaGetLastError());
+    g_up_ev.push_back(e);
+  }
+  // the copies must not start before the caller's prior work on `stream`
+  cudaEventRecord(g_up_ev[L + 1], st);
+  cudaStreamWaitEvent(cs, g_up_ev[L + 1], 0);
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs) == cudaSuccess;
+  };
+  const size_t panel = (size_t)n * r * es;
+  bool ok = cp(f->D, D_host, (size_t)n * m * es) && cp(f->Y, U_host, (size_t)L * panel);
+  if (L > 0)
+    ok = ok && cp((char*)f->V + (size_t)(L - 1) * panel, (const char*)V_host + (size_t)(L - 1) * panel, panel);
+  if (!ok) return hodlr_set_cuda_error(cudaGetLastError());
+  cudaEventRecord(g_up_ev[L > 0 ? L : 0], cs);
+  for (int lv = L - 1; lv >= 1; --lv) {
+    if (!cp((char*)f->V + (size_t)(lv - 1) * panel, (const char*)V_host + (size_t)(lv - 1) * panel, panel))
+      return hodlr_set_cuda_error(cudaGetLastError());
+    cudaEventRecord(g_up_ev[lv], cs);
+  }
+  if (L == 0) cudaStreamWaitEvent(st, g_up_ev[0], 0);
+  return factor_local(d, f, n, 0, 0, static_cast<char*>(work), ws, st, g_up_ev.data());
 }
 
 extern "C" hodlr_status hodlr_factorize_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,

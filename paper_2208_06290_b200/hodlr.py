@@ -284,6 +284,68 @@ def factorize(h: HodlrMatrix, variant: str = "pivoted_standard", check: bool = T
     return f
 
 
+_COPY_STREAMS: dict = {}
+
+
+def factorize_from_host(n: int, m: int, r: int, D, U, V, variant: str = "pivoted_standard", check: bool = True,
+                        device="cuda", stream=None) -> HodlrFactorization:
+    """Factorize a HODLR matrix held in host memory (reference layout, fp64),
+    overlapping the upload with the factorization: D, U and the last level's V
+    go first, then the V panels in the order the levels consume them, on a
+    side copy stream (``hodlr_factorize_from_host``).  Host buffers should be
+    pinned (``tensor.pin_memory()``); pageable inputs are pinned first (a copy).
+    Equivalent to ``factorize(HodlrMatrix.from_buffers(...))``."""
+    torch = _torch()
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r} (supported: {VARIANTS})")
+    lib = _lib.load()
+    L = int(round(math.log2(n // m))) if n >= m else 0
+    if n != m << L:
+        raise ValueError(f"GPU layout needs N = m 2^L (got N={n}, m={m})")
+    nl, nk = 1 << L, (1 << L) - 1
+
+    def host(x, size, name):
+        t = torch.as_tensor(x).reshape(-1)
+        if t.dtype != torch.float64:
+            raise TypeError(f"{name} must be float64 (got {t.dtype})")
+        if t.numel() != size:
+            raise ValueError(f"{name} has {t.numel()} entries, expected {size}")
+        if t.is_cuda:
+            raise ValueError(f"{name} is already on the device; use HodlrMatrix.from_buffers")
+        t = t.contiguous()
+        return t if t.is_pinned() else t.pin_memory()
+
+    Dh, Uh, Vh = host(D, nl * m * m, "D"), host(U, n * r * L, "U"), host(V, n * r * L, "V")
+    dev = torch.device(device)
+    f64 = dict(dtype=torch.float64, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    f = HodlrFactorization(
+        tree=ClusterTree(n, L), rank=r, D=torch.empty(nl * m * m, **f64), Dinv=torch.empty(nl * m * m, **f64),
+        Y=torch.empty(n * r * L, **f64), V=torch.empty(n * r * L, **f64),
+        K=torch.empty(max(nk, 1) * 4 * r * r, **f64), Kinv=torch.empty(max(nk, 1) * 4 * r * r, **f64),
+        dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
+        kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
+        kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r),
+    )
+    f.host_inputs = (Dh, Uh, Vh)  # alive until the asynchronous upload has completed
+    desc = f.desc()
+    wsb = lib.hodlr_factorize_workspace(C.byref(desc))
+    ws = _workspace(wsb, dev)
+    st = (stream or torch.cuda.current_stream(dev))
+    key = str(dev)
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+    cs = _COPY_STREAMS[key]
+    cf = f.cfactors()
+    _lib.check(lib.hodlr_factorize_from_host(C.byref(desc), C.byref(cf), C.c_void_p(Dh.data_ptr()),
+                                             C.c_void_p(Uh.data_ptr()), C.c_void_p(Vh.data_ptr()),
+                                             C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st.cuda_stream),
+                                             C.c_void_p(cs.cuda_stream)), "hodlr_factorize_from_host")
+    if check:
+        _raise_if_singular(f)
+    return f
+
+
 def _raise_if_singular(f: HodlrFactorization) -> None:
     torch = _torch()
     flags = torch.cat([f.dinfo, f.kinfo]).cpu().numpy()

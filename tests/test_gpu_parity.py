@@ -217,3 +217,16 @@ def test_fp32_multi_rhs_columns_bitwise_equal_single():
     X = hb.solve(f, B)
     for j in (0, 7, 19):
         assert torch.equal(X[:, j], hb.solve(f, B[:, j].contiguous())), j
+
+
+def test_factorize_from_host_equals_device_path():
+    # streamed-upload factorization == factorize(from_buffers(...)) bit for bit
+    n, m, r = 1 << 13, 64, 32
+    h = orc.make_exact_hodlr(n, m, r, seed=21, s=4.0)
+    f1 = hb.factorize(to_gpu(h))
+    Dh, Uh, Vh = (torch.from_numpy(x).pin_memory() for x in (h.D, h.U, h.V))
+    f2 = hb.factorize_from_host(n, m, r, Dh, Uh, Vh)
+    for name in ("D", "Y", "K", "kswaps", "dperm"):
+        assert torch.equal(getattr(f1, name), getattr(f2, name)), name
+    b = np.random.default_rng(3).standard_normal(n)
+    assert np.array_equal(hb.solve(f1, b), hb.solve(f2, b))
