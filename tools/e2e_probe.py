@@ -1,0 +1,17 @@
+"""e2e components (dev probe): upload-overlapped factorization, solve with host rhs."""
+import sys, time
+sys.path.insert(0, ".")
+import torch
+import paper_2208_06290_b200 as hb
+n, m, r = 1 << 20, 64, 32
+h0 = hb.random_hodlr(n, m, r, seed=0, s=1.0)
+Dh, Uh, Vh = h0.D.cpu().pin_memory(), h0.U.cpu().pin_memory(), h0.V.cpu().pin_memory()
+b = torch.randn(n, dtype=torch.float64).pin_memory()
+for it in range(4):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    f = hb.factorize_from_host(n, m, r, Dh, Uh, Vh, check=False)
+    torch.cuda.synchronize(); t1 = time.perf_counter()
+    x = hb.solve(f, b)
+    torch.cuda.synchronize(); t2 = time.perf_counter()
+    print(f"factorize_from_host {1e3 * (t1 - t0):.1f} ms ({(Dh.numel() + Uh.numel() + Vh.numel()) * 8 / (t1 - t0) / 1e9:.1f} GB/s)  solve {1e3 * (t2 - t1):.2f} ms")
+    del f
