@@ -546,14 +546,14 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
     double* As = sm + s * Cfg::STAGE;
     double* Vs = As + Cfg::PANEL;
     const double* a1 = g.A1 + seg0 + (int64_t)ch * CH;
-    const double* v1 = g.V ? g.V + seg0 + (int64_t)ch * CH : nullptr;
+    const double* v1 = (!SOLVE || g.V) ? g.V + seg0 + (int64_t)ch * CH : nullptr;
     static_assert((R * (CH / 2)) % 256 == 0, "panel split");
 #pragma unroll
     for (int q = 0; q < R * (CH / 2) / 256; ++q) {
       const int idx = t + q * 256;
       const int k = idx / (CH / 2), m = (idx % (CH / 2)) * 2;
       cp_async_16(As + k * P + m, a1 + m + (int64_t)k * g.lda, 16);
-      if (g.V) cp_async_16(Vs + k * P + m, v1 + m + (int64_t)k * g.lda, 16);
+      if (!SOLVE || g.V) cp_async_16(Vs + k * P + m, v1 + m + (int64_t)k * g.lda, 16);
     }
   };
 
@@ -603,8 +603,8 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
 #pragma unroll
           for (int i = 0; i < NI; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
         }
-        const double* wc = Wp + (int64_t)(cok ? col : 0) * (2 * R) + 2 * ac;
         // ---- C^T += (-W'^T) A1^T ----
+        const double* wc = Wp + (int64_t)(cok ? col : 0) * (2 * R) + 2 * ac;
 #pragma unroll
         for (int kt = 0; kt < R / 8; ++kt) {
           double2 w2 = make_double2(0.0, 0.0);
@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
           for (int i = 0; i < NI; ++i)
             stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
         }
-        if (g.V == nullptr) continue;
+        if (SOLVE && g.V == nullptr) continue;
         // ---- TW^T += C^T V ----
         if constexpr (SOLVE) {
           double p[RT][2];
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
     __syncthreads();
   }
   // tw[q][jr][h] = TW^T[col][rank 8 jr + 2 ac + h]
-  if (g.V == nullptr) return;
+  if (SOLVE && g.V == nullptr) return;
   const int64_t qn = seg0 / g.node_rows;
   double* out;
   int64_t ld;
@@ -688,10 +688,13 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
   }
 }
 
+#ifndef LEVEL4_LATE
+#define LEVEL4_LATE 1
+#endif
 template <int R, int GPW>
 static hodlr_status launch_level4(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
   using Cfg = Level4Cfg<R>;
-  constexpr bool LATE = GPW <= 2;
+  constexpr bool LATE = GPW <= 2 && LEVEL4_LATE;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(level_update4_kernel<R, GPW, LATE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
