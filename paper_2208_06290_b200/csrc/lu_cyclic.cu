@@ -640,18 +640,20 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
 // inverses are formed by a separate kernel (trtri_sm_kernel).
 // ---------------------------------------------------------------------------
 
-template <int S>
-__global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode, const double* __restrict__ src,
-                                                                      int64_t lds, int64_t strides, double* out,
-                                                                      int64_t ldo, int64_t strideo,
-                                                                      int32_t* __restrict__ swaps,
-                                                                      int32_t* __restrict__ perm,
-                                                                      int32_t* __restrict__ info,
-                                                                      double* __restrict__ dbi, int64_t stridedbi) {
-  constexpr int NW = S / 32, NB = S / 8, RP = S + 1;
-  __shared__ double A[S * RP];                     // staging (row-major, odd pitch)
-  __shared__ __align__(16) double urow[2][NW][S];  // per-warp candidate pivot rows
-  __shared__ double cmax[S];
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+
+template <int S, typename T = double>
+__global__ void __launch_bounds__(S, S == 64 ? (sizeof(T) == 8 ? 6 : 10) : 16)
+    getrf_reg_kernel(int mode, const T* __restrict__ src, int64_t lds, int64_t strides, T* out, int64_t ldo,
+                     int64_t strideo, int32_t* __restrict__ swaps, int32_t* __restrict__ perm,
+                     int32_t* __restrict__ info, double* __restrict__ dbi, int64_t stridedbi) {
+  using V2 = typename Vec2<T>::type;
+  constexpr int NW = S / 32, RP = S + 1;
+  __shared__ T A[S * RP];                     // staging (row-major, odd pitch)
+  __shared__ __align__(16) T urow[2][NW][S];  // per-warp candidate pivot rows
+  __shared__ T cmax[S];
   __shared__ unsigned redh[2][NW], redl[2][NW];
   __shared__ int redp[2][NW];
   __shared__ int swk[S];
@@ -659,14 +661,14 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
 
   const int64_t blk = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const double* g = src + blk * strides;
+  const T* g = src + blk * strides;
   // ---- stage: coalesced column reads -> row-major smem (16 loads in flight per
   // thread: the top-level single-block factorizations are load-latency bound) ----
   {
     const int i = t;  // thread t stages row i = t of every column j
 #pragma unroll
     for (int j0 = 0; j0 < S; j0 += 16) {
-      double v[16];
+      T v[16];
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj) {
         const int j = j0 + jj;
@@ -679,7 +681,7 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
           else if (i >= R && j >= R)
             v[jj] = g[i + (int64_t)(j - R) * lds];
           else
-            v[jj] = (i < R) ? (double)(i == j - R) : (double)(i - R == j);
+            v[jj] = (i < R) ? (T)(i == j - R) : (T)(i - R == j);
         }
       }
 #pragma unroll
@@ -689,26 +691,26 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
   if (t == 0) sflag = 0;
   __syncthreads();
   {  // thread t: max |a_it| over the original column t (NaN-propagating)
-    double m0 = 0.0, m1 = 0.0;
+    T m0 = (T)0, m1 = (T)0;
 #pragma unroll 8
     for (int i = 0; i < S; i += 2) {
-      m0 = cyc_nanmax(m0, fabs(A[i * RP + t]));
-      m1 = cyc_nanmax(m1, fabs(A[(i + 1) * RP + t]));
+      m0 = cyc_nanmax(m0, (T)fabs((double)A[i * RP + t]));
+      m1 = cyc_nanmax(m1, (T)fabs((double)A[(i + 1) * RP + t]));
     }
     cmax[t] = cyc_nanmax(m0, m1);
   }
-  double a[S];
+  T a[S];
 #pragma unroll
   for (int j = 0; j < S; ++j) a[j] = A[t * RP + j];
   __syncthreads();  // cmax visible
 
-  const double thr_scale = mul_rn(Eps<double>::v, (double)S);
+  const T thr_scale = mul_rn(Eps<T>::v, (T)S);
   int pos = t;
   bool active = true;
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     const int par = k & 1;
-    const double ak = a[k];
+    const T ak = a[k];
     unsigned kh = 0u, kl = 0u;
     int pv = 0x7fffffff;
     if (active) {
@@ -717,9 +719,9 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
     }
     warp_argmax(kh, kl, pv);
     if (pv != 0x7fffffff && (pv & 255) == t) {
-      double* ur = urow[par][warp];
+      T* ur = urow[par][warp];
 #pragma unroll
-      for (int j = k & ~1; j < S; j += 2) *reinterpret_cast<double2*>(ur + j) = make_double2(a[j], a[j + 1]);
+      for (int j = k & ~1; j < S; j += 2) *reinterpret_cast<V2*>(ur + j) = V2{a[j], a[j + 1]};
     }
     if (lane == 0) {
       redh[par][warp] = kh;
@@ -746,11 +748,11 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
     }
     const int pt = pv & 255;
     pv >>= 8;
-    const double* u = urow[par][ww];
-    const double piv = u[k];
+    const T* u = urow[par][ww];
+    const T piv = u[k];
     if (t == 0) {
       swk[k] = pv;
-      if (fabs(piv) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
+      if ((T)fabs((double)piv) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
     }
     if (pos == k) pos = pv;
     if (t == pt) {
@@ -758,13 +760,13 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
       active = false;
     }
     if (active) {
-      const double d = (piv == 0.0) ? 1.0 : piv;
-      const double l = (ak == 0.0 && d == d) ? ((signbit(ak) != signbit(d)) ? -0.0 : 0.0) : div_rn(ak, d);
+      const T d = (piv == (T)0) ? (T)1 : piv;
+      const T l = (ak == (T)0 && d == d) ? ((signbit(ak) != signbit(d)) ? (T)-0.0 : (T)0.0) : div_rn(ak, d);
       a[k] = l;
       if ((k & 1) == 0 && k + 1 < S) a[k + 1] = sub_rn(a[k + 1], mul_rn(l, u[k + 1]));
 #pragma unroll
       for (int j = (k + 2) & ~1; j < S; j += 2) {
-        const double2 uu = *reinterpret_cast<const double2*>(u + j);
+        const V2 uu = *reinterpret_cast<const V2*>(u + j);
         a[j] = sub_rn(a[j], mul_rn(l, uu.x));
         a[j + 1] = sub_rn(a[j + 1], mul_rn(l, uu.y));
       }
@@ -775,16 +777,18 @@ __global__ void __launch_bounds__(S, S == 64 ? 6 : 16) getrf_reg_kernel(int mode
   for (int j = 0; j < S; ++j) A[pos * RP + j] = a[j];
   perm[blk * S + pos] = t;
   __syncthreads();
-  double* o = out + blk * strideo;
+  T* o = out + blk * strideo;
   for (int idx = t; idx < S * S; idx += S) {
     const int i = idx % S, j = idx / S;
     o[i + (int64_t)j * ldo] = A[i * RP + j];
   }
   swaps[blk * S + t] = swk[t];
   if (t == 0) info[blk] = sflag;
-  if (dbi == nullptr) return;
-  // ---- diagonal-block inverses (the blocked triangular solves' 8x8 pivots) ----
-  diag_block_inverses<S>(A, RP, 1, dbi + blk * stridedbi);
+  if constexpr (sizeof(T) == 8) {
+    if (dbi == nullptr) return;
+    // ---- diagonal-block inverses (the blocked triangular solves' 8x8 pivots) ----
+    diag_block_inverses<S>(A, RP, 1, dbi + blk * stridedbi);
+  }
 }
 
 // Packed triangular inverses of already-factored blocks (L2-hot right after
@@ -914,10 +918,22 @@ hodlr_status launch_getrf_cyclic(int s, int batch, int mode, const T* src, int64
     case 32:
       if constexpr (sizeof(T) == 8)
         if (lu_variant()) return run_reg<32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+      if constexpr (sizeof(T) == 4)
+        if (lu_variant() && tinv == nullptr) {
+          getrf_reg_kernel<32, float><<<batch, 32, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, nullptr, 0);
+          HODLR_CHECK_LAUNCH();
+          return HODLR_OK;
+        }
       return run_sr<T, 32>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     case 64:
       if constexpr (sizeof(T) == 8)
         if (lu_variant()) return run_reg<64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
+      if constexpr (sizeof(T) == 4)
+        if (lu_variant() && tinv == nullptr) {
+          getrf_reg_kernel<64, float><<<batch, 64, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, nullptr, 0);
+          HODLR_CHECK_LAUNCH();
+          return HODLR_OK;
+        }
       return run_sr<T, 64>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     case 128: return run_sr<T, 128>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     default: return HODLR_ERR_ARG;
