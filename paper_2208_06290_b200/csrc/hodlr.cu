@@ -36,6 +36,9 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
                              int nrhs, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
                              cudaStream_t st);
 int64_t level_segment_rows(int64_t n, int64_t node, int sms);
+hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
+                       const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
+                       int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st);
 hodlr_status gemm_f32(int transA, int M, int N, int K, float alpha, const float* A, int64_t lda, int64_t sA_hi,
                       int64_t sA_lo, const float* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, float beta, float* C,
                       int64_t ldc, int64_t sC_hi, int64_t sC_lo, int batch, int bdiv, void* work, size_t work_bytes,
@@ -404,6 +407,17 @@ static hodlr_status gemm_T(int transA, int M, int N, int K, double alpha, const 
                   wb, st);
 }
 
+// fused rank-8 fp32 level step where it applies (level_f32.cu), else ERR_ARG
+static hodlr_status level_T(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
+                            const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
+                            int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st) {
+  return level_f32(r, n, n_c, node_rows, C, ldc, A1, V, lda, W, wstride, ncols, TW, tw_stride, part, part_bytes, st);
+}
+static hodlr_status level_T(int, int64_t, int64_t, int64_t, double*, int64_t, const double*, const double*, int64_t,
+                            const double*, int64_t, int, double*, int64_t, double*, size_t, cudaStream_t) {
+  return HODLR_ERR_ARG;
+}
+
 template <typename T>
 static hodlr_status factor_generic(const hodlr_desc* d, const hodlr_factors* f, char* wp, const FactWs& ws,
                                    cudaStream_t st) {
@@ -427,12 +441,21 @@ static hodlr_status factor_generic(const hodlr_desc* d, const hodlr_factors* f, 
     Phase ph(HODLR_PHASE_LEAF_APPLY, st);
     TRY(launch_getrs<T>(m, r * L, (int)nleaf, D, m, (int64_t)m * m, f->dperm, Y, N, m, Y, N, m, 0, st));
   }
+  T* part = reinterpret_cast<T*>(wp + ws.split + ws.tw + ws.w);
+  bool tw_ready = false;
+  {  // leaf-level [W|T]_a = V_a^T Y(I_a, :) by the fused kernel (no update)
+    Phase ph(HODLR_PHASE_LEVEL, st);
+    const hodlr_status s = level_T(r, N, m, m, Y, N, nullptr, V + (int64_t)(L - 1) * r * N, N, nullptr, 0, r * L, TW,
+                                   (int64_t)2 * r * r * L, part, ws.part, st);
+    if (s == HODLR_OK) tw_ready = true;
+    else if (s != HODLR_ERR_ARG) return s;
+  }
   for (int lv = L - 1; lv >= 0; --lv) {
     const int64_t nc = N >> (lv + 1);
     const int nch = 2 << lv, npar = 1 << lv;
     const int ncol = r * (lv + 1), wc = r * lv;
     const int64_t kblk = (int64_t)npar - 1, koff = kblk * 4 * r * r;
-    {
+    if (!tw_ready) {
       Phase ph(HODLR_PHASE_GEMM, st);
       TRY(gemm_T(1, r, ncol, (int)nc, 1.0, V + (int64_t)lv * r * N, N, 2 * nc, nc, Y, N, 2 * nc, nc, 0.0, TW, 2 * r,
                  (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
@@ -448,6 +471,17 @@ static hodlr_status factor_generic(const hodlr_desc* d, const hodlr_factors* f, 
       Phase ph(HODLR_PHASE_K_APPLY, st);
       TRY(launch_getrs<T>(2 * r, wc, npar, K + koff, 2 * r, (int64_t)4 * r * r, f->kperm + kblk * 2 * r, TW, 2 * r,
                           (int64_t)2 * r * ncol, W, 2 * r, (int64_t)2 * r * wc, 0, st));
+    }
+    {  // update + the next level's [W|T], fused when it applies
+      Phase ph(HODLR_PHASE_LEVEL, st);
+      const hodlr_status s = level_T(r, N, nc, 2 * nc, Y, N, Y + (int64_t)lv * r * N, V + (int64_t)(lv - 1) * r * N,
+                                     N, W, (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st);
+      if (s == HODLR_OK) {
+        tw_ready = true;
+        continue;
+      }
+      if (s != HODLR_ERR_ARG) return s;
+      tw_ready = false;
     }
     {
       Phase ph(HODLR_PHASE_GEMM, st);
@@ -476,11 +510,21 @@ static hodlr_status solve_generic(const hodlr_desc* d, const hodlr_factors* f, T
     TRY(launch_getrs<T>(m, nrhs, (int)(N / m), D, m, (int64_t)m * m, f->dperm, X, ldx, m, X, ldx, m, 0, st));
   }
   if (r == 0 || L == 0) return HODLR_OK;
+  T* part = reinterpret_cast<T*>(wp + kSplitBytes + 2 * wsz);
+  const size_t part_bytes = solve_part_bytes(d, nrhs);
+  bool w_ready = false;
+  {
+    Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
+    const hodlr_status s = level_T(r, N, m, m, X, ldx, nullptr, V + (int64_t)(L - 1) * r * N, N, nullptr, 0, nrhs, w,
+                                   (int64_t)2 * r * nrhs, part, part_bytes, st);
+    if (s == HODLR_OK) w_ready = true;
+    else if (s != HODLR_ERR_ARG) return s;
+  }
   for (int lv = L - 1; lv >= 0; --lv) {
     const int64_t nc = N >> (lv + 1);
     const int nch = 2 << lv, npar = 1 << lv;
     const int64_t kblk = (int64_t)npar - 1, koff = kblk * 4 * r * r;
-    {
+    if (!w_ready) {
       Phase ph(HODLR_PHASE_GEMM, st);
       TRY(gemm_T(1, r, nrhs, (int)nc, 1.0, V + (int64_t)lv * r * N, N, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w, 2 * r,
                  (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
@@ -489,6 +533,18 @@ static hodlr_status solve_generic(const hodlr_desc* d, const hodlr_factors* f, T
       Phase ph(HODLR_PHASE_SOLVE_K, st);
       TRY(launch_getrs<T>(2 * r, nrhs, npar, K + koff, 2 * r, (int64_t)4 * r * r, f->kperm + kblk * 2 * r, w, 2 * r,
                           (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, 0, st));
+    }
+    {
+      Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
+      const hodlr_status s = level_T(r, N, nc, 2 * nc, X, ldx, Y + (int64_t)lv * r * N,
+                                     lv > 0 ? V + (int64_t)(lv - 1) * r * N : nullptr, N, w2, (int64_t)2 * r * nrhs,
+                                     nrhs, w, (int64_t)2 * r * nrhs, part, part_bytes, st);
+      if (s == HODLR_OK) {
+        w_ready = true;
+        continue;
+      }
+      if (s != HODLR_ERR_ARG) return s;
+      w_ready = false;
     }
     {
       Phase ph(HODLR_PHASE_GEMM, st);

@@ -1,0 +1,165 @@
+// FP32 level step for rank 8 (the preconditioner configuration, cfg4), SIMT:
+//
+//   C(I_c, :) -= Y_c^{l+1} W'_c            (update; skipped when W == null)
+//   TW_q      += V_q^{(l)T} C(I_q, :)      (next level's [W|T] / w; skipped when V == null)
+//
+// fp32 has no tensor-core path of fp64 accuracy, and at rank 8 the step is
+// HBM-bound (2 flops per byte): one warp owns 8 columns of a row segment, each
+// lane streams rows (coalesced column reads), keeps the 8 x 8 W' block of the
+// current child and the 8 x 8 [W|T] partial in registers, and the warp's
+// partials are combined with a fixed xor-butterfly.  Segment partials are
+// summed in segment order.  The column split and the reduction order do not
+// depend on the number of columns, so a column of a multi-RHS solve is
+// bit-identical to the single-column solve.
+#include "common.cuh"
+
+namespace hodlr {
+
+constexpr int F32_R = 8;
+constexpr int F32_SEG = 1024;  // rows per segment (32 per lane)
+
+struct LevelF32Args {
+  float* C;
+  int64_t ldc;
+  const float* A1;  // Y^{l+1} panel, ld lda
+  const float* V;   // V^{(l)} panel (null: no reduction)
+  int64_t lda;
+  const float* W;   // paired W per parent (2R x ncols, ld 2R) at W + p * wstride (null: no update)
+  int64_t wstride;
+  int64_t n_c;
+  int64_t node_rows;
+  int ncols;
+  int seg_rows;
+  int chunks;       // ceil(ncols / 8) CTAs (one warp each) per segment
+  float* TW;        // final: paired layout; partial: [seg][R x ncols] ld R
+  int64_t tw_stride;
+  int partial;
+};
+
+// one warp per CTA: work item = (segment, 8-column chunk)
+__global__ void __launch_bounds__(32) level_f32_kernel(LevelF32Args g) {
+  constexpr int R = F32_R;
+  const int lane = threadIdx.x;
+  const int seg = blockIdx.x / g.chunks, chunk = blockIdx.x % g.chunks;
+  const int col0 = chunk * 8;
+  const int ncw = min(8, g.ncols - col0);  // columns of this warp (ragged last chunk)
+  const int64_t seg0 = (int64_t)seg * g.seg_rows;
+  float tw[R][8];
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tw[k][j] = 0.f;
+  __shared__ float w[R][8];  // W' block of the current child (broadcast reads)
+  int64_t wchild = -1;
+#pragma unroll 2
+  for (int64_t i = lane; i < g.seg_rows; i += 32) {
+    const int64_t row = seg0 + i;
+    float c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = (j < ncw) ? g.C[row + (int64_t)(col0 + j) * g.ldc] : 0.f;
+    if (g.W) {
+      const int64_t ch = row / g.n_c;  // warp-uniform (n_c >= 32)
+      if (ch != wchild) {
+        const float* wp = g.W + (ch >> 1) * g.wstride + (ch & 1) * R;
+        __syncwarp();
+#pragma unroll
+        for (int e = lane; e < R * 8; e += 32) {
+          const int k = e % R, j = e / R;
+          w[k][j] = (j < ncw) ? __ldg(wp + k + (int64_t)(col0 + j) * (2 * R)) : 0.f;
+        }
+        __syncwarp();
+        wchild = ch;
+      }
+      float a[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) a[k] = __ldg(g.A1 + row + (int64_t)k * g.lda);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < R; ++k) t = fmaf(a[k], w[k][j], t);
+        c[j] = __fsub_rn(c[j], t);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < ncw) g.C[row + (int64_t)(col0 + j) * g.ldc] = c[j];
+    }
+    if (g.V) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const float v = __ldg(g.V + row + (int64_t)k * g.lda);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tw[k][j] = fmaf(v, c[j], tw[k][j]);
+      }
+    }
+  }
+  if (!g.V) return;
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = tw[k][j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      tw[k][j] = v;
+    }
+  if (lane == 0) {
+    if (g.partial) {
+      float* out = g.TW + (int64_t)seg * R * g.ncols;
+      for (int j = 0; j < ncw; ++j)
+#pragma unroll
+        for (int k = 0; k < R; ++k) out[k + (int64_t)(col0 + j) * R] = tw[k][j];
+    } else {
+      const int64_t q = seg0 / g.node_rows;
+      float* out = g.TW + (q >> 1) * g.tw_stride + (q & 1) * R;
+      for (int j = 0; j < ncw; ++j)
+#pragma unroll
+        for (int k = 0; k < R; ++k) out[k + (int64_t)(col0 + j) * 2 * R] = tw[k][j];
+    }
+  }
+}
+
+// TW_q = sum of the q's segment partials in segment order; paired output
+__global__ void level_reduce_f32_kernel(const float* part, float* TW, int ncols, int segs, int nnodes,
+                                        int64_t tw_stride) {
+  constexpr int R = F32_R;
+  const int64_t per = (int64_t)R * ncols;
+  const int64_t total = per * nnodes;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / per, mn = e % per;
+    const int m = (int)(mn % R), n = (int)(mn / R);
+    float s = 0.f;
+    for (int k = 0; k < segs; ++k) s += part[(q * segs + k) * per + mn];
+    TW[(q >> 1) * tw_stride + (q & 1) * R + m + (int64_t)n * 2 * R] = s;
+  }
+}
+
+size_t level_f32_partial_bytes(int64_t n, int ncols) { return (size_t)(n / 64 + 1) * F32_R * ncols * sizeof(float); }
+
+// One fp32 level step over n rows (r = 8, n_c >= 32).  ERR_ARG: unsupported shape.
+hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
+                       const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
+                       int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st) {
+  if (ncols == 0) return HODLR_OK;
+  if (r != F32_R || n_c < 32 || n % 32 || node_rows % 32) return HODLR_ERR_ARG;
+  const int64_t seg = std::min<int64_t>(node_rows, F32_SEG);
+  if (n % seg || (node_rows % seg)) return HODLR_ERR_ARG;
+  const int64_t nseg = n / seg;
+  const bool split = seg < node_rows && V != nullptr;
+  if (split && (size_t)nseg * F32_R * ncols * sizeof(float) > part_bytes) return HODLR_ERR_ARG;
+  LevelF32Args g{C, ldc, A1, V, lda, W, wstride, n_c, node_rows, ncols, (int)seg, (int)ceil_div(ncols, 8),
+                 split ? part : TW, tw_stride, split ? 1 : 0};
+  const int64_t grid = nseg * g.chunks;
+  if (grid > 2147483647LL) return HODLR_ERR_ARG;
+  level_f32_kernel<<<(unsigned)grid, 32, 0, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  if (!split) return HODLR_OK;
+  const int nnodes = (int)(n / node_rows);
+  const int64_t total = (int64_t)F32_R * ncols * nnodes;
+  level_reduce_f32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 1184), 256, 0, st>>>(
+      part, TW, ncols, (int)(node_rows / seg), nnodes, tw_stride);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+}  // namespace hodlr
