@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(32) level_f32_kernel(LevelF32Args g) {
     for (int j = 0; j < 8; ++j) tw[k][j] = 0.f;
   __shared__ float w[R][8];  // W' block of the current child (broadcast reads)
   int64_t wchild = -1;
-#pragma unroll 2
+#pragma unroll 1
   for (int64_t i = lane; i < g.seg_rows; i += 32) {
     const int64_t row = seg0 + i;
     float c[8];
