@@ -939,6 +939,15 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   return HODLR_OK;
 }
 
+static int level4_min_groups() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HODLR_LEVEL4_MIN_GROUPS");
+    v = e ? atoi(e) : 4;
+  }
+  return v;
+}
+
 static int level_variant() {
   static int v = -1;
   if (v < 0) {
@@ -1069,7 +1078,7 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   const int ntile = (int)ceil_div(ncols, 64);
   FactSched fs{level_segment_rows(n, node, sm_count()), 1, ntile};
   // column-group kernel: 16 or more groups of 8, 32-byte aligned C columns
-  const bool v4 = fact && level_variant() == 4 && ncols % 8 == 0 && ncols / 8 >= 8 && !(ldc & 3) &&
+  const bool v4 = fact && level_variant() == 4 && ncols % 8 == 0 && ncols / 8 >= level4_min_groups() && !(ldc & 3) &&
                   !(reinterpret_cast<uintptr_t>(C) & 31);
   if (v4) fs = level4_schedule(n, node, ncols / 8, sm_count(), level4_maxg(r));
   else if (fact) fs = level_fact_schedule(n, node, ntile, sm_count());
