@@ -144,6 +144,35 @@ def test_lu_known_answers():  # :261-275
     assert piv.sign()[0] == -1.0
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("s", [16, 32, 64, 128])
+def test_lu_nonfinite_and_degenerate_blocks_bit_exact(s, dtype):
+    # NaN wins the pivot search (np.argmax), +-inf, exact ties, zero columns, duplicate
+    # rows (singular flags) -- factors (NaN-aware), pivots and flags as the reference
+    rng = np.random.default_rng(s)
+    nb = 12
+    base = rng.standard_normal((nb, s, s))
+    base[0, 3, 0] = np.nan
+    base[1, :, 2] = 0.0
+    base[2, 5, :] = base[2, 1, :]
+    base[3, 2, 1] = np.inf
+    base[4, 7, 0] = -np.inf
+    base[5] = np.round(base[5])  # many exact ties
+    base[6, :, :] = 0.0  # all-zero block
+    base[7, 4, 4] = np.nan
+    base[8] *= 1e-300 if dtype == np.float64 else 1e-37  # tiny values (subnormal multipliers)
+    base[9, :, 0] = base[9, 0, 0]  # every candidate ties on the first pivot
+    flat = np.ascontiguousarray(base.transpose(0, 2, 1)).astype(dtype).ravel()  # column-major blocks
+    buf = flat.copy()
+    with np.errstate(all="ignore"):
+        piv, _ = batched_lu_factor_inplace([BlockRef(buf, i * s * s, s, s, s) for i in range(nb)])
+        ref = flat.copy()
+        p = orc.lu_factor(orc.sview(ref, 0, s * s, nb, s, s, s))
+    assert np.array_equal(buf, ref, equal_nan=True)
+    assert np.array_equal(piv.swaps, p.swaps) and np.array_equal(piv.perm, p.perm)
+    assert sorted(piv.singular) == sorted(np.flatnonzero(p.singular).tolist())
+
+
 @pytest.mark.parametrize("s,nb", [(64, 512), (32, 300), (16, 1000), (128, 40), (7, 33)])
 def test_lu_bit_exact_vs_reference_order(s, nb):
     rng = np.random.default_rng(s * 1000 + nb)
