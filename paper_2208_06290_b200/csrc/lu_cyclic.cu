@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "lu_device.cuh"
 
 namespace hodlr {
 
@@ -33,37 +34,7 @@ __device__ __forceinline__ bool cyc_beats(T v, int pv, T b, int pb) {
   return v > b || (v == b && pv < pb);
 }
 
-template <typename T>
-__device__ __forceinline__ T cyc_nanmax(T a, T b) {
-  if (a != a) return a;
-  if (b != b) return b;
-  return a > b ? a : b;
-}
 
-
-// np.argmax key of |v|: the IEEE bit pattern of a non-negative number orders
-// like its value, NaN (canonicalised) sorts above +inf, and ties are broken
-// by the smallest logical position -- so the pivot search is two integer
-// max-reductions plus one min-reduction (REDUX), no float compares.
-__device__ __forceinline__ void abs_key(double v, unsigned& hi, unsigned& lo) {
-  unsigned long long b = (v != v) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(fabs(v));
-  hi = (unsigned)(b >> 32);
-  lo = (unsigned)b;
-}
-__device__ __forceinline__ void abs_key(float v, unsigned& hi, unsigned& lo) {
-  hi = (v != v) ? 0x7fc00000u : (unsigned)__float_as_uint(fabsf(v));
-  lo = 0u;
-}
-// warp argmax over (key, pos) with key descending, pos ascending; returns the
-// winning (hi, lo, pos) in every lane (inactive lanes: key 0, pos INT_MAX)
-__device__ __forceinline__ void warp_argmax(unsigned& hi, unsigned& lo, int& pos) {
-  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-  const int mp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? pos : 0x7fffffff);
-  hi = mh;
-  lo = ml;
-  pos = mp;
-}
 
 // opaque select (keeps register arrays in registers)
 __device__ __forceinline__ double csel(int p, double a, double b) {
@@ -371,52 +342,6 @@ __global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __
   }
 }
 
-
-// Diagonal-block inverses of an S x S LU held in shared memory (element (r, c)
-// at T[r * rs + c * cs]): P_q = strict_lower(L_qq^-1) + upper(U_qq^-1) for the
-// 8x8 diagonal tiles, row-major at di + 64 q.  Task = (which, tile, row).
-template <int S>
-__device__ __forceinline__ void diag_block_inverses(const double* T, int rs, int cs, double* di) {
-  for (int u = threadIdx.x; u < 2 * S; u += blockDim.x) {
-    const int which = u / S, q = (u % S) >> 3, i = u & 7, o0 = 8 * q;
-    auto e = [&](int rr, int cc) { return T[(o0 + rr) * rs + (o0 + cc) * cs]; };
-    double x[8];
-    if (which == 0) {  // row i of inv(U_qq)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = 0.0;
-      x[i] = 1.0 / e(i, i);
-#pragma unroll
-      for (int j = 1; j < 8; ++j) {
-        if (j > i) {
-          double sacc = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < j; ++kk)
-            if (kk >= i) sacc = fma(x[kk], e(kk, j), sacc);
-          x[j] = -sacc / e(j, j);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j >= i) di[64 * q + 8 * i + j] = x[j];
-    } else {  // row i of inv(L_qq), unit diagonal
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = (j == i) ? 1.0 : 0.0;
-#pragma unroll
-      for (int j = 6; j >= 0; --j) {
-        if (j < i) {
-          double sacc = 0.0;
-#pragma unroll
-          for (int kk = 1; kk < 8; ++kk)
-            if (kk > j && kk <= i) sacc = fma(x[kk], e(kk, j), sacc);
-          x[j] = -sacc;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < i) di[64 * q + 8 * i + j] = x[j];
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Shared-memory row LU: thread t owns row t of the block, stored row-major in
