@@ -308,6 +308,18 @@ def run_ours(args):
     phases = {name: ph[i] for i, name in enumerate(_lib.PHASES)}
     # accuracy of this step: relres against the HODLR operator
     relres = float(torch.linalg.norm(h0.matvec(x) - b) / torch.linalg.norm(b))
+    # HODLR matvec (hodlr_matvec): HBM-bound, bytes = 8 (m N + 2 r N L) + 24 N
+    mv_ms = []
+    for it in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h0.matvec(x)
+        e1.record()
+        e1.synchronize()
+        if it > 0:
+            mv_ms.append(e0.elapsed_time(e1))
+    mv_t = statistics.median(mv_ms)
+    mv_bytes = 8 * (m * n + 2 * r * n * L) + 24 * n
     del f, x
     if world > 1:
         tt = torch.tensor([t_step, tf, ts], device="cuda")
@@ -366,6 +378,8 @@ def run_ours(args):
             "step_ms_min_med_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
             "solve_gbps": (8 * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 16 * n) / (ts * 1e-3) / 1e9,
             "relres": relres, "flops_factor": f_flops, "flops_solve": s_flops,
+            "matvec": {"ms": mv_t, "GB_per_s": mv_bytes / (mv_t * 1e-3) / 1e9, "bytes": mv_bytes,
+                       "frac_hbm": (mv_bytes / (mv_t * 1e-3) / 1e9 / peaks["hbm_gbs"]) if peaks.get("hbm_gbs") else None},
             "phase_ms": phases, "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "tensor", "kernel": "level_update4_kernel (fused Y update + next-level [W|T]); traffic = "
                                    "mean DRAM bytes per level_update4 launch (ncu, profiles/traffic.json)",

@@ -155,6 +155,17 @@ hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hodlr_factors*
 hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f, void* X, int64_t ldx, int nrhs,
                          void* work, size_t work_bytes, void* stream);
 
+/* HODLR matvec Y = A X on the unfactored representation (SPEC.md:183-191
+ * [OP] matvec): D / U / V in the layout above (U, not the
+ * factored Y), X and Y N x nrhs (ld ldx / ldy, Y must not alias X).  Two HBM
+ * streams: w = V^T X for every child of every level, then Y = D X + U w_sib.
+ * Vector loads when m % 4 == 0 and V / U / D are 4 / 2 / 2-scalar aligned,
+ * scalar loads otherwise.  Per-column results do not depend on nrhs. */
+size_t hodlr_matvec_workspace(const hodlr_desc* d, int nrhs);
+hodlr_status hodlr_matvec(const hodlr_desc* d, const void* D, const void* U, const void* V, const void* X,
+                          int64_t ldx, void* Y, int64_t ldy, int nrhs, void* work, size_t work_bytes,
+                          void* stream);
+
 /* ------------------------------------------------------------------------
  * Row-sharded (multi-GPU) schedule, SURVEY.md §8e.  The caller holds the rows
  * [row0, row0 + n_loc) of one level-p node (n_loc = N / 2^p): its leaves' D

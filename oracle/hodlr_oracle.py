@@ -272,6 +272,24 @@ def dense(h: HodlrData) -> np.ndarray:
     return A
 
 
+def matvec(h: HodlrData, x: np.ndarray) -> np.ndarray:
+    """A x block-wise (SPEC.md:183-191 [OP] matvec):
+    y(I_a) = D_a x(I_a) + sum_l' U_c (V_sib^T x_sib) over the sibling pairs,
+    without forming A.  x: (N,) or (N, k)."""
+    lay = h.lay
+    n, m, r, L = lay.n, lay.m, lay.r, lay.L
+    X = np.asarray(x, dtype=h.D.dtype).reshape(n, -1)
+    Dm = h.D.reshape(1 << L, m, m).transpose(0, 2, 1)  # block a row-major (column-major storage)
+    y = np.einsum("aij,ajk->aik", Dm, X.reshape(1 << L, m, -1)).reshape(n, -1)
+    for lv in range(1, L + 1):
+        nl = n >> lv
+        U = h.U[(lv - 1) * r * n : lv * r * n].reshape(r, n).T.reshape(1 << (lv - 1), 2, nl, r)
+        V = h.V[(lv - 1) * r * n : lv * r * n].reshape(r, n).T.reshape(1 << (lv - 1), 2, nl, r)
+        w = np.einsum("pcir,pcik->pcrk", V, X.reshape(1 << (lv - 1), 2, nl, -1))  # V_c^T x_c
+        y += np.einsum("pcir,pcrk->pcik", U, w[:, ::-1]).reshape(n, -1)  # child 0 gets U_0 w_1
+    return y.reshape(np.shape(x))
+
+
 # ---------------------------------------------------------------------------
 # factorize / solve drivers (PAPER Alg. 3/4, SPEC.md:296-419, SURVEY App. B)
 # ---------------------------------------------------------------------------

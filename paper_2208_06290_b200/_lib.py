@@ -68,6 +68,8 @@ SIGNATURES = {
     "hodlr_solve_local": (_i, [C.POINTER(Desc), C.POINTER(Factors), _i64, _i64, _i, _p, _i64, _i, _p, _p, _sz, _p]),
     "hodlr_solve_top": (_i, [C.POINTER(Desc), C.POINTER(Factors), _i64, _i64, _i, _p, _p, _p, _i64, _i, _p, _sz, _p]),
     "hodlr_solve": (_i, [C.POINTER(Desc), C.POINTER(Factors), _p, _i64, _i, _p, _sz, _p]),
+    "hodlr_matvec_workspace": (_sz, [C.POINTER(Desc), _i]),
+    "hodlr_matvec": (_i, [C.POINTER(Desc), _p, _p, _p, _p, _i64, _p, _i64, _i, _p, _sz, _p]),
 }
 
 _lib = None

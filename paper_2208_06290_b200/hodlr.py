@@ -114,25 +114,36 @@ class HodlrMatrix:
             "factorization_scalars_thm2": m * n + r * n * L,
         }
 
-    def matvec(self, x):
-        """A x on the device (block-wise U (V^T x)); x is (N,) or (N, k) torch."""
+    def matvec(self, x, stream=None):
+        """A x on the device: ``hodlr_matvec``, two HBM
+        streams (w = V^T x for all levels, then D x + U w_sibling).  ``x`` is
+        (N,) or (N, k) torch (device or host) or numpy; same kind/shape out."""
         torch = _torch()
-        n, m, r, L = self.n, self.m, self.rank, self.L
-        X = x.reshape(n, -1)
-        Dm = self.D.view(1 << L, m, m).transpose(1, 2)  # row-major view of column-major blocks
-        y = torch.bmm(Dm, X.view(1 << L, m, -1)).reshape(n, -1)
-        for lv in range(1, L + 1):
-            nl = n >> lv
-            U = self.U[(lv - 1) * r * n : lv * r * n].view(r, n).t()  # (n, r)
-            V = self.V[(lv - 1) * r * n : lv * r * n].view(r, n).t()
-            Ub = U.reshape(1 << (lv - 1), 2, nl, r)
-            Vb = V.reshape(1 << (lv - 1), 2, nl, r)
-            Xb = X.reshape(1 << (lv - 1), 2, nl, -1)
-            w = torch.einsum("pcir,pcik->pcrk", Vb, Xb)  # V_c^T x_c
-            # A[I_a, I_b] = U_a V_b^T: child 0 receives U_0 w_1, child 1 receives U_1 w_0
-            contrib = torch.einsum("pcir,pcrk->pcik", Ub, w.flip(1))
-            y += contrib.reshape(n, -1)
-        return y.reshape(x.shape)
+        lib = _lib.load()
+        is_np = isinstance(x, np.ndarray)
+        xt = torch.from_numpy(np.ascontiguousarray(x)) if is_np else x
+        n = self.n
+        if xt.dim() not in (1, 2) or xt.shape[0] != n:
+            raise ValueError(f"matvec: x must have {n} rows (got shape {tuple(xt.shape)})")
+        nrhs = 1 if xt.dim() == 1 else xt.shape[1]
+        dev = self.D.device
+        X = xt.reshape(n, nrhs).t().to(device=dev, dtype=self.dtype).contiguous()  # column-major N x nrhs
+        Y = torch.empty_like(X)
+        desc = self.desc()
+        wsb = lib.hodlr_matvec_workspace(C.byref(desc), nrhs)
+        ws = _workspace(wsb, dev) if wsb else None
+        st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        _lib.check(
+            lib.hodlr_matvec(C.byref(desc), C.c_void_p(self.D.data_ptr()), C.c_void_p(self.U.data_ptr()),
+                             C.c_void_p(self.V.data_ptr()), C.c_void_p(X.data_ptr()), n,
+                             C.c_void_p(Y.data_ptr()), n, nrhs, C.c_void_p(ws.data_ptr() if ws is not None else 0),
+                             wsb, C.c_void_p(st)),
+            "hodlr_matvec",
+        )
+        out = Y.t().reshape(xt.shape)
+        if is_np:
+            return out.cpu().numpy()
+        return out.to(xt.device) if xt.device != dev else out
 
     def reconstruct_dense(self):
         torch = _torch()

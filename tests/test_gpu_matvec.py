@@ -1,0 +1,116 @@
+"""GPU: hodlr_matvec against the oracle.
+
+Bars: fp64 within 1e-13 relative of the oracle's dense product;
+fp32 within 1e-5; the SPEC known answers exactly; every column of a
+multi-RHS product bit-identical to the single-vector product (the per-column
+summation order depends only on the shape); the scalar-load path (m % 4 != 0
+or misaligned slabs) equal to the vector path's answer within rounding.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import hodlr_oracle as orc  # noqa: E402
+import paper_2208_06290_b200 as hb  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def to_gpu(h, dtype=None):
+    hm = hb.HodlrMatrix.from_buffers(h.lay.n, h.lay.m, h.lay.r, h.D, h.U, h.V)
+    if dtype is not None:
+        hm = hb.HodlrMatrix(hm.tree, hm.rank, hm.D.to(dtype), hm.U.to(dtype), hm.V.to(dtype))
+    return hm
+
+
+def test_spec_known_answers():
+    h = orc.HodlrData(orc.Layout(2, 1, 1), np.array([2.0, 2.0]), np.array([1.0, 1.0]), np.array([1.0, 1.0]))
+    assert hb.HodlrMatrix.from_buffers(2, 1, 1, h.D, h.U, h.V).matvec(np.array([1.0, 1.0])).tolist() == [3.0, 3.0]
+    n, m, r, L = 1024, 64, 8, 4
+    eye = hb.HodlrMatrix.from_buffers(n, m, r, np.tile(np.eye(m).ravel(), 1 << L), np.zeros(n * r * L),
+                                      np.zeros(n * r * L))
+    x = np.random.default_rng(0).standard_normal(n)
+    assert np.array_equal(eye.matvec(x), x)
+
+
+@pytest.mark.parametrize("n,m,r", [(1024, 64, 8), (4096, 32, 16), (2048, 64, 32), (1536, 48, 8), (768, 6, 4),
+                                   (512, 16, 1), (64, 64, 8), (8192, 16, 4)])
+@pytest.mark.parametrize("nrhs", [1, 3, 11])
+def test_matvec_vs_dense(n, m, r, nrhs):
+    h = orc.make_exact_hodlr(n, m, r, seed=n + m + r, s=8.0)
+    X = np.random.default_rng(nrhs).standard_normal((n, nrhs) if nrhs > 1 else n)
+    y = to_gpu(h).matvec(torch.from_numpy(X).cuda()).cpu().numpy()
+    ref = orc.dense(h) @ X if n <= 4096 else orc.matvec(h, X)
+    assert rel(y, ref) <= 1e-13
+
+
+def test_matvec_columns_bitwise():
+    h = orc.make_exact_hodlr(1 << 14, 64, 16, seed=7, s=4.0)
+    hm = to_gpu(h)
+    X = torch.randn(1 << 14, 13, dtype=torch.float64, device="cuda")
+    Y = hm.matvec(X)
+    for k in (0, 4, 8, 12):
+        assert torch.equal(Y[:, k], hm.matvec(X[:, k].contiguous()))
+    assert torch.equal(Y[:, :5], hm.matvec(X[:, :5].contiguous()))
+
+
+def test_matvec_scalar_path_matches_vector_path():
+    # a 1-scalar-offset view of the slabs forces the scalar-load kernels
+    n, m, r = 4096, 64, 8
+    h = orc.make_exact_hodlr(n, m, r, seed=11, s=2.0)
+    hm = to_gpu(h)
+    L = hm.L
+
+    def shifted(t):
+        buf = torch.empty(t.numel() + 1, dtype=t.dtype, device=t.device)
+        buf[1:] = t
+        return buf[1:]
+
+    hs = hb.HodlrMatrix(hm.tree, r, shifted(hm.D), shifted(hm.U), shifted(hm.V))
+    assert hs.V.data_ptr() % 32 != 0
+    x = torch.randn(n, 2, dtype=torch.float64, device="cuda")
+    assert rel(hs.matvec(x).cpu(), hm.matvec(x).cpu()) <= 1e-15
+    assert L == 6
+
+
+def test_matvec_fp32():
+    n, m, r = 1 << 13, 64, 8
+    h = orc.make_exact_hodlr(n, m, r, seed=3, s=4.0)
+    x = np.random.default_rng(3).standard_normal((n, 2))
+    y = to_gpu(h, torch.float32).matvec(torch.from_numpy(x).float().cuda()).double().cpu().numpy()
+    assert rel(y, orc.matvec(h, x)) <= 1e-5
+
+
+def test_matvec_large_linearity_and_solve_roundtrip():
+    # cfg2-scale shape (N = 2^18 here to keep the test short): A (x1 + x2) = A x1 + A x2 within
+    # rounding, and A (A^-1 b) = b to the solve's residual
+    n, m, r = 1 << 18, 64, 32
+    h = orc.make_exact_hodlr(n, m, r, seed=5, s=1.0)
+    hm = to_gpu(h)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x1 = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    x2 = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    lhs = hm.matvec(x1 + x2)
+    assert float(torch.linalg.norm(lhs - hm.matvec(x1) - hm.matvec(x2)) / torch.linalg.norm(lhs)) <= 1e-14
+    ref = orc.matvec(h, (x1 + x2).cpu().numpy())
+    assert rel(lhs.cpu().numpy(), ref) <= 1e-13
+    f = hb.factorize(hm.clone())
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    x = hb.solve(f, b)
+    assert float(torch.linalg.norm(hm.matvec(x) - b) / torch.linalg.norm(b)) <= 1e-12
+
+
+def test_matvec_errors():
+    h = orc.make_exact_hodlr(1024, 64, 8, seed=1)
+    hm = to_gpu(h)
+    with pytest.raises(ValueError):
+        hm.matvec(torch.zeros(1000, dtype=torch.float64, device="cuda"))

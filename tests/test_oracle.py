@@ -147,3 +147,19 @@ def test_reference_driver_matches_oracle_bitwise_threaded():
     b = np.random.default_rng(2).standard_normal((n, 1))
     x = rd.ref_solve(D, dpiv, Y, V, Ks, kp, b, n, m, r, h.lay.L, rd.executor(4))
     assert x.tobytes() == orc.solve(fo, b, threads=4).tobytes()
+
+
+def test_matvec_spec_examples_and_dense():
+    # [[2,1],[1,2]] x [1,1] -> [3,3]; identity -> x; n=256 vs dense <= 1e-13
+    h = orc.HodlrData(orc.Layout(2, 1, 1), np.array([2.0, 2.0]), np.array([1.0, 1.0]), np.array([1.0, 1.0]))
+    assert orc.matvec(h, np.array([1.0, 1.0])).tolist() == [3.0, 3.0]
+    n, m, r = 256, 16, 4
+    L = 4
+    eye = orc.HodlrData(orc.Layout(n, m, r), np.tile(np.eye(m).ravel(), 1 << L), np.zeros(n * r * L),
+                        np.zeros(n * r * L))
+    x = np.random.default_rng(1).standard_normal(n)
+    assert np.array_equal(orc.matvec(eye, x), x)
+    h = orc.make_exact_hodlr(n, m, r, seed=2, s=4.0)
+    X = np.random.default_rng(2).standard_normal((n, 3))
+    A = orc.dense(h)
+    assert np.linalg.norm(orc.matvec(h, X) - A @ X) <= 1e-13 * np.linalg.norm(A @ X)
