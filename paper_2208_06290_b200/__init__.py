@@ -26,6 +26,7 @@ from .hodlr import (  # noqa: F401
     HodlrFactorization,
     HodlrMatrix,
     HodlrSingularError,
+    RefinementResult,
     factorize,
     factorize_from_host,
     flop_report,
@@ -33,6 +34,7 @@ from .hodlr import (  # noqa: F401
     random_hodlr,
     solve,
     solve_flops,
+    solve_with_refinement,
 )
 from ._lib import HodlrNativeError, LIB_PATH  # noqa: F401
 

@@ -433,6 +433,64 @@ def logdet(fact: HodlrFactorization):
     return float(logabs), (-1.0 if parity else 1.0)
 
 
+@dataclass
+class RefinementResult:
+    """Best iterate of :func:`solve_with_refinement` plus its relres history."""
+
+    x: "object"
+    history: list
+    iterations: int
+    diverged: bool
+
+
+def solve_with_refinement(fact: HodlrFactorization, h: HodlrMatrix, b, max_iters: int = 10,
+                          tol: float = 0.0) -> RefinementResult:
+    """Iterative refinement x <- x + fact.solve(b - A x).
+
+    ``h`` is the unfactored operator in the working precision (its dtype is
+    the refinement dtype; ``fact`` may be a lower-precision factorization,
+    e.g. the fp32 preconditioner of cfg4).  Residuals use the device matvec
+    (``hodlr_matvec``).  Stops after ``max_iters`` corrections, once relres
+    <= ``tol``, or when relres stops improving; divergence (relres grows on
+    two consecutive iterations) returns the best iterate with
+    ``diverged=True``.  ``history[k]`` is the relres after k corrections.
+    """
+    torch = _torch()
+    is_np = isinstance(b, np.ndarray)
+    bt = torch.from_numpy(np.ascontiguousarray(b)) if is_np else b
+    dev = h.D.device
+    bw = bt.to(device=dev, dtype=h.dtype)
+    nb = float(torch.linalg.norm(bw))
+
+    def out(x, hist, it, div):
+        xo = x.cpu().numpy() if is_np else (x.to(bt.device) if bt.device != dev else x)
+        return RefinementResult(xo, hist, it, div)
+
+    if nb == 0.0:  # b = 0 -> x = 0 immediately
+        return out(torch.zeros_like(bw), [0.0], 0, False)
+    x = solve(fact, bw).to(h.dtype)
+    res = bw - h.matvec(x)
+    rel = float(torch.linalg.norm(res)) / nb
+    hist = [rel]
+    best, best_rel, stall, diverged, it = x, rel, 0, False, 0
+    while it < max_iters and best_rel > tol:
+        x = x + solve(fact, res).to(h.dtype)
+        it += 1
+        res = bw - h.matvec(x)
+        new = float(torch.linalg.norm(res)) / nb
+        hist.append(new)
+        if new < best_rel * (1.0 - 1e-3):  # still improving
+            best, best_rel, stall = x, new, 0
+            continue
+        stall += 1
+        if len(hist) >= 3 and hist[-1] > hist[-2] > hist[-3]:  # grew on two consecutive iterations
+            diverged = True
+            break
+        if stall >= 2:  # stopped improving
+            break
+    return out(best, hist, it, diverged)
+
+
 # ---------------------------------------------------------------------------
 # synthetic inputs (SURVEY.md §8d exact-HODLR stand-in), generated on device
 # ---------------------------------------------------------------------------

@@ -114,3 +114,34 @@ def test_matvec_errors():
     hm = to_gpu(h)
     with pytest.raises(ValueError):
         hm.matvec(torch.zeros(1000, dtype=torch.float64, device="cuda"))
+
+
+def test_refinement_spec_examples():
+    n, m, r = 4096, 64, 16
+    h = orc.make_exact_hodlr(n, m, r, seed=21, s=2.0)
+    hm = to_gpu(h)
+    f = hb.factorize(hm.clone())
+    # b = 0 -> x = 0 immediately
+    res = hb.solve_with_refinement(f, hm, np.zeros(n))
+    assert res.iterations == 0 and not res.x.any()
+    # exact factorization: converged after the first solve (relres at rounding level), at most
+    # the two stall iterations follow and do not improve materially
+    b = np.random.default_rng(1).standard_normal(n)
+    res = hb.solve_with_refinement(f, hm, b, max_iters=5)
+    assert res.history[0] <= 1e-13 and min(res.history) <= res.history[0]
+    assert rel(orc.dense(h) @ res.x, b) <= 1e-13 and not res.diverged
+
+
+def test_refinement_fp32_preconditioner_reaches_fp64():
+    # cfg4-style: fp32 factorization as the preconditioner, fp64 operator for the residual
+    n, m, r = 1 << 16, 64, 8
+    h = orc.make_exact_hodlr(n, m, r, seed=4, s=4.0)
+    h64 = to_gpu(h)
+    f32 = hb.factorize(to_gpu(h, torch.float32))
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(2))
+    res = hb.solve_with_refinement(f32, h64, b, max_iters=8)
+    hist = res.history
+    assert hist[0] > 1e-8  # fp32 accuracy after the first solve
+    assert all(hist[k + 1] < hist[k] for k in range(3))  # monotone for >= 3 iterations
+    assert min(hist) <= 1e-13 and not res.diverged
+    assert float(torch.linalg.norm(h64.matvec(res.x) - b) / torch.linalg.norm(b)) == pytest.approx(min(hist))

@@ -65,6 +65,32 @@ if "cfg3" in which:
 if "cfg4" in which:
     tf, ts, res = time_factor_solve(1 << 21, 64, 8, torch.float32)
     line("cfg4", 1 << 21, 64, 8, "f32", tf, ts, res)
+if "cfg4r" in which or "cfg4" in which:
+    # cfg4 as a preconditioner: fp32 factorization + fp64-operator refinement
+    n, m, r = 1 << 21, 64, 8
+    h64 = hb.random_hodlr(n, m, r, seed=0, s=1.0)
+    h32 = hb.HodlrMatrix(h64.tree, r, h64.D.float(), h64.U.float(), h64.V.float())
+    b = torch.randn(n, dtype=torch.float64, device="cuda")
+    runs = []
+    for it in range(4):
+        torch.cuda.synchronize()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(); f32 = hb.factorize(h32.clone(), check=False); e[1].record()
+        res = hb.solve_with_refinement(f32, h64, b, max_iters=10, tol=1e-12); e[2].record()
+        torch.cuda.synchronize()
+        if it >= 1:
+            runs.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), res))
+        del f32
+    tf = statistics.median(t[0] for t in runs); tr = statistics.median(t[1] for t in runs)
+    res = runs[-1][2]
+    tf64, ts64, res64 = time_factor_solve(n, m, r, torch.float64, reps=3)
+    print(json.dumps({"config": "cfg4 preconditioner: fp32 factor + fp64 refinement", "N": n, "leaf": m, "rank": r,
+                      "t_factor_f32_ms": round(tf, 3), "t_refine_ms": round(tr, 3),
+                      "iterations": res.iterations, "relres_history": res.history,
+                      "fp64_direct": {"t_factor_ms": round(tf64, 3), "t_solve_ms": round(ts64, 3), "relres": res64}}),
+          flush=True)
+    del h64, h32
+    torch.cuda.empty_cache()
 if "cfg5" in which:
     n, m, r = 1 << 20, 64, 32
     f = hb.factorize(hb.random_hodlr(n, m, r, seed=0, s=1.0), check=False)
