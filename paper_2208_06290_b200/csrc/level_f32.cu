@@ -36,60 +36,83 @@ struct LevelF32Args {
   int partial;
 };
 
-// one warp per CTA: work item = (segment, 8-column chunk)
-__global__ void __launch_bounds__(32) level_f32_kernel(LevelF32Args g) {
+// one warp per CTA: work item = (segment, 8-column chunk).  The W' blocks of
+// all children in the segment are staged in shared memory up front; each lane
+// then streams two rows per iteration (all 48 loads issued before use).
+constexpr int F32_MAXCH = F32_SEG / 32;  // children per segment (n_c >= 32)
+
+__global__ void __launch_bounds__(32, 16) level_f32_kernel(LevelF32Args g) {
   constexpr int R = F32_R;
   const int lane = threadIdx.x;
   const int seg = blockIdx.x / g.chunks, chunk = blockIdx.x % g.chunks;
   const int col0 = chunk * 8;
   const int ncw = min(8, g.ncols - col0);  // columns of this warp (ragged last chunk)
   const int64_t seg0 = (int64_t)seg * g.seg_rows;
+  const float* __restrict__ A1 = g.A1;
+  const float* __restrict__ V = g.V;
+  float* __restrict__ C = g.C;
+  __shared__ __align__(16) float ws[F32_MAXCH][R][8];  // W' of the segment's children (broadcast reads)
+  const int64_t ch0 = seg0 / g.n_c;
+  const int nch = (int)ceil_div(g.seg_rows, g.n_c);
+  if (g.W) {
+    for (int e = lane; e < nch * R * 8; e += 32) {
+      const int cc = e / (R * 8), k = e % R, j = (e / R) % 8;
+      const int64_t ch = ch0 + cc;
+      const float* wp = g.W + (ch >> 1) * g.wstride + (ch & 1) * R;
+      ws[cc][k][j] = (j < ncw) ? __ldg(wp + k + (int64_t)(col0 + j) * (2 * R)) : 0.f;
+    }
+    __syncwarp();
+  }
   float tw[R][8];
 #pragma unroll
   for (int k = 0; k < R; ++k)
 #pragma unroll
     for (int j = 0; j < 8; ++j) tw[k][j] = 0.f;
-  __shared__ float w[R][8];  // W' block of the current child (broadcast reads)
-  int64_t wchild = -1;
+  const int nc32 = (int)(g.n_c / 32);  // 32-row groups per child
 #pragma unroll 1
-  for (int64_t i = lane; i < g.seg_rows; i += 32) {
-    const int64_t row = seg0 + i;
-    float c[8];
+  for (int i0 = 0; i0 < g.seg_rows; i0 += 64) {
+    float c[2][8], a[2][R], v[2][R];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) c[j] = (j < ncw) ? g.C[row + (int64_t)(col0 + j) * g.ldc] : 0.f;
-    if (g.W) {
-      const int64_t ch = row / g.n_c;  // warp-uniform (n_c >= 32)
-      if (ch != wchild) {
-        const float* wp = g.W + (ch >> 1) * g.wstride + (ch & 1) * R;
-        __syncwarp();
+    for (int u = 0; u < 2; ++u) {
+      const int64_t row = seg0 + i0 + 32 * u + lane;
 #pragma unroll
-        for (int e = lane; e < R * 8; e += 32) {
-          const int k = e % R, j = e / R;
-          w[k][j] = (j < ncw) ? __ldg(wp + k + (int64_t)(col0 + j) * (2 * R)) : 0.f;
-        }
-        __syncwarp();
-        wchild = ch;
+      for (int j = 0; j < 8; ++j) c[u][j] = (j < ncw) ? C[row + (int64_t)(col0 + j) * g.ldc] : 0.f;
+      if (g.W) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) a[u][k] = __ldg(A1 + row + (int64_t)k * g.lda);
       }
-      float a[R];
+      if (V) {
 #pragma unroll
-      for (int k = 0; k < R; ++k) a[k] = __ldg(g.A1 + row + (int64_t)k * g.lda);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float t = 0.f;
-#pragma unroll
-        for (int k = 0; k < R; ++k) t = fmaf(a[k], w[k][j], t);
-        c[j] = __fsub_rn(c[j], t);
+        for (int k = 0; k < R; ++k) v[u][k] = __ldg(V + row + (int64_t)k * g.lda);
       }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < ncw) g.C[row + (int64_t)(col0 + j) * g.ldc] = c[j];
     }
-    if (g.V) {
 #pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const float v = __ldg(g.V + row + (int64_t)k * g.lda);
+    for (int u = 0; u < 2; ++u) {
+      const int64_t row = seg0 + i0 + 32 * u + lane;
+      if (g.W) {
+        const int cc = ((i0 >> 5) + u) / nc32;  // child within the segment (warp-uniform)
+        float t[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) tw[k][j] = fmaf(v, c[j], tw[k][j]);
+        for (int j = 0; j < 8; ++j) t[j] = 0.f;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {  // W' row k as two broadcast 16-byte loads
+          const float4 w0 = *reinterpret_cast<const float4*>(&ws[cc][k][0]);
+          const float4 w1 = *reinterpret_cast<const float4*>(&ws[cc][k][4]);
+          const float wk[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t[j] = fmaf(a[u][k], wk[j], t[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[u][j] = __fsub_rn(c[u][j], t[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < ncw) C[row + (int64_t)(col0 + j) * g.ldc] = c[u][j];
+      }
+      if (V) {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) tw[k][j] = fmaf(v[u][k], c[u][j], tw[k][j]);
       }
     }
   }
@@ -141,9 +164,9 @@ hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* 
                        const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
                        int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st) {
   if (ncols == 0) return HODLR_OK;
-  if (r != F32_R || n_c < 32 || n % 32 || node_rows % 32) return HODLR_ERR_ARG;
+  if (r != F32_R || n_c < 32 || n_c % 32 || n % 64 || node_rows % 64) return HODLR_ERR_ARG;
   const int64_t seg = std::min<int64_t>(node_rows, F32_SEG);
-  if (n % seg || (node_rows % seg)) return HODLR_ERR_ARG;
+  if (n % seg || (node_rows % seg) || seg % 64) return HODLR_ERR_ARG;
   const int64_t nseg = n / seg;
   const bool split = seg < node_rows && V != nullptr;
   if (split && (size_t)nseg * F32_R * ncols * sizeof(float) > part_bytes) return HODLR_ERR_ARG;

@@ -532,37 +532,57 @@ hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds,
   return HODLR_OK;
 }
 
-// Thread-per-column substitution for S in {16, 32, 64}: the block's LU is
-// staged once in shared memory, every thread carries one right-hand-side column
-// in registers (fully unrolled, compile-time indices) and runs the
+// Thread-per-column substitution for S in {16, 32, 64}: the block's LU and a
+// CW-column slice of the right-hand sides are staged in shared memory with
+// coalesced loads (a column's S rows are contiguous), every thread carries one
+// column in registers (fully unrolled, compile-time indices) and runs the
 // column-oriented (axpy) forward / backward sweeps -- after x_j is final the
 // S-1-j updates it feeds are independent, so each thread has S-way ILP and no
-// barrier is needed between steps.  L / U columns are read as broadcast
-// 16-byte shared loads.
+// barrier is needed between steps.  L / U entries are broadcast shared loads.
+// Per element the update order is j ascending (forward) / descending
+// (backward) with fused multiply-subtract and true division, exactly as in
+// getrs_warp_kernel, so a column's result does not depend on nrhs.
+template <int S>
+struct ColCfg {
+  static constexpr int CW = S == 64 ? 64 : 128;  // columns (threads) per CTA
+  static constexpr int P = CW + 1;               // staging pitch
+  static constexpr int MINB = S == 64 ? 8 : 1;   // S = 64: cap registers (x[64] + operands) for 16 warps/SM
+};
+
 template <typename T, int S>
-__global__ void __launch_bounds__(128) getrs_col_kernel(int nrhs, int cpb, const T* __restrict__ LU, int64_t lda,
-                                                        int64_t strideA, const int32_t* __restrict__ perm, const T* B,
-                                                        int64_t ldb, int64_t strideB, T* X, int64_t ldx,
-                                                        int64_t strideX, int identity) {
+__global__ void __launch_bounds__(ColCfg<S>::CW, ColCfg<S>::MINB) getrs_col_kernel(int nrhs, int cpb, const T* __restrict__ LU,
+                                                                  int64_t lda, int64_t strideA,
+                                                                  const int32_t* __restrict__ perm, const T* B,
+                                                                  int64_t ldb, int64_t strideB, T* X, int64_t ldx,
+                                                                  int64_t strideX, int identity) {
+  constexpr int CW = ColCfg<S>::CW, P = ColCfg<S>::P;
   __shared__ __align__(16) T lu[S * S];  // column-major, ld S
+  __shared__ T xs[S * P];                // [row][column]
   __shared__ int pm[S];
   const int64_t blk = blockIdx.x / cpb;
-  const int c = (int)(blockIdx.x % cpb) * 128 + threadIdx.x;
+  const int c0 = (int)(blockIdx.x % cpb) * CW;
+  const int ncw = min(CW, nrhs - c0);
+  const int t = threadIdx.x;
   const T* g = LU + blk * strideA;
-  for (int idx = threadIdx.x; idx < S * S; idx += 128) lu[idx] = g[(idx % S) + (int64_t)(idx / S) * lda];
-  if (threadIdx.x < S) pm[threadIdx.x] = perm[blk * S + threadIdx.x];
+  for (int idx = t; idx < S * S; idx += CW) lu[idx] = g[(idx % S) + (int64_t)(idx / S) * lda];
+  if (t < S) pm[t] = perm[blk * S + t];
+  if (!identity) {
+    const T* gb = B + blk * strideB + (int64_t)c0 * ldb;
+    for (int idx = t; idx < S * ncw; idx += CW) {
+      const int i = idx % S, c = idx / S;
+      xs[i * P + c] = gb[i + (int64_t)c * ldb];
+    }
+  }
   __syncthreads();
-  if (c >= nrhs) return;
   T x[S];
-  const T* gb = B + blk * strideB + (int64_t)c * ldb;
 #pragma unroll
-  for (int i = 0; i < S; ++i) x[i] = identity ? (T)(pm[i] == c) : gb[pm[i]];
+  for (int i = 0; i < S; ++i) x[i] = identity ? (T)(pm[i] == c0 + t) : xs[pm[i] * P + t];
   // forward: unit lower
 #pragma unroll
   for (int j = 0; j < S - 1; ++j) {
     const T xj = x[j];
 #pragma unroll
-    for (int i = j + 1; i < S; ++i) x[i] -= lu[i + j * S] * xj;
+    for (int i = j + 1; i < S; ++i) x[i] = fma(-lu[i + j * S], xj, x[i]);
   }
   // backward: upper with true division
 #pragma unroll
@@ -570,22 +590,103 @@ __global__ void __launch_bounds__(128) getrs_col_kernel(int nrhs, int cpb, const
     x[j] = x[j] / lu[j + j * S];
     const T xj = x[j];
 #pragma unroll
-    for (int i = 0; i < j; ++i) x[i] -= lu[i + j * S] * xj;
+    for (int i = 0; i < j; ++i) x[i] = fma(-lu[i + j * S], xj, x[i]);
   }
+  __syncthreads();  // every thread has read its column (X may alias B)
+#pragma unroll
+  for (int i = 0; i < S; ++i) xs[i * P + t] = x[i];
+  __syncthreads();
+  T* gx = X + blk * strideX + (int64_t)c0 * ldx;
+  for (int idx = t; idx < S * ncw; idx += CW) {
+    const int i = idx % S, c = idx / S;
+    gx[i + (int64_t)c * ldx] = xs[i * P + c];
+  }
+}
+
+// Few right-hand sides: warp per (block, column), lane = rows lane + 32 q.  The
+// LU columns are read straight from global memory (one coalesced line per
+// column step); x_j is broadcast from its owner lane.  Same per-element
+// operation order as getrs_col_kernel (bit-identical columns).
+template <typename T, int S>
+__global__ void __launch_bounds__(256) getrs_warp_kernel(int nrhs, int batch, const T* __restrict__ LU, int64_t lda,
+                                                         int64_t strideA, const int32_t* __restrict__ perm,
+                                                         const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx,
+                                                         int64_t strideX, int identity) {
+  constexpr int Q = S > 32 ? 2 : 1;  // rows per lane (S <= 64)
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (item >= (int64_t)batch * nrhs) return;
+  const int64_t blk = item / nrhs;
+  const int c = (int)(item % nrhs);
+  const T* g = LU + blk * strideA;
+  const int32_t* pb = perm + blk * S;
+  const T* gb = B + blk * strideB + (int64_t)c * ldb;
+  T x[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = lane + 32 * q;
+    x[q] = T(0);
+    if (i < S) {
+      const int pi = __ldg(pb + i);
+      x[q] = identity ? (T)(pi == c) : gb[pi];
+    }
+  }
+  // x_j lives in register j / 32 of lane j % 32 (select, not a dynamic index)
+  auto own = [&](int j) -> T& { return (Q == 1 || j < 32) ? x[0] : x[Q - 1]; };
+  // forward: unit lower
+#pragma unroll 4
+  for (int j = 0; j < S - 1; ++j) {
+    const T xj = __shfl_sync(0xffffffffu, own(j), j % 32);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      if (i > j && i < S) x[q] = fma(-__ldg(g + i + (int64_t)j * lda), xj, x[q]);
+    }
+  }
+  // backward: upper with true division
+#pragma unroll 4
+  for (int j = S - 1; j >= 0; --j) {
+    if ((j % 32) == lane) own(j) = own(j) / __ldg(g + j + (int64_t)j * lda);
+    const T xj = __shfl_sync(0xffffffffu, own(j), j % 32);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      if (i < j) x[q] = fma(-__ldg(g + i + (int64_t)j * lda), xj, x[q]);
+    }
+  }
+  __syncwarp();  // all lanes have read B (X may alias B)
   T* gx = X + blk * strideX + (int64_t)c * ldx;
 #pragma unroll
-  for (int i = 0; i < S; ++i) gx[i] = x[i];
+  for (int q = 0; q < Q; ++q) {
+    const int i = lane + 32 * q;
+    if (i < S) gx[i] = x[q];
+  }
 }
 
 template <typename T, int S>
 static hodlr_status run_getrs_col(int nrhs, int batch, const T* LU, int64_t lda, int64_t strideA, const int32_t* perm,
                                   const T* B, int64_t ldb, int64_t strideB, T* X, int64_t ldx, int64_t strideX,
                                   int identity, cudaStream_t st) {
-  const int cpb = (nrhs + 127) / 128;
+  if (nrhs <= 8) {
+    const int64_t items = (int64_t)batch * nrhs;
+    const int64_t grid = ceil_div(items, 8);
+    if (grid > 2147483647LL) return HODLR_ERR_ARG;
+    getrs_warp_kernel<T, S><<<(unsigned)grid, 256, 0, st>>>(nrhs, batch, LU, lda, strideA, perm, B, ldb, strideB, X,
+                                                           ldx, strideX, identity);
+    HODLR_CHECK_LAUNCH();
+    return HODLR_OK;
+  }
+  constexpr int CW = ColCfg<S>::CW;
+  const int cpb = (nrhs + CW - 1) / CW;
   const int64_t grid = (int64_t)batch * cpb;
   if (grid > 2147483647LL) return HODLR_ERR_ARG;
-  getrs_col_kernel<T, S><<<(unsigned)grid, 128, 0, st>>>(nrhs, cpb, LU, lda, strideA, perm, B, ldb, strideB, X, ldx,
-                                                        strideX, identity);
+  static const bool carve = [] {
+    cudaFuncSetAttribute(getrs_col_kernel<T, S>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)carve;
+  getrs_col_kernel<T, S><<<(unsigned)grid, CW, 0, st>>>(nrhs, cpb, LU, lda, strideA, perm, B, ldb, strideB, X, ldx,
+                                                       strideX, identity);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
