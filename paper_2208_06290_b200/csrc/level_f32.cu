@@ -41,7 +41,7 @@ struct LevelF32Args {
 // then streams two rows per iteration (all 48 loads issued before use).
 constexpr int F32_MAXCH = F32_SEG / 32;  // children per segment (n_c >= 32)
 
-__global__ void __launch_bounds__(32, 16) level_f32_kernel(LevelF32Args g) {
+__global__ void __launch_bounds__(32, 12) level_f32_kernel(LevelF32Args g) {
   constexpr int R = F32_R;
   const int lane = threadIdx.x;
   const int seg = blockIdx.x / g.chunks, chunk = blockIdx.x % g.chunks;
@@ -68,29 +68,36 @@ __global__ void __launch_bounds__(32, 16) level_f32_kernel(LevelF32Args g) {
   for (int k = 0; k < R; ++k)
 #pragma unroll
     for (int j = 0; j < 8; ++j) tw[k][j] = 0.f;
-  const int nc32 = (int)(g.n_c / 32);  // 32-row groups per child
+  const int ncr = (int)g.n_c;
 #pragma unroll 1
   for (int i0 = 0; i0 < g.seg_rows; i0 += 64) {
+    // lane owns rows i0 + 2 lane + {0, 1}: 8-byte loads of C, Y^{l+1} and V
+    const int64_t row = seg0 + i0 + 2 * lane;
     float c[2][8], a[2][R], v[2][R];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t row = seg0 + i0 + 32 * u + lane;
+    for (int j = 0; j < 8; ++j) {
+      const float2 t = (j < ncw) ? *reinterpret_cast<const float2*>(C + row + (int64_t)(col0 + j) * g.ldc)
+                                 : make_float2(0.f, 0.f);
+      c[0][j] = t.x, c[1][j] = t.y;
+    }
+    if (g.W) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) c[u][j] = (j < ncw) ? C[row + (int64_t)(col0 + j) * g.ldc] : 0.f;
-      if (g.W) {
-#pragma unroll
-        for (int k = 0; k < R; ++k) a[u][k] = __ldg(A1 + row + (int64_t)k * g.lda);
-      }
-      if (V) {
-#pragma unroll
-        for (int k = 0; k < R; ++k) v[u][k] = __ldg(V + row + (int64_t)k * g.lda);
+      for (int k = 0; k < R; ++k) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(A1 + row + (int64_t)k * g.lda));
+        a[0][k] = t.x, a[1][k] = t.y;
       }
     }
+    if (V) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t row = seg0 + i0 + 32 * u + lane;
-      if (g.W) {
-        const int cc = ((i0 >> 5) + u) / nc32;  // child within the segment (warp-uniform)
+      for (int k = 0; k < R; ++k) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(V + row + (int64_t)k * g.lda));
+        v[0][k] = t.x, v[1][k] = t.y;
+      }
+    }
+    if (g.W) {
+      const int cc = (i0 + 2 * lane) / ncr;  // child within the segment (rows 2 lane + {0,1} share it)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
         float t[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) t[j] = 0.f;
@@ -104,16 +111,18 @@ __global__ void __launch_bounds__(32, 16) level_f32_kernel(LevelF32Args g) {
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) c[u][j] = __fsub_rn(c[u][j], t[j]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < ncw) C[row + (int64_t)(col0 + j) * g.ldc] = c[u][j];
       }
-      if (V) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < ncw) *reinterpret_cast<float2*>(C + row + (int64_t)(col0 + j) * g.ldc) = make_float2(c[0][j], c[1][j]);
+    }
+    if (V) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int k = 0; k < R; ++k)
 #pragma unroll
           for (int j = 0; j < 8; ++j) tw[k][j] = fmaf(v[u][k], c[u][j], tw[k][j]);
-      }
     }
   }
   if (!g.V) return;
@@ -167,6 +176,8 @@ hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* 
   if (r != F32_R || n_c < 32 || n_c % 32 || n % 64 || node_rows % 64) return HODLR_ERR_ARG;
   const int64_t seg = std::min<int64_t>(node_rows, F32_SEG);
   if (n % seg || (node_rows % seg) || seg % 64) return HODLR_ERR_ARG;
+  // 8-byte row-pair accesses
+  if ((ldc | lda) & 1 || (uintptr_t)C % 8 || (uintptr_t)A1 % 8 || (uintptr_t)V % 8) return HODLR_ERR_ARG;
   const int64_t nseg = n / seg;
   const bool split = seg < node_rows && V != nullptr;
   if (split && (size_t)nseg * F32_R * ncols * sizeof(float) > part_bytes) return HODLR_ERR_ARG;
