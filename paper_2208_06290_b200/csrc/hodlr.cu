@@ -27,6 +27,7 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
                               int ncols, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
                               cudaStream_t st, bool reg_resident);
 size_t level_partial_bytes(int64_t n, int m, int r, int L);
+size_t level_f32_partial_bytes(int64_t n, int ncols);
 hodlr_status launch_getrf_dbi_f64(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides,
                                   double* out, int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm,
                                   int32_t* info, double* dbi, int64_t stridedbi, cudaStream_t st);
@@ -38,7 +39,7 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
 int64_t level_segment_rows(int64_t n, int64_t node, int sms);
 hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
                        const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
-                       int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st);
+                       int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st, int seg_max = 1024);
 hodlr_status gemm_f32(int transA, int M, int N, int K, float alpha, const float* A, int64_t lda, int64_t sA_hi,
                       int64_t sA_lo, const float* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, float beta, float* C,
                       int64_t ldc, int64_t sC_hi, int64_t sC_lo, int batch, int bdiv, void* work, size_t work_bytes,
@@ -247,6 +248,7 @@ static FactWs fact_ws_local(const hodlr_desc* d, int64_t n_loc) {
   // top levels: the caller's rows form one output node
   const int64_t seg = level_segment_rows(n_loc, n_loc, 148);
   part = std::max(part, (size_t)(n_loc / std::max<int64_t>(seg, 1)) * r * r * L * sizeof(double));
+  if (d->dtype == HODLR_F32) part = std::max(part, level_f32_partial_bytes(n_loc, (int)(r * L)));
   w.part = align_up(part);
   w.total = w.split + w.tw + w.w + w.part;
   return w;
@@ -265,7 +267,9 @@ extern "C" size_t hodlr_factorize_local_workspace(const hodlr_desc* d, int64_t n
 }
 
 static size_t solve_part_bytes(const hodlr_desc* d, int nrhs) {
-  return align_up(std::max(sizeof(double) * (size_t)4 * 148 * d->r * nrhs, solve_level_partial_bytes(d->n, d->r, nrhs)));
+  size_t b = std::max(sizeof(double) * (size_t)4 * 148 * d->r * nrhs, solve_level_partial_bytes(d->n, d->r, nrhs));
+  if (d->dtype == HODLR_F32) b = std::max(b, level_f32_partial_bytes(d->n, nrhs));
+  return align_up(b);
 }
 
 extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
@@ -410,11 +414,12 @@ static hodlr_status gemm_T(int transA, int M, int N, int K, double alpha, const 
 // fused rank-8 fp32 level step where it applies (level_f32.cu), else ERR_ARG
 static hodlr_status level_T(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
                             const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
-                            int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st) {
-  return level_f32(r, n, n_c, node_rows, C, ldc, A1, V, lda, W, wstride, ncols, TW, tw_stride, part, part_bytes, st);
+                            int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st, int seg_max = 1024) {
+  return level_f32(r, n, n_c, node_rows, C, ldc, A1, V, lda, W, wstride, ncols, TW, tw_stride, part, part_bytes, st,
+                   seg_max);
 }
 static hodlr_status level_T(int, int64_t, int64_t, int64_t, double*, int64_t, const double*, const double*, int64_t,
-                            const double*, int64_t, int, double*, int64_t, double*, size_t, cudaStream_t) {
+                            const double*, int64_t, int, double*, int64_t, double*, size_t, cudaStream_t, int = 0) {
   return HODLR_ERR_ARG;
 }
 
@@ -492,6 +497,10 @@ static hodlr_status factor_generic(const hodlr_desc* d, const hodlr_factors* f, 
   return HODLR_OK;
 }
 
+// fp32 solve: shorter fixed row segments than the factorization (few columns
+// -> more warps); fixed for every nrhs, so columns stay bit-identical
+constexpr int kSolveSeg = 256;
+
 template <typename T>
 static hodlr_status solve_generic(const hodlr_desc* d, const hodlr_factors* f, T* X, int64_t ldx, int nrhs, char* wp,
                                   cudaStream_t st) {
@@ -516,7 +525,7 @@ static hodlr_status solve_generic(const hodlr_desc* d, const hodlr_factors* f, T
   {
     Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
     const hodlr_status s = level_T(r, N, m, m, X, ldx, nullptr, V + (int64_t)(L - 1) * r * N, N, nullptr, 0, nrhs, w,
-                                   (int64_t)2 * r * nrhs, part, part_bytes, st);
+                                   (int64_t)2 * r * nrhs, part, part_bytes, st, kSolveSeg);
     if (s == HODLR_OK) w_ready = true;
     else if (s != HODLR_ERR_ARG) return s;
   }
@@ -538,7 +547,7 @@ static hodlr_status solve_generic(const hodlr_desc* d, const hodlr_factors* f, T
       Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
       const hodlr_status s = level_T(r, N, nc, 2 * nc, X, ldx, Y + (int64_t)lv * r * N,
                                      lv > 0 ? V + (int64_t)(lv - 1) * r * N : nullptr, N, w2, (int64_t)2 * r * nrhs,
-                                     nrhs, w, (int64_t)2 * r * nrhs, part, part_bytes, st);
+                                     nrhs, w, (int64_t)2 * r * nrhs, part, part_bytes, st, kSolveSeg);
       if (s == HODLR_OK) {
         w_ready = true;
         continue;

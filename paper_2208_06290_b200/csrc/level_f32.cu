@@ -16,7 +16,7 @@
 namespace hodlr {
 
 constexpr int F32_R = 8;
-constexpr int F32_SEG = 1024;  // rows per segment (32 per lane)
+constexpr int F32_SEG = 1024;  // max rows per segment (the caller's seg_max, fixed per phase)
 
 struct LevelF32Args {
   float* C;
@@ -151,18 +151,24 @@ __global__ void __launch_bounds__(32, 12) level_f32_kernel(LevelF32Args g) {
   }
 }
 
-// TW_q = sum of the q's segment partials in segment order; paired output
+// TW_q = sum of the q's segment partials: warp per entry, lane l sums segments
+// l, l + 32, ... in order, then a fixed xor butterfly (order depends only on the
+// segment count, never on ncols); paired output
 __global__ void level_reduce_f32_kernel(const float* part, float* TW, int ncols, int segs, int nnodes,
                                         int64_t tw_stride) {
   constexpr int R = F32_R;
   const int64_t per = (int64_t)R * ncols;
   const int64_t total = per * nnodes;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total; e += warps) {
     const int64_t q = e / per, mn = e % per;
     const int m = (int)(mn % R), n = (int)(mn / R);
     float s = 0.f;
-    for (int k = 0; k < segs; ++k) s += part[(q * segs + k) * per + mn];
-    TW[(q >> 1) * tw_stride + (q & 1) * R + m + (int64_t)n * 2 * R] = s;
+    for (int k = lane; k < segs; k += 32) s += part[(q * segs + k) * per + mn];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) TW[(q >> 1) * tw_stride + (q & 1) * R + m + (int64_t)n * 2 * R] = s;
   }
 }
 
@@ -171,10 +177,10 @@ size_t level_f32_partial_bytes(int64_t n, int ncols) { return (size_t)(n / 64 + 
 // One fp32 level step over n rows (r = 8, n_c >= 32).  ERR_ARG: unsupported shape.
 hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
                        const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
-                       int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st) {
+                       int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st, int seg_max) {
   if (ncols == 0) return HODLR_OK;
   if (r != F32_R || n_c < 32 || n_c % 32 || n % 64 || node_rows % 64) return HODLR_ERR_ARG;
-  const int64_t seg = std::min<int64_t>(node_rows, F32_SEG);
+  const int64_t seg = std::min<int64_t>(node_rows, std::min(seg_max, F32_SEG));
   if (n % seg || (node_rows % seg) || seg % 64) return HODLR_ERR_ARG;
   // 8-byte row-pair accesses
   if ((ldc | lda) & 1 || (uintptr_t)C % 8 || (uintptr_t)A1 % 8 || (uintptr_t)V % 8) return HODLR_ERR_ARG;
@@ -190,7 +196,7 @@ hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* 
   if (!split) return HODLR_OK;
   const int nnodes = (int)(n / node_rows);
   const int64_t total = (int64_t)F32_R * ncols * nnodes;
-  level_reduce_f32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 1184), 256, 0, st>>>(
+  level_reduce_f32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 8), 4736), 256, 0, st>>>(
       part, TW, ncols, (int)(node_rows / seg), nnodes, tw_stride);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;

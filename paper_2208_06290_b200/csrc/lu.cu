@@ -633,25 +633,67 @@ __global__ void __launch_bounds__(256) getrs_warp_kernel(int nrhs, int batch, co
   }
   // x_j lives in register j / 32 of lane j % 32 (select, not a dynamic index)
   auto own = [&](int j) -> T& { return (Q == 1 || j < 32) ? x[0] : x[Q - 1]; };
-  // forward: unit lower
-#pragma unroll 4
-  for (int j = 0; j < S - 1; ++j) {
-    const T xj = __shfl_sync(0xffffffffu, own(j), j % 32);
+  // LU columns are prefetched 8 steps ahead into a register ring (the
+  // substitution chain never waits on a global load)
+  constexpr int PF = S < 8 ? S : 8;
+  T lc[PF][Q];
+  auto load_col = [&](int j, T (&dst)[Q]) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int i = lane + 32 * q;
-      if (i > j && i < S) x[q] = fma(-__ldg(g + i + (int64_t)j * lda), xj, x[q]);
+      dst[q] = (i < S && j >= 0 && j < S) ? __ldg(g + i + (int64_t)j * lda) : T(0);
+    }
+  };
+  // forward: unit lower, columns 0 .. S-2
+#pragma unroll
+  for (int p = 0; p < PF; ++p) load_col(p, lc[p]);
+#pragma unroll 1
+  for (int jb = 0; jb < S; jb += PF) {
+    T cur[PF][Q];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) cur[p][q] = lc[p][q];
+      load_col(jb + PF + p < S - 1 ? jb + PF + p : -1, lc[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+      const int j = jb + p;
+      if (j < S - 1) {
+        const T xj = __shfl_sync(0xffffffffu, own(j), j % 32);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int i = lane + 32 * q;
+          if (i > j && i < S) x[q] = fma(-cur[p][q], xj, x[q]);
+        }
+      }
     }
   }
-  // backward: upper with true division
-#pragma unroll 4
-  for (int j = S - 1; j >= 0; --j) {
-    if ((j % 32) == lane) own(j) = own(j) / __ldg(g + j + (int64_t)j * lda);
-    const T xj = __shfl_sync(0xffffffffu, own(j), j % 32);
+  // backward: upper with true division, columns S-1 .. 0
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int i = lane + 32 * q;
-      if (i < j) x[q] = fma(-__ldg(g + i + (int64_t)j * lda), xj, x[q]);
+  for (int p = 0; p < PF; ++p) load_col(S - 1 - p, lc[p]);
+#pragma unroll 1
+  for (int jb = S - 1; jb >= 0; jb -= PF) {
+    T cur[PF][Q];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) cur[p][q] = lc[p][q];
+      load_col(jb - PF - p, lc[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+      const int j = jb - p;
+      if (j >= 0) {
+        // the owner lane holds U[j][j] in cur[p][j / 32]
+        if ((j % 32) == lane) own(j) = own(j) / ((Q == 1 || j < 32) ? cur[p][0] : cur[p][Q - 1]);
+        const T xj = __shfl_sync(0xffffffffu, own(j), j % 32);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int i = lane + 32 * q;
+          if (i < j) x[q] = fma(-cur[p][q], xj, x[q]);
+        }
+      }
     }
   }
   __syncwarp();  // all lanes have read B (X may alias B)
