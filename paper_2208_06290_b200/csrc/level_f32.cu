@@ -30,52 +30,55 @@ struct LevelF32Args {
   int64_t node_rows;
   int ncols;
   int seg_rows;
-  int chunks;       // ceil(ncols / 8) CTAs (one warp each) per segment
+  int chunks;       // ceil(ncols / 8) CTAs (one warp each) per segment (1 when ncols <= 4)
   float* TW;        // final: paired layout; partial: [seg][R x ncols] ld R
   int64_t tw_stride;
   int partial;
 };
 
-// one warp per CTA: work item = (segment, 8-column chunk).  The W' blocks of
+// one warp per CTA: work item = (segment, NCW-column chunk).  The W' blocks of
 // all children in the segment are staged in shared memory up front; each lane
-// then streams two rows per iteration (all 48 loads issued before use).
+// then streams two rows per iteration (all loads issued before use).  NCW = 8
+// for wide panels; 1 / 2 / 4 for few right-hand sides (same per-column
+// operation sequence, so a column's result does not depend on NCW).
 constexpr int F32_MAXCH = F32_SEG / 32;  // children per segment (n_c >= 32)
 
-__global__ void __launch_bounds__(32, 12) level_f32_kernel(LevelF32Args g) {
+template <int NCW>
+__global__ void __launch_bounds__(32, NCW == 8 ? 12 : (NCW == 4 ? 16 : 24)) level_f32_kernel(LevelF32Args g) {
   constexpr int R = F32_R;
   const int lane = threadIdx.x;
   const int seg = blockIdx.x / g.chunks, chunk = blockIdx.x % g.chunks;
-  const int col0 = chunk * 8;
-  const int ncw = min(8, g.ncols - col0);  // columns of this warp (ragged last chunk)
+  const int col0 = chunk * NCW;
+  const int ncw = min(NCW, g.ncols - col0);  // columns of this warp (ragged last chunk)
   const int64_t seg0 = (int64_t)seg * g.seg_rows;
   const float* __restrict__ A1 = g.A1;
   const float* __restrict__ V = g.V;
   float* __restrict__ C = g.C;
-  __shared__ __align__(16) float ws[F32_MAXCH][R][8];  // W' of the segment's children (broadcast reads)
+  __shared__ __align__(16) float ws[F32_MAXCH][R][NCW];  // W' of the segment's children (broadcast reads)
   const int64_t ch0 = seg0 / g.n_c;
   const int nch = (int)ceil_div(g.seg_rows, g.n_c);
   if (g.W) {
-    for (int e = lane; e < nch * R * 8; e += 32) {
-      const int cc = e / (R * 8), k = e % R, j = (e / R) % 8;
+    for (int e = lane; e < nch * R * NCW; e += 32) {
+      const int cc = e / (R * NCW), k = e % R, j = (e / R) % NCW;
       const int64_t ch = ch0 + cc;
       const float* wp = g.W + (ch >> 1) * g.wstride + (ch & 1) * R;
       ws[cc][k][j] = (j < ncw) ? __ldg(wp + k + (int64_t)(col0 + j) * (2 * R)) : 0.f;
     }
     __syncwarp();
   }
-  float tw[R][8];
+  float tw[R][NCW];
 #pragma unroll
   for (int k = 0; k < R; ++k)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) tw[k][j] = 0.f;
+    for (int j = 0; j < NCW; ++j) tw[k][j] = 0.f;
   const int ncr = (int)g.n_c;
 #pragma unroll 1
   for (int i0 = 0; i0 < g.seg_rows; i0 += 64) {
     // lane owns rows i0 + 2 lane + {0, 1}: 8-byte loads of C, Y^{l+1} and V
     const int64_t row = seg0 + i0 + 2 * lane;
-    float c[2][8], a[2][R], v[2][R];
+    float c[2][NCW], a[2][R], v[2][R];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NCW; ++j) {
       const float2 t = (j < ncw) ? *reinterpret_cast<const float2*>(C + row + (int64_t)(col0 + j) * g.ldc)
                                  : make_float2(0.f, 0.f);
       c[0][j] = t.x, c[1][j] = t.y;
@@ -98,22 +101,30 @@ __global__ void __launch_bounds__(32, 12) level_f32_kernel(LevelF32Args g) {
       const int cc = (i0 + 2 * lane) / ncr;  // child within the segment (rows 2 lane + {0,1} share it)
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        float t[8];
+        float t[NCW];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) t[j] = 0.f;
+        for (int j = 0; j < NCW; ++j) t[j] = 0.f;
 #pragma unroll
         for (int k = 0; k < R; ++k) {  // W' row k as two broadcast 16-byte loads
-          const float4 w0 = *reinterpret_cast<const float4*>(&ws[cc][k][0]);
-          const float4 w1 = *reinterpret_cast<const float4*>(&ws[cc][k][4]);
-          const float wk[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+          float wk[NCW];
+          if constexpr (NCW >= 4) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) t[j] = fmaf(a[u][k], wk[j], t[j]);
+            for (int j4 = 0; j4 < NCW; j4 += 4) {
+              const float4 w4 = *reinterpret_cast<const float4*>(&ws[cc][k][j4]);
+              wk[j4] = w4.x, wk[j4 + 1] = w4.y, wk[j4 + 2] = w4.z, wk[j4 + 3] = w4.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < NCW; ++j) wk[j] = ws[cc][k][j];
+          }
+#pragma unroll
+          for (int j = 0; j < NCW; ++j) t[j] = fmaf(a[u][k], wk[j], t[j]);
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) c[u][j] = __fsub_rn(c[u][j], t[j]);
+        for (int j = 0; j < NCW; ++j) c[u][j] = __fsub_rn(c[u][j], t[j]);
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < NCW; ++j)
         if (j < ncw) *reinterpret_cast<float2*>(C + row + (int64_t)(col0 + j) * g.ldc) = make_float2(c[0][j], c[1][j]);
     }
     if (V) {
@@ -122,14 +133,14 @@ __global__ void __launch_bounds__(32, 12) level_f32_kernel(LevelF32Args g) {
 #pragma unroll
         for (int k = 0; k < R; ++k)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) tw[k][j] = fmaf(v[u][k], c[u][j], tw[k][j]);
+          for (int j = 0; j < NCW; ++j) tw[k][j] = fmaf(v[u][k], c[u][j], tw[k][j]);
     }
   }
   if (!g.V) return;
 #pragma unroll
   for (int k = 0; k < R; ++k)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NCW; ++j) {
       float v = tw[k][j];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -191,7 +202,15 @@ hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* 
                  split ? part : TW, tw_stride, split ? 1 : 0};
   const int64_t grid = nseg * g.chunks;
   if (grid > 2147483647LL) return HODLR_ERR_ARG;
-  level_f32_kernel<<<(unsigned)grid, 32, 0, st>>>(g);
+  if (g.ncols > 4) {  // chunks of 8 columns (ceil(ncols / 8) warps per segment)
+    level_f32_kernel<8><<<(unsigned)grid, 32, 0, st>>>(g);
+  } else if (g.ncols > 2) {
+    level_f32_kernel<4><<<(unsigned)grid, 32, 0, st>>>(g);
+  } else if (g.ncols == 2) {
+    level_f32_kernel<2><<<(unsigned)grid, 32, 0, st>>>(g);
+  } else {
+    level_f32_kernel<1><<<(unsigned)grid, 32, 0, st>>>(g);
+  }
   HODLR_CHECK_LAUNCH();
   if (!split) return HODLR_OK;
   const int nnodes = (int)(n / node_rows);

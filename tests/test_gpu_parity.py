@@ -218,6 +218,8 @@ def test_fp32_multi_rhs_columns_bitwise_equal_single():
     X = hb.solve(f, B)
     for j in (0, 7, 19):
         assert torch.equal(X[:, j], hb.solve(f, B[:, j].contiguous())), j
+    for k in (2, 3, 6):  # the 2- / 4- / 8-column level kernels and the warp getrs
+        assert torch.equal(X[:, :k], hb.solve(f, B[:, :k].contiguous())), k
 
 
 def test_factorize_from_host_equals_device_path():
