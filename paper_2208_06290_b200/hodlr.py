@@ -385,24 +385,31 @@ def solve(fact: HodlrFactorization, b, stream=None):
         raise ValueError(f"rhs must have {n} rows (got shape {tuple(bt.shape)})")
     nrhs = 1 if bt.dim() == 1 else bt.shape[1]
     dev = fact.D.device
-    # column-major device copy: (nrhs, n) row-major == (n, nrhs) column-major
-    x = bt.reshape(n, nrhs).t().to(device=dev, dtype=fact.D.dtype).contiguous()
-    if x.data_ptr() == bt.data_ptr():
-        x = x.clone()
-    desc = fact.desc()
-    wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
-    ws = _workspace(wsb, dev)
-    st = (stream or torch.cuda.current_stream(dev)).cuda_stream
-    cf = fact.cfactors()
-    _lib.check(
-        lib.hodlr_solve(C.byref(desc), C.byref(cf), C.c_void_p(x.data_ptr()), n, nrhs, C.c_void_p(ws.data_ptr()),
-                        wsb, C.c_void_p(st)),
-        "hodlr_solve",
-    )
-    out = x.t().reshape(bt.shape)
-    if is_np:
-        return out.cpu().numpy()
-    return out.to(bt.device) if bt.device != dev else out
+    so = stream or torch.cuda.current_stream(dev)
+    with torch.cuda.stream(so):
+        # upload first (a pinned host rhs is one async DMA), then lay out column-major
+        # on the device: (nrhs, n) row-major == (n, nrhs) column-major
+        bd = bt.to(device=dev, non_blocking=True) if bt.device != dev else bt
+        x = bd.reshape(n, nrhs).t().to(dtype=fact.D.dtype).contiguous()
+        if x.data_ptr() == bt.data_ptr():
+            x = x.clone()
+        desc = fact.desc()
+        wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
+        ws = _workspace(wsb, dev)
+        cf = fact.cfactors()
+        _lib.check(
+            lib.hodlr_solve(C.byref(desc), C.byref(cf), C.c_void_p(x.data_ptr()), n, nrhs,
+                            C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(so.cuda_stream)),
+            "hodlr_solve",
+        )
+        out = x.t().reshape(bt.shape)
+        if bt.device == dev:
+            return out
+        # host result: async copy into pinned memory, then wait for the stream
+        host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        host.copy_(out, non_blocking=True)
+        so.synchronize()
+    return host.numpy() if is_np else host
 
 
 def logdet(fact: HodlrFactorization):
