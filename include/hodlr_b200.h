@@ -166,6 +166,24 @@ hodlr_status hodlr_matvec(const hodlr_desc* d, const void* D, const void* U, con
                           int64_t ldx, void* Y, int64_t ldy, int nrhs, void* work, size_t work_bytes,
                           void* stream);
 
+/* HODLR assembly on the device (SPEC.md:163-171 [OP] assemble): leaf blocks
+ * D materialized exactly; every sibling off-diagonal block A(I_a, I_b)
+ * compressed to U_a V_b^T by ACA with rook pivoting at rank cap r (replaces
+ * compress.py:87-200 compress(..., CompressionConfig(tol=0, max_rank=r,
+ * method="aca_rook_pivot")) called per block; same operation order, so the
+ * crosses are bit-identical for bit-identical entries).  Blocks of exact rank
+ * < r keep zero columns.  Synchronous with respect to `stream` (the ACA
+ * control loop reads per-level flags back).  ERR_ARG also flags a non-finite
+ * oracle entry (the reference raises ValueError).
+ * hodlr_build_laplace_dl: geom = 7 x N doubles (x, y, nx, ny, weights,
+ *   -log|x - z| / 2pi, -curvature / 4pi) of the contour (problems.py:133-217).
+ * hodlr_build_dense: entries of a dense column-major N x N device matrix. */
+size_t hodlr_build_workspace(const hodlr_desc* d);
+hodlr_status hodlr_build_laplace_dl(const hodlr_desc* d, const double* geom, void* D, void* U, void* V, void* work,
+                                    size_t work_bytes, void* stream);
+hodlr_status hodlr_build_dense(const hodlr_desc* d, const double* A, int64_t lda, void* D, void* U, void* V,
+                               void* work, size_t work_bytes, void* stream);
+
 /* ------------------------------------------------------------------------
  * Row-sharded (multi-GPU) schedule, SURVEY.md §8e.  The caller holds the rows
  * [row0, row0 + n_loc) of one level-p node (n_loc = N / 2^p): its leaves' D

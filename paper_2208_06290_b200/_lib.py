@@ -70,6 +70,9 @@ SIGNATURES = {
     "hodlr_solve": (_i, [C.POINTER(Desc), C.POINTER(Factors), _p, _i64, _i, _p, _sz, _p]),
     "hodlr_matvec_workspace": (_sz, [C.POINTER(Desc), _i]),
     "hodlr_matvec": (_i, [C.POINTER(Desc), _p, _p, _p, _p, _i64, _p, _i64, _i, _p, _sz, _p]),
+    "hodlr_build_workspace": (_sz, [C.POINTER(Desc)]),
+    "hodlr_build_laplace_dl": (_i, [C.POINTER(Desc), _p, _p, _p, _p, _p, _sz, _p]),
+    "hodlr_build_dense": (_i, [C.POINTER(Desc), _p, _i64, _p, _p, _p, _p, _sz, _p]),
 }
 
 _lib = None

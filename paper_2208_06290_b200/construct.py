@@ -1,0 +1,119 @@
+"""HODLR assembly on the device (SPEC.md:163-171 [OP] assemble).
+
+Leaf blocks are materialized exactly and every sibling off-diagonal block is
+compressed by adaptive cross approximation with rook pivoting at a fixed rank
+cap (the reference's ``compress(..., CompressionConfig(tol=0, max_rank=r,
+method="aca_rook_pivot"))``, compress.py:87-200), all blocks of a level in
+lockstep on the GPU (``hodlr_build_*``, csrc/build.cu).
+
+Entry oracles:
+
+* :func:`laplace_dl_hodlr` -- the cfg2 problem: exterior Dirichlet Laplace
+  double layer with log completion on the star contour ``contour_default``
+  (problems.py:133-217).  The O(N) contour geometry is evaluated here with the
+  reference's numpy expressions (so it is bit-identical); the O(N r L)
+  kernel entries and the ACA run on the device.
+* :func:`assemble_dense` -- entries of a dense device matrix (small n, tests,
+  the SPEC examples).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib
+from .hodlr import HodlrMatrix, _torch, _workspace
+from .tree import ClusterTree
+
+
+def contour_default(n: int, amplitude: float = 0.3, lobes: int = 5) -> dict:
+    """Star contour ``r(t) = 1 + amplitude cos(lobes t)`` sampled at ``n``
+    equispaced parameters: nodes, exterior unit normals, curvature and
+    trapezoidal arclength weights (problems.py:133-156, same expressions)."""
+    if n < 16:
+        raise ValueError("need at least 16 contour nodes")
+    t = 2.0 * np.pi * np.arange(n) / n
+    rad = 1.0 + amplitude * np.cos(lobes * t)
+    drad = -amplitude * lobes * np.sin(lobes * t)
+    ddrad = -amplitude * lobes * lobes * np.cos(lobes * t)
+    ct, st = np.cos(t), np.sin(t)
+    dx, dy = drad * ct - rad * st, drad * st + rad * ct
+    speed = np.hypot(dx, dy)
+    return {
+        "t": t, "x": rad * ct, "y": rad * st, "nx": dy / speed, "ny": -dx / speed,
+        "curvature": (rad * rad + 2.0 * drad * drad - rad * ddrad) / speed**3,
+        "weights": speed * (2.0 * np.pi / n),
+    }
+
+
+def laplace_dl_geometry(n: int, amplitude: float = 0.3, lobes: int = 5, z=(0.0, 0.0)) -> np.ndarray:
+    """(7, n) float64: x, y, nx, ny, weights, log completion term, diagonal
+    kernel limit -- the per-node data the device oracle reads
+    (problems.py:158-180: logterm = -log|x - z| / 2pi, diag = -curvature / 4pi)."""
+    c = contour_default(n, amplitude, lobes)
+    zz = np.asarray(z, dtype=np.float64)
+    rz = np.hypot(c["x"] - zz[0], c["y"] - zz[1])
+    if np.any(rz == 0.0):
+        raise ValueError("completion point z must not lie on the contour")
+    logterm = -np.log(rz) / (2.0 * np.pi)
+    diag = -c["curvature"] / (4.0 * np.pi)
+    return np.stack([c["x"], c["y"], c["nx"], c["ny"], c["weights"], logterm, diag]).astype(np.float64)
+
+
+def _alloc(n: int, m: int, r: int, device):
+    torch = _torch()
+    L = int(round(math.log2(n // m))) if n >= m else 0
+    if n != m << L:
+        raise ValueError(f"GPU layout needs N = m 2^L (got N={n}, m={m})")
+    f64 = dict(dtype=torch.float64, device=device)
+    D = torch.empty((1 << L) * m * m, **f64)
+    U = torch.empty(max(n * r * L, 1), **f64)
+    V = torch.empty(max(n * r * L, 1), **f64)
+    return L, D, U, V
+
+
+def _finish(n, m, r, L, D, U, V):
+    return HodlrMatrix(ClusterTree(n, L), r, D, U[: n * r * L], V[: n * r * L])
+
+
+def laplace_dl_hodlr(n: int, m: int, r: int, amplitude: float = 0.3, lobes: int = 5, z=(0.0, 0.0),
+                     device="cuda", stream=None) -> HodlrMatrix:
+    """The cfg2 operator (``laplace_dl_oracle(contour_default(n))``, z = 0)
+    assembled on the device at uniform rank ``r`` (ACA rook, tol = 0)."""
+    torch = _torch()
+    lib = _lib.load()
+    L, D, U, V = _alloc(n, m, r, device)
+    geom = torch.from_numpy(laplace_dl_geometry(n, amplitude, lobes, z)).to(device)
+    desc = _lib.Desc(n, m, r, L, 0)
+    wsb = lib.hodlr_build_workspace(C.byref(desc))
+    ws = _workspace(wsb, geom.device)
+    st = (stream or torch.cuda.current_stream(geom.device)).cuda_stream
+    _lib.check(lib.hodlr_build_laplace_dl(C.byref(desc), C.c_void_p(geom.data_ptr()), C.c_void_p(D.data_ptr()),
+                                          C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()),
+                                          C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st)), "hodlr_build_laplace_dl")
+    return _finish(n, m, r, L, D, U, V)
+
+
+def assemble_dense(A, m: int, r: int, device="cuda", stream=None) -> HodlrMatrix:
+    """Assemble the HODLR representation of a dense (n, n) matrix (numpy or
+    torch): exact leaf blocks, ACA-rook crosses of rank <= r per sibling block
+    (zero-padded to r)."""
+    torch = _torch()
+    lib = _lib.load()
+    At = torch.as_tensor(A, dtype=torch.float64)
+    if At.dim() != 2 or At.shape[0] != At.shape[1]:
+        raise ValueError("assemble_dense needs a square matrix")
+    n = At.shape[0]
+    L, D, U, V = _alloc(n, m, r, device)
+    Acm = At.t().contiguous().to(device)  # column-major entries
+    desc = _lib.Desc(n, m, r, L, 0)
+    wsb = lib.hodlr_build_workspace(C.byref(desc))
+    ws = _workspace(wsb, Acm.device)
+    st = (stream or torch.cuda.current_stream(Acm.device)).cuda_stream
+    _lib.check(lib.hodlr_build_dense(C.byref(desc), C.c_void_p(Acm.data_ptr()), n, C.c_void_p(D.data_ptr()),
+                                     C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()), C.c_void_p(ws.data_ptr()),
+                                     wsb, C.c_void_p(st)), "hodlr_build_dense")
+    return _finish(n, m, r, L, D, U, V)
