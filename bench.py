@@ -2,21 +2,25 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1] shape): N = 2^20, leaf m = 64, uniform rank
-r = 32, L = 14, fp64, 1 RHS.  Data: seeded exact-HODLR stand-in generated in
-HBM -- the 2-D Laplace BIE compression at this N needs the GPU
-builder, which is a "next" row.  A step = one factorize (PAPER
-Alg. 3) + one solve (Alg. 4) of a freshly restored copy of the matrix; the
-restore copy is outside the timed events.  Inputs (8 GB) exceed L2 (126 MB),
-so no explicit flush is needed.
+Workload (BASELINE.json configs[1]): N = 2^20, leaf m = 64, uniform rank
+r = 32, L = 14, fp64, 1 RHS, on the cfg2 operator itself -- the exterior
+Laplace double-layer BIE on contour_default(N) (problems.py:133-217), z = 0,
+assembled in HBM by the device builder (ACA rook, rank 32, bit-exact vs the
+reference's compress(); ``build_ms`` reports it, outside the step).
+``--problem standin`` uses the seeded exact-HODLR stand-in instead.  A step =
+one factorize (PAPER Alg. 3) + one solve (Alg. 4) of a freshly restored copy
+of the matrix; the restore copy is outside the timed events.  Inputs (8 GB)
+exceed L2 (126 MB), so no explicit flush is needed.
 
 Multi-GPU: one process per GPU (torchrun); round 1 runs independent replicas
 (every rank factors its own N = 2^20 matrix, scaling "weak"); subtree sharding
 with NCCL is DESIGN.md §Multi-GPU.  Rank 0 prints one JSON line.
 
---impl reference: the reference's CPU path (oracle restatement of the
-reference kernels, oracle/hodlr_oracle.py, all host threads) on a bounded
-sample of the same workload (one 2^16-row subtree, m = 64, r = 32), rank 0 only.
+--impl reference: the reference's CPU path (its own batched kernels driven by
+the SPEC recipe, oracle/ref_driver.py, all host threads) on a bounded sample
+of the same workload: the leading 2^16-row subtree of the cfg2 operator,
+assembled by the reference's own compress() (built once, outside the timing),
+rank 0 only.
 """
 
 from __future__ import annotations
@@ -39,6 +43,34 @@ N_DEFAULT, M_LEAF, RANK = 1 << 20, 64, 32
 SEED, SCALE = 1234, 1.0
 METRIC = "hodlr_factor_solve_tflops"
 CPU_SAMPLE_N = 1 << 16
+
+
+PROBLEM_DESC = {
+    "laplace": "Laplace double-layer BIE on contour_default(N), z=0, assembled on the device (ACA rook, rank 32)",
+    "standin": "seeded exact-HODLR stand-in",
+}
+
+
+def make_operator(hb, torch, n, m, r, problem, rank):
+    """The workload operator in HBM and its assembly time (ms)."""
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if problem == "laplace":
+        h = hb.laplace_dl_hodlr(n, m, r)
+    else:
+        h = hb.random_hodlr(n, m, r, seed=SEED + rank, s=SCALE)
+    torch.cuda.synchronize()
+    return h, 1e3 * (time.perf_counter() - t0)
+
+
+def subtree_of(h, n_sub):
+    """(D, U, V) numpy of the leading n_sub-row subtree of a device HODLR."""
+    m, r, L, n = h.m, h.rank, h.L, h.n
+    Ls = int(round(math.log2(n_sub // m)))
+    D = h.D[: (n_sub // m) * m * m].cpu().numpy()
+    U = h.U.view(L, r, n)[L - Ls :, :, :n_sub].contiguous().view(-1).cpu().numpy()
+    V = h.V.view(L, r, n)[L - Ls :, :, :n_sub].contiguous().view(-1).cpu().numpy()
+    return D, U, V
 
 
 def factor_flops(n, m, r):
@@ -167,7 +199,28 @@ def traffic_from_profiles():
         return None, None
 
 
-def cpu_reference(n, threads):
+def cpu_sample(n, problem, sub=None):
+    """The bounded CPU sample: the leading n-row subtree of the workload
+    operator.  ``sub`` = (D, U, V) already extracted from the device copy (bit
+    identical to the reference's compress(), tests/test_gpu_build.py); else the
+    reference assembles it with its own compress() (stand-in: the oracle generator)."""
+    from oracle import hodlr_oracle as orc
+    from oracle import ref_driver as rd
+
+    lay = orc.Layout(n, M_LEAF, RANK)
+    if problem == "standin":
+        return orc.make_exact_hodlr(n, M_LEAF, RANK, seed=SEED, s=SCALE)
+    if sub is None:
+        if rd.AVAILABLE:
+            sub = rd.ref_assemble_laplace(N_DEFAULT, n, M_LEAF, RANK)
+        else:
+            from oracle import build_oracle as bo
+
+            sub = bo.assemble(bo.LaplaceDL(N_DEFAULT), n, M_LEAF, RANK)
+    return orc.HodlrData(lay, *(x.copy() for x in sub))
+
+
+def cpu_reference(n, threads, sample=None):
     """The reference's CPU path on a bounded sample: Alg. 3/4 issuing the
     reference's own batched kernels (baseline/_ref, threads:<ncores> executor)
     when installed -- kind "reference" -- else the oracle restatement ("port")."""
@@ -176,7 +229,7 @@ def cpu_reference(n, threads):
     from oracle import hodlr_oracle as orc
     from oracle import ref_driver as rd
 
-    h = orc.make_exact_hodlr(n, M_LEAF, RANK, seed=SEED, s=SCALE)
+    h = sample.copy() if sample is not None else orc.make_exact_hodlr(n, M_LEAF, RANK, seed=SEED, s=SCALE)
     b = np.random.default_rng(SEED + 1).standard_normal((n, 1))
     L = h.lay.L
     fl = orc.factor_flops(n, M_LEAF, RANK) + orc.solve_flops(n, M_LEAF, RANK)
@@ -204,26 +257,29 @@ def run_reference(args):
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
     n = CPU_SAMPLE_N
     cpu_reference(1 << 12, threads)  # warm-up (imports, thread pool)
+    t0 = time.perf_counter()
+    sample = cpu_sample(n, args.problem)  # built once, outside the timed steps
+    build_s = time.perf_counter() - t0
     vals, tfs, tss = [], [], []
     kind = "port"
     for _ in range(args.steps):
-        fl, tf, ts, kind = cpu_reference(n, threads)
+        fl, tf, ts, kind = cpu_reference(n, threads, sample)
         vals.append(fl / (tf + ts) / 1e12)
         tfs.append(tf)
         tss.append(ts)
     v = statistics.mean(vals)
     how = ("reference batched kernels (baseline/_ref hodlr.backend, threads executor) driven by the SPEC "
            "Alg. 3/4 recipe" if kind == "reference" else "oracle restatement of the reference kernels")
-    sample = (f"{how}: factor+solve of one 2^16-row subtree of the cfg2 workload (m=64, r=32, fp64), "
-              f"{args.steps} step(s)")
+    sample = (f"{how}: factor+solve of the leading 2^16-row subtree of the cfg2 workload (m=64, r=32, fp64; "
+              f"{PROBLEM_DESC[args.problem]}), {args.steps} step(s); sample assembled once in {build_s:.1f} s")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean([a + b for a, b in zip(tfs, tss)]),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         # the arm's config is the GPU arm's (cfg2 shape); each step is a bounded
         # sample of it (one 2^16-row subtree, stated in cpu_baseline.sample)
-        "config": {"workload": "HODLR factor+solve, cfg2 shape (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
-                               "seeded exact-HODLR stand-in", "N": N_DEFAULT, "leaf": M_LEAF, "rank": RANK,
+        "config": {"workload": "HODLR factor+solve, cfg2 (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
+                               + PROBLEM_DESC[args.problem], "N": N_DEFAULT, "leaf": M_LEAF, "rank": RANK,
                    "L": int(math.log2(N_DEFAULT // M_LEAF)), "nrhs": 1, "parallelism": "cpu (reference)",
                    "sample_rows": n, "device": "cpu"},
         "t_factor_s": statistics.mean(tfs), "t_solve_s": statistics.mean(tss),
@@ -250,7 +306,7 @@ def run_ours(args):
     f_flops, s_flops = factor_flops(n, m, r), solve_flops(n, m, r)
 
     # resident input (HBM) and a pristine copy for restores
-    h0 = hb.random_hodlr(n, m, r, seed=SEED + rank, s=SCALE)
+    h0, build_ms = make_operator(hb, torch, n, m, r, args.problem, rank)
     hw = h0.clone()
     g = torch.Generator(device="cuda")
     g.manual_seed(SEED + 7 + rank)
@@ -362,19 +418,20 @@ def run_ours(args):
         cpu = None
         if not args.no_cpu:
             threads = os.cpu_count() or 1
-            fl, ctf, cts, kind = cpu_reference(CPU_SAMPLE_N, threads)
+            samp = cpu_sample(CPU_SAMPLE_N, args.problem, subtree_of(h0, CPU_SAMPLE_N) if args.problem == "laplace" else None)
+            fl, ctf, cts, kind = cpu_reference(CPU_SAMPLE_N, threads, samp)
             cpu = {"value": fl / (ctf + cts) / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
                    "sample": ("reference kernels (baseline/_ref) via the SPEC recipe" if kind == "reference"
-                              else "oracle restatement") + ": factor+solve of one 2^16-row subtree of this "
+                              else "oracle restatement") + ": factor+solve of the leading 2^16-row subtree of this "
                    f"workload (m=64, r=32, fp64), {ctf:.1f} s factor + {cts:.2f} s solve"}
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "HODLR factor+solve, cfg2 shape (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
-                                   "seeded exact-HODLR stand-in", "N": n, "leaf": m, "rank": r, "L": L, "nrhs": 1,
+            "config": {"workload": "HODLR factor+solve, cfg2 (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
+                                   + PROBLEM_DESC[args.problem], "N": n, "leaf": m, "rank": r, "L": L, "nrhs": 1,
                        "parallelism": f"replicas{world}", "l2_flush": "inputs 8 GB > L2"},
-            "t_factor_ms": tf, "t_solve_ms": ts, "factor_tflops": f_flops / (tf * 1e-3) / 1e12,
+            "t_factor_ms": tf, "t_solve_ms": ts, "factor_tflops": f_flops / (tf * 1e-3) / 1e12, "build_ms": build_ms,
             "step_ms_min_med_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
             "solve_gbps": (8 * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 16 * n) / (ts * 1e-3) / 1e9,
             "relres": relres, "flops_factor": f_flops, "flops_solve": s_flops,
@@ -415,7 +472,7 @@ def run_sharded(args):
     n, m, r = args.n, M_LEAF, RANK
     L = int(round(math.log2(n // m)))
     f_flops, s_flops = factor_flops(n, m, r), solve_flops(n, m, r)
-    h0 = hb.random_hodlr(n, m, r, seed=SEED, s=SCALE)  # identical on every rank
+    h0, build_ms = make_operator(hb, torch, n, m, r, args.problem, 0)  # identical on every rank
     g = torch.Generator(device="cuda")
     g.manual_seed(SEED + 7)
     b = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
@@ -490,11 +547,11 @@ def run_sharded(args):
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "HODLR factor+solve, cfg2 shape (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
-                                   "seeded exact-HODLR stand-in, row-sharded", "N": n, "leaf": m, "rank": r, "L": L,
+            "config": {"workload": "HODLR factor+solve, cfg2 (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
+                                   + PROBLEM_DESC[args.problem] + ", row-sharded", "N": n, "leaf": m, "rank": r, "L": L,
                        "nrhs": 1, "parallelism": f"subtree-shard{world} ({args.dist_backend} all-reduce per top level)",
                        "l2_flush": "inputs 8 GB > L2"},
-            "t_factor_ms": tf, "t_solve_ms": ts, "relres": relres, "phase_ms_rank0": phases,
+            "t_factor_ms": tf, "t_solve_ms": ts, "relres": relres, "phase_ms_rank0": phases, "build_ms": build_ms,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "wall_s_timed": wall,
             "roofline": {"bound": "tensor", "kernel": "level_update_kernel", "achieved": None, "peak": None,
                          "unit": "TFLOP/s", "frac": None, "traffic": None,
@@ -513,6 +570,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--problem", choices=("laplace", "standin"), default="laplace",
+                    help="laplace: the cfg2 operator assembled on the device; standin: seeded exact HODLR")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the row-sharded path even on one GPU")

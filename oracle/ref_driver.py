@@ -135,3 +135,37 @@ def ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L, ex=None):
     return x.reshape(nrhs, n).T.copy()
 
 
+
+
+def ref_assemble_laplace(n_total: int, n: int, m: int, r: int):
+    """The leading n x n diagonal block of the cfg2 operator
+    (``laplace_dl_oracle(contour_default(n_total))``, problems.py:133-217)
+    assembled by the reference's own ``compress`` (compress.py:173-200,
+    CompressionConfig(tol=0, max_rank=r, method="aca_rook_pivot")) on both
+    orientations of every sibling block of the n-row subtree.
+    Returns flat D, U, V in the SPEC layout."""
+    import math
+
+    from hodlr.compress import CompressionConfig, compress  # type: ignore
+    from hodlr.problems import contour_default, laplace_dl_oracle  # type: ignore
+    from hodlr.tree import IndexRange  # type: ignore
+
+    entry = laplace_dl_oracle(contour_default(n_total))
+    L = int(round(math.log2(n // m)))
+    D = np.empty((1 << L) * m * m)
+    for a in range(1 << L):
+        idx = np.arange(a * m, (a + 1) * m)
+        D[a * m * m : (a + 1) * m * m] = np.asarray(entry(idx[:, None], idx[None, :])).ravel(order="F")
+    U, V = np.zeros(n * r * L), np.zeros(n * r * L)
+    cfg = CompressionConfig(tol=0.0, max_rank=r, method="aca_rook_pivot")
+    for lv in range(1, L + 1):
+        nl = n >> lv
+        for p in range(1 << (lv - 1)):
+            for o in range(2):
+                ra, cb = (2 * p + o) * nl, (2 * p + 1 - o) * nl
+                f = compress(entry, IndexRange(ra, ra + nl), IndexRange(cb, cb + nl), cfg)
+                for l in range(f.rank):
+                    c = ((lv - 1) * r + l) * n
+                    U[c + ra : c + ra + nl] = f.u[:, l]
+                    V[c + cb : c + cb + nl] = np.conj(f.v[:, l])
+    return D, U, V
