@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "lu_device.cuh"
 
 namespace hodlr {
 
@@ -280,9 +281,15 @@ struct Apply2Cfg {
   static constexpr int PT = S + 8;  // Tinv [row][k] and V [rank][row] pitch (8 mod 16)
 };
 
-template <int S, int TWR>
+// IO = float: the fp32 factorization's leaf apply (cfg4) on the same fp64 DMMA
+// chain -- operands widened on load, results rounded to fp32 on store, the
+// diagonal-block inverses formed in the kernel from the staged (widened) fp32
+// LU (the fp32 LU kernel emits none).  The ApplyArgs pointers then address
+// float data.
+template <int S, int TWR, typename IO = double>
 __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply2_kernel(ApplyArgs g) {
   constexpr int NJ = S / 8, PT = Apply2Cfg<S>::PT, RT = TWR / 8;
+  constexpr bool F32 = sizeof(IO) == 4;
   extern __shared__ __align__(16) double sm[];
   double* Tm = sm;            // [row][k]
   double* Vs = sm + S * PT;   // [rank][row]
@@ -293,31 +300,49 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply2_kerne
 
   // ---- one-time staging, [row][k] (k pairs per thread): the LU factors off the
   // diagonal 8x8 tiles, the diagonal-block inverses P_q on them ----
-  const double* lb = g.lu + (int64_t)b * g.strideT;
+  const IO* lb = reinterpret_cast<const IO*>(g.lu) + (int64_t)b * g.strideT;
   const double* di = g.tinv + (int64_t)b * g.strideT;
   for (int idx = t; idx < S * (S / 2); idx += AP_THREADS) {
     const int m = idx % S, k = (idx / S) * 2;
     double2 x;
-    if ((m >> 3) == (k >> 3))
+    if (!F32 && (m >> 3) == (k >> 3))
       x = *reinterpret_cast<const double2*>(di + 64 * (m >> 3) + 8 * (m & 7) + (k & 7));
     else
-      x = make_double2(lb[m + (int64_t)k * g.ldi], lb[m + (int64_t)(k + 1) * g.ldi]);
+      x = make_double2((double)lb[m + (int64_t)k * g.ldi], (double)lb[m + (int64_t)(k + 1) * g.ldi]);
     *reinterpret_cast<double2*>(Tm + m * PT + k) = x;
   }
   if constexpr (TWR > 0) {
-    const double* vb = g.V + (int64_t)b * g.vstride;
-    for (int idx = t; idx < TWR * (S / 2); idx += AP_THREADS) {
-      const int j = idx / (S / 2), k = (idx % (S / 2)) * 2;
-      cp_async_16(Vs + j * PT + k, vb + k + (int64_t)j * g.ldv, 16);
+    if constexpr (F32) {
+      const float* vb = reinterpret_cast<const float*>(g.V) + (int64_t)b * g.vstride;
+      for (int idx = t; idx < TWR * S; idx += AP_THREADS) {
+        const int j = idx / S, k = idx % S;
+        Vs[j * PT + k] = (double)vb[k + (int64_t)j * g.ldv];
+      }
+    } else {
+      const double* vb = g.V + (int64_t)b * g.vstride;
+      for (int idx = t; idx < TWR * (S / 2); idx += AP_THREADS) {
+        const int j = idx / (S / 2), k = (idx % (S / 2)) * 2;
+        cp_async_16(Vs + j * PT + k, vb + k + (int64_t)j * g.ldv, 16);
+      }
+      cp_async_commit();
     }
-    cp_async_commit();
   }
   if (t < S) pm[t] = g.perm[(int64_t)b * S + t];
-  cp_async_wait<0>();
+  if constexpr (!F32) cp_async_wait<0>();
   __syncthreads();
+  if constexpr (F32) {  // P_q from the staged LU, then onto the diagonal tiles
+    double* dtmp = Vs + TWR * PT;
+    diag_block_inverses<S>(Tm, PT, 1, dtmp, AP_THREADS);
+    __syncthreads();
+    for (int idx = t; idx < S * 8; idx += AP_THREADS) {
+      const int m = idx >> 3, k = (m & ~7) + (idx & 7);
+      Tm[m * PT + k] = dtmp[64 * (m >> 3) + 8 * (m & 7) + (idx & 7)];
+    }
+    __syncthreads();
+  }
 
-  const double* Bb = g.B + aoff(b, g.bdiv, g.sB_hi, g.sB_lo);
-  double* Xb = g.X + aoff(b, g.bdiv, g.sX_hi, g.sX_lo);
+  const IO* Bb = reinterpret_cast<const IO*>(g.B) + aoff(b, g.bdiv, g.sB_hi, g.sB_lo);
+  IO* Xb = reinterpret_cast<IO*>(g.X) + aoff(b, g.bdiv, g.sX_hi, g.sX_lo);
 
   const int G = (g.ncols + 7) >> 3;
   const int gpc = (G + g.groups - 1) / g.groups;
@@ -325,12 +350,12 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply2_kerne
   auto load_b = [&](int grp, double (&v)[NJ][2]) {
     const int col = grp * 8 + ar;
     const bool ok = col < g.ncols;
-    const double* bc = Bb + (int64_t)(ok ? col : 0) * g.ldb;
+    const IO* bc = Bb + (int64_t)(ok ? col : 0) * g.ldb;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {  // this lane's gathered rows: P rows 8j + 2ac + {0, 1}
       const int2 p = *reinterpret_cast<const int2*>(pm + 8 * j + 2 * ac);
-      v[j][0] = ok ? bc[p.x] : 0.0;
-      v[j][1] = ok ? bc[p.y] : 0.0;
+      v[j][0] = ok ? (double)bc[p.x] : 0.0;
+      v[j][1] = ok ? (double)bc[p.y] : 0.0;
     }
   };
 
@@ -382,9 +407,14 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply2_kerne
     }
     const int col = grp * 8 + ar;
     if (col < g.ncols) {
-      double* xc = Xb + (int64_t)col * g.ldx + 2 * ac;
+      IO* xc = Xb + (int64_t)col * g.ldx + 2 * ac;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) *reinterpret_cast<double2*>(xc + 8 * j) = make_double2(a2[j][0], a2[j][1]);
+      for (int j = 0; j < NJ; ++j) {
+        if constexpr (F32)
+          *reinterpret_cast<float2*>(xc + 8 * j) = make_float2((float)a2[j][0], (float)a2[j][1]);
+        else
+          *reinterpret_cast<double2*>(xc + 8 * j) = make_double2(a2[j][0], a2[j][1]);
+      }
     }
     if constexpr (TWR > 0) {
       // ---- TW^T = X^T V, in passes of at most 32 ranks (bounded registers) ----
@@ -403,10 +433,15 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply2_kerne
             dmma_8x8x4(tw[jr][0], tw[jr][1], a2[j][1], v.y);
           }
         if (col < g.ncols) {
-          double* out = g.TW + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR + (int64_t)col * 2 * TWR + 2 * ac;
+          IO* out = reinterpret_cast<IO*>(g.TW) + (int64_t)(b >> 1) * g.tw_stride + (b & 1) * TWR +
+                    (int64_t)col * 2 * TWR + 2 * ac;
 #pragma unroll
-          for (int jr = 0; jr < RP; ++jr)
-            *reinterpret_cast<double2*>(out + 8 * (r0 + jr)) = make_double2(tw[jr][0], tw[jr][1]);
+          for (int jr = 0; jr < RP; ++jr) {
+            if constexpr (F32)
+              *reinterpret_cast<float2*>(out + 8 * (r0 + jr)) = make_float2((float)tw[jr][0], (float)tw[jr][1]);
+            else
+              *reinterpret_cast<double2*>(out + 8 * (r0 + jr)) = make_double2(tw[jr][0], tw[jr][1]);
+          }
         }
       }
     }
@@ -576,6 +611,34 @@ static hodlr_status run_apply(ApplyArgs g, cudaStream_t st) {
   tri_apply_kernel<S, BN, TWR><<<(unsigned)grid, AP_THREADS, smem, st>>>(g);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
+}
+
+// fp32 leaf apply (cfg4): Y_b = U_b^-1 L_b^-1 P_b Y_b for s = 64 blocks of the
+// fp32 LU, on the fp64 DMMA chain, optionally fused with TW_b = V_b^T Y_b
+// (twr = 8).  ERR_ARG for other shapes / alignments (caller falls back).
+hodlr_status tri_apply_f32(int s, int ncols, int batch, const float* lu, int64_t strideT, const int32_t* perm, float* Y,
+                           int64_t ldy, int64_t sY, const float* V, int64_t ldv, int64_t vstride, int twr, float* TW,
+                           int64_t tw_stride, cudaStream_t st) {
+  if (batch == 0 || ncols == 0) return HODLR_OK;
+  if (s != 64 || (V && twr != 8) || (ldy & 1) || (sY & 1) || (reinterpret_cast<uintptr_t>(Y) & 7) ||
+      (TW && ((tw_stride & 1) || (reinterpret_cast<uintptr_t>(TW) & 7))))
+    return HODLR_ERR_ARG;
+  ApplyArgs g{nullptr, reinterpret_cast<const double*>(lu), 64, strideT, perm, reinterpret_cast<const double*>(Y),
+              ldy, sY, 0, reinterpret_cast<double*>(Y), ldy, sY, 0, ncols, batch, 1, 1,
+              reinterpret_cast<const double*>(V), ldv, vstride, reinterpret_cast<double*>(TW), tw_stride};
+  constexpr int S = 64, PT = Apply2Cfg<S>::PT;
+  auto go = [&](auto kern, int twr_) -> hodlr_status {
+    const size_t smem = (size_t)(S + twr_) * PT * sizeof(double) + (size_t)S * 8 * sizeof(double);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int G = (int)ceil_div(ncols, 8);
+    int cpb = 1;
+    while ((int64_t)batch * cpb < 2 * 148 && cpb * 8 < G) cpb *= 2;
+    g.groups = cpb;
+    kern<<<(unsigned)((int64_t)batch * cpb), AP_THREADS, smem, st>>>(g);
+    HODLR_CHECK_LAUNCH();
+    return HODLR_OK;
+  };
+  return V ? go(tri_apply2_kernel<64, 8, float>, 8) : go(tri_apply2_kernel<64, 0, float>, 0);
 }
 
 // X_b = Tinv-apply(P_b B_b) for s in {16, 32, 64, 128}; returns ERR_ARG otherwise.

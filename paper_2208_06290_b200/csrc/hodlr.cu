@@ -22,6 +22,14 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const 
                            int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st,
                            const double* V = nullptr, int64_t ldv = 0, int64_t vstride = 0, int twr = 0,
                            double* TW = nullptr, int64_t tw_stride = 0);
+hodlr_status tri_apply_f32(int s, int ncols, int batch, const float* lu, int64_t strideT, const int32_t* perm, float* Y,
+                           int64_t ldy, int64_t sY, const float* V, int64_t ldv, int64_t vstride, int twr, float* TW,
+                           int64_t tw_stride, cudaStream_t st);
+static inline hodlr_status tri_apply_f32(int, int, int, const double*, int64_t, const int32_t*, double*, int64_t,
+                                         int64_t, const double*, int64_t, int64_t, int, double*, int64_t,
+                                         cudaStream_t) {
+  return HODLR_ERR_ARG;
+}
 hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, double* C, int64_t ldc,
                               const double* A1, const double* V, int64_t lda, const double* W, int64_t wstride,
                               int ncols, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
@@ -442,13 +450,23 @@ static hodlr_status factor_generic(const hodlr_desc* d, const hodlr_factors* f, 
                         nullptr, 0, 0, st));
   }
   if (L == 0 || r == 0) return HODLR_OK;
-  {
-    Phase ph(HODLR_PHASE_LEAF_APPLY, st);
-    TRY(launch_getrs<T>(m, r * L, (int)nleaf, D, m, (int64_t)m * m, f->dperm, Y, N, m, Y, N, m, 0, st));
-  }
   T* part = reinterpret_cast<T*>(wp + ws.split + ws.tw + ws.w);
   bool tw_ready = false;
-  {  // leaf-level [W|T]_a = V_a^T Y(I_a, :) by the fused kernel (no update)
+  {
+    Phase ph(HODLR_PHASE_LEAF_APPLY, st);
+    hodlr_status s = HODLR_ERR_ARG;
+    if constexpr (sizeof(T) == 4) {  // fp64 DMMA chain on fp32 operands, fused leaf-level [W|T]
+      const bool fuse = r == 8;
+      s = tri_apply_f32(m, r * L, (int)nleaf, D, (int64_t)m * m, f->dperm, Y, N, m,
+                        fuse ? V + (int64_t)(L - 1) * r * N : nullptr, N, m, r, fuse ? TW : nullptr,
+                        (int64_t)2 * r * r * L, st);
+      if (s == HODLR_OK) tw_ready = fuse;
+      else if (s != HODLR_ERR_ARG) return s;
+    }
+    if (s != HODLR_OK)
+      TRY(launch_getrs<T>(m, r * L, (int)nleaf, D, m, (int64_t)m * m, f->dperm, Y, N, m, Y, N, m, 0, st));
+  }
+  if (!tw_ready) {  // leaf-level [W|T]_a = V_a^T Y(I_a, :) by the fused kernel (no update)
     Phase ph(HODLR_PHASE_LEVEL, st);
     const hodlr_status s = level_T(r, N, m, m, Y, N, nullptr, V + (int64_t)(L - 1) * r * N, N, nullptr, 0, r * L, TW,
                                    (int64_t)2 * r * r * L, part, ws.part, st);
