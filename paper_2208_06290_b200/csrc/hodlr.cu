@@ -48,6 +48,9 @@ int64_t level_segment_rows(int64_t n, int64_t node, int sms);
 hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
                        const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
                        int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st, int seg_max = 1024);
+hodlr_status level_f32_dmma(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
+                            const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
+                            int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st);
 hodlr_status gemm_f32(int transA, int M, int N, int K, float alpha, const float* A, int64_t lda, int64_t sA_hi,
                       int64_t sA_lo, const float* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, float beta, float* C,
                       int64_t ldc, int64_t sC_hi, int64_t sC_lo, int batch, int bdiv, void* work, size_t work_bytes,
@@ -430,6 +433,27 @@ static hodlr_status level_T(int, int64_t, int64_t, int64_t, double*, int64_t, co
                             const double*, int64_t, int, double*, int64_t, double*, size_t, cudaStream_t, int = 0) {
   return HODLR_ERR_ARG;
 }
+// factorization level step: the fp64-DMMA rank-8 kernel first, else the SIMT one
+static hodlr_status level_fact_T(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc,
+                                 const float* A1, const float* V, int64_t lda, const float* W, int64_t wstride,
+                                 int ncols, float* TW, int64_t tw_stride, float* part, size_t part_bytes,
+                                 cudaStream_t st) {
+  static const bool simt = [] {
+    const char* e = getenv("HODLR_F32_LEVEL");
+    return e && e[0] == 's';
+  }();
+  if (!simt) {
+    const hodlr_status s = level_f32_dmma(r, n, n_c, node_rows, C, ldc, A1, V, lda, W, wstride, ncols, TW, tw_stride,
+                                          part, part_bytes, st);
+    if (s != HODLR_ERR_ARG) return s;
+  }
+  return level_f32(r, n, n_c, node_rows, C, ldc, A1, V, lda, W, wstride, ncols, TW, tw_stride, part, part_bytes, st);
+}
+static hodlr_status level_fact_T(int, int64_t, int64_t, int64_t, double*, int64_t, const double*, const double*,
+                                 int64_t, const double*, int64_t, int, double*, int64_t, double*, size_t,
+                                 cudaStream_t) {
+  return HODLR_ERR_ARG;
+}
 
 template <typename T>
 static hodlr_status factor_generic(const hodlr_desc* d, const hodlr_factors* f, char* wp, const FactWs& ws,
@@ -497,8 +521,9 @@ static hodlr_status factor_generic(const hodlr_desc* d, const hodlr_factors* f, 
     }
     {  // update + the next level's [W|T], fused when it applies
       Phase ph(HODLR_PHASE_LEVEL, st);
-      const hodlr_status s = level_T(r, N, nc, 2 * nc, Y, N, Y + (int64_t)lv * r * N, V + (int64_t)(lv - 1) * r * N,
-                                     N, W, (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st);
+      const hodlr_status s = level_fact_T(r, N, nc, 2 * nc, Y, N, Y + (int64_t)lv * r * N,
+                                          V + (int64_t)(lv - 1) * r * N, N, W, (int64_t)2 * r * wc, wc, TW,
+                                          (int64_t)2 * r * wc, part, ws.part, st);
       if (s == HODLR_OK) {
         tw_ready = true;
         continue;

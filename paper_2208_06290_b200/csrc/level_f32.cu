@@ -183,6 +183,173 @@ __global__ void level_reduce_f32_kernel(const float* part, float* TW, int ncols,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Factorization step on the fp64 DMMA chain (the same transposed scheme as
+// level_update4_kernel, here at R = 8 with fp32 operands widened on load and
+// results rounded on store):
+//   C^T  = C^T + (-W'^T) A1^T      A: W' entries, B: A1 panel (LDS.128 pairs)
+//   TW^T += C^T V                  A: the updated (rounded) C^T accumulators
+// CTA = 8 warps over a row segment, panels of a 64-row chunk widened into
+// shared memory (register prefetch of the next chunk, one barrier per chunk),
+// warps stream their 8-column groups.  The fp32 solve keeps the SIMT kernel
+// (its per-column arithmetic must not depend on nrhs).
+// ---------------------------------------------------------------------------
+constexpr int F32D_CH = 64, F32D_P = 66;
+
+template <int GPW>
+__global__ void __launch_bounds__(256, 3) level_f32_dmma_kernel(LevelF32Args g, int ncg, int tpc) {
+  constexpr int R = F32_R, CH = F32D_CH, NI = CH / 16, P = F32D_P, PANEL = R * P;
+  __shared__ __align__(16) double sm[2][2 * PANEL];  // [stage][A1 panel | V panel], [rank][row]
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int seg = blockIdx.x / ncg, cg = blockIdx.x % ncg;
+  const int64_t seg0 = (int64_t)seg * g.seg_rows;
+  const int nch = g.seg_rows / CH;
+  const int G = g.ncols >> 3;
+  const int gb = cg * tpc, ge = min(G, gb + tpc);
+  const bool upd = g.W != nullptr, red = g.V != nullptr;
+  // staging share: rank sk, rows 2 (t % 32) + {0, 1}
+  const int sk = t >> 5, sr = (t & 31) * 2;
+  float2 pa = make_float2(0.f, 0.f), pv = make_float2(0.f, 0.f);
+  auto fetch = [&](int ch) {
+    const int64_t r0 = seg0 + (int64_t)ch * CH + sr + (int64_t)sk * g.lda;
+    if (upd) pa = *reinterpret_cast<const float2*>(g.A1 + r0);
+    if (red) pv = *reinterpret_cast<const float2*>(g.V + r0);
+  };
+  auto put = [&](int s) {
+    *reinterpret_cast<double2*>(sm[s] + sk * P + sr) = make_double2(pa.x, pa.y);
+    *reinterpret_cast<double2*>(sm[s] + PANEL + sk * P + sr) = make_double2(pv.x, pv.y);
+  };
+  double tw[GPW][2];
+#pragma unroll
+  for (int q = 0; q < GPW; ++q) tw[q][0] = tw[q][1] = 0.0;
+  if (nch > 0) {
+    fetch(0);
+    put(0);
+  }
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    const int s = ch & 1;
+    if (ch + 1 < nch) fetch(ch + 1);  // lands while this chunk is computed
+    const double* As = sm[s];
+    const double* Vs = sm[s] + PANEL;
+    const int64_t row0 = seg0 + (int64_t)ch * CH;
+    const int c = (int)(row0 / g.n_c);
+    const float* Wp = upd ? g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R : nullptr;
+#pragma unroll
+    for (int q = 0; q < GPW; ++q) {
+      const int grp = gb + warp + 8 * q;
+      if (grp < ge) {
+        const int col = grp * 8 + ar;
+        float* cptr = g.C + row0 + (int64_t)col * g.ldc + 4 * ac;
+        float4 cin[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) cin[i] = *reinterpret_cast<const float4*>(cptr + 16 * i);
+        double acc[2 * NI][2];
+#pragma unroll
+        for (int i = 0; i < 2 * NI; ++i) acc[i][0] = acc[i][1] = 0.0;
+        if (upd) {
+          const float2 w2 = __ldg(reinterpret_cast<const float2*>(Wp + (int64_t)col * (2 * R) + 2 * ac));
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const double a = -(double)(u ? w2.y : w2.x);
+            const double* ak = As + (2 * ac + u) * P + 2 * ar;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+              const double2 b2 = *reinterpret_cast<const double2*>(ak + 16 * i);
+              dmma_8x8x4(acc[2 * i][0], acc[2 * i][1], a, b2.x);
+              dmma_8x8x4(acc[2 * i + 1][0], acc[2 * i + 1][1], a, b2.y);
+            }
+          }
+        }
+        // C + (-(A1 W')), rounded to fp32; the rounded values feed the reduction
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const float x = (float)((double)cin[i].x + acc[2 * i][0]);
+          const float y = (float)((double)cin[i].y + acc[2 * i + 1][0]);
+          const float z = (float)((double)cin[i].z + acc[2 * i][1]);
+          const float w = (float)((double)cin[i].w + acc[2 * i + 1][1]);
+          if (upd) *reinterpret_cast<float4*>(cptr + 16 * i) = make_float4(x, y, z, w);
+          acc[2 * i][0] = x, acc[2 * i + 1][0] = y, acc[2 * i][1] = z, acc[2 * i + 1][1] = w;
+        }
+        if (red) {
+#pragma unroll
+          for (int i = 0; i < NI; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double2 v2 = *reinterpret_cast<const double2*>(Vs + ar * P + 16 * i + 4 * ac + 2 * h);
+              dmma_8x8x4(tw[q][0], tw[q][1], acc[2 * i][h], v2.x);
+              dmma_8x8x4(tw[q][0], tw[q][1], acc[2 * i + 1][h], v2.y);
+            }
+        }
+      }
+    }
+    if (ch + 1 < nch) put(s ^ 1);  // stage s ^ 1 was last read before the previous barrier
+    // a segment may hold several whole nodes: emit a node's [W|T] at its last chunk
+    if (red && !g.partial && (row0 + CH) % g.node_rows == 0) {
+      const int64_t qn = row0 / g.node_rows;
+      float* out = g.TW + (qn >> 1) * g.tw_stride + (qn & 1) * R;
+#pragma unroll
+      for (int q = 0; q < GPW; ++q) {
+        const int grp = gb + warp + 8 * q;
+        if (grp < ge)
+          *reinterpret_cast<float2*>(out + 2 * ac + (int64_t)(grp * 8 + ar) * (2 * R)) =
+              make_float2((float)tw[q][0], (float)tw[q][1]);
+        tw[q][0] = tw[q][1] = 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  if (!red || !g.partial) return;
+  // tw[q][h] = TW^T[col][rank 2 ac + h], segment partial
+  float* out = g.TW + (int64_t)seg * R * g.ncols;
+#pragma unroll
+  for (int q = 0; q < GPW; ++q) {
+    const int grp = gb + warp + 8 * q;
+    if (grp < ge)
+      *reinterpret_cast<float2*>(out + 2 * ac + (int64_t)(grp * 8 + ar) * R) =
+          make_float2((float)tw[q][0], (float)tw[q][1]);
+  }
+}
+
+// One factorization level step (r = 8) on the DMMA chain.  ERR_ARG: shape or
+// alignment not supported (the caller uses level_f32).
+hodlr_status level_f32_dmma(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
+                            const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
+                            int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st) {
+  if (ncols == 0) return HODLR_OK;
+  if (r != F32_R || ncols % 8 || n_c % F32D_CH || n % F32D_CH || node_rows % F32D_CH) return HODLR_ERR_ARG;
+  if ((ldc & 3) || (uintptr_t)C % 16 || (lda & 1) || (A1 && (uintptr_t)A1 % 8) || (V && (uintptr_t)V % 8) ||
+      (W && ((wstride & 1) || (uintptr_t)W % 8)) || (TW && (tw_stride & 1)))
+    return HODLR_ERR_ARG;
+  // segments of up to F32_SEG rows: several whole nodes, or a node's slice (partials)
+  const int64_t seg = std::min<int64_t>(n, F32_SEG);
+  if (n % seg || (node_rows % seg && seg % node_rows)) return HODLR_ERR_ARG;
+  const int64_t nseg = n / seg;
+  const bool split = seg < node_rows && V != nullptr;
+  if (split && (size_t)nseg * F32_R * ncols * sizeof(float) > part_bytes) return HODLR_ERR_ARG;
+  LevelF32Args g{C, ldc, A1, V, lda, W, wstride, n_c, node_rows, ncols, (int)seg, 0, split ? part : TW, tw_stride,
+                 split ? 1 : 0};
+  const int G = ncols / 8;
+  const int gpw = G <= 8 ? 1 : 2;
+  const int tpc = std::min(G, 8 * gpw);
+  const int ncg = (G + tpc - 1) / tpc;
+  const int64_t grid = nseg * ncg;
+  if (grid > 2147483647LL) return HODLR_ERR_ARG;
+  if (gpw == 1)
+    level_f32_dmma_kernel<1><<<(unsigned)grid, 256, 0, st>>>(g, ncg, tpc);
+  else
+    level_f32_dmma_kernel<2><<<(unsigned)grid, 256, 0, st>>>(g, ncg, tpc);
+  HODLR_CHECK_LAUNCH();
+  if (!split) return HODLR_OK;
+  const int nnodes = (int)(n / node_rows);
+  const int64_t total = (int64_t)F32_R * ncols * nnodes;
+  level_reduce_f32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 8), 4736), 256, 0, st>>>(
+      part, TW, ncols, (int)(node_rows / seg), nnodes, tw_stride);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
 size_t level_f32_partial_bytes(int64_t n, int ncols) { return (size_t)(n / 64 + 1) * F32_R * ncols * sizeof(float); }
 
 // One fp32 level step over n rows (r = 8, n_c >= 32).  ERR_ARG: unsupported shape.
