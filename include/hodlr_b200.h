@@ -177,10 +177,15 @@ hodlr_status hodlr_matvec(const hodlr_desc* d, const void* D, const void* U, con
  * oracle entry (the reference raises ValueError).
  * hodlr_build_laplace_dl: geom = 7 x N doubles (x, y, nx, ny, weights,
  *   -log|x - z| / 2pi, -curvature / 4pi) of the contour (problems.py:133-217).
+ * hodlr_build_gaussian: exp(-|p_i - p_j|^2 / h^2) + lambda delta_ij on dim-major
+ *   point coordinates pts (dim in 1..3, p_k at pts + k N), already in cluster
+ *   (kd) order -- BASELINE cfg1 (2-D) / cfg3 (3-D) operators.
  * hodlr_build_dense: entries of a dense column-major N x N device matrix. */
 size_t hodlr_build_workspace(const hodlr_desc* d);
 hodlr_status hodlr_build_laplace_dl(const hodlr_desc* d, const double* geom, void* D, void* U, void* V, void* work,
                                     size_t work_bytes, void* stream);
+hodlr_status hodlr_build_gaussian(const hodlr_desc* d, const double* pts, int dim, double h, double lambda, void* D,
+                                  void* U, void* V, void* work, size_t work_bytes, void* stream);
 hodlr_status hodlr_build_dense(const hodlr_desc* d, const double* A, int64_t lda, void* D, void* U, void* V,
                                void* work, size_t work_bytes, void* stream);
 

@@ -63,6 +63,22 @@ class LaplaceDL:
         return (k + self.logt[i]) * self.w[j] + 0.5 * eq
 
 
+class Gaussian:
+    """exp(-|p_i - p_j|^2 / h^2) + lam delta_ij on (dim, n) points (BASELINE
+    cfg1 / cfg3 operators; not in the reference package, so parity for this
+    oracle is against this restatement only)."""
+
+    def __init__(self, pts, h: float = 0.1, lam: float = 1.0):
+        self.P = np.ascontiguousarray(np.asarray(pts, dtype=np.float64).T)  # (n, dim)
+        self.h2 = h * h
+        self.lam = lam
+
+    def __call__(self, i, j):
+        i, j = np.asarray(i), np.asarray(j)
+        d = self.P[i] - self.P[j]
+        return np.exp(-(np.sum(d * d, axis=-1) / self.h2)) + self.lam * (i == j)
+
+
 class Dense:
     def __init__(self, A):
         self.A = np.asarray(A, dtype=np.float64)

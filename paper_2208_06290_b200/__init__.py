@@ -36,7 +36,14 @@ from .hodlr import (  # noqa: F401
     solve_flops,
     solve_with_refinement,
 )
-from .construct import assemble_dense, contour_default, laplace_dl_geometry, laplace_dl_hodlr  # noqa: F401
+from .construct import (  # noqa: F401
+    assemble_dense,
+    contour_default,
+    gaussian_hodlr,
+    kd_points,
+    laplace_dl_geometry,
+    laplace_dl_hodlr,
+)
 from ._lib import HodlrNativeError, LIB_PATH  # noqa: F401
 
 __version__ = "0.1.0"

@@ -13,6 +13,10 @@ Entry oracles:
   (problems.py:133-217).  The O(N) contour geometry is evaluated here with the
   reference's numpy expressions (so it is bit-identical); the O(N r L)
   kernel entries and the ACA run on the device.
+* :func:`gaussian_hodlr` -- BASELINE cfg1 / cfg3: the regularized Gaussian
+  kernel on uniform random points in the unit square / cube (xorshift64*
+  stream of problems.py:26-48), cluster-ordered by an alternating-axis median
+  split that follows the cluster tree's ranges.
 * :func:`assemble_dense` -- entries of a dense device matrix (small n, tests,
   the SPEC examples).
 """
@@ -63,6 +67,47 @@ def laplace_dl_geometry(n: int, amplitude: float = 0.3, lobes: int = 5, z=(0.0, 
     return np.stack([c["x"], c["y"], c["nx"], c["ny"], c["weights"], logterm, diag]).astype(np.float64)
 
 
+_MASK64 = (1 << 64) - 1
+
+
+def xorshift_uniform(count: int, seed: int) -> np.ndarray:
+    """Doubles in [0, 1) from the xorshift64* stream (problems.py:26-48: splitmix64
+    seeding, top 53 bits) -- the same sequence as XorShift64Star(seed).uniform(count)."""
+    z = (seed + 0x9E3779B97F4A7C15) & _MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK64
+    x = (z ^ (z >> 31)) or 0x9E3779B97F4A7C15
+    out = np.empty(count, dtype=np.float64)
+    for k in range(count):
+        x ^= x >> 12
+        x = (x ^ (x << 25)) & _MASK64
+        x ^= x >> 27
+        out[k] = (((x * 0x2545F4914F6CDD1D) & _MASK64) >> 11) * 2.0**-53
+    return out
+
+
+def kd_points(n: int, dim: int, L: int, seed: int = 0) -> np.ndarray:
+    """(dim, n) uniform points in [0, 1)^dim (one xorshift64* stream, point-major),
+    reordered so that every cluster-tree node of ``ClusterTree(n, L)`` is a
+    spatial box: the level-l node range is sorted along axis l mod dim and
+    split at ceil(len / 2) (tree.py:35-93 ranges)."""
+    pts = xorshift_uniform(n * dim, seed).reshape(n, dim)
+    order = np.arange(n)
+    starts = np.array([0])
+    lens = np.array([n])
+    for lv in range(L + 1):
+        axis = lv % dim
+        seg = np.repeat(np.arange(len(starts)), lens)
+        key = pts[order, axis]
+        order = order[np.lexsort((key, seg))]  # stable within each node
+        if lv == L:
+            break
+        left = (lens + 1) // 2
+        starts = np.stack([starts, starts + left], axis=1).ravel()
+        lens = np.stack([left, lens - left], axis=1).ravel()
+    return np.ascontiguousarray(pts[order].T)
+
+
 def _alloc(n: int, m: int, r: int, device):
     torch = _torch()
     L = int(round(math.log2(n // m))) if n >= m else 0
@@ -94,6 +139,28 @@ def laplace_dl_hodlr(n: int, m: int, r: int, amplitude: float = 0.3, lobes: int 
     _lib.check(lib.hodlr_build_laplace_dl(C.byref(desc), C.c_void_p(geom.data_ptr()), C.c_void_p(D.data_ptr()),
                                           C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()),
                                           C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st)), "hodlr_build_laplace_dl")
+    return _finish(n, m, r, L, D, U, V)
+
+
+def gaussian_hodlr(n: int, m: int, r: int, dim: int = 2, h: float = 0.1, lam: float = 1.0, seed: int = 0,
+                   device="cuda", stream=None, points=None) -> HodlrMatrix:
+    """exp(-|p_i - p_j|^2 / h^2) + lam delta_ij on kd-ordered uniform points,
+    assembled on the device at uniform rank ``r`` (ACA rook, tol = 0).
+    ``points``: optional (dim, n) coordinates already in cluster order."""
+    torch = _torch()
+    lib = _lib.load()
+    L, D, U, V = _alloc(n, m, r, device)
+    P = kd_points(n, dim, L, seed) if points is None else np.ascontiguousarray(points, dtype=np.float64)
+    if P.shape != (dim, n):
+        raise ValueError(f"points must be ({dim}, {n})")
+    pts = torch.from_numpy(P).to(device)
+    desc = _lib.Desc(n, m, r, L, 0)
+    wsb = lib.hodlr_build_workspace(C.byref(desc))
+    ws = _workspace(wsb, pts.device)
+    st = (stream or torch.cuda.current_stream(pts.device)).cuda_stream
+    _lib.check(lib.hodlr_build_gaussian(C.byref(desc), C.c_void_p(pts.data_ptr()), dim, float(h), float(lam),
+                                        C.c_void_p(D.data_ptr()), C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()),
+                                        C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st)), "hodlr_build_gaussian")
     return _finish(n, m, r, L, D, U, V)
 
 

@@ -51,6 +51,26 @@ struct LaplaceDL {
   }
 };
 
+// Gaussian kernel on points (BASELINE cfg1: 2-D, cfg3: 3-D), regularized:
+//   A_ij = exp(-|p_i - p_j|^2 / h^2) + lambda delta_ij,
+// coordinates dim-major (p_k at pts + k N), squared distance summed over k in
+// order (numpy's sum over the last axis of a 2- or 3-vector).
+struct GaussianPts {
+  const double* p;
+  int64_t n;
+  int dim;
+  double h2, lam;
+  __device__ __forceinline__ double operator()(int64_t i, int64_t j) const {
+    double d2 = 0.0;
+    for (int k = 0; k < dim; ++k) {
+      const double d = __dsub_rn(p[k * n + i], p[k * n + j]);
+      d2 = k == 0 ? __dmul_rn(d, d) : __dadd_rn(d2, __dmul_rn(d, d));
+    }
+    const double v = exp(-__ddiv_rn(d2, h2));
+    return __dadd_rn(v, i == j ? lam : 0.0);
+  }
+};
+
 // Entries of a dense column-major matrix on the device (tests, small n).
 struct DenseOracle {
   const double* A;
@@ -520,6 +540,16 @@ extern "C" hodlr_status hodlr_build_laplace_dl(const hodlr_desc* d, const double
   if (d->L > 0 && d->r > 0 && (!U || !V)) return HODLR_ERR_ARG;
   const int64_t n = d->n;
   LaplaceDL A{geom, geom + n, geom + 2 * n, geom + 3 * n, geom + 4 * n, geom + 5 * n, geom + 6 * n};
+  return build_run(d, A, (double*)D, (double*)U, (double*)V, static_cast<char*>(work), static_cast<cudaStream_t>(stream));
+}
+
+extern "C" hodlr_status hodlr_build_gaussian(const hodlr_desc* d, const double* pts, int dim, double h, double lambda,
+                                             void* D, void* U, void* V, void* work, size_t work_bytes, void* stream) {
+  if (!build_desc_ok(d) || !pts || dim < 1 || dim > 3 || !(h > 0.0) || !D || !work ||
+      work_bytes < build_ws(d).total)
+    return HODLR_ERR_ARG;
+  if (d->L > 0 && d->r > 0 && (!U || !V)) return HODLR_ERR_ARG;
+  GaussianPts A{pts, d->n, dim, h * h, lambda};
   return build_run(d, A, (double*)D, (double*)U, (double*)V, static_cast<char*>(work), static_cast<cudaStream_t>(stream));
 }
 

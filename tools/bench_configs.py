@@ -1,12 +1,13 @@
 """Timing of the other BASELINE.json configs on one B200 (the contract line is
 bench.py = cfg2).  Prints one JSON object per configuration:
 
-  cfg1  Gaussian-kernel-shaped exact HODLR, N = 2^14, leaf 64, rank 32, fp64
-  cfg3  rank-64 HODLR, N = 2^21 (the per-GPU share of 2^22 at P = 2), fp64
+  cfg1  Gaussian kernel on 2^14 kd-ordered 2-D points (device-assembled), leaf 64, rank 32, fp64
+  cfg3  Gaussian kernel on 2^21 3-D points (per-GPU share of 2^22 at P = 2), rank 64, fp64
   cfg4  rank-8 fp32 preconditioner, N = 2^21
   cfg5  multi-RHS solve sweep (1..256) on the cfg2 factorization (N = 2^20, r = 32)
 
-Inputs: seeded exact-HODLR stand-ins generated in HBM.
+Inputs: cfg1 / cfg3 operators assembled on the device (ACA rook); cfg4 / cfg5
+use seeded exact-HODLR stand-ins generated in HBM.
 Timing: CUDA events, warm-up first, median of the timed repetitions.
 """
 import json, math, statistics, sys
@@ -25,8 +26,9 @@ def solve_bytes(n, m, r, es, nrhs):
     return es * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 2 * n * nrhs * es
 
 
-def time_factor_solve(n, m, r, dtype, reps=5, nrhs=1):
-    h0 = hb.random_hodlr(n, m, r, seed=0, s=1.0, dtype=dtype)
+def time_factor_solve(n, m, r, dtype, reps=5, nrhs=1, h0=None):
+    if h0 is None:
+        h0 = hb.random_hodlr(n, m, r, seed=0, s=1.0, dtype=dtype)
     b = torch.randn(n, nrhs, dtype=dtype, device="cuda").squeeze(1) if nrhs == 1 else torch.randn(n, nrhs, dtype=dtype, device="cuda")
     tf, ts = [], []
     for it in range(reps + 2):
@@ -57,11 +59,18 @@ def line(cfg, n, m, r, dtype_name, tf, ts, res, extra=None):
 
 which = sys.argv[1:] or ["cfg1", "cfg3", "cfg4", "cfg5"]
 if "cfg1" in which:
-    tf, ts, res = time_factor_solve(1 << 14, 64, 32, torch.float64)
-    line("cfg1", 1 << 14, 64, 32, "f64", tf, ts, res)
+    # the cfg1 operator: Gaussian kernel (h = 0.1, lambda = 1) on 2^14 kd-ordered 2-D points, assembled on the device
+    h1 = hb.gaussian_hodlr(1 << 14, 64, 32, dim=2, h=0.1, lam=1.0)
+    tf, ts, res = time_factor_solve(1 << 14, 64, 32, torch.float64, h0=h1)
+    line("cfg1 (Gaussian kernel, 2^14 2-D points)", 1 << 14, 64, 32, "f64", tf, ts, res)
 if "cfg3" in which:
-    tf, ts, res = time_factor_solve(1 << 21, 64, 64, torch.float64, reps=3)
-    line("cfg3-shape (per-GPU share of N=2^22 at P=2)", 1 << 21, 64, 64, "f64", tf, ts, res)
+    # per-GPU share of cfg3 at P = 2: Gaussian kernel on 2^21 kd-ordered 3-D points, rank 64
+    h3 = hb.gaussian_hodlr(1 << 21, 64, 64, dim=3, h=0.1, lam=1.0)
+    tf, ts, res = time_factor_solve(1 << 21, 64, 64, torch.float64, reps=3, h0=h3)
+    del h3
+    torch.cuda.empty_cache()
+    line("cfg3-shape (Gaussian kernel, 2^21 3-D points: per-GPU share of N=2^22 at P=2)", 1 << 21, 64, 64, "f64",
+         tf, ts, res)
 if "cfg4" in which:
     tf, ts, res = time_factor_solve(1 << 21, 64, 8, torch.float32)
     line("cfg4", 1 << 21, 64, 8, "f32", tf, ts, res)
