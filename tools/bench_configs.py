@@ -62,7 +62,26 @@ if "cfg1" in which:
     # the cfg1 operator: Gaussian kernel (h = 0.1, lambda = 1) on 2^14 kd-ordered 2-D points, assembled on the device
     h1 = hb.gaussian_hodlr(1 << 14, 64, 32, dim=2, h=0.1, lam=1.0)
     tf, ts, res = time_factor_solve(1 << 14, 64, 32, torch.float64, h0=h1)
-    line("cfg1 (Gaussian kernel, 2^14 2-D points)", 1 << 14, 64, 32, "f64", tf, ts, res)
+    # the reference's own CPU path on the same operator (its batched kernels, all host threads)
+    extra = None
+    try:
+        import os, time as _t
+        import numpy as np
+        from oracle import ref_driver as rd
+        if rd.AVAILABLE:
+            thr = os.cpu_count() or 1
+            D, U, V = (x.cpu().numpy().copy() for x in (h1.D, h1.U, h1.V))
+            bb = np.random.default_rng(1).standard_normal((1 << 14, 1))
+            t0 = _t.perf_counter()
+            dpiv, Ks, kp = rd.ref_factorize(D, U, V, 1 << 14, 64, 32, 8, rd.executor(thr))
+            t1 = _t.perf_counter()
+            rd.ref_solve(D, dpiv, U, V, Ks, kp, bb, 1 << 14, 64, 32, 8, rd.executor(thr))
+            t2 = _t.perf_counter()
+            extra = {"reference_cpu": {"t_factor_ms": round(1e3 * (t1 - t0), 1), "t_solve_ms": round(1e3 * (t2 - t1), 1),
+                                       "threads": thr}}
+    except Exception as e:  # noqa: BLE001
+        extra = {"reference_cpu": f"unavailable: {e}"}
+    line("cfg1 (Gaussian kernel, 2^14 2-D points)", 1 << 14, 64, 32, "f64", tf, ts, res, extra)
 if "cfg3" in which:
     # per-GPU share of cfg3 at P = 2: Gaussian kernel on 2^21 kd-ordered 3-D points, rank 64
     h3 = hb.gaussian_hodlr(1 << 21, 64, 64, dim=3, h=0.1, lam=1.0)
