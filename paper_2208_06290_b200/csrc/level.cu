@@ -505,9 +505,11 @@ __global__ void __launch_bounds__(256, 2) level_update3_kernel(LevelArgs g) {
 // [W|T] partial sums stay in registers (GPW groups per warp) for the whole
 // segment.
 // ---------------------------------------------------------------------------
-template <int R>
+template <int R, bool SOLVE = false>
 struct Level4Cfg {
-  static constexpr int CH = R >= 64 ? 32 : 64;  // rows per chunk (the warp's C^T tile height)
+  // rows per chunk (the warp's C^T tile height); the solve mode always uses the
+  // streaming solve kernel's 64-row chunks (identical chunk partials)
+  static constexpr int CH = (R >= 64 && !SOLVE) ? 32 : 64;
   static constexpr int NI = CH / 16;            // 16-row bands per chunk
   static constexpr int P = CH + 2;              // [rank][row] pitch: 2P = 4 (mod 16) doubles
   static constexpr int PANEL = R * P;
@@ -531,7 +533,7 @@ __device__ __forceinline__ void stg_v4(double* p, double x, double y, double z, 
 // sum in row order -- so the result is bit-identical to solve_level_kernel.
 template <int R, int GPW, bool LATE, bool SOLVE = false>
 __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
-  using Cfg = Level4Cfg<R>;
+  using Cfg = Level4Cfg<R, SOLVE>;
   constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8, NI = Cfg::NI;
   extern __shared__ __align__(16) double sm[];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -762,7 +764,7 @@ constexpr int kSolveCtaRows = 512;
 template <int R>
 __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
   constexpr int RT = R / 8;
-  __shared__ double ps[8][R * 8];  // chunk partials of the current column group: [chunk][rank + 8? ]
+  __shared__ double ps[8][R * 8];  // chunk partials of the current column group: [chunk][col_local * R + rank]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ar = lane >> 2, ac = lane & 3;
   const int64_t cta0 = (int64_t)blockIdx.x * g.seg_rows;
@@ -865,7 +867,7 @@ static hodlr_status run_solve_level(const LevelArgs& g, int64_t nblk, cudaStream
 
 template <int R>
 static hodlr_status run_level4_solve(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
-  using Cfg = Level4Cfg<R>;
+  using Cfg = Level4Cfg<R, true>;
   const int gpw = (g.tpc + 7) / 8;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -914,16 +916,18 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   LevelArgs g{X, ldx, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)cta_rows,
               node_rows, nrhs, 1, 1};
   hodlr_status s;
-  if (nrhs >= 16 && r <= 32 && solve_wide()) {
+  if (nrhs >= (r >= 64 ? 25 : 16) && solve_wide()) {  // crossovers measured (cfg5 sweeps)
     // many right-hand sides: shared-memory panels reused by every column group
     // (same segments and reduction order as solve_level_kernel)
     const int G = (nrhs + 7) / 8;
-    const int gpc = std::min(G, 32);
+    const int gpc = std::min(G, r >= 64 ? 8 : 32);  // R = 64: one group per warp (register budget)
     g.seg_rows = (int)std::min<int64_t>(node_rows, cta_rows);
     g.ncg = (G + gpc - 1) / gpc;
     g.tpc = gpc;
     const int64_t nseg = n / g.seg_rows;
-    s = r == 16 ? run_level4_solve<16>(g, nseg, st) : run_level4_solve<32>(g, nseg, st);
+    s = r == 16 ? run_level4_solve<16>(g, nseg, st)
+        : r == 32 ? run_level4_solve<32>(g, nseg, st)
+                  : run_level4_solve<64>(g, nseg, st);
   } else {
     s = r == 16 ? run_solve_level<16>(g, nblk, st)
         : r == 32 ? run_solve_level<32>(g, nblk, st)

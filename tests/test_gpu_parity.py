@@ -138,10 +138,12 @@ def test_random_vs_oracle(n, m, r, s):
     assert relres(x) <= max(1e-12, 4 * relres(orc.solve(fo, b, threads=8)))
 
 
-@pytest.mark.parametrize("nrhs", [5, 20])
-def test_multi_rhs_columns_bitwise_equal_single(nrhs):
+@pytest.mark.parametrize("nrhs", [5, 20, 27])
+@pytest.mark.parametrize("r", [32, 64])
+def test_multi_rhs_columns_bitwise_equal_single(nrhs, r):
     # column j of a blocked solve == single-vector solve, bit for bit
-    n, m, r = 1 << 13, 64, 32
+    # (the shared-panel kernel runs from 16 (r = 32) / 25 (r = 64) columns, the streaming one below)
+    n, m = 1 << 13, 64
     h = hb.random_hodlr(n, m, r, seed=3, s=16.0)
     f = hb.factorize(h)
     B = torch.randn(n, nrhs, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
