@@ -37,6 +37,10 @@ from .hodlr import (  # noqa: F401
     solve_with_refinement,
 )
 from .construct import (  # noqa: F401
+    CompressionConfig,
+    GaussianPoints,
+    LaplaceDoubleLayer,
+    assemble,
     assemble_dense,
     contour_default,
     gaussian_hodlr,

@@ -184,3 +184,59 @@ def assemble_dense(A, m: int, r: int, device="cuda", stream=None) -> HodlrMatrix
                                      C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()), C.c_void_p(ws.data_ptr()),
                                      wsb, C.c_void_p(st)), "hodlr_build_dense")
     return _finish(n, m, r, L, D, U, V)
+
+
+# ---------------------------------------------------------------------------
+# SPEC-shaped entry point: assemble(entry_oracle, tree, config)
+# ---------------------------------------------------------------------------
+
+
+class CompressionConfig:
+    """The reference's compression settings (compress.py:22-45).  The device
+    builder implements the fixed-rank ACA path: ``method="aca_rook_pivot"``,
+    ``tol=0`` and a ``max_rank`` (the uniform rank of the GPU layout)."""
+
+    def __init__(self, tol: float = 0.0, max_rank: int | None = None, method: str = "aca_rook_pivot"):
+        if method != "aca_rook_pivot":
+            raise ValueError(f"device assembly implements method='aca_rook_pivot' (got {method!r})")
+        if tol != 0.0 or max_rank is None:
+            raise ValueError("device assembly is fixed-rank: tol=0 and max_rank=r (uniform-rank GPU layout)")
+        if max_rank < 0:
+            raise ValueError("max_rank must be >= 0")
+        self.tol, self.max_rank, self.method = tol, max_rank, method
+
+
+class LaplaceDoubleLayer:
+    """Device entry oracle of ``laplace_dl_oracle(contour_default(n, amplitude, lobes), z)``."""
+
+    def __init__(self, n: int, amplitude: float = 0.3, lobes: int = 5, z=(0.0, 0.0)):
+        self.n, self.amplitude, self.lobes, self.z = n, amplitude, lobes, z
+
+
+class GaussianPoints:
+    """Device entry oracle exp(-|p_i - p_j|^2 / h^2) + lam delta_ij on (dim, n)
+    points already in cluster order (see :func:`kd_points`)."""
+
+    def __init__(self, points, h: float = 0.1, lam: float = 1.0):
+        self.points = np.ascontiguousarray(points, dtype=np.float64)
+        self.h, self.lam = h, lam
+
+
+def assemble(entry_oracle, tree: ClusterTree, config: CompressionConfig, device="cuda") -> HodlrMatrix:
+    """SPEC.md:163-171 ``assemble`` on the device.  ``entry_oracle``: a
+    :class:`LaplaceDoubleLayer`, a :class:`GaussianPoints` or a dense (n, n)
+    matrix; ``tree``: a uniform ``ClusterTree(n, L)`` (n = m 2^L)."""
+    n, L = tree.n, tree.depth
+    m = n >> L
+    if m << L != n:
+        raise ValueError("device assembly needs a uniform tree (n = m 2^L)")
+    r = config.max_rank
+    if isinstance(entry_oracle, LaplaceDoubleLayer):
+        if entry_oracle.n != n:
+            raise ValueError("oracle and tree sizes differ")
+        return laplace_dl_hodlr(n, m, r, entry_oracle.amplitude, entry_oracle.lobes, entry_oracle.z, device=device)
+    if isinstance(entry_oracle, GaussianPoints):
+        P = entry_oracle.points
+        return gaussian_hodlr(n, m, r, dim=P.shape[0], h=entry_oracle.h, lam=entry_oracle.lam, points=P, device=device)
+    return assemble_dense(entry_oracle, m, r, device=device)
+

@@ -92,3 +92,20 @@ def test_gaussian_cfg1_factor_solve():
     b = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
     x = hb.solve(hb.factorize(h.clone()), b)
     assert float(torch.linalg.norm(h.matvec(x) - b) / torch.linalg.norm(b)) <= 1e-12
+
+
+def test_spec_assemble_entry_point():
+    # SPEC.md:163-171 shape: assemble(oracle, tree, config) for the three device oracles
+    n, m, r = 2048, 32, 16
+    tree = hb.ClusterTree(n, 6)
+    cfg = hb.CompressionConfig(tol=0.0, max_rank=r)
+    g = np.load(GOLDEN / "build_laplace_n2048_m32_r16.npz")
+    h = hb.assemble(hb.LaplaceDoubleLayer(n), tree, cfg)
+    assert h.U.cpu().numpy().tobytes() == g["U"].tobytes()
+    P = hb.kd_points(n, 2, 6, seed=1)
+    h2 = hb.assemble(hb.GaussianPoints(P, h=0.2), tree, cfg)
+    assert h2.rank == r and h2.n == n
+    h3 = hb.assemble(np.eye(64), hb.ClusterTree(64, 2), hb.CompressionConfig(max_rank=4))
+    assert not h3.U.any()
+    with pytest.raises(ValueError):
+        hb.CompressionConfig(tol=1e-8, max_rank=4)
