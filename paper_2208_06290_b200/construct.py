@@ -134,8 +134,9 @@ def laplace_dl_hodlr(n: int, m: int, r: int, amplitude: float = 0.3, lobes: int 
     geom = torch.from_numpy(laplace_dl_geometry(n, amplitude, lobes, z)).to(device)
     desc = _lib.Desc(n, m, r, L, 0)
     wsb = lib.hodlr_build_workspace(C.byref(desc))
-    ws = _workspace(wsb, geom.device)
-    st = (stream or torch.cuda.current_stream(geom.device)).cuda_stream
+    so = stream or torch.cuda.current_stream(geom.device)
+    ws = _workspace(wsb, geom.device, so)
+    st = so.cuda_stream
     _lib.check(lib.hodlr_build_laplace_dl(C.byref(desc), C.c_void_p(geom.data_ptr()), C.c_void_p(D.data_ptr()),
                                           C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()),
                                           C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st)), "hodlr_build_laplace_dl")
@@ -156,8 +157,9 @@ def gaussian_hodlr(n: int, m: int, r: int, dim: int = 2, h: float = 0.1, lam: fl
     pts = torch.from_numpy(P).to(device)
     desc = _lib.Desc(n, m, r, L, 0)
     wsb = lib.hodlr_build_workspace(C.byref(desc))
-    ws = _workspace(wsb, pts.device)
-    st = (stream or torch.cuda.current_stream(pts.device)).cuda_stream
+    so = stream or torch.cuda.current_stream(pts.device)
+    ws = _workspace(wsb, pts.device, so)
+    st = so.cuda_stream
     _lib.check(lib.hodlr_build_gaussian(C.byref(desc), C.c_void_p(pts.data_ptr()), dim, float(h), float(lam),
                                         C.c_void_p(D.data_ptr()), C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()),
                                         C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st)), "hodlr_build_gaussian")
@@ -178,8 +180,9 @@ def assemble_dense(A, m: int, r: int, device="cuda", stream=None) -> HodlrMatrix
     Acm = At.t().contiguous().to(device)  # column-major entries
     desc = _lib.Desc(n, m, r, L, 0)
     wsb = lib.hodlr_build_workspace(C.byref(desc))
-    ws = _workspace(wsb, Acm.device)
-    st = (stream or torch.cuda.current_stream(Acm.device)).cuda_stream
+    so = stream or torch.cuda.current_stream(Acm.device)
+    ws = _workspace(wsb, Acm.device, so)
+    st = so.cuda_stream
     _lib.check(lib.hodlr_build_dense(C.byref(desc), C.c_void_p(Acm.data_ptr()), n, C.c_void_p(D.data_ptr()),
                                      C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()), C.c_void_p(ws.data_ptr()),
                                      wsb, C.c_void_p(st)), "hodlr_build_dense")

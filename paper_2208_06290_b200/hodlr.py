@@ -131,8 +131,9 @@ class HodlrMatrix:
         Y = torch.empty_like(X)
         desc = self.desc()
         wsb = lib.hodlr_matvec_workspace(C.byref(desc), nrhs)
-        ws = _workspace(wsb, dev) if wsb else None
-        st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        so = stream or torch.cuda.current_stream(dev)
+        ws = _workspace(wsb, dev, so) if wsb else None
+        st = so.cuda_stream
         _lib.check(
             lib.hodlr_matvec(C.byref(desc), C.c_void_p(self.D.data_ptr()), C.c_void_p(self.U.data_ptr()),
                              C.c_void_p(self.V.data_ptr()), C.c_void_p(X.data_ptr()), n,
@@ -219,13 +220,19 @@ class HodlrFactorization:
 _WS_CACHE: dict = {}
 
 
-def _workspace(nbytes: int, device):
-    """Reusable device workspace (bytes), grown on demand."""
+def _workspace(nbytes: int, device, stream=None):
+    """Reusable device workspace (bytes) per (device, stream), grown on demand.
+    Calls on one stream are ordered, so they can share it; calls on different
+    streams (e.g. concurrent solves on one factorization) get
+    their own buffer, allocated on that stream."""
     torch = _torch()
-    key = (str(device),)
+    s = stream or torch.cuda.current_stream(device)
+    key = (str(device), s.cuda_stream)
     buf = _WS_CACHE.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS_CACHE.pop(key, None)
+        with torch.cuda.stream(s):
+            buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
         _WS_CACHE[key] = buf
     return buf
 
@@ -285,8 +292,9 @@ def factorize(h: HodlrMatrix, variant: str = "pivoted_standard", check: bool = T
     )
     desc = h.desc()
     wsb = lib.hodlr_factorize_workspace(C.byref(desc))
-    ws = _workspace(wsb, dev)
-    st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    so = stream or torch.cuda.current_stream(dev)
+    ws = _workspace(wsb, dev, so)
+    st = so.cuda_stream
     cf = f.cfactors()
     _lib.check(lib.hodlr_factorize(C.byref(desc), C.byref(cf), C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st)),
                "hodlr_factorize")
@@ -341,8 +349,8 @@ def factorize_from_host(n: int, m: int, r: int, D, U, V, variant: str = "pivoted
     f.host_inputs = (Dh, Uh, Vh)  # alive until the asynchronous upload has completed
     desc = f.desc()
     wsb = lib.hodlr_factorize_workspace(C.byref(desc))
-    ws = _workspace(wsb, dev)
     st = (stream or torch.cuda.current_stream(dev))
+    ws = _workspace(wsb, dev, st)
     key = str(dev)
     if key not in _COPY_STREAMS:
         _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
@@ -395,7 +403,7 @@ def solve(fact: HodlrFactorization, b, stream=None):
             x = x.clone()
         desc = fact.desc()
         wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
-        ws = _workspace(wsb, dev)
+        ws = _workspace(wsb, dev, so)
         cf = fact.cfactors()
         _lib.check(
             lib.hodlr_solve(C.byref(desc), C.byref(cf), C.c_void_p(x.data_ptr()), n, nrhs,

@@ -145,3 +145,21 @@ def test_refinement_fp32_preconditioner_reaches_fp64():
     assert all(hist[k + 1] < hist[k] for k in range(3))  # monotone for >= 3 iterations
     assert min(hist) <= 1e-13 and not res.diverged
     assert float(torch.linalg.norm(h64.matvec(res.x) - b) / torch.linalg.norm(b)) == pytest.approx(min(hist))
+
+
+def test_concurrent_solves_on_two_streams():
+    # solve is safe to call concurrently on one factorization with
+    # distinct right-hand sides (per-stream workspaces)
+    n, m, r = 1 << 15, 64, 32
+    f = hb.factorize(hb.random_hodlr(n, m, r, seed=9))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    b1 = torch.randn(n, 3, dtype=torch.float64, device="cuda", generator=g)
+    b2 = torch.randn(n, 3, dtype=torch.float64, device="cuda", generator=g)
+    x1_ref, x2_ref = hb.solve(f, b1), hb.solve(f, b2)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        x1 = hb.solve(f, b1, stream=s1)
+        x2 = hb.solve(f, b2, stream=s2)
+        torch.cuda.synchronize()
+        assert torch.equal(x1, x1_ref) and torch.equal(x2, x2_ref)
