@@ -109,3 +109,13 @@ def test_spec_assemble_entry_point():
     assert not h3.U.any()
     with pytest.raises(ValueError):
         hb.CompressionConfig(tol=1e-8, max_rank=4)
+
+
+def test_builder_edge_shapes():
+    # single leaf (L = 0): D only; rank 0: zero panels; m = 1 (the SPEC 2 x 2 case) covered by the goldens
+    A = np.random.default_rng(0).standard_normal((64, 64))
+    h = hb.assemble_dense(A, 64, 4)
+    assert h.L == 0 and h.U.numel() == 0
+    assert np.array_equal(h.D.cpu().numpy(), A.ravel(order="F"))
+    h0 = hb.assemble_dense(A, 16, 0)
+    assert h0.U.numel() == 0 and np.array_equal(h0.D.cpu().numpy()[: 16 * 16], A[:16, :16].ravel(order="F"))
