@@ -1,6 +1,6 @@
 """CPU: the sharded (multi-GPU) schedule's host logic -- partitioning, packing
 and the per-top-level sum all-reduces -- driven with the numpy (oracle)
-backend, in lockstep and over a real gloo process group (world_size 2)."""
+backend, in lockstep (world 1..8) and over real gloo process groups (world_size 2 and 4)."""
 
 from __future__ import annotations
 
@@ -81,10 +81,10 @@ def _gloo_worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_gloo_world2_matches_oracle(tmp_path):
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_world_matches_oracle(tmp_path, world):
     import torch.multiprocessing as mp
 
-    world = 2
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
