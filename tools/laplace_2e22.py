@@ -17,3 +17,18 @@ for it in range(2):
     rel = float(torch.linalg.norm(h.matvec(x) - b) / torch.linalg.norm(b))
     print(f"Laplace DL N=2^22 r=32: build {tb:.2f} s  factor {e[0].elapsed_time(e[1]):.1f} ms  solve {e[1].elapsed_time(e[2]):.2f} ms  relres {rel:.2e}", flush=True)
     del f, hh
+
+# fp32, rank 8, N = 2^21: the paper's "low accuracy" Laplace case (assembled in fp64, cast)
+n2 = 1 << 21
+h64 = hb.laplace_dl_hodlr(n2, 64, 8)
+h32 = hb.HodlrMatrix(h64.tree, 8, h64.D.float(), h64.U.float(), h64.V.float())
+b2 = torch.randn(n2, dtype=torch.float64, device="cuda")
+for it in range(3):
+    hh = h32.clone(); torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record(); f = hb.factorize(hh, check=False); e[1].record(); x = hb.solve(f, b2.float()); e[2].record()
+    torch.cuda.synchronize()
+    rel = float(torch.linalg.norm(h64.matvec(x.double()) - b2) / torch.linalg.norm(b2))
+    if it:
+        print(f"Laplace DL N=2^21 r=8 fp32: factor {e[0].elapsed_time(e[1]):.2f} ms  solve {e[1].elapsed_time(e[2]):.3f} ms  relres {rel:.2e}", flush=True)
+    del f, hh
