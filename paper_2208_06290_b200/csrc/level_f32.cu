@@ -1,10 +1,12 @@
-// FP32 level step for rank 8 (the preconditioner configuration, cfg4), SIMT:
+// FP32 level steps for rank 8 (the preconditioner configuration, cfg4):
 //
 //   C(I_c, :) -= Y_c^{l+1} W'_c            (update; skipped when W == null)
 //   TW_q      += V_q^{(l)T} C(I_q, :)      (next level's [W|T] / w; skipped when V == null)
 //
-// fp32 has no tensor-core path of fp64 accuracy, and at rank 8 the step is
-// HBM-bound (2 flops per byte): one warp owns 8 columns of a row segment, each
+// The factorization runs level_f32_dmma_kernel (below): the fp64 DMMA chain
+// on widened fp32 operands.  The solve runs the SIMT level_f32_kernel, whose
+// per-column arithmetic does not depend on the number of right-hand sides.
+// At rank 8 the step is HBM-bound (2 flops per byte).  SIMT kernel: one warp owns 8 columns of a row segment, each
 // lane streams rows (coalesced column reads), keeps the 8 x 8 W' block of the
 // current child and the 8 x 8 [W|T] partial in registers, and the warp's
 // partials are combined with a fixed xor-butterfly.  Segment partials are
