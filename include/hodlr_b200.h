@@ -182,6 +182,9 @@ hodlr_status hodlr_matvec(const hodlr_desc* d, const void* D, const void* U, con
  *   (kd) order -- BASELINE cfg1 (2-D) / cfg3 (3-D) operators.
  * hodlr_build_dense: entries of a dense column-major N x N device matrix. */
 size_t hodlr_build_workspace(const hodlr_desc* d);
+/* The xorshift64* uniform stream of problems.py:26-48 (XorShift64Star(seed).uniform(count))
+ * written to out[0..count) on the device, bit-identical (point sets of the cfg1/cfg3 operators). */
+hodlr_status hodlr_xorshift_uniform(uint64_t seed, int64_t count, double* out, void* stream);
 hodlr_status hodlr_build_laplace_dl(const hodlr_desc* d, const double* geom, void* D, void* U, void* V, void* work,
                                     size_t work_bytes, void* stream);
 hodlr_status hodlr_build_gaussian(const hodlr_desc* d, const double* pts, int dim, double h, double lambda, void* D,

@@ -71,6 +71,7 @@ SIGNATURES = {
     "hodlr_matvec_workspace": (_sz, [C.POINTER(Desc), _i]),
     "hodlr_matvec": (_i, [C.POINTER(Desc), _p, _p, _p, _p, _i64, _p, _i64, _i, _p, _sz, _p]),
     "hodlr_build_workspace": (_sz, [C.POINTER(Desc)]),
+    "hodlr_xorshift_uniform": (_i, [C.c_uint64, _i64, _p, _p]),
     "hodlr_build_laplace_dl": (_i, [C.POINTER(Desc), _p, _p, _p, _p, _p, _sz, _p]),
     "hodlr_build_dense": (_i, [C.POINTER(Desc), _p, _i64, _p, _p, _p, _p, _sz, _p]),
     "hodlr_build_gaussian": (_i, [C.POINTER(Desc), _p, _i, _d, _d, _p, _p, _p, _p, _sz, _p]),

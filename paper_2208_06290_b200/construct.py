@@ -86,12 +86,27 @@ def xorshift_uniform(count: int, seed: int) -> np.ndarray:
     return out
 
 
-def kd_points(n: int, dim: int, L: int, seed: int = 0) -> np.ndarray:
+def xorshift_uniform_device(count: int, seed: int, device="cuda"):
+    """The same stream generated on the device (``hodlr_xorshift_uniform``)."""
+    torch = _torch()
+    lib = _lib.load()
+    out = torch.empty(max(count, 1), dtype=torch.float64, device=device)
+    st = torch.cuda.current_stream(out.device).cuda_stream
+    _lib.check(lib.hodlr_xorshift_uniform(C.c_uint64(seed & ((1 << 64) - 1)), count, C.c_void_p(out.data_ptr()),
+                                          C.c_void_p(st)), "hodlr_xorshift_uniform")
+    return out[:count]
+
+
+def kd_points(n: int, dim: int, L: int, seed: int = 0, device=None) -> np.ndarray:
     """(dim, n) uniform points in [0, 1)^dim (one xorshift64* stream, point-major),
     reordered so that every cluster-tree node of ``ClusterTree(n, L)`` is a
     spatial box: the level-l node range is sorted along axis l mod dim and
-    split at ceil(len / 2) (tree.py:35-93 ranges)."""
-    pts = xorshift_uniform(n * dim, seed).reshape(n, dim)
+    split at ceil(len / 2) (tree.py:35-93 ranges).  ``device``: draw the stream
+    there (large n) instead of the host loop."""
+    if device is not None:
+        pts = xorshift_uniform_device(n * dim, seed, device).cpu().numpy().reshape(n, dim)
+    else:
+        pts = xorshift_uniform(n * dim, seed).reshape(n, dim)
     order = np.arange(n)
     starts = np.array([0])
     lens = np.array([n])
@@ -151,7 +166,8 @@ def gaussian_hodlr(n: int, m: int, r: int, dim: int = 2, h: float = 0.1, lam: fl
     torch = _torch()
     lib = _lib.load()
     L, D, U, V = _alloc(n, m, r, device)
-    P = kd_points(n, dim, L, seed) if points is None else np.ascontiguousarray(points, dtype=np.float64)
+    P = (kd_points(n, dim, L, seed, device=device if n * dim > (1 << 16) else None) if points is None
+         else np.ascontiguousarray(points, dtype=np.float64))
     if P.shape != (dim, n):
         raise ValueError(f"points must be ({dim}, {n})")
     pts = torch.from_numpy(P).to(device)

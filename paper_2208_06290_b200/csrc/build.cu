@@ -380,6 +380,23 @@ __global__ void aca_init_kernel(AcaLv g) {
   g.st[b] = s;
 }
 
+// xorshift64* stream (problems.py:26-48): splitmix64-scrambled seed, top 53
+// bits of state * 0x2545F4914F6CDD1D as a double in [0, 1).  Sequential by
+// nature: one thread walks the stream (the state never leaves registers).
+__global__ void xorshift_uniform_kernel(uint64_t seed, int64_t count, double* out) {
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  uint64_t x = z ^ (z >> 31);
+  if (x == 0) x = 0x9E3779B97F4A7C15ull;
+  for (int64_t k = 0; k < count; ++k) {
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    out[k] = (double)((x * 0x2545F4914F6CDD1Dull) >> 11) * 0x1.0p-53;
+  }
+}
+
 // leaf blocks: D_a = A(I_a, I_a), column-major m x m at a m^2
 template <class Oracle>
 __global__ void leaf_blocks_kernel(int64_t nleaf, int m, double* D, Oracle A, int* err) {
@@ -531,6 +548,14 @@ hodlr_status build_run(const hodlr_desc* d, const Oracle& A, double* D, double* 
 }  // namespace hodlr
 
 using namespace hodlr;
+
+extern "C" hodlr_status hodlr_xorshift_uniform(uint64_t seed, int64_t count, double* out, void* stream) {
+  if (count < 0 || (count > 0 && !out)) return HODLR_ERR_ARG;
+  if (count == 0) return HODLR_OK;
+  xorshift_uniform_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(seed, count, out);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
 
 extern "C" size_t hodlr_build_workspace(const hodlr_desc* d) { return build_desc_ok(d) ? build_ws(d).total : 0; }
 

@@ -119,3 +119,14 @@ def test_builder_edge_shapes():
     assert np.array_equal(h.D.cpu().numpy(), A.ravel(order="F"))
     h0 = hb.assemble_dense(A, 16, 0)
     assert h0.U.numel() == 0 and np.array_equal(h0.D.cpu().numpy()[: 16 * 16], A[:16, :16].ravel(order="F"))
+
+
+def test_device_xorshift_matches_host_stream():
+    from paper_2208_06290_b200.construct import xorshift_uniform, xorshift_uniform_device
+
+    for seed in (0, 7, 2**63 + 5):
+        a = xorshift_uniform(5000, seed)
+        b = xorshift_uniform_device(5000, seed).cpu().numpy()
+        assert a.tobytes() == b.tobytes()
+    # the point sets (and so the assembled operators) do not depend on where the stream is drawn
+    assert hb.kd_points(4096, 3, 6, seed=2).tobytes() == hb.kd_points(4096, 3, 6, seed=2, device="cuda").tobytes()
