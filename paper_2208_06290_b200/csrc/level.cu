@@ -761,10 +761,12 @@ static FactSched level4_schedule(int64_t n, int64_t node, int G, int sms, int ma
 // ---------------------------------------------------------------------------
 constexpr int kSolveCtaRows = 512;
 
-template <int R>
+// NG = column groups per pass: two groups share every panel load (R <= 32);
+// each group's DMMA sequence is exactly the single-group one.
+template <int R, int NG>
 __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
   constexpr int RT = R / 8;
-  __shared__ double ps[8][R * 8];  // chunk partials of the current column group: [chunk][col_local * R + rank]
+  __shared__ double ps[8][NG][R * 8];  // chunk partials of the current groups: [chunk][group][col_local * R + rank]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ar = lane >> 2, ac = lane & 3;
   const int64_t cta0 = (int64_t)blockIdx.x * g.seg_rows;
@@ -775,48 +777,65 @@ __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
   const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
   const bool want_w = g.V != nullptr;
   const int G = (g.ncols + 7) >> 3;
-  for (int grp = 0; grp < G; ++grp) {
-    const int col = grp * 8 + ar;
-    const bool ok = col < g.ncols;
+  for (int gp = 0; gp < G; gp += NG) {
     if (has_chunk) {
-      double acc[8][2];
-      double* xp = g.C + row0 + (int64_t)(ok ? col : 0) * g.ldc + 4 * ac;
+      double acc[NG][8][2];
+      bool ok[NG];
+      double* xp[NG];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (ok) {
-          ldg_v4(xp + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
-        } else {
-          acc[2 * i][0] = acc[2 * i + 1][0] = acc[2 * i][1] = acc[2 * i + 1][1] = 0.0;
+      for (int q = 0; q < NG; ++q) {
+        const int col = (gp + q) * 8 + ar;
+        ok[q] = col < g.ncols;
+        xp[q] = g.C + row0 + (int64_t)(ok[q] ? col : 0) * g.ldc + 4 * ac;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (ok[q]) {
+            ldg_v4(xp[q] + 16 * i, acc[q][2 * i][0], acc[q][2 * i + 1][0], acc[q][2 * i][1], acc[q][2 * i + 1][1]);
+          } else {
+            acc[q][2 * i][0] = acc[q][2 * i + 1][0] = acc[q][2 * i][1] = acc[q][2 * i + 1][1] = 0.0;
+          }
         }
       }
-      const double* wc = Wp + (int64_t)(ok ? col : 0) * (2 * R) + 2 * ac;
       const double* a1 = g.A1 + row0 + 2 * ar;
       // ---- x^T += (-w'^T) Y^T ----
 #pragma unroll
       for (int kt = 0; kt < R / 8; ++kt) {
-        double2 w2 = make_double2(0.0, 0.0);
-        if (ok) w2 = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
+        double2 w2[NG];
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+          w2[q] = make_double2(0.0, 0.0);
+          if (ok[q])
+            w2[q] = __ldg(reinterpret_cast<const double2*>(Wp + (int64_t)((gp + q) * 8 + ar) * (2 * R) + 2 * ac + 8 * kt));
+        }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const double a = -(u ? w2.y : w2.x);
           const double* ak = a1 + (int64_t)(8 * kt + 2 * ac + u) * g.lda;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const double2 b2 = __ldcs(reinterpret_cast<const double2*>(ak + 16 * i));
-            dmma_8x8x4(acc[2 * i][0], acc[2 * i][1], a, b2.x);
-            dmma_8x8x4(acc[2 * i + 1][0], acc[2 * i + 1][1], a, b2.y);
+#pragma unroll
+            for (int q = 0; q < NG; ++q) {
+              const double a = -(u ? w2[q].y : w2[q].x);
+              dmma_8x8x4(acc[q][2 * i][0], acc[q][2 * i][1], a, b2.x);
+              dmma_8x8x4(acc[q][2 * i + 1][0], acc[q][2 * i + 1][1], a, b2.y);
+            }
           }
         }
       }
-      if (ok) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) stg_v4(xp + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
-      }
+      for (int q = 0; q < NG; ++q)
+        if (ok[q]) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            stg_v4(xp[q] + 16 * i, acc[q][2 * i][0], acc[q][2 * i + 1][0], acc[q][2 * i][1], acc[q][2 * i + 1][1]);
+        }
       if (want_w) {
-        // ---- chunk partial p^T = x_new^T V (from zero) ----
-        double p[RT][2];
+        // ---- chunk partials p^T = x_new^T V (each from zero) ----
+        double p[NG][RT][2];
 #pragma unroll
-        for (int jr = 0; jr < RT; ++jr) p[jr][0] = p[jr][1] = 0.0;
+        for (int q = 0; q < NG; ++q)
+#pragma unroll
+          for (int jr = 0; jr < RT; ++jr) p[q][jr][0] = p[q][jr][1] = 0.0;
         const double* vb = g.V + row0 + 4 * ac;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -825,13 +844,17 @@ __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
 #pragma unroll
             for (int jr = 0; jr < RT; ++jr) {
               const double2 v2 = __ldcs(reinterpret_cast<const double2*>(vb + (int64_t)(8 * jr + ar) * g.lda + 16 * i + 2 * h));
-              dmma_8x8x4(p[jr][0], p[jr][1], acc[2 * i][h], v2.x);
-              dmma_8x8x4(p[jr][0], p[jr][1], acc[2 * i + 1][h], v2.y);
-            }
-        // ps[chunk][col_local * R + rank]
 #pragma unroll
-        for (int jr = 0; jr < RT; ++jr)
-          *reinterpret_cast<double2*>(&ps[warp][ar * R + 8 * jr + 2 * ac]) = make_double2(p[jr][0], p[jr][1]);
+              for (int q = 0; q < NG; ++q) {
+                dmma_8x8x4(p[q][jr][0], p[q][jr][1], acc[q][2 * i][h], v2.x);
+                dmma_8x8x4(p[q][jr][0], p[q][jr][1], acc[q][2 * i + 1][h], v2.y);
+              }
+            }
+#pragma unroll
+        for (int q = 0; q < NG; ++q)
+#pragma unroll
+          for (int jr = 0; jr < RT; ++jr)
+            *reinterpret_cast<double2*>(&ps[warp][q][ar * R + 8 * jr + 2 * ac]) = make_double2(p[q][jr][0], p[q][jr][1]);
       }
     }
     if (!want_w) continue;
@@ -839,18 +862,19 @@ __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
     // ---- fixed-order sums of the chunk partials per output node / CTA segment ----
     const int cpn = (int)(g.node_rows / 64 < nchunk ? g.node_rows / 64 : nchunk);  // chunks per output unit
     const int units = nchunk / cpn;
-    for (int e = t; e < units * 8 * R; e += 256) {
-      const int uidx = e / (8 * R), mn = e % (8 * R);
+    for (int e = t; e < units * NG * 8 * R; e += 256) {
+      const int uidx = e / (NG * 8 * R), rem = e % (NG * 8 * R);
+      const int q = rem / (8 * R), mn = rem % (8 * R);
       const int cl = mn / R, rank = mn % R;
-      const int colg = grp * 8 + cl;
+      const int colg = (gp + q) * 8 + cl;
       double sacc = 0.0;
-      for (int k = 0; k < cpn; ++k) sacc += ps[uidx * cpn + k][mn];
+      for (int k = 0; k < cpn; ++k) sacc += ps[uidx * cpn + k][q][mn];
       if (colg < g.ncols) {
         if (g.partial) {
           g.TW[(int64_t)blockIdx.x * R * g.ncols + rank + (int64_t)colg * R] = sacc;
         } else {
-          const int64_t q = (cta0 + (int64_t)uidx * cpn * 64) / g.node_rows;
-          g.TW[(q >> 1) * g.tw_stride + (q & 1) * R + rank + (int64_t)colg * 2 * R] = sacc;
+          const int64_t qn = (cta0 + (int64_t)uidx * cpn * 64) / g.node_rows;
+          g.TW[(qn >> 1) * g.tw_stride + (qn & 1) * R + rank + (int64_t)colg * 2 * R] = sacc;
         }
       }
     }
@@ -858,9 +882,21 @@ __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
   }
 }
 
+static int solve_pairs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HODLR_SOLVE_PAIRS");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 template <int R>
 static hodlr_status run_solve_level(const LevelArgs& g, int64_t nblk, cudaStream_t st) {
-  solve_level_kernel<R><<<(unsigned)nblk, 256, 0, st>>>(g);
+  if (R <= 32 && g.ncols > 8 && solve_pairs())
+    solve_level_kernel<R, R <= 32 ? 2 : 1><<<(unsigned)nblk, 256, 0, st>>>(g);
+  else
+    solve_level_kernel<R, 1><<<(unsigned)nblk, 256, 0, st>>>(g);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
@@ -916,7 +952,7 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   LevelArgs g{X, ldx, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)cta_rows,
               node_rows, nrhs, 1, 1};
   hodlr_status s;
-  if (nrhs >= (r >= 64 ? 25 : 16) && solve_wide()) {  // crossovers measured (cfg5 sweeps)
+  if (nrhs >= (r >= 64 ? 25 : 17) && solve_wide()) {  // crossovers measured (cfg5 sweeps; 9-16 RHS: paired streaming)
     // many right-hand sides: shared-memory panels reused by every column group
     // (same segments and reduction order as solve_level_kernel)
     const int G = (nrhs + 7) / 8;
