@@ -1,0 +1,55 @@
+"""GPU: a seeded sweep over shapes the fused and generic paths dispatch on --
+leaf m, rank r, depth L, pivoting regime s, nrhs -- against the CPU oracle
+(leaf / K pivots bit-exact, x within 1e-9 of the oracle, relres within 4x of
+the oracle's own residual)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import hodlr_oracle as orc  # noqa: E402
+import paper_2208_06290_b200 as hb  # noqa: E402
+
+
+def _cases():
+    rng = np.random.default_rng(2024)
+    out = []
+    for k in range(16):
+        m = int(rng.choice([16, 32, 64]))
+        r = int(rng.choice([4, 8, 16, 32, 64]))
+        L = int(rng.integers(1, 6))
+        if 2 * r > (m << L) // 2:  # keep the coarsest blocks at least rank-wide
+            r = max(4, ((m << L) // 4) // 8 * 8) if ((m << L) // 4) >= 8 else 4
+        s = float(rng.choice([1.0, 16.0]))
+        nrhs = int(rng.choice([1, 3, 9, 17]))
+        out.append((m, r, L, s, nrhs, 100 + k))
+    return out
+
+
+@pytest.mark.parametrize("m,r,L,s,nrhs,seed", _cases())
+def test_sweep_against_oracle(m, r, L, s, nrhs, seed):
+    n = m << L
+    h = orc.make_exact_hodlr(n, m, r, seed=seed, s=s)
+    b = np.random.default_rng(seed).standard_normal((n, nrhs))
+    fo = orc.factorize(h.copy())
+    xo = orc.solve(fo, b)
+    hm = hb.HodlrMatrix.from_buffers(n, m, r, h.D, h.U, h.V)
+    f = hb.factorize(hm.clone())
+    x = hb.solve(f, b)
+    assert np.array_equal(f.dperm.cpu().numpy().reshape(-1, m), fo.dpiv.perm)
+    if L > 0:
+        assert np.array_equal(f.kswaps.cpu().numpy()[: ((1 << L) - 1) * 2 * r].reshape(-1, 2 * r),
+                              np.concatenate([p.swaps for p in fo.kpiv]))
+    rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
+    assert rel <= 1e-9, rel
+    bt = torch.from_numpy(b).cuda()
+
+    def relres(xx):
+        return float(torch.linalg.norm(hm.matvec(torch.from_numpy(xx).cuda()) - bt) / torch.linalg.norm(bt))
+
+    # the s = 16 regime is ill-conditioned: measure against the oracle's own residual
+    assert relres(x) <= max(1e-12, 4 * relres(xo)), (relres(x), relres(xo))
