@@ -53,3 +53,20 @@ def test_sweep_against_oracle(m, r, L, s, nrhs, seed):
 
     # the s = 16 regime is ill-conditioned: measure against the oracle's own residual
     assert relres(x) <= max(1e-12, 4 * relres(xo)), (relres(x), relres(xo))
+
+
+@pytest.mark.parametrize("m,r,L,nrhs", [(64, 8, 5, 1), (64, 8, 3, 9), (32, 8, 4, 3), (64, 16, 4, 2), (32, 4, 5, 1),
+                                        (16, 8, 4, 5)])
+def test_sweep_fp32_against_oracle(m, r, L, nrhs):
+    # fp32 (cfg4 preconditioner path): fused r = 8 / m = 64 kernels and the generic fp32 path
+    n = m << L
+    h = orc.make_exact_hodlr(n, m, r, seed=n + r, s=1.0, dtype=np.float32)
+    b = np.random.default_rng(5).standard_normal((n, nrhs)).astype(np.float32)
+    fo = orc.factorize(h.copy())
+    xo = orc.solve(fo, b)
+    f = hb.factorize(hb.HodlrMatrix.from_buffers(n, m, r, h.D, h.U, h.V))
+    assert f.D.dtype == torch.float32
+    assert np.array_equal(f.dperm.cpu().numpy().reshape(-1, m), fo.dpiv.perm)
+    x = hb.solve(f, b)
+    rel = np.linalg.norm(x.astype(np.float64) - xo) / np.linalg.norm(xo)
+    assert rel <= 1e-4, rel
