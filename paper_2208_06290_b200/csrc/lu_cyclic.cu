@@ -462,16 +462,9 @@ __global__ void __launch_bounds__(S < 32 ? 32 : S) getrf_sr_kernel(int mode, con
     if (active) {
       const T d = (piv == (T)0) ? (T)1 : piv;
       const T x = row[k];
-#ifdef HODLR_PROBE_NODIV
-      const T l = x * d;
-#else
       const T l = (x == (T)0 && d == d) ? ((signbit(x) != signbit(d)) ? (T)-0.0 : (T)0.0) : div_rn(x, d);
-#endif
       row[k] = l;
       int j = k + 1;
-#ifdef HODLR_PROBE_NOUPD
-      j = S;
-#endif
       if (j & 1) {  // align to 16B pairs
         if (j < S) row[j] = sub_rn(row[j], mul_rn(l, prow[j]));
         ++j;
