@@ -12,9 +12,13 @@ one factorize (PAPER Alg. 3) + one solve (Alg. 4) of a freshly restored copy
 of the matrix; the restore copy is outside the timed events.  Inputs (8 GB)
 exceed L2 (126 MB), so no explicit flush is needed.
 
-Multi-GPU: one process per GPU (torchrun); round 1 runs independent replicas
-(every rank factors its own N = 2^20 matrix, scaling "weak"); subtree sharding
-with NCCL is DESIGN.md §Multi-GPU.  Rank 0 prints one JSON line.
+Multi-GPU (--gpus N > 1; re-executed under torch.distributed.run when not
+already launched by torchrun): one process per GPU running the subtree-sharded
+factorization + solve of ONE matrix -- by default the north_star scaling case,
+BASELINE cfg3 (N = 2^22, leaf 64, rank 64, 3-D Gaussian kernel) -- with one
+NCCL sum all-reduce per top level, "scaling": "strong", time = max over ranks
+of the CUDA-event step time.  `--workload cfg3` at N = 1 gives the matching
+single-GPU base.  Rank 0 prints one JSON line.
 
 --impl reference: the reference's CPU path (its own batched kernels driven by
 the SPEC recipe, oracle/ref_driver.py, all host threads) on a bounded sample
@@ -220,10 +224,11 @@ def cpu_sample(n, problem, sub=None):
     return orc.HodlrData(lay, *(x.copy() for x in sub))
 
 
-def cpu_reference(n, threads, sample=None):
+def cpu_reference(n, threads, sample=None, keep=False):
     """The reference's CPU path on a bounded sample: Alg. 3/4 issuing the
     reference's own batched kernels (baseline/_ref, threads:<ncores> executor)
-    when installed -- kind "reference" -- else the oracle restatement ("port")."""
+    when installed -- kind "reference" -- else the oracle restatement ("port").
+    keep=True also returns the outputs (leaf LU + swaps, Y, K + swaps, x, b)."""
     import numpy as np
 
     from oracle import hodlr_oracle as orc
@@ -231,22 +236,65 @@ def cpu_reference(n, threads, sample=None):
 
     h = sample.copy() if sample is not None else orc.make_exact_hodlr(n, M_LEAF, RANK, seed=SEED, s=SCALE)
     b = np.random.default_rng(SEED + 1).standard_normal((n, 1))
-    L = h.lay.L
-    fl = orc.factor_flops(n, M_LEAF, RANK) + orc.solve_flops(n, M_LEAF, RANK)
+    L, r = h.lay.L, h.lay.r
+    fl = orc.factor_flops(n, M_LEAF, r) + orc.solve_flops(n, M_LEAF, r)
     if rd.AVAILABLE:
         ex = rd.executor(threads)
         t0 = time.perf_counter()
-        dpiv, Ks, kpivs = rd.ref_factorize(h.D, h.U, h.V, n, M_LEAF, RANK, L, ex)
+        dpiv, Ks, kpivs = rd.ref_factorize(h.D, h.U, h.V, n, M_LEAF, r, L, ex)
         t1 = time.perf_counter()
-        rd.ref_solve(h.D, dpiv, h.U, h.V, Ks, kpivs, b, n, M_LEAF, RANK, L, ex)
+        x = rd.ref_solve(h.D, dpiv, h.U, h.V, Ks, kpivs, b, n, M_LEAF, r, L, ex)
         t2 = time.perf_counter()
-        return fl, t1 - t0, t2 - t1, "reference"
+        outs = dict(D=h.D, dswaps=dpiv.swaps, Y=h.U, K=np.concatenate(Ks),
+                    kswaps=np.concatenate([p.swaps for p in kpivs]), x=x, b=b) if keep else None
+        return fl, t1 - t0, t2 - t1, "reference", outs
     t0 = time.perf_counter()
     f = orc.factorize(h, threads=threads)
     t1 = time.perf_counter()
-    orc.solve(f, b, threads=threads)
+    x = orc.solve(f, b, threads=threads)
     t2 = time.perf_counter()
-    return fl, t1 - t0, t2 - t1, "port"
+    outs = dict(D=f.D, dswaps=f.dpiv.swaps, Y=f.Y, K=np.concatenate(f.K),
+                kswaps=np.concatenate([p.swaps for p in f.kpiv]), x=x, b=b) if keep else None
+    return fl, t1 - t0, t2 - t1, "port", outs
+
+
+def parity_vs_cpu(hb, sample, outs, kind):
+    """The GPU factorize/solve of the CPU arm's exact sample vs the CPU arm's
+    outputs (north_star: pivots bit-exact, x within 1e-10)."""
+    import numpy as np
+
+    n, m, r = sample.lay.n, sample.lay.m, sample.lay.r
+    f = hb.factorize(hb.HodlrMatrix.from_buffers(n, m, r, sample.D, sample.U, sample.V))
+    x = hb.solve(f, outs["b"])
+
+    def rel(a, b):
+        return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+    return {
+        "against": "reference kernels (baseline/_ref)" if kind == "reference" else "oracle restatement",
+        "sample": f"leading 2^{int(math.log2(n))}-row subtree of the workload (the cpu_baseline sample)",
+        "leaf_lu_bitexact": bool(np.array_equal(f.D.cpu().numpy(), outs["D"])),
+        "pivots_bitexact": bool(np.array_equal(f.dswaps.cpu().numpy().reshape(-1, m), outs["dswaps"])
+                                and np.array_equal(f.kswaps.cpu().numpy().reshape(-1, 2 * r), outs["kswaps"])),
+        "x_relerr": rel(x, outs["x"]), "y_relerr": rel(f.Y.cpu().numpy(), outs["Y"]),
+        "k_relerr": rel(f.K.cpu().numpy(), outs["K"]), "tol": 1e-10,
+    }
+
+
+def cfg3_cpu_sample(n):
+    """The cfg3 CPU sample: the cfg3 operator family at n rows (Gaussian kernel,
+    h = 0.1, lam = 1, on n kd-ordered xorshift64* 3-D points, seed 0), rank 64,
+    assembled with the reference's own compress() on a numpy entry oracle."""
+    from oracle import build_oracle as bo
+    from oracle import hodlr_oracle as orc
+    from oracle import ref_driver as rd
+    from paper_2208_06290_b200.construct import kd_points  # host-side point generation only
+
+    r = WORKLOADS["cfg3"][1]
+    L = int(round(math.log2(n // M_LEAF)))
+    ent = bo.Gaussian(kd_points(n, 3, L, seed=0), h=0.1, lam=1.0)
+    D, U, V = rd.ref_assemble(ent, n, M_LEAF, r) if rd.AVAILABLE else bo.assemble(ent, n, M_LEAF, r)
+    return orc.HodlrData(orc.Layout(n, M_LEAF, r), D, U, V)
 
 
 def run_reference(args):
@@ -255,33 +303,37 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
-    n = CPU_SAMPLE_N
+    workload = args.workload or ("cfg3" if (args.gpus > 1 or world > 1) else "cfg2")
+    N, r = WORKLOADS[workload]
+    n = CPU_SAMPLE_N if workload == "cfg2" else CPU_SAMPLE_N // 2
     cpu_reference(1 << 12, threads)  # warm-up (imports, thread pool)
     t0 = time.perf_counter()
-    sample = cpu_sample(n, args.problem)  # built once, outside the timed steps
+    sample = cpu_sample(n, args.problem) if workload == "cfg2" else cfg3_cpu_sample(n)  # outside the timed steps
     build_s = time.perf_counter() - t0
     vals, tfs, tss = [], [], []
     kind = "port"
     for _ in range(args.steps):
-        fl, tf, ts, kind = cpu_reference(n, threads, sample)
+        fl, tf, ts, kind, _ = cpu_reference(n, threads, sample)
         vals.append(fl / (tf + ts) / 1e12)
         tfs.append(tf)
         tss.append(ts)
     v = statistics.mean(vals)
     how = ("reference batched kernels (baseline/_ref hodlr.backend, threads executor) driven by the SPEC "
            "Alg. 3/4 recipe" if kind == "reference" else "oracle restatement of the reference kernels")
-    sample = (f"{how}: factor+solve of the leading 2^16-row subtree of the cfg2 workload (m=64, r=32, fp64; "
-              f"{PROBLEM_DESC[args.problem]}), {args.steps} step(s); sample assembled once in {build_s:.1f} s")
+    what = (f"the leading 2^{int(math.log2(n))}-row subtree of the cfg2 workload (m=64, r=32, fp64; "
+            f"{PROBLEM_DESC[args.problem]})" if workload == "cfg2" else
+            f"the cfg3 operator family at 2^{int(math.log2(n))} rows (3-D Gaussian kernel, m=64, r=64, fp64, "
+            "compressed by the reference's compress())")
+    sample = f"{how}: factor+solve of {what}, {args.steps} step(s); sample assembled once in {build_s:.1f} s"
+    wdesc = WORKLOADS[workload][2] + (PROBLEM_DESC[args.problem] if workload == "cfg2" else "")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean([a + b for a, b in zip(tfs, tss)]),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        # the arm's config is the GPU arm's (cfg2 shape); each step is a bounded
-        # sample of it (one 2^16-row subtree, stated in cpu_baseline.sample)
-        "config": {"workload": "HODLR factor+solve, cfg2 (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
-                               + PROBLEM_DESC[args.problem], "N": N_DEFAULT, "leaf": M_LEAF, "rank": RANK,
-                   "L": int(math.log2(N_DEFAULT // M_LEAF)), "nrhs": 1, "parallelism": "cpu (reference)",
-                   "sample_rows": n, "device": "cpu"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        # the arm's config is the GPU arm's; each step is a bounded sample of it
+        # (stated in cpu_baseline.sample)
+        "config": {"workload": wdesc, "N": N, "leaf": M_LEAF, "rank": r, "L": int(math.log2(N // M_LEAF)), "nrhs": 1,
+                   "parallelism": "cpu (reference)", "sample_rows": n, "device": "cpu"},
         "t_factor_s": statistics.mean(tfs), "t_solve_s": statistics.mean(tss),
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -415,18 +467,19 @@ def run_ours(args):
     traffic, _ = traffic_from_profiles()
 
     if rank == 0:
-        cpu = None
+        cpu = parity = None
         if not args.no_cpu:
             threads = os.cpu_count() or 1
             samp = cpu_sample(CPU_SAMPLE_N, args.problem, subtree_of(h0, CPU_SAMPLE_N) if args.problem == "laplace" else None)
-            fl, ctf, cts, kind = cpu_reference(CPU_SAMPLE_N, threads, samp)
+            fl, ctf, cts, kind, outs = cpu_reference(CPU_SAMPLE_N, threads, samp, keep=True)
             cpu = {"value": fl / (ctf + cts) / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
                    "sample": ("reference kernels (baseline/_ref) via the SPEC recipe" if kind == "reference"
                               else "oracle restatement") + ": factor+solve of the leading 2^16-row subtree of this "
                    f"workload (m=64, r=32, fp64), {ctf:.1f} s factor + {cts:.2f} s solve"}
+            parity = parity_vs_cpu(hb, samp, outs, kind)
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "HODLR factor+solve, cfg2 (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
                                    + PROBLEM_DESC[args.problem], "N": n, "leaf": m, "rank": r, "L": L, "nrhs": 1,
@@ -447,16 +500,41 @@ def run_ours(args):
                          "flops_per_step": level_flops(n, m, r)},
             "clocks": clk.summary(), "wall_s_timed": wall,
             "hbm_peak_measured_gbps": peaks.get("hbm_gbs"),
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+WORKLOADS = {
+    # name: (N, rank, description) -- BASELINE.json configs[1] / configs[2]
+    "cfg2": (1 << 20, 32, "HODLR factor+solve, cfg2 (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "),
+    "cfg3": (1 << 22, 64, "HODLR factor+solve, cfg3 (N=2^22, leaf 64, rank 64, L=16, 1 RHS), Gaussian kernel "
+                          "exp(-|x-y|^2/h^2) + I (h=0.1) on 2^22 kd-ordered 3-D points, assembled on the device"),
+}
+
+
+def make_sharded_operator(hb, torch, workload, n, problem):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if workload == "cfg3":
+        h = hb.gaussian_hodlr(n, M_LEAF, WORKLOADS["cfg3"][1], dim=3, h=0.1, lam=1.0)
+    elif problem == "laplace":
+        h = hb.laplace_dl_hodlr(n, M_LEAF, RANK)
+    else:
+        h = hb.random_hodlr(n, M_LEAF, RANK, seed=SEED, s=SCALE)
+    torch.cuda.synchronize()
+    return h, 1e3 * (time.perf_counter() - t0)
+
+
 def run_sharded(args):
-    """N > 1: the same N = 2^20 matrix row-sharded over the ranks (strong scaling):
-    levels >= log2 P local, one NCCL sum all-reduce per top level."""
+    """N > 1 (or --sharded): one matrix row-sharded over the ranks (strong
+    scaling; default workload cfg3, the north_star scaling case N = 2^22,
+    r = 64): rank g owns the rows of level-p node g (P = 2^p), levels >= p are
+    local, one sum all-reduce of the packed [W|T] (resp. w) per top level over
+    NCCL.  Every rank assembles the operator on its own GPU and
+    keeps only its shard."""
     import ctypes as C
 
     import torch
@@ -469,20 +547,23 @@ def run_sharded(args):
     torch.cuda.set_device(local if args.dist_backend == "nccl" else 0)
     dist = init_dist(max(world, 2) if world > 1 else 1, args.dist_backend)
     lib = _lib.load()
-    n, m, r = args.n, M_LEAF, RANK
+    workload = args.workload or ("cfg3" if world > 1 else "cfg2")
+    n = args.n or WORKLOADS[workload][0]
+    m, r = M_LEAF, WORKLOADS[workload][1]
     L = int(round(math.log2(n // m)))
     f_flops, s_flops = factor_flops(n, m, r), solve_flops(n, m, r)
-    h0, build_ms = make_operator(hb, torch, n, m, r, args.problem, 0)  # identical on every rank
+    h0, build_ms = make_sharded_operator(hb, torch, workload, n, args.problem)  # identical on every rank
     g = torch.Generator(device="cuda")
     g.manual_seed(SEED + 7)
     b = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
     pristine = dd.make_shard(h0, rank, world)
-    work = dd.make_shard(h0, rank, world)
     n_loc, row0 = pristine.n_loc, pristine.row0
     b_loc = b[row0 : row0 + n_loc].clone()
-    if rank != 0:
+    keep_full = rank == 0 and not args.no_relres
+    if not keep_full:
         del h0
         torch.cuda.empty_cache()
+    work = dd.make_shard_like(pristine)
     backend = dd.GpuBackend()
 
     def all_reduce(buf):
@@ -494,7 +575,7 @@ def run_sharded(args):
         work.U.copy_(pristine.U)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
-        st = dd.factorize_sharded(work, all_reduce, backend)
+        st = dd.factorize_sharded(work, all_reduce, backend, check=False)
         e1.record()
         x = b_loc.clone()
         dd.solve_sharded(st, x, 1, all_reduce, backend)
@@ -517,10 +598,12 @@ def run_sharded(args):
     if world > 1:
         dist.all_gather(xs, x)
     relres = None
-    if rank == 0:
+    if keep_full:
         xg = torch.cat(xs)
         relres = float(torch.linalg.norm(h0.matvec(xg) - b) / torch.linalg.norm(b))
-        del h0
+        del h0, xg
+        torch.cuda.empty_cache()
+    del xs
 
     if world > 1:
         dist.barrier()
@@ -543,24 +626,42 @@ def run_sharded(args):
     t_step, tf, ts = tt.tolist()
     value = (f_flops + s_flops) / (t_step * 1e-3) / 1e12
     if rank == 0:
+        desc = WORKLOADS[workload][2] + (PROBLEM_DESC[args.problem] if workload == "cfg2" else "")
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "HODLR factor+solve, cfg2 (N=2^20, leaf 64, rank 32, L=14, 1 RHS), "
-                                   + PROBLEM_DESC[args.problem] + ", row-sharded", "N": n, "leaf": m, "rank": r, "L": L,
+            "config": {"workload": desc + ", row-sharded", "N": n, "leaf": m, "rank": r, "L": L,
                        "nrhs": 1, "parallelism": f"subtree-shard{world} ({args.dist_backend} all-reduce per top level)",
-                       "l2_flush": "inputs 8 GB > L2"},
+                       "l2_flush": "inputs > L2 (126 MB)"},
             "t_factor_ms": tf, "t_solve_ms": ts, "relres": relres, "phase_ms_rank0": phases, "build_ms": build_ms,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "wall_s_timed": wall,
-            "roofline": {"bound": "tensor", "kernel": "level_update_kernel", "achieved": None, "peak": None,
-                         "unit": "TFLOP/s", "frac": None, "traffic": None,
-                         "note": "per-kernel roofline reported by the N=1 run"},
+            "roofline": {"bound": "tensor", "kernel": "level_update4_kernel", "achieved":
+                         (level_flops(n // world, m, r) / (phases["level"] * 1e-3) / 1e12) if phases["level"] else None,
+                         "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None,
+                         "note": "rank 0's local level phase; the per-kernel roofline is reported by the N=1 run"},
             "e2e": None, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: re-exec under
+    torch.distributed.run with one process per GPU (127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    if args.dist_backend == "nccl":
+        env.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) on stdout
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py")] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -569,21 +670,31 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--n", type=int, default=None, help="matrix size (default: the workload's)")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default=None,
+                    help="cfg2 (default at N=1) or cfg3 (default for the sharded N>1 run)")
     ap.add_argument("--problem", choices=("laplace", "standin"), default="laplace",
-                    help="laplace: the cfg2 operator assembled on the device; standin: seeded exact HODLR")
+                    help="cfg2 operator: laplace (assembled on the device) or the seeded exact-HODLR stand-in")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-relres", action="store_true", help="sharded run: skip the full-operator residual")
     ap.add_argument("--sharded", action="store_true", help="use the row-sharded path even on one GPU")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (single-GPU testing)")
     args = ap.parse_args()
     if args.impl == "reference":
-        run_reference(args)
-    elif dist_env()[1] > 1 or args.sharded:
+        if dist_env()[0] == 0:
+            run_reference(args)
+        return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if dist_env()[1] > 1 or args.sharded or (args.workload == "cfg3"):
         run_sharded(args)
     else:
+        if args.n is None:
+            args.n = N_DEFAULT
         run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

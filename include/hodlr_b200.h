@@ -40,6 +40,11 @@ typedef enum {
 const char* hodlr_version(void);
 const char* hodlr_last_error(void);
 
+/* Scalars per s x s block of the factorization-internal solve aids (the Dinv /
+ * Kinv buffers of hodlr_factors): 8 s for s in {32, 64, 128} (8x8
+ * diagonal-block inverses), s^2 for s = 16 (packed inverses), 0 otherwise. */
+size_t hodlr_inv_elems(int s);
+
 /* Instrumentation (no reference counterpart; the reference only returns flop
  * counts, backend.py:18-20).  hodlr_launch_count: kernels launched by this
  * library since load.  hodlr_profile_enable(1) brackets every factorize /
@@ -116,14 +121,16 @@ typedef struct {
 /* Device buffers of a factorization (all owned by the caller). */
 typedef struct {
   void* D;        /* in: leaf blocks; out: leaf LU                       */
-  void* Dinv;     /* out: leaf solve aids, 2^L m^2 slots: for m in {32,64,128}
-                     the 8x8 diagonal-block inverses P_q = strict_lower(L_qq^-1)
-                     + upper(U_qq^-1), row-major at slot + 64 q (blocked DMMA
+  void* Dinv;     /* out: leaf solve aids, 2^L * hodlr_inv_elems(m) scalars
+                     (fp64; unused by fp32): for m in {32,64,128} the 8x8
+                     diagonal-block inverses P_q = strict_lower(L_qq^-1) +
+                     upper(U_qq^-1), row-major at block + 64 q (blocked DMMA
                      substitutions); m = 16: packed L^-1 / U^-1             */
   void* Y;        /* in: U slab; out: Y slab                             */
   void* V;        /* in: V slab                                          */
   void* K;        /* out: K LU per level ((2^L - 1) (2r)^2)              */
-  void* Kinv;     /* out: the same for the K blocks (2r), K layout        */
+  void* Kinv;     /* out: the same for the K blocks: (2^L - 1) *
+                     hodlr_inv_elems(2r), level l at (2^l - 1) * that      */
   int32_t* dswaps; /* out: 2^L m                                          */
   int32_t* dperm;  /* out: 2^L m                                          */
   int32_t* dinfo;  /* out: 2^L                                            */

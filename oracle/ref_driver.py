@@ -137,20 +137,16 @@ def ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L, ex=None):
 
 
 
-def ref_assemble_laplace(n_total: int, n: int, m: int, r: int):
-    """The leading n x n diagonal block of the cfg2 operator
-    (``laplace_dl_oracle(contour_default(n_total))``, problems.py:133-217)
-    assembled by the reference's own ``compress`` (compress.py:173-200,
-    CompressionConfig(tol=0, max_rank=r, method="aca_rook_pivot")) on both
-    orientations of every sibling block of the n-row subtree.
-    Returns flat D, U, V in the SPEC layout."""
+def ref_assemble(entry, n: int, m: int, r: int):
+    """HODLR of the n x n matrix entry(i, j) assembled by the reference's own
+    ``compress`` (compress.py:173-200, CompressionConfig(tol=0, max_rank=r,
+    method="aca_rook_pivot")) on both orientations of every sibling block
+    (SPEC.md:163-171); leaves materialised exactly.  Flat D, U, V (SPEC layout)."""
     import math
 
     from hodlr.compress import CompressionConfig, compress  # type: ignore
-    from hodlr.problems import contour_default, laplace_dl_oracle  # type: ignore
     from hodlr.tree import IndexRange  # type: ignore
 
-    entry = laplace_dl_oracle(contour_default(n_total))
     L = int(round(math.log2(n // m)))
     D = np.empty((1 << L) * m * m)
     for a in range(1 << L):
@@ -169,3 +165,12 @@ def ref_assemble_laplace(n_total: int, n: int, m: int, r: int):
                     U[c + ra : c + ra + nl] = f.u[:, l]
                     V[c + cb : c + cb + nl] = np.conj(f.v[:, l])
     return D, U, V
+
+
+def ref_assemble_laplace(n_total: int, n: int, m: int, r: int):
+    """The leading n x n diagonal block of the cfg2 operator
+    (``laplace_dl_oracle(contour_default(n_total))``, problems.py:133-217)
+    assembled by the reference's own ``compress`` (see :func:`ref_assemble`)."""
+    from hodlr.problems import contour_default, laplace_dl_oracle  # type: ignore
+
+    return ref_assemble(laplace_dl_oracle(contour_default(n_total)), n, m, r)

@@ -49,6 +49,7 @@ _i, _i64, _p, _d, _sz = C.c_int, C.c_int64, C.c_void_p, C.c_double, C.c_size_t
 SIGNATURES = {
     "hodlr_version": (C.c_char_p, []),
     "hodlr_last_error": (C.c_char_p, []),
+    "hodlr_inv_elems": (_sz, [_i]),
     "hodlr_getrf_batched": (_i, [_i, _i, _i, _p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _p]),
     "hodlr_getrs_batched": (_i, [_i, _i, _i, _i, _p, _i64, _i64, _p, _p, _i64, _i64, _p]),
     "hodlr_gemm_batched": (

@@ -27,7 +27,8 @@ namespace hodlr {
 struct ApplyArgs {
   const double* tinv;  // packed full inverses (S in {16, 128}) or diagonal-block inverses (S in {32, 64})
   const double* lu;    // the LU factors (same layout as tinv); used with the diagonal-block format
-  int64_t ldi, strideT;
+  int64_t ldi, strideT;  // LU: block b at lu + b * strideT (ld ldi)
+  int64_t strideI;       // inverses: block b at tinv + b * strideI
   const int32_t* perm;
   const double* B;
   int64_t ldb, sB_hi, sB_lo;
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(AP_THREADS) tri_apply_kernel(ApplyArgs g) {
   const bool mma_warp = warp < Cfg::WM * WN;
   const int ar = lane >> 2, ac = lane & 3;
 
-  const double* ti = g.tinv + (int64_t)b * g.strideT;
+  const double* ti = g.tinv + (int64_t)b * g.strideI;
   for (int idx = t; idx < S * (S / 2); idx += AP_THREADS) {
     const int k = idx / (S / 2), m = (idx % (S / 2)) * 2;
     cp_async_16(At + k * P + m, ti + m + (int64_t)k * g.ldi, 16);
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply2_kerne
   // ---- one-time staging, [row][k] (k pairs per thread): the LU factors off the
   // diagonal 8x8 tiles, the diagonal-block inverses P_q on them ----
   const IO* lb = reinterpret_cast<const IO*>(g.lu) + (int64_t)b * g.strideT;
-  const double* di = g.tinv + (int64_t)b * g.strideT;
+  const double* di = g.tinv + (int64_t)b * g.strideI;
   for (int idx = t; idx < S * (S / 2); idx += AP_THREADS) {
     const int m = idx % S, k = (idx / S) * 2;
     double2 x;
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply_narrow
   const int b = blockIdx.x * (AP_THREADS / 32) + warp;
   if (b >= g.batch) return;
   const int ar = lane >> 2, ac = lane & 3;
-  const double* ti = g.tinv + (int64_t)b * g.strideT;
+  const double* ti = g.tinv + (int64_t)b * g.strideI;
   const int32_t* pmb = g.perm + (int64_t)b * S;
   const double* Bb = g.B + aoff(b, g.bdiv, g.sB_hi, g.sB_lo);
   double* Xb = g.X + aoff(b, g.bdiv, g.sX_hi, g.sX_lo);
@@ -623,7 +624,7 @@ hodlr_status tri_apply_f32(int s, int ncols, int batch, const float* lu, int64_t
   if (s != 64 || (V && twr != 8) || (ldy & 1) || (sY & 1) || (reinterpret_cast<uintptr_t>(Y) & 7) ||
       (TW && ((tw_stride & 1) || (reinterpret_cast<uintptr_t>(TW) & 7))))
     return HODLR_ERR_ARG;
-  ApplyArgs g{nullptr, reinterpret_cast<const double*>(lu), 64, strideT, perm, reinterpret_cast<const double*>(Y),
+  ApplyArgs g{nullptr, reinterpret_cast<const double*>(lu), 64, strideT, 0, perm, reinterpret_cast<const double*>(Y),
               ldy, sY, 0, reinterpret_cast<double*>(Y), ldy, sY, 0, ncols, batch, 1, 1,
               reinterpret_cast<const double*>(V), ldv, vstride, reinterpret_cast<double*>(TW), tw_stride};
   constexpr int S = 64, PT = Apply2Cfg<S>::PT;
@@ -651,7 +652,7 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const 
                            double* TW = nullptr, int64_t tw_stride = 0) {
   if (batch == 0 || ncols == 0 || s == 0) return HODLR_OK;
   if ((ldi & 1) || (reinterpret_cast<uintptr_t>(tinv) & 15) || (strideT & 1)) return HODLR_ERR_ARG;
-  ApplyArgs g{tinv, lu, ldi, strideT, perm, B, ldb, sB_hi, sB_lo, X, ldx, sX_hi, sX_lo, ncols, batch, bdiv, 1,
+  ApplyArgs g{tinv, lu, ldi, strideT, inv_block_elems(s), perm, B, ldb, sB_hi, sB_lo, X, ldx, sX_hi, sX_lo, ncols, batch, bdiv, 1,
               V, ldv, vstride, TW, tw_stride};
   const bool narrow = ncols <= 8;
   if (s == 128) {  // diagonal-block-inverse format, no fused reduction

@@ -76,6 +76,13 @@ struct Eps<float> {
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Scalars of the factorization-internal solve aids per s x s block (Dinv /
+// Kinv): the 8x8 diagonal-block inverses (8 s) for s in {32, 64, 128}, the
+// packed full inverses (s^2) for s = 16, nothing otherwise (row substitution).
+__host__ __device__ inline int64_t inv_block_elems(int s) {
+  return (s == 32 || s == 64 || s == 128) ? (int64_t)8 * s : s == 16 ? (int64_t)s * s : 0;
+}
+
 }  // namespace hodlr
 
 // records the CUDA error string for hodlr_last_error(); defined in hodlr.cu

@@ -7,6 +7,7 @@
 // of every leaf and K block, so every triangular solve of the factor and solve
 // phases becomes a pair of batched DMMA GEMMs (apply.cu).
 #include <cstdio>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -76,6 +77,7 @@ hodlr_status hodlr_set_cuda_error(cudaError_t e) {
 
 extern "C" const char* hodlr_version(void) { return "hodlr_b200 0.1 (sm_100a, fp64 DMMA)"; }
 extern "C" const char* hodlr_last_error(void) { return g_last_error.c_str(); }
+extern "C" size_t hodlr_inv_elems(int s) { return s < 0 ? 0 : (size_t)inv_block_elems(s); }
 
 // ---- instrumentation ----
 #include <atomic>
@@ -215,10 +217,10 @@ static hodlr_status lu_factor(int s, int batch, int mode, const double* src, int
                               int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, double* tinv,
                               cudaStream_t st) {
   if (s == 32 || s == 64 || s == 128)  // diagonal-block inverses for the blocked DMMA substitutions
-    return launch_getrf_dbi_f64(s, batch, mode, src, lds, strides, out, s, strideo, swaps, perm, info, tinv, strideo,
-                                st);
+    return launch_getrf_dbi_f64(s, batch, mode, src, lds, strides, out, s, strideo, swaps, perm, info, tinv,
+                                inv_block_elems(s), st);
   return launch_getrf<double>(s, batch, mode, src, lds, strides, out, s, strideo, swaps, perm, info,
-                              tri_size_ok(s) ? tinv : nullptr, s, strideo, st);
+                              tri_size_ok(s) ? tinv : nullptr, s, inv_block_elems(s), st);
 }
 
 // X_b = A_b^-1 B_b from the stored factors: two triangular DMMA GEMMs with the
@@ -320,7 +322,8 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
   double* Kinv = (double*)f->Kinv;
 
   // (1) leaf getrf (bit-exact) + packed triangular inverses     Alg.3 l.2
-  if (vready && L > 0) cudaStreamWaitEvent(st, vready[L], 0);  // D, U and V^(L) resident
+  if (vready && L > 0 && cudaStreamWaitEvent(st, vready[L], 0) != cudaSuccess)  // D, U and V^(L) resident
+    return hodlr_set_cuda_error(cudaGetLastError());
   {
     Phase ph(HODLR_PHASE_LEAF_GETRF, st);
     TRY(lu_factor(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo, Dinv, st));
@@ -347,7 +350,7 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
     const int64_t p0 = row0 / (2 * nc);  // global index of the first local parent
     const int ncol = r * (lv + 1), wc = r * lv;
     const int64_t kblk = ((int64_t)1 << lv) - 1 + p0;  // first local K block (global layout)
-    const int64_t koff = kblk * 4 * r * r;
+    const int64_t koff = kblk * 4 * r * r, kioff = kblk * inv_block_elems(2 * r);
     if (!tw_ready) {
       Phase ph(HODLR_PHASE_GEMM, st);
       // [W|T]_c = V_c^T Y(I_c, 0:r(l+1)), paired per parent: 2r x ncol, ld 2r
@@ -359,17 +362,18 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
     {
       Phase ph(HODLR_PHASE_K_GETRF, st);
       TRY(lu_factor(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff,
-                    (int64_t)4 * r * r, f->kswaps + kblk * 2 * r, kperm, f->kinfo + kblk, Kinv + koff, st));
+                    (int64_t)4 * r * r, f->kswaps + kblk * 2 * r, kperm, f->kinfo + kblk, Kinv + kioff, st));
     }
     if (lv == 0) break;
     // W_p <- K_p^-1 [W_2p; W_2p+1]
     {
       Phase ph(HODLR_PHASE_K_APPLY, st);
-      TRY(lu_apply(2 * r, wc, npar, K + koff, Kinv + koff, kperm, TW, 2 * r, (int64_t)2 * r * ncol, W, 2 * r,
+      TRY(lu_apply(2 * r, wc, npar, K + koff, Kinv + kioff, kperm, TW, 2 * r, (int64_t)2 * r * ncol, W, 2 * r,
                    (int64_t)2 * r * wc, st));
     }
     // Y(I_c, 0:rl) -= Y_c^{l+1} W_c, fused with the next level's [W|T] (V^{(l)T} Y(I_q, 0:rl))
-    if (vready) cudaStreamWaitEvent(st, vready[lv], 0);  // V^(lv) resident (streamed upload)
+    if (vready && cudaStreamWaitEvent(st, vready[lv], 0) != cudaSuccess)  // V^(lv) resident (streamed upload)
+      return hodlr_set_cuda_error(cudaGetLastError());
     hodlr_status s;
     {
       Phase ph(HODLR_PHASE_LEVEL, st);
@@ -438,11 +442,7 @@ static hodlr_status level_fact_T(int r, int64_t n, int64_t n_c, int64_t node_row
                                  const float* A1, const float* V, int64_t lda, const float* W, int64_t wstride,
                                  int ncols, float* TW, int64_t tw_stride, float* part, size_t part_bytes,
                                  cudaStream_t st) {
-  static const bool simt = [] {
-    const char* e = getenv("HODLR_F32_LEVEL");
-    return e && e[0] == 's';
-  }();
-  if (!simt) {
+  {
     const hodlr_status s = level_f32_dmma(r, n, n_c, node_rows, C, ldc, A1, V, lda, W, wstride, ncols, TW, tw_stride,
                                           part, part_bytes, st);
     if (s != HODLR_ERR_ARG) return s;
@@ -623,7 +623,7 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
 // level, so all but the first 4.6 GB (cfg2) of the transfer hide behind the
 // factorization.  f's D / Y / V are the device destinations (Y receives U).
 static std::mutex g_up_mu;
-static std::vector<cudaEvent_t> g_up_ev;
+static std::map<int, std::vector<cudaEvent_t>> g_up_ev;  // per device: events live in that device's context
 extern "C" hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hodlr_factors* f, const void* D_host,
                                                   const void* U_host, const void* V_host, void* work,
                                                   size_t work_bytes, void* stream, void* copy_stream) {
@@ -635,15 +635,19 @@ extern "C" hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hod
   const int64_t n = d->n;
   const int m = d->m, r = d->r, L = d->L;
   const size_t es = sizeof(double);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return hodlr_set_cuda_error(cudaGetLastError());
   std::lock_guard<std::mutex> lk(g_up_mu);
-  while ((int)g_up_ev.size() < L + 2) {
+  std::vector<cudaEvent_t>& ev = g_up_ev[dev];
+  while ((int)ev.size() < L + 2) {
     cudaEvent_t e;
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return hodlr_set_cuda_error(cudaGetLastError());
-    g_up_ev.push_back(e);
+    ev.push_back(e);
   }
+  auto ok_ = [](cudaError_t e) { return e == cudaSuccess; };
   // the copies must not start before the caller's prior work on `stream`
-  cudaEventRecord(g_up_ev[L + 1], st);
-  cudaStreamWaitEvent(cs, g_up_ev[L + 1], 0);
+  if (!ok_(cudaEventRecord(ev[L + 1], st)) || !ok_(cudaStreamWaitEvent(cs, ev[L + 1], 0)))
+    return hodlr_set_cuda_error(cudaGetLastError());
   auto cp = [&](void* dst, const void* src, size_t bytes) {
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs) == cudaSuccess;
   };
@@ -651,15 +655,15 @@ extern "C" hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hod
   bool ok = cp(f->D, D_host, (size_t)n * m * es) && cp(f->Y, U_host, (size_t)L * panel);
   if (L > 0)
     ok = ok && cp((char*)f->V + (size_t)(L - 1) * panel, (const char*)V_host + (size_t)(L - 1) * panel, panel);
+  ok = ok && ok_(cudaEventRecord(ev[L > 0 ? L : 0], cs));
   if (!ok) return hodlr_set_cuda_error(cudaGetLastError());
-  cudaEventRecord(g_up_ev[L > 0 ? L : 0], cs);
   for (int lv = L - 1; lv >= 1; --lv) {
-    if (!cp((char*)f->V + (size_t)(lv - 1) * panel, (const char*)V_host + (size_t)(lv - 1) * panel, panel))
+    if (!cp((char*)f->V + (size_t)(lv - 1) * panel, (const char*)V_host + (size_t)(lv - 1) * panel, panel) ||
+        !ok_(cudaEventRecord(ev[lv], cs)))
       return hodlr_set_cuda_error(cudaGetLastError());
-    cudaEventRecord(g_up_ev[lv], cs);
   }
-  if (L == 0) cudaStreamWaitEvent(st, g_up_ev[0], 0);
-  return factor_local(d, f, n, 0, 0, static_cast<char*>(work), ws, st, g_up_ev.data());
+  if (L == 0 && !ok_(cudaStreamWaitEvent(st, ev[0], 0))) return hodlr_set_cuda_error(cudaGetLastError());
+  return factor_local(d, f, n, 0, 0, static_cast<char*>(work), ws, st, ev.data());
 }
 
 extern "C" hodlr_status hodlr_factorize_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
@@ -705,7 +709,8 @@ extern "C" hodlr_status hodlr_factorize_top(const hodlr_desc* d, const hodlr_fac
   const int npar = 1 << lv, ncol = r * (lv + 1), wc = r * lv;
   const int64_t kblk = (int64_t)npar - 1;
   double* K = (double*)f->K + kblk * 4 * r * r;
-  double* Kinv = (double*)f->Kinv + kblk * 4 * r * r;
+  const int64_t kis = inv_block_elems(2 * r);
+  double* Kinv = (double*)f->Kinv + kblk * kis;
   int32_t* kperm = f->kperm + kblk * 2 * r;
   {
     Phase ph(HODLR_PHASE_K_GETRF, st);
@@ -717,7 +722,7 @@ extern "C" hodlr_status hodlr_factorize_top(const hodlr_desc* d, const hodlr_fac
   const int64_t p = row0 / (2 * nc), half = (row0 / nc) & 1;
   {
     Phase ph(HODLR_PHASE_K_APPLY, st);
-    TRY(lu_apply(2 * r, wc, 1, K + p * 4 * r * r, Kinv + p * 4 * r * r, kperm + p * 2 * r,
+    TRY(lu_apply(2 * r, wc, 1, K + p * 4 * r * r, Kinv + p * kis, kperm + p * 2 * r,
                  tw_all + p * 2 * r * ncol, 2 * r, 0, W, 2 * r, 0, st));
   }
   double* Y = (double*)f->Y;
@@ -778,7 +783,7 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
     const int nch = (int)(n / nc), npar = nch / 2;
     const int64_t p0 = row0 / (2 * nc);
     const int64_t kblk = ((int64_t)1 << lv) - 1 + p0;
-    const int64_t koff = kblk * 4 * r * r;
+    const int64_t koff = kblk * 4 * r * r, kioff = kblk * inv_block_elems(2 * r);
     // w_c = V_c^T x_c  (paired per parent, 2r x nrhs, ld 2r)       Alg.4 l.5
     if (!w_ready) {
       Phase ph(HODLR_PHASE_GEMM, st);
@@ -788,7 +793,7 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
     // w_p <- K_p^-1 w_p                                              Alg.4 l.6
     {
       Phase ph(HODLR_PHASE_SOLVE_K, st);
-      TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + koff, f->kperm + kblk * 2 * r, w, 2 * r,
+      TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + kioff, f->kperm + kblk * 2 * r, w, 2 * r,
                    (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st));
     }
     // x_c -= Y_c w_c  fused with the next level's w = V^{(l)T} x    Alg.4 l.7 (+ l.5 of level l-1)
@@ -877,7 +882,7 @@ extern "C" hodlr_status hodlr_solve_top(const hodlr_desc* d, const hodlr_factors
   const int64_t kblk = ((int64_t)1 << lv) - 1 + p;
   {
     Phase ph(HODLR_PHASE_SOLVE_K, st);
-    TRY(lu_apply(2 * r, nrhs, 1, (const double*)f->K + kblk * 4 * r * r, (const double*)f->Kinv + kblk * 4 * r * r,
+    TRY(lu_apply(2 * r, nrhs, 1, (const double*)f->K + kblk * 4 * r * r, (const double*)f->Kinv + kblk * inv_block_elems(2 * r),
                  f->kperm + kblk * 2 * r, w_all + p * 2 * r * nrhs, 2 * r, 0, w2, 2 * r, 0, st));
   }
   const double* Y = (const double*)f->Y;

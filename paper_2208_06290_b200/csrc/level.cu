@@ -268,227 +268,6 @@ __global__ void level_reduce_kernel(const double* part, double* TW, int R, int n
 
 
 // ---------------------------------------------------------------------------
-// Register-resident variant for the factorization (64 x 64 tiles).
-// Each of the 8 warps owns 8 columns x 64 rows of the C tile in DMMA
-// accumulator registers: C is loaded straight from HBM into the accumulators
-// (prefetched one tile ahead), the update is accumulated into it
-// (C + A1 (-W'), FP64 tensor core), stored back, and the next level's
-// [W|T]^T = C^T V is formed from the same registers.
-//
-// Fragment layout (all operand reads are 16-byte LDS.128 / LDG.128):
-//  * rows are paired: accumulator row-tile i, lane row a holds physical row
-//    rho(i, a) = 16 (i/2) + 2a + (i%2), so tiles 2j and 2j+1 of a lane are two
-//    adjacent rows -> one 16B global load/store per (j, column) and one
-//    LDS.128 of the [k][row] A1 panel feeds two row-tiles;
-//  * k is paired: k-steps 2t and 2t+1 use k = 8t + 2c + {0, 1} (c = lane%4),
-//    so one LDS.128 of the [col][k] W' tile feeds both;
-//  * the [W|T] reduction's k (= rows) runs over (tile pair j, half s, tile
-//    parity): one LDS.128 of the [rank][row] V panel feeds two k-steps, and
-//    the C^T fragments are transposed out of the accumulators with one
-//    shuffle per k-step (each source lane sends the element the requesting
-//    half of the warp needs).
-// Pitches make every quarter-warp LDS.128 hit 32 distinct banks.
-// Work item = (row segment, group of column tiles); warps whose 8 columns are
-// past ncols skip the math.  Segments shorter than the node write partial
-// [W|T] sums (fixed-order reduction afterwards).
-// ---------------------------------------------------------------------------
-template <int R>
-struct Level3Cfg {
-  static constexpr int BM = 64, BN = 64;
-  static constexpr int PA = BM + 2;  // A1 [k][row]: 2P = 4 (mod 16) doubles
-  static constexpr int PV = BM + 8;  // V [rank][row]: P = 8 (mod 16)
-  static constexpr int PW = R + 8;   // W' [col][k]:   P = 8 (mod 16)
-  static constexpr int A_SZ = R * PA;
-  static constexpr int V_SZ = R * PV;
-  static constexpr int W_SZ = BN * PW;
-  static constexpr int STAGE = A_SZ + V_SZ + W_SZ;
-  static constexpr size_t SMEM = (size_t)2 * STAGE * sizeof(double);
-};
-
-template <int R, int PF>
-__global__ void __launch_bounds__(256, 2) level_update3_kernel(LevelArgs g) {
-  using Cfg = Level3Cfg<R>;
-  constexpr int BM = Cfg::BM, BN = Cfg::BN, PA = Cfg::PA, PV = Cfg::PV, PW = Cfg::PW;
-  constexpr int NT = 256, RT = R / 8;
-  static_assert(R % 8 == 0, "rank must be a multiple of 8");
-  extern __shared__ __align__(16) double sm[];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int ar = lane >> 2, ac = lane & 3;
-  const int seg = blockIdx.x / g.ncg, cg = blockIdx.x % g.ncg;
-  const int64_t seg0 = (int64_t)seg * g.seg_rows;
-  const int nsub = g.seg_rows / BM;
-  const int ntile_all = (g.ncols + BN - 1) / BN;
-  const int ct0 = cg * g.tpc;
-  const int ntile = min(g.tpc, ntile_all - ct0);
-  const int niter = nsub * max(ntile, 0);
-  const uint64_t keep = l2_evict_last();
-
-  auto stage_ptr = [&](int s) { return sm + s * Cfg::STAGE; };
-  auto load_panels = [&](int it, int s) {
-    const int ct = ct0 + it / nsub, st = it % nsub;
-    const int64_t row0 = seg0 + (int64_t)st * BM;
-    const int c = (int)(row0 / g.n_c);
-    const int n0 = ct * BN;
-    double* As = stage_ptr(s);
-    double* Vs = As + Cfg::A_SZ;
-    double* Ws = Vs + Cfg::V_SZ;
-    static_assert((R * (BM / 2)) % NT == 0 && (BN * (R / 2)) % NT == 0, "panel split");
-    const double* a1 = g.A1 + row0;
-    const double* v1 = g.V + row0;
-#pragma unroll
-    for (int q = 0; q < R * (BM / 2) / NT; ++q) {
-      const int idx = t + q * NT;
-      const int k = idx / (BM / 2), m = (idx % (BM / 2)) * 2;
-      cp_async_16_pol(As + k * PA + m, a1 + m + (int64_t)k * g.lda, 16, keep);
-      cp_async_16_pol(Vs + k * PV + m, v1 + m + (int64_t)k * g.lda, 16, keep);
-    }
-    const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R + (int64_t)n0 * (2 * R);
-#pragma unroll
-    for (int q = 0; q < BN * (R / 2) / NT; ++q) {
-      const int idx = t + q * NT;
-      const int n = idx / (R / 2), k = (idx % (R / 2)) * 2;
-      const bool ok = n0 + n < g.ncols;
-      cp_async_16_pol(Ws + n * PW + k, ok ? Wp + k + n * (2 * R) : g.W, ok ? 16 : 0, keep);
-    }
-  };
-  // L2 prefetch of a C tile: one 512-byte column run per thread (64 threads)
-  auto prefetch_c = [&](int it) {
-    const int ct = ct0 + it / nsub, st = it % nsub;
-    const int col = ct * BN + t;
-    if (t < BN && col < g.ncols) {
-      const double* p = g.C + seg0 + (int64_t)st * BM + (int64_t)col * g.ldc;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;\n" ::"l"(p));
-    }
-  };
-  // lane's C elements of iteration `it`: (acc[2j][h], acc[2j+1][h]) = rows
-  // 16j + 2ar + {0,1} of column col + h
-  auto load_c = [&](int it, double (&v)[8][2]) {
-    const int ct = ct0 + it / nsub, st = it % nsub;
-    const int64_t row0 = seg0 + (int64_t)st * BM;
-    const int col = ct * BN + warp * 8 + 2 * ac;
-    if (ct * BN + warp * 8 >= g.ncols) return;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const double2 x = __ldcs(reinterpret_cast<const double2*>(g.C + row0 + 16 * j + 2 * ar + (int64_t)(col + h) * g.ldc));
-        v[2 * j][h] = x.x;
-        v[2 * j + 1][h] = x.y;
-      }
-  };
-
-  double cn[PF ? 1 : 8][2], tw[RT][2];
-  if (niter > 0) {
-    load_panels(0, 0);
-    if constexpr (PF) prefetch_c(0);
-    else load_c(0, reinterpret_cast<double(&)[8][2]>(cn));
-  }
-  cp_async_commit();
-  for (int it = 0; it < niter; ++it) {
-    const int s = it & 1;
-    const int ct = ct0 + it / nsub, st = it % nsub;
-    const bool active = ct * BN + warp * 8 < g.ncols;  // warp-uniform
-    double acc[8][2];
-    if constexpr (PF) {
-      load_c(it, acc);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i][0] = cn[i][0], acc[i][1] = cn[i][1];
-    }
-    if (it + 1 < niter) {
-      load_panels(it + 1, s ^ 1);
-      if constexpr (PF) prefetch_c(it + 1);
-      else load_c(it + 1, reinterpret_cast<double(&)[8][2]>(cn));
-    }
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const double* As = stage_ptr(s);
-    const double* Vs = As + Cfg::A_SZ;
-    const double* Ws = Vs + Cfg::V_SZ;
-    if (st == 0) {
-#pragma unroll
-      for (int j = 0; j < RT; ++j) tw[j][0] = tw[j][1] = 0.0;
-    }
-    if (active) {
-      // ---- C <- C + A1 (-W') on this warp's 8 columns ----
-#pragma unroll
-      for (int kt = 0; kt < R / 8; ++kt) {
-        const double2 b2 = *reinterpret_cast<const double2*>(Ws + (warp * 8 + ar) * PW + 8 * kt + 2 * ac);
-#pragma unroll
-        for (int kh = 0; kh < 2; ++kh) {
-          const double bf = -(kh ? b2.y : b2.x);
-          const double* ak = As + (8 * kt + 2 * ac + kh) * PA + 2 * ar;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const double2 a2 = *reinterpret_cast<const double2*>(ak + 16 * j);
-            dmma_8x8x4(acc[2 * j][0], acc[2 * j][1], a2.x, bf);
-            dmma_8x8x4(acc[2 * j + 1][0], acc[2 * j + 1][1], a2.y, bf);
-          }
-        }
-      }
-      // ---- store the updated 64 x 8 slice (16B per lane) ----
-      {
-        const int64_t row0 = seg0 + (int64_t)st * BM;
-        const int col = ct * BN + warp * 8 + 2 * ac;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            __stcs(reinterpret_cast<double2*>(g.C + row0 + 16 * j + 2 * ar + (int64_t)(col + h) * g.ldc),
-                   make_double2(acc[2 * j][h], acc[2 * j + 1][h]));
-      }
-      // ---- [W|T]^T += C_new^T V ----
-      // k-step (tile i, half hs): row rho(i, 4 hs + ac); A = C[row][col 8 warp + ar]
-      // lives in lane (4 hs + ac, ar / 2) as acc[i][ar % 2].
-      const int hsel = ar & 1;
-      const int src_lo = ac * 4 + (ar >> 1), src_hi = (4 + ac) * 4 + (ar >> 1);
-      const bool send_hi = ar >= 4;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        double av[2][2];  // [tile parity][half]
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-          const double x0 = acc[2 * j + p][0], x1 = acc[2 * j + p][1];
-          const double sa = send_hi ? x1 : x0, sb = send_hi ? x0 : x1;
-          const double va = __shfl_sync(0xffffffffu, sa, hsel ? src_hi : src_lo);
-          const double vb = __shfl_sync(0xffffffffu, sb, hsel ? src_lo : src_hi);
-          av[p][0] = hsel ? vb : va;
-          av[p][1] = hsel ? va : vb;
-        }
-#pragma unroll
-        for (int hs = 0; hs < 2; ++hs) {
-#pragma unroll
-          for (int jr = 0; jr < RT; ++jr) {
-            const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * PV + 16 * j + 8 * hs + 2 * ac);
-            dmma_8x8x4(tw[jr][0], tw[jr][1], av[0][hs], v2.x);
-            dmma_8x8x4(tw[jr][0], tw[jr][1], av[1][hs], v2.y);
-          }
-        }
-      }
-      if (st == nsub - 1) {
-        // tw[jr][h] = TW^T[col = 8 warp + ar][rank = 8 jr + 2 ac + h]
-        const int64_t q = seg0 / g.node_rows;
-        double* out;
-        int64_t ld;
-        if (g.partial) {
-          out = g.TW + (int64_t)seg * R * g.ncols;
-          ld = R;
-        } else {
-          out = g.TW + (q >> 1) * g.tw_stride + (q & 1) * R;
-          ld = 2 * R;
-        }
-        const int col = ct * BN + warp * 8 + ar;
-#pragma unroll
-        for (int jr = 0; jr < RT; ++jr)
-          *reinterpret_cast<double2*>(out + 8 * jr + 2 * ac + (int64_t)col * ld) = make_double2(tw[jr][0], tw[jr][1]);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Column-group variant for the factorization (no per-tile CTA barrier).
 // The CTA stages the A1 / V panels of a 64-row chunk (2-stage cp.async ring,
 // one barrier per chunk); every warp then streams its own column groups of 8
@@ -882,18 +661,12 @@ __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
   }
 }
 
-static int solve_pairs() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_SOLVE_PAIRS");
-    v = e ? atoi(e) : 1;
-  }
-  return v;
-}
+// 9-16 RHS at r <= 32: two 8-column groups share every panel load (12 RHS 4.17 -> 3.41 ms)
+constexpr bool kSolvePairs = true;
 
 template <int R>
 static hodlr_status run_solve_level(const LevelArgs& g, int64_t nblk, cudaStream_t st) {
-  if (R <= 32 && g.ncols > 8 && solve_pairs())
+  if (R <= 32 && g.ncols > 8 && kSolvePairs)
     solve_level_kernel<R, R <= 32 ? 2 : 1><<<(unsigned)nblk, 256, 0, st>>>(g);
   else
     solve_level_kernel<R, 1><<<(unsigned)nblk, 256, 0, st>>>(g);
@@ -914,15 +687,6 @@ static hodlr_status run_level4_solve(const LevelArgs& g, int64_t nseg, cudaStrea
   else launch(level_update4_kernel<R, 4, false, true>);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
-}
-
-static int solve_wide() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_SOLVE_WIDE");
-    v = e ? atoi(e) : 1;
-  }
-  return v;
 }
 
 // partial-sum bytes of the solve level steps (one R x nrhs partial per CTA)
@@ -952,7 +716,7 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   LevelArgs g{X, ldx, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)cta_rows,
               node_rows, nrhs, 1, 1};
   hodlr_status s;
-  if (nrhs >= (r >= 64 ? 25 : 17) && solve_wide()) {  // crossovers measured (cfg5 sweeps; 9-16 RHS: paired streaming)
+  if (nrhs >= (r >= 64 ? 25 : 17)) {  // crossovers measured (cfg5 sweeps; 9-16 RHS: paired streaming)
     // many right-hand sides: shared-memory panels reused by every column group
     // (same segments and reduction order as solve_level_kernel)
     const int G = (nrhs + 7) / 8;
@@ -979,58 +743,8 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   return HODLR_OK;
 }
 
-static int level4_min_groups() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_LEVEL4_MIN_GROUPS");
-    v = e ? atoi(e) : 4;
-  }
-  return v;
-}
-
-static int level_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_LEVEL_V");
-    v = e ? atoi(e) : 4;
-  }
-  return v;
-}
-
-static int level4_maxg(int r) {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_LEVEL4_MAXG");
-    v = e ? atoi(e) : 0;
-  }
-  return v > 0 ? v : (r <= 16 ? 56 : r <= 32 ? 32 : 16);
-}
-
-static int level_pf() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_LEVEL_PF");
-    v = e ? atoi(e) : 1;
-  }
-  return v;
-}
-
-template <int R>
-static hodlr_status run_level3(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
-  using Cfg = Level3Cfg<R>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(level_update3_kernel<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaFuncSetAttribute(level_update3_kernel<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    attr = true;
-  }
-  if (level_pf())
-    level_update3_kernel<R, 1><<<(unsigned)(nseg * g.ncg), 256, Cfg::SMEM, st>>>(g);
-  else
-    level_update3_kernel<R, 0><<<(unsigned)(nseg * g.ncg), 256, Cfg::SMEM, st>>>(g);
-  HODLR_CHECK_LAUNCH();
-  return HODLR_OK;
-}
+// column groups of 8 per level-kernel CTA: the [W|T] partials live in registers
+static int level4_maxg(int r) { return r <= 16 ? 56 : r <= 32 ? 32 : 16; }
 
 template <int R, int BN>
 static hodlr_status run_level(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
@@ -1055,33 +769,6 @@ int64_t level_segment_rows(int64_t n, int64_t node, int sms) {
   while (seg > 64 && n / seg < want && seg % 128 == 0) seg >>= 1;
   while (seg > 4096 && seg % 128 == 0) seg >>= 1;
   return seg;
-}
-
-// Factorization schedule: work item = (row segment, group of column tiles).
-// Minimises (waves of 2 CTAs/SM) x (64x64 tiles per CTA + pipeline fill),
-// splitting a node's rows (partial [W|T] sums) only when that wins by > 5%,
-// and never into more than kMaxSegs segments (bounds the partial workspace).
-static FactSched level_fact_schedule(int64_t n, int64_t node, int ntile, int sms) {
-  const int64_t slots = 2 * (int64_t)sms;
-  FactSched best{node, 1, ntile};
-  double best_cost = 1e300;
-  for (int64_t seg = node; seg >= 64; seg >>= 1) {
-    const int64_t nseg = n / seg;
-    if (seg < node && nseg > kMaxSegs) break;
-    for (int ncg = 1; ncg <= ntile; ++ncg) {
-      const int tpc = (ntile + ncg - 1) / ncg;
-      if ((ncg - 1) * tpc >= ntile) continue;  // an empty group
-      const double waves = (double)ceil_div(nseg * ncg, slots);
-      double cost = waves * ((double)(seg / 64) * tpc + 1.5);
-      if (seg < node) cost *= 1.05;
-      if (cost < best_cost) {
-        best_cost = cost;
-        best = {seg, ncg, tpc};
-      }
-    }
-    if (seg % 128) break;
-  }
-  return best;
 }
 
 // partial-sum bytes the level steps need (max over levels and both schedules)
@@ -1117,11 +804,10 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   const bool fact = V != nullptr && reg_resident && ncols > 8;
   const int ntile = (int)ceil_div(ncols, 64);
   FactSched fs{level_segment_rows(n, node, sm_count()), 1, ntile};
-  // column-group kernel: 16 or more groups of 8, 32-byte aligned C columns
-  const bool v4 = fact && level_variant() == 4 && ncols % 8 == 0 && ncols / 8 >= level4_min_groups() && !(ldc & 3) &&
-                  !(reinterpret_cast<uintptr_t>(C) & 31);
+  // factorization: the column-group kernel (32-byte aligned C columns, groups of 8)
+  const bool v4 = fact && ncols % 8 == 0 && !(ldc & 3) && !(reinterpret_cast<uintptr_t>(C) & 31);
+  if (fact && !v4) return HODLR_ERR_ARG;  // generic GEMM path
   if (v4) fs = level4_schedule(n, node, ncols / 8, sm_count(), level4_maxg(r));
-  else if (fact) fs = level_fact_schedule(n, node, ntile, sm_count());
   const int64_t seg = fs.seg;
   const int64_t nseg = n / seg;
   if (nseg * fs.ncg > 2147483647LL) return HODLR_ERR_ARG;
@@ -1132,8 +818,8 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   const bool small = ncols <= 8;
   hodlr_status s;
   switch (r) {
-    case 16: s = small ? run_level<16, 8>(g, nseg, st) : v4 ? run_level4<16>(g, nseg, st) : (fact ? run_level3<16>(g, nseg, st) : run_level<16, 64>(g, nseg, st)); break;
-    case 32: s = small ? run_level<32, 8>(g, nseg, st) : v4 ? run_level4<32>(g, nseg, st) : (fact ? run_level3<32>(g, nseg, st) : run_level<32, 64>(g, nseg, st)); break;
+    case 16: s = small ? run_level<16, 8>(g, nseg, st) : v4 ? run_level4<16>(g, nseg, st) : run_level<16, 64>(g, nseg, st); break;
+    case 32: s = small ? run_level<32, 8>(g, nseg, st) : v4 ? run_level4<32>(g, nseg, st) : run_level<32, 64>(g, nseg, st); break;
     case 64: if (!v4) return HODLR_ERR_ARG; s = run_level4<64>(g, nseg, st); break;
     default: return HODLR_ERR_ARG;  // r = 64: generic path (fused tiles exceed shared memory)
   }

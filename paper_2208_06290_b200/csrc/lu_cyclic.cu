@@ -1,4 +1,4 @@
-// Batched bit-exact LU on a 2-D cyclic thread grid + DMMA triangular inversion.
+// Batched bit-exact LU kernels (register-row and shared-row) + triangular inverses.
 //
 // Replays backend.py:444-478 (_lu_factor_stack) exactly: right-looking,
 // first-max pivot over |a[k:, k]| (NaN wins, smallest logical index on ties),
@@ -6,18 +6,18 @@
 // division by the pivot (0 -> 1), trailing update a - (l*u) with the product
 // rounded before the subtraction (__dmul_rn / __dsub_rn, no FMA).
 //
-// One CTA (256 threads) per block.  Thread (tr, tc) = (t % 16, t / 16) owns rows
-// {tr + 16a} x columns {tc + 16b} (a, b < S/16) in registers, so every step's
-// rank-1 update is spread over all threads and each thread loads only its S/16
-// multipliers and S/16 pivot-row entries from shared memory.  Row exchanges are
-// logical (each row carries its logical position), which is the reference's
-// physical swap with the same per-element operation sequence.
+// getrf_reg_kernel (fp64/fp32, s in {32, 64}): thread t owns row t in registers,
+// fully unrolled steps -- full waves of blocks (leaf LUs, deep K levels).
+// getrf_sr_kernel (any s <= 128): thread t owns row t in shared memory with a
+// runtime step loop -- small batches (top K levels) and s = 16 / 128.
+// Row exchanges are logical (each row carries its logical position), which is
+// the reference's physical swap with the same per-element operation sequence.
 //
-// The packed triangular inverses Tinv = strict_lower(L^-1) + upper(U^-1) that
-// the DMMA solves consume (apply.cu) are then formed in shared memory by
-// recursive doubling: 8x8 diagonal blocks are inverted per thread-row, and each
-// doubling step X = -A^-1 U_AB B^-1 (resp. X = -B^-1 C A^-1) is two small DMMA
-// GEMMs.
+// Solve aids: the 8x8 diagonal-block inverses (diag_block_inverses, the
+// blocked DMMA substitutions of apply.cu) or, for the batched-kernel API, the
+// packed triangular inverses Tinv = strict_lower(L^-1) + upper(U^-1) formed in
+// shared memory by recursive doubling (packed_trtri: 8x8 diagonal blocks per
+// thread-row, each doubling step two small DMMA GEMMs).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -158,190 +158,6 @@ __device__ void packed_trtri(T* Tm, T* Tt, int P) {
     }
   }
 }
-
-template <typename T, int S>
-__global__ void __launch_bounds__(256) getrf_cyclic_kernel(int mode, const T* __restrict__ src, int64_t lds,
-                                                           int64_t strides, T* out, int64_t ldo, int64_t strideo,
-                                                           int32_t* __restrict__ swaps, int32_t* __restrict__ perm,
-                                                           int32_t* __restrict__ info, T* __restrict__ tinv,
-                                                           int64_t ldi, int64_t stridei) {
-  constexpr int LOC = S / 16;  // rows / columns per thread
-  constexpr int P = S + 4;     // pitch of the staged matrices
-  __shared__ T lbuf[S], ubuf[S], cmax[S];
-  __shared__ int piv_pos, piv_row, swk[S], sflag;
-  __shared__ T piv_val;
-  extern __shared__ __align__(16) unsigned char cyc_smem[];
-  T* Tm = reinterpret_cast<T*>(cyc_smem);  // packed LU -> packed inverses, column-major, pitch P
-  T* Tt = Tm + S * P;                      // (S/2) x (S/2) scratch, pitch S/2 + 4
-
-  const int64_t blk = blockIdx.x;
-  const int t = threadIdx.x, tr = t & 15, tc = t >> 4;
-  const T* g = src + blk * strides;
-
-  T e[LOC][LOC];
-#pragma unroll
-  for (int a = 0; a < LOC; ++a)
-#pragma unroll
-    for (int b = 0; b < LOC; ++b) {
-      const int i = tr + 16 * a, j = tc + 16 * b;
-      T v;
-      if (mode == 0) {
-        v = g[i + j * lds];
-      } else {
-        constexpr int R = S / 2;
-        if (i < R && j < R)
-          v = g[i + j * lds];
-        else if (i >= R && j >= R)
-          v = g[i + (j - R) * lds];
-        else
-          v = (i < R) ? (T)(i == j - R) : (T)(i - R == j);
-      }
-      e[a][b] = v;
-    }
-  // original column magnitudes: reduce over the 16 row-owners of each column
-#pragma unroll
-  for (int b = 0; b < LOC; ++b) {
-    T m = (T)0;
-#pragma unroll
-    for (int a = 0; a < LOC; ++a) m = cyc_nanmax(m, (T)fabs((double)e[a][b]));
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) m = cyc_nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (tr == 0) cmax[tc + 16 * b] = m;
-  }
-  if (t == 0) sflag = 0;
-  int pos[LOC];
-  bool act[LOC];
-#pragma unroll
-  for (int a = 0; a < LOC; ++a) {
-    pos[a] = tr + 16 * a;
-    act[a] = true;
-  }
-  __syncthreads();
-  const T thr_scale = mul_rn(Eps<T>::v, (T)S);
-
-  for (int k = 0; k < S; ++k) {
-    const int kc = k & 15, kb = k >> 4;
-    // ---- pivot search by the 16 owners of column k (one half-warp) ----
-    if (tc == kc) {
-      T bv = (T)0, bs = (T)0;
-      int bp = -1, br = 0;
-#pragma unroll
-      for (int a = 0; a < LOC; ++a) {
-        T x = e[a][0];
-#pragma unroll
-        for (int b = 1; b < LOC; ++b) x = csel(kb == b, e[a][b], x);
-        const T v = (T)fabs((double)x);
-        const int pv = act[a] ? pos[a] : -1;
-        if (cyc_beats(v, pv, bv, bp)) {
-          bv = v;
-          bp = pv;
-          br = tr + 16 * a;
-          bs = x;
-        }
-      }
-      const unsigned half = (tc & 1) ? 0xffff0000u : 0x0000ffffu;  // this column group's lanes
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        const T ov = __shfl_xor_sync(half, bv, o);
-        const int op = __shfl_xor_sync(half, bp, o);
-        const int orr = __shfl_xor_sync(half, br, o);
-        const T os = __shfl_xor_sync(half, bs, o);
-        if (cyc_beats(ov, op, bv, bp)) {
-          bv = ov;
-          bp = op;
-          br = orr;
-          bs = os;
-        }
-      }
-      if (tr == 0) {
-        piv_pos = bp;
-        piv_row = br;
-        piv_val = bs;  // signed pivot value
-        swk[k] = bp;
-        if ((T)fabs((double)bs) <= mul_rn(thr_scale, cmax[k])) sflag = 1;
-      }
-    }
-    __syncthreads();
-    const int prow = piv_row, ppos = piv_pos;
-    const T piv = piv_val;
-    // pivot-row owners publish u_kj; rows exchange logical positions
-    if ((prow & 15) == tr) {
-      const int ap = prow >> 4;
-#pragma unroll
-      for (int b = 0; b < LOC; ++b) {
-        T x = e[0][b];
-#pragma unroll
-        for (int a = 1; a < LOC; ++a) x = csel(ap == a, e[a][b], x);
-        const int j = tc + 16 * b;
-        if (j > k) ubuf[j] = x;
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < LOC; ++a) {
-      if (pos[a] == k) pos[a] = ppos;
-      if (tr + 16 * a == prow) {
-        pos[a] = k;
-        act[a] = false;
-      }
-    }
-    // column-k owners form the multipliers l = a_ik / piv
-    const T d = (piv == (T)0) ? (T)1 : piv;
-    if (tc == kc) {
-#pragma unroll
-      for (int a = 0; a < LOC; ++a) {
-        if (act[a]) {
-          T x = e[a][0];
-#pragma unroll
-          for (int b = 1; b < LOC; ++b) x = csel(kb == b, e[a][b], x);
-          // 0 / d is +-0 (sign xor); skip the division's slow path for it
-          const T l = (x == (T)0 && d == d) ? ((signbit(x) != signbit(d)) ? (T)-0.0 : (T)0.0) : div_rn(x, d);
-#pragma unroll
-          for (int b = 0; b < LOC; ++b) e[a][b] = csel(kb == b, l, e[a][b]);
-          lbuf[tr + 16 * a] = l;
-        }
-      }
-    }
-    __syncthreads();
-    // trailing update: a_ij - (l_i * u_j) for active rows, columns j > k
-#pragma unroll
-    for (int a = 0; a < LOC; ++a) {
-      if (act[a]) {
-        const T l = lbuf[tr + 16 * a];
-#pragma unroll
-        for (int b = 0; b < LOC; ++b) {
-          const int j = tc + 16 * b;
-          if (b >= kb && j > k) e[a][b] = sub_rn(e[a][b], mul_rn(l, ubuf[j]));
-        }
-      }
-    }
-  }
-  // ---- outputs: LU rows at their logical positions, pivots, flag ----
-  T* o = out + blk * strideo;
-#pragma unroll
-  for (int a = 0; a < LOC; ++a)
-#pragma unroll
-    for (int b = 0; b < LOC; ++b) {
-      const int j = tc + 16 * b;
-      o[pos[a] + j * ldo] = e[a][b];
-      Tm[pos[a] + j * P] = e[a][b];
-    }
-  if (tc == 0) {
-#pragma unroll
-    for (int a = 0; a < LOC; ++a) perm[blk * S + pos[a]] = tr + 16 * a;
-  }
-  __syncthreads();
-  if (t < S) swaps[blk * S + t] = swk[t];
-  if (t == 0) info[blk] = sflag;
-  if (tinv == nullptr) return;
-
-  packed_trtri<T, S>(Tm, Tt, P);
-  T* ti = tinv + blk * stridei;
-  for (int idx = t; idx < S * S; idx += 256) {
-    const int i = idx % S, j = idx / S;
-    ti[i + (int64_t)j * ldi] = Tm[i + j * P];
-  }
-}
-
 
 // ---------------------------------------------------------------------------
 // Shared-memory row LU: thread t owns row t of the block, stored row-major in
@@ -754,15 +570,10 @@ static hodlr_status run_reg(int batch, int mode, const double* src, int64_t lds,
 // Factorization-internal LU (fp64, s in {32, 64}): factors + diagonal-block
 // inverses (8 s doubles per block at dbi + b * stridedbi) instead of the
 // packed full inverses -- the apply kernels run blocked substitutions.
-// s = 64 batches up to this size use the shared-row kernel (HODLR_LU_SMALL)
-static int small_lu_batch() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("HODLR_LU_SMALL");
-    v = e ? atoi(e) : 1024;  // cfg2: K levels 0..10 (same-box A/B: factor 23.61 -> 23.39 ms)
-  }
-  return v;
-}
+// s = 64 batches up to this size use the shared-row kernel, larger ones the
+// register-row kernel (cfg2: K levels 0..10; same-box A/B: factor 23.61 -> 23.39 ms)
+constexpr int kSmallLuBatch = 1024;
+static int small_lu_batch() { return kSmallLuBatch; }
 
 hodlr_status launch_getrf_dbi_f64(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides,
                                   double* out, int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm,
@@ -807,14 +618,9 @@ hodlr_status launch_getrf_dbi_f64(int s, int batch, int mode, const double* src,
   return HODLR_OK;
 }
 
-static int lu_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HODLR_LU_SR");
-    v = (e && atoi(e)) ? 0 : 1;
-  }
-  return v;
-}
+// s in {32, 64}: the register-row kernel (fp64 with packed inverses; fp32
+// without) -- measured faster than the shared-row kernel for full waves
+static int lu_variant() { return 1; }
 
 template <typename T, int S>
 static hodlr_status run_sr(int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
@@ -832,22 +638,6 @@ static hodlr_status run_sr(int batch, int mode, const T* src, int64_t lds, int64
   }
   getrf_sr_kernel<T, S><<<batch, NT, smem, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv,
                                                   ldi, stridei);
-  HODLR_CHECK_LAUNCH();
-  return HODLR_OK;
-}
-
-template <typename T, int S>
-static hodlr_status run_cyclic(int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out, int64_t ldo,
-                               int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv, int64_t ldi,
-                               int64_t stridei, cudaStream_t st) {
-  constexpr size_t smem = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(T);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(getrf_cyclic_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  getrf_cyclic_kernel<T, S><<<batch, 256, smem, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
-                                                       tinv, ldi, stridei);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }

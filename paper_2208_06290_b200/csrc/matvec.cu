@@ -418,6 +418,8 @@ extern "C" hodlr_status hodlr_matvec(const hodlr_desc* d, const void* D, const v
   if (!mv_shape_ok(d) || nrhs < 0 || ldx < d->n || ldy < d->n) return HODLR_ERR_ARG;
   if (nrhs == 0) return HODLR_OK;
   if (!D || !X || !Y || X == Y || (d->r > 0 && d->L > 0 && (!U || !V))) return HODLR_ERR_ARG;
+  const size_t need = hodlr_matvec_workspace(d, nrhs);
+  if (work_bytes < need || (need && !work)) return HODLR_ERR_ARG;
   const size_t es = d->dtype == HODLR_F64 ? sizeof(double) : sizeof(float);
   // vector loads (V 4 scalars, U / D 2 scalars) when the layout allows them
   const bool vec = d->m % 4 == 0 && (uintptr_t)V % (4 * es) == 0 && (uintptr_t)U % (2 * es) == 0 &&

@@ -66,10 +66,21 @@ def slice_rows(xp, buf, n, ncols, row0, n_loc):
 
 
 def make_shard(h, rank: int, world: int) -> Shard:
-    """Split a global HodlrMatrix (torch) into rank `rank`'s shard."""
+    """Split a global HodlrMatrix (torch, float64) into rank `rank`'s shard.
+
+    The row-sharded entry points (``hodlr_*_local`` / ``hodlr_*_top``) are
+    fp64-only, so anything else is rejected here rather than reinterpreted."""
+    import torch
+
     n, m, r, L = h.n, h.m, h.rank, h.L
-    if world & (world - 1) or world > (1 << L):
+    if world < 1 or world & (world - 1) or world > (1 << L):
         raise ValueError(f"world size {world} must be a power of two <= 2^L")
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside [0, {world})")
+    for name in ("D", "U", "V"):
+        t = getattr(h, name)
+        if t.dtype != torch.float64:
+            raise TypeError(f"sharded factorization is fp64-only ({name} is {t.dtype})")
     n_loc = n // world
     row0 = rank * n_loc
     nl = n_loc // m
@@ -78,30 +89,65 @@ def make_shard(h, rank: int, world: int) -> Shard:
                  slice_rows(None, h.V, n, r * L, row0, n_loc))
 
 
+def make_shard_like(sh: Shard) -> Shard:
+    """A second shard with the same geometry and (copied) buffers: the working
+    copy the factorization consumes, restored from ``sh`` between runs."""
+    return Shard(sh.n, sh.m, sh.r, sh.rank, sh.world, sh.D.clone(), sh.U.clone(), sh.V)
+
+
+def check_shard_buffers(sh: Shard) -> None:
+    """fp64, contiguous, exactly the local sizes (the C ABI trusts them)."""
+    import torch
+
+    n_loc, m, r, L = sh.n_loc, sh.m, sh.r, sh.L
+    want = {"D": (n_loc // m) * m * m, "U": n_loc * r * L, "V": n_loc * r * L}
+    for name, size in want.items():
+        t = getattr(sh, name)
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"shard {name} must be a torch tensor (got {type(t).__name__})")
+        if t.dtype != torch.float64:
+            raise TypeError(f"shard {name} must be float64 (got {t.dtype})")
+        if not t.is_contiguous() or t.numel() != size:
+            raise ValueError(f"shard {name} must be contiguous with {size} entries (got {t.numel()})")
+
+
 # ---------------------------------------------------------------------------
 # the schedule (backend-independent host logic)
 # ---------------------------------------------------------------------------
 
 
-def _pack(backend, contrib, q, lv, ncols, r):
+def _pack(backend, st, contrib, q, lv, ncols, r):
     """Place node q's r x ncols contribution (ld r) in the packed buffer of all
-    2^(lv+1) level-(lv+1) nodes (paired per parent: 2r x ncols, ld 2r)."""
-    buf = backend.zeros((1 << lv) * 2 * r * ncols)
+    2^(lv+1) level-(lv+1) nodes (paired per parent: 2r x ncols, ld 2r).  The
+    buffer is the rank state's reusable per-(level, ncols) one, zeroed in place."""
+    size = (1 << lv) * 2 * r * ncols
+    if hasattr(backend, "pack_buffer"):
+        buf = backend.pack_buffer(st, ("pack", lv, ncols), size)
+    else:
+        buf = backend.zeros(size)
     view = buf.reshape(1 << lv, ncols, 2 * r)
     view[q >> 1, :, (q & 1) * r : (q & 1) * r + r] = contrib.reshape(ncols, r)
     return buf
 
 
-def factorize_steps(shard: Shard, backend):
-    """Generator: yields buffers to sum-all-reduce; returns the factor state."""
+def factorize_steps(shard: Shard, backend, check: bool = True):
+    """Generator: yields buffers to sum-all-reduce; returns the factor state.
+
+    The last buffer yielded carries the singular-block flags of every rank
+    (leaf and K blocks it factored), so all ranks raise together
+    (:class:`~paper_2208_06290_b200.hodlr.HodlrSingularError`, SPEC.md:314)."""
     st = backend.factor_init(shard)
     p, r, n = shard.p, shard.r, shard.n
     contrib = backend.factor_local(st, p)  # [W|T] of this rank's level-p node (p > 0)
     for lv in range(p - 1, -1, -1):
         q = shard.row0 // (n >> (lv + 1))  # this rank's level-(lv+1) node
-        buf = _pack(backend, contrib, q, lv, r * (lv + 1), r)
+        buf = _pack(backend, st, contrib, q, lv, r * (lv + 1), r)
         buf = yield buf
         contrib = backend.factor_top(st, lv, buf)
+    flags = backend.singular_flags(st) if (check and hasattr(backend, "singular_flags")) else None
+    if flags is not None:
+        flags = yield flags
+        backend.raise_if_singular(st, flags)
     return st
 
 
@@ -111,7 +157,7 @@ def solve_steps(state, shard: Shard, backend, x_local, nrhs: int):
     contrib = backend.solve_local(state, x_local, nrhs, p)
     for lv in range(p - 1, -1, -1):
         q = shard.row0 // (n >> (lv + 1))
-        buf = _pack(backend, contrib, q, lv, nrhs, r)
+        buf = _pack(backend, state, contrib, q, lv, nrhs, r)
         buf = yield buf
         contrib = backend.solve_top(state, lv, buf, x_local, nrhs)
     return x_local
@@ -158,6 +204,26 @@ def run_lockstep(gens):
     return results
 
 
+def raise_singular_from_flags(flags, L: int) -> None:
+    """Raise HodlrSingularError (level, nodes) from the all-reduced flag vector
+    [leaf flags (2^L) | K flags (2^L - 1, level l at 2^l - 1)] -- the same
+    report as the single-GPU factorize."""
+    import numpy as np
+
+    from .hodlr import HodlrSingularError
+
+    flags = np.asarray(flags)
+    nleaf = 1 << L
+    bad = np.flatnonzero(flags[:nleaf] > 0)
+    if bad.size:
+        raise HodlrSingularError("leaf", L, bad.tolist())
+    kf = flags[nleaf:]
+    for lv in range(L):
+        seg = kf[(1 << lv) - 1 : (2 << lv) - 1]
+        if (seg > 0).any():
+            raise HodlrSingularError("K", lv, np.flatnonzero(seg > 0).tolist())
+
+
 def torch_all_reduce(buf):
     import torch.distributed as dist
 
@@ -186,6 +252,7 @@ class GpuBackend:
         self.torch = _lib.require_cuda()
         self.lib = _lib.load()
         self.device = device
+        self._ws = {}
 
     def zeros(self, n):
         return self.torch.zeros(n, dtype=self.torch.float64, device=self.device)
@@ -196,16 +263,18 @@ class GpuBackend:
     def factor_init(self, sh: Shard) -> GpuShardFactor:
         torch = self.torch
         dev = self.device
+        check_shard_buffers(sh)
         n, m, r, L = sh.n, sh.m, sh.r, sh.L
         nl = sh.n_loc // m
         nk = (1 << L) - 1
+        inv = lambda nb, s: max(nb * int(self.lib.hodlr_inv_elems(s)), 1)  # noqa: E731
         i32 = dict(dtype=torch.int32, device=dev)
         b = dict(
-            D=sh.D, Dinv=torch.empty_like(sh.D), Y=sh.U, V=sh.V,
+            D=sh.D, Dinv=torch.empty(inv(nl, m), dtype=torch.float64, device=dev), Y=sh.U, V=sh.V,
             # K blocks of other ranks' deep parents are never written nor read here:
             # no zero-fill (it would be a 1 GB memset per factorization at cfg2)
             K=torch.empty(max(nk, 1) * 4 * r * r, dtype=torch.float64, device=dev),
-            Kinv=torch.empty(max(nk, 1) * 4 * r * r, dtype=torch.float64, device=dev),
+            Kinv=torch.empty(inv(max(nk, 1), 2 * r), dtype=torch.float64, device=dev),
             dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
             kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
             kinfo=torch.zeros(max(nk, 1), **i32),
@@ -216,12 +285,43 @@ class GpuBackend:
         desc = _lib.Desc(n, m, r, L, _lib.F64)
         st = GpuShardFactor(sh, desc, fac, b)
         st.wsb = self.lib.hodlr_factorize_local_workspace(C.byref(desc), sh.n_loc)
-        st.ws = torch.empty(max(st.wsb, 1), dtype=torch.uint8, device=dev)
+        ws = self._ws.get((sh.rank, sh.world, st.wsb))  # one workspace per shard, reused across factorizations
+        if ws is None:
+            ws = self._ws[(sh.rank, sh.world, st.wsb)] = torch.empty(max(st.wsb, 1), dtype=torch.uint8, device=dev)
+        st.ws = ws
         return st
+
+    def pack_buffer(self, st: GpuShardFactor, key, n, dtype=None, zero=True):
+        """Reusable device buffers of one rank's state (all-reduce packs, outputs),
+        allocated once per (key, size) and zeroed in place on reuse."""
+        dtype = dtype or self.torch.float64
+        key = ("_cache",) + tuple(key)
+        buf = st.bufs.get(key)
+        if buf is None or buf.numel() != n or buf.dtype != dtype:
+            buf = self.torch.zeros(n, dtype=dtype, device=self.device)
+            st.bufs[key] = buf
+        elif zero:
+            buf.zero_()
+        return buf
+
+    def singular_flags(self, st: GpuShardFactor):
+        """[leaf flags of all 2^L leaves | K flags of all 2^L - 1 blocks], this
+        rank's entries filled (sum-all-reduced by the schedule)."""
+        sh = st.shard
+        nleaf, nl = 1 << sh.L, sh.n_loc // sh.m
+        f = self.pack_buffer(st, ("flags",), 2 * nleaf - 1)
+        a = sh.row0 // sh.m
+        f[a : a + nl] = st.bufs["dinfo"].to(self.torch.float64)
+        if sh.L:
+            f[nleaf:] = st.bufs["kinfo"][: nleaf - 1].to(self.torch.float64)
+        return f
+
+    def raise_if_singular(self, st: GpuShardFactor, flags) -> None:
+        raise_singular_from_flags(flags.cpu().numpy(), st.shard.L)
 
     def factor_local(self, st: GpuShardFactor, p: int):
         sh = st.shard
-        out = self.zeros(sh.r * sh.r * max(p, 1))
+        out = self.pack_buffer(st, ("tw_out",), sh.r * sh.r * max(p, 1), zero=False)
         _lib.check(self.lib.hodlr_factorize_local(
             C.byref(st.desc), C.byref(st.fac), sh.n_loc, sh.row0, p, C.c_void_p(out.data_ptr()),
             C.c_void_p(st.ws.data_ptr()), st.wsb, self._stream()), "hodlr_factorize_local")
@@ -229,7 +329,7 @@ class GpuBackend:
 
     def factor_top(self, st: GpuShardFactor, lv: int, tw_all):
         sh = st.shard
-        out = self.zeros(sh.r * sh.r * max(lv, 1))
+        out = self.pack_buffer(st, ("tw_out", lv), sh.r * sh.r * max(lv, 1), zero=False)
         _lib.check(self.lib.hodlr_factorize_top(
             C.byref(st.desc), C.byref(st.fac), sh.n_loc, sh.row0, lv, C.c_void_p(tw_all.data_ptr()),
             C.c_void_p(out.data_ptr()), C.c_void_p(st.ws.data_ptr()), st.wsb, self._stream()), "hodlr_factorize_top")
@@ -242,10 +342,19 @@ class GpuBackend:
             st.bufs[key] = self.torch.empty(max(wsb, 1), dtype=self.torch.uint8, device=self.device)
         return st.bufs[key], wsb
 
+    def _check_x(self, st: GpuShardFactor, x, nrhs: int):
+        torch = self.torch
+        want = st.shard.n_loc * nrhs
+        if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 or not x.is_cuda:
+            raise TypeError("x_local must be a float64 CUDA tensor (the sharded solve is fp64-only)")
+        if not x.is_contiguous() or x.numel() != want:
+            raise ValueError(f"x_local must be contiguous with n_loc * nrhs = {want} entries (got {x.numel()})")
+
     def solve_local(self, st: GpuShardFactor, x, nrhs: int, p: int):
         sh = st.shard
+        self._check_x(st, x, nrhs)
         ws, wsb = self._solve_ws(st, nrhs)
-        out = self.zeros(sh.r * nrhs)
+        out = self.pack_buffer(st, ("w_out", nrhs), sh.r * nrhs, zero=False)
         _lib.check(self.lib.hodlr_solve_local(
             C.byref(st.desc), C.byref(st.fac), sh.n_loc, sh.row0, p, C.c_void_p(x.data_ptr()), sh.n_loc, nrhs,
             C.c_void_p(out.data_ptr()), C.c_void_p(ws.data_ptr()), wsb, self._stream()), "hodlr_solve_local")
@@ -253,8 +362,9 @@ class GpuBackend:
 
     def solve_top(self, st: GpuShardFactor, lv: int, w_all, x, nrhs: int):
         sh = st.shard
+        self._check_x(st, x, nrhs)
         ws, wsb = self._solve_ws(st, nrhs)
-        out = self.zeros(sh.r * nrhs)
+        out = self.pack_buffer(st, ("w_out", nrhs, lv), sh.r * nrhs, zero=False)
         _lib.check(self.lib.hodlr_solve_top(
             C.byref(st.desc), C.byref(st.fac), sh.n_loc, sh.row0, lv, C.c_void_p(w_all.data_ptr()),
             C.c_void_p(out.data_ptr()), C.c_void_p(x.data_ptr()), sh.n_loc, nrhs, C.c_void_p(ws.data_ptr()), wsb,
@@ -262,10 +372,12 @@ class GpuBackend:
         return out
 
 
-def factorize_sharded(shard: Shard, all_reduce=torch_all_reduce, backend=None):
-    """One rank's part of the sharded factorization (call on every rank)."""
+def factorize_sharded(shard: Shard, all_reduce=torch_all_reduce, backend=None, check: bool = True):
+    """One rank's part of the sharded factorization (call on every rank).
+    check=True all-reduces the singular flags and raises HodlrSingularError on
+    every rank (one extra tiny all-reduce + a host sync)."""
     backend = backend or GpuBackend()
-    return run(factorize_steps(shard, backend), all_reduce)
+    return run(factorize_steps(shard, backend, check), all_reduce)
 
 
 def solve_sharded(state, x_local, nrhs: int = 1, all_reduce=torch_all_reduce, backend=None):

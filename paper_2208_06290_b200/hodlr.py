@@ -127,24 +127,31 @@ class HodlrMatrix:
             raise ValueError(f"matvec: x must have {n} rows (got shape {tuple(xt.shape)})")
         nrhs = 1 if xt.dim() == 1 else xt.shape[1]
         dev = self.D.device
-        X = xt.reshape(n, nrhs).t().to(device=dev, dtype=self.dtype).contiguous()  # column-major N x nrhs
-        Y = torch.empty_like(X)
         desc = self.desc()
         wsb = lib.hodlr_matvec_workspace(C.byref(desc), nrhs)
         so = stream or torch.cuda.current_stream(dev)
-        ws = _workspace(wsb, dev, so) if wsb else None
-        st = so.cuda_stream
-        _lib.check(
-            lib.hodlr_matvec(C.byref(desc), C.c_void_p(self.D.data_ptr()), C.c_void_p(self.U.data_ptr()),
-                             C.c_void_p(self.V.data_ptr()), C.c_void_p(X.data_ptr()), n,
-                             C.c_void_p(Y.data_ptr()), n, nrhs, C.c_void_p(ws.data_ptr() if ws is not None else 0),
-                             wsb, C.c_void_p(st)),
-            "hodlr_matvec",
-        )
-        out = Y.t().reshape(xt.shape)
-        if is_np:
-            return out.cpu().numpy()
-        return out.to(xt.device) if xt.device != dev else out
+        with torch.cuda.device(dev), torch.cuda.stream(so):
+            X = xt.reshape(n, nrhs).t().to(device=dev, dtype=self.dtype).contiguous()  # column-major N x nrhs
+            Y = torch.empty_like(X)
+            ws = _workspace(wsb, dev, so) if wsb else None
+            _lib.check(
+                lib.hodlr_matvec(C.byref(desc), C.c_void_p(self.D.data_ptr()), C.c_void_p(self.U.data_ptr()),
+                                 C.c_void_p(self.V.data_ptr()), C.c_void_p(X.data_ptr()), n,
+                                 C.c_void_p(Y.data_ptr()), n, nrhs,
+                                 C.c_void_p(ws.data_ptr() if ws is not None else 0), wsb, C.c_void_p(so.cuda_stream)),
+                "hodlr_matvec",
+            )
+            out = Y.t().reshape(xt.shape)
+            if is_np:
+                res = out.cpu().numpy()  # synchronous on `so`
+            elif xt.device != dev:
+                res = out.to(xt.device)
+            else:
+                res = out
+        if stream is not None and not is_np:
+            # the caller's current stream consumes the result: order it after `so`
+            torch.cuda.current_stream(dev).wait_stream(so)
+        return res
 
     def reconstruct_dense(self):
         torch = _torch()
@@ -220,6 +227,15 @@ class HodlrFactorization:
 _WS_CACHE: dict = {}
 
 
+def _dinv_size(nblocks: int, s: int, fp64: bool = True) -> int:
+    """Scalars of the factorization-internal solve aids (``Dinv`` / ``Kinv``)
+    for ``nblocks`` s x s blocks: 8 s per block (8x8 diagonal-block inverses,
+    s in {32, 64, 128}), s^2 (packed inverses, s = 16), none otherwise; the fp32
+    path forms them on the fly (``hodlr_inv_elems``, include/hodlr_b200.h)."""
+    per = int(_lib.load().hodlr_inv_elems(s)) if fp64 else 0
+    return max(nblocks * per, 1)
+
+
 def _workspace(nbytes: int, device, stream=None):
     """Reusable device workspace (bytes) per (device, stream), grown on demand.
     Calls on one stream are ordered, so they can share it; calls on different
@@ -278,14 +294,15 @@ def factorize(h: HodlrMatrix, variant: str = "pivoted_standard", check: bool = T
         raise TypeError(f"unsupported dtype {h.D.dtype} (float64: DMMA path; float32: preconditioner path)")
     lib = _lib.load()
     dev = h.D.device
+    fp64 = h.D.dtype == torch.float64
     n, m, r, L = h.n, h.m, h.rank, h.L
     nl = 1 << L
     nk = nl - 1
     i32 = dict(dtype=torch.int32, device=dev)
     f = HodlrFactorization(
-        tree=h.tree, rank=r, D=h.D, Dinv=torch.empty_like(h.D), Y=h.U, V=h.V,
-        K=torch.empty(nk * 4 * r * r, dtype=h.D.dtype, device=dev),
-        Kinv=torch.empty(nk * 4 * r * r, dtype=h.D.dtype, device=dev),
+        tree=h.tree, rank=r, D=h.D, Dinv=torch.empty(_dinv_size(nl, m, fp64), dtype=h.D.dtype, device=dev),
+        Y=h.U, V=h.V, K=torch.empty(nk * 4 * r * r, dtype=h.D.dtype, device=dev),
+        Kinv=torch.empty(_dinv_size(nk, 2 * r, fp64), dtype=h.D.dtype, device=dev),
         dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
         kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
         kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r),
@@ -336,30 +353,33 @@ def factorize_from_host(n: int, m: int, r: int, D, U, V, variant: str = "pivoted
 
     Dh, Uh, Vh = host(D, nl * m * m, "D"), host(U, n * r * L, "U"), host(V, n * r * L, "V")
     dev = torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
     f64 = dict(dtype=torch.float64, device=dev)
     i32 = dict(dtype=torch.int32, device=dev)
-    f = HodlrFactorization(
-        tree=ClusterTree(n, L), rank=r, D=torch.empty(nl * m * m, **f64), Dinv=torch.empty(nl * m * m, **f64),
-        Y=torch.empty(n * r * L, **f64), V=torch.empty(n * r * L, **f64),
-        K=torch.empty(max(nk, 1) * 4 * r * r, **f64), Kinv=torch.empty(max(nk, 1) * 4 * r * r, **f64),
-        dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
-        kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
-        kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r),
-    )
-    f.host_inputs = (Dh, Uh, Vh)  # alive until the asynchronous upload has completed
-    desc = f.desc()
-    wsb = lib.hodlr_factorize_workspace(C.byref(desc))
-    st = (stream or torch.cuda.current_stream(dev))
-    ws = _workspace(wsb, dev, st)
-    key = str(dev)
-    if key not in _COPY_STREAMS:
-        _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
-    cs = _COPY_STREAMS[key]
-    cf = f.cfactors()
-    _lib.check(lib.hodlr_factorize_from_host(C.byref(desc), C.byref(cf), C.c_void_p(Dh.data_ptr()),
-                                             C.c_void_p(Uh.data_ptr()), C.c_void_p(Vh.data_ptr()),
-                                             C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st.cuda_stream),
-                                             C.c_void_p(cs.cuda_stream)), "hodlr_factorize_from_host")
+    with torch.cuda.device(dev):
+        f = HodlrFactorization(
+            tree=ClusterTree(n, L), rank=r, D=torch.empty(nl * m * m, **f64), Dinv=torch.empty(_dinv_size(nl, m), **f64),
+            Y=torch.empty(n * r * L, **f64), V=torch.empty(n * r * L, **f64),
+            K=torch.empty(max(nk, 1) * 4 * r * r, **f64), Kinv=torch.empty(_dinv_size(max(nk, 1), 2 * r), **f64),
+            dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
+            kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
+            kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r),
+        )
+        f.host_inputs = (Dh, Uh, Vh)  # alive until the asynchronous upload has completed
+        desc = f.desc()
+        wsb = lib.hodlr_factorize_workspace(C.byref(desc))
+        st = (stream or torch.cuda.current_stream(dev))
+        ws = _workspace(wsb, dev, st)
+        key = dev.index
+        if key not in _COPY_STREAMS:
+            _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+        cs = _COPY_STREAMS[key]
+        cf = f.cfactors()
+        _lib.check(lib.hodlr_factorize_from_host(C.byref(desc), C.byref(cf), C.c_void_p(Dh.data_ptr()),
+                                                 C.c_void_p(Uh.data_ptr()), C.c_void_p(Vh.data_ptr()),
+                                                 C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st.cuda_stream),
+                                                 C.c_void_p(cs.cuda_stream)), "hodlr_factorize_from_host")
     if check:
         _raise_if_singular(f)
     return f

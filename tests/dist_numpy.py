@@ -23,6 +23,7 @@ class NpState:
     K: dict = field(default_factory=dict)   # level -> (npar_global, 2r, 2r) LU stacks (global indices)
     kperm: dict = field(default_factory=dict)
     kswaps: dict = field(default_factory=dict)
+    ksing: dict = field(default_factory=dict)  # level -> set of global parents flagged singular
 
 
 def _col(buf, n, j0, ncols):
@@ -33,6 +34,23 @@ def _col(buf, n, j0, ncols):
 class NumpyBackend:
     def zeros(self, n):
         return np.zeros(n)
+
+    def singular_flags(self, st):
+        sh = st.shard
+        L, nleaf = sh.L, 1 << sh.L
+        f = np.zeros(2 * nleaf - 1)
+        a = sh.row0 // sh.m
+        for i in np.flatnonzero(st.dpiv.singular):
+            f[a + int(i)] = 1.0
+        for lv, ps in st.ksing.items():
+            for p in ps:
+                f[nleaf + (1 << lv) - 1 + p] = 1.0
+        return f
+
+    def raise_if_singular(self, st, flags):
+        from paper_2208_06290_b200.distributed import raise_singular_from_flags
+
+        raise_singular_from_flags(flags, st.shard.L)
 
     def factor_init(self, sh):
         return NpState(sh, np.array(sh.D, dtype=np.float64), np.array(sh.U, dtype=np.float64),
@@ -51,6 +69,7 @@ class NumpyBackend:
         flat = np.ascontiguousarray(K.transpose(0, 2, 1)).reshape(-1)  # column-major blocks
         stack = orc.sview(flat, 0, 4 * r * r, npar, 2 * r, 2 * r, 2 * r)
         piv = orc.lu_factor(stack)
+        st.ksing.setdefault(lv, set()).update(p_glob0 + int(i) for i in np.flatnonzero(piv.singular))
         for i in range(npar):
             st.K.setdefault(lv, {})[p_glob0 + i] = np.array(stack[i])
             st.kperm.setdefault(lv, {})[p_glob0 + i] = piv.perm[i].copy()

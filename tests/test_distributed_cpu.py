@@ -105,3 +105,60 @@ def test_gloo_world_matches_oracle(tmp_path, world):
         for row in d["kswaps"]:
             lv, p, sw = int(row[0]), int(row[1]), row[2:]
             assert np.array_equal(sw, fo.kpiv[lv].swaps[p])
+
+
+def _gloo_singular_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2208_06290_b200.hodlr import HodlrSingularError
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, m, r = 512, 32, 4
+        h = orc.make_exact_hodlr(n, m, r, seed=3, s=1.0)
+        h.D[13 * m * m : 14 * m * m] = 0.0  # leaf 13 (owned by rank 1 of 2) is singular
+        sh = np_shard(h, rank, world)
+
+        def all_reduce(buf):
+            dist.all_reduce(torch.from_numpy(buf), op=dist.ReduceOp.SUM)
+
+        try:
+            dd.run(dd.factorize_steps(sh, NumpyBackend()), all_reduce)
+            msg = "no error"
+        except HodlrSingularError as e:
+            msg = str(e)
+        with open(out.format(rank=rank), "w") as fh:
+            fh.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_singular_leaf_raises_on_every_rank(tmp_path):
+    # a singular leaf on one rank makes ALL ranks raise with level and node
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = str(tmp_path / "sing{rank}.txt")
+    mp.start_processes(_gloo_singular_worker, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    for g in range(2):
+        with open(out.format(rank=g)) as fh:
+            assert fh.read() == "singular leaf block at level 4, node(s) [13]"
+
+
+def test_lockstep_singular_k_block_reported():
+    # zero leaves on both halves -> K singular is impossible to provoke portably; check the
+    # flag decoder directly on a synthetic flag vector (level 2, node 1)
+    from paper_2208_06290_b200.distributed import raise_singular_from_flags
+    from paper_2208_06290_b200.hodlr import HodlrSingularError
+
+    L = 3
+    flags = np.zeros(2 * (1 << L) - 1)
+    flags[(1 << L) + 3 + 1] = 2.0  # K level 2 starts at 2^2 - 1 = 3
+    with pytest.raises(HodlrSingularError, match=r"K block at level 2, node\(s\) \[1\]"):
+        raise_singular_from_flags(flags, L)
+    raise_singular_from_flags(np.zeros(2 * (1 << L) - 1), L)  # clean: no raise

@@ -19,9 +19,19 @@ pytestmark = pytest.mark.gpu
 
 from oracle import hodlr_oracle as orc  # noqa: E402
 import paper_2208_06290_b200 as hb  # noqa: E402
+from tests.conftest import record_parity  # noqa: E402
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 TOL = 1e-10  # fp64 solution / factor agreement (north_star)
+SENS_MULT = 4.0  # hard-pivoting (s = 16) inputs only: gate = max(TOL, 4 x the oracle's own 1-ulp sensitivity)
+
+
+def gate(s: float, sens: float) -> float:
+    """North-star 1e-10 for well-conditioned inputs (U scale s <= 4); for the
+    s = 16 stress regime (cond ~2e4, ~80 % real K pivot choices) any
+    non-OpenBLAS summation order moves Y / x by the oracle's own 1-ulp
+    sensitivity, so the gate is max(1e-10, 4 x that sensitivity)."""
+    return TOL if s <= 4 else max(TOL, SENS_MULT * sens)
 
 
 def rel(a, b):
@@ -53,10 +63,13 @@ def test_golden_factor_and_solve(path):
     assert np.array_equal(f.kswaps.cpu().numpy().reshape(-1, 2 * r), g["k_swaps"])
     assert np.array_equal(f.kperm.cpu().numpy().reshape(-1, 2 * r), g["k_perm"])
     _, sy, sx = oracle_sensitivity(h, g["b"])
-    assert rel(f.Y.cpu().numpy(), g["Y"]) <= max(TOL, 20 * sy)
-    assert rel(f.K.cpu().numpy(), g["K"]) <= max(TOL, 20 * sy)
+    s = float(g["s"])
     x = hb.solve(f, g["b"])
-    assert rel(x, g["x"]) <= max(TOL, 20 * sx)
+    ey, ek, ex = rel(f.Y.cpu().numpy(), g["Y"]), rel(f.K.cpu().numpy(), g["K"]), rel(x, g["x"])
+    record_parity(f"golden/{path.stem}", y=ey, k=ek, x=ex, gate_y=gate(s, sy), gate_x=gate(s, sx), sens_y=sy, sens_x=sx)
+    assert ey <= gate(s, sy)
+    assert ek <= gate(s, sy)
+    assert ex <= gate(s, sx)
     la, sg = hb.logdet(f)
     assert sg == float(g["logdet_sign"])
     assert abs(la - float(g["logdet"])) <= 1e-10 * abs(float(g["logdet"]))
@@ -95,9 +108,8 @@ def oracle_sensitivity(h, b):
 
     Any implementation that is not bit-identical to OpenBLAS (different GEMM
     summation order) can only agree with the oracle to about this level, so the
-    1e-10 gate is applied as max(1e-10, 20 x sensitivity) -- identical to the
-    plain 1e-10 on well-conditioned inputs (s <= 4), and meaningful on the
-    hard-pivoting s = 16 inputs whose K blocks amplify rounding.
+    1e-10 gate is applied as max(1e-10, 4 x sensitivity) on the hard-pivoting
+    s = 16 inputs only (their K blocks amplify rounding); s <= 4 uses 1e-10.
     """
     f1 = orc.factorize(h.copy(), threads=8)
     h2 = h.copy()
@@ -124,10 +136,14 @@ def test_random_vs_oracle(n, m, r, s):
     assert np.array_equal(f.dperm.cpu().numpy().reshape(-1, m), fo.dpiv.perm)
     ks = f.kswaps.cpu().numpy().reshape(-1, 2 * r)
     assert np.array_equal(ks, np.concatenate([kp.swaps for kp in fo.kpiv]))
-    assert rel(f.Y.cpu().numpy(), fo.Y) <= max(TOL, 20 * sy)
-    assert rel(f.K.cpu().numpy(), np.concatenate(fo.K)) <= max(TOL, 20 * sy)
     x = hb.solve(f, b)
-    assert rel(x, orc.solve(fo, b, threads=8)) <= max(TOL, 20 * sx)
+    ey, ek = rel(f.Y.cpu().numpy(), fo.Y), rel(f.K.cpu().numpy(), np.concatenate(fo.K))
+    ex = rel(x, orc.solve(fo, b, threads=8))
+    record_parity(f"random/n{n}_m{m}_r{r}_s{s:g}", y=ey, k=ek, x=ex, gate_y=gate(s, sy), gate_x=gate(s, sx),
+                  sens_y=sy, sens_x=sx)
+    assert ey <= gate(s, sy)
+    assert ek <= gate(s, sy)
+    assert ex <= gate(s, sx)
     # relative residual against the HODLR operator itself, vs the oracle's own
     hm = to_gpu(h)
     bt = torch.from_numpy(b).cuda()
@@ -207,10 +223,12 @@ def test_fp32_preconditioner_path_vs_oracle(n, m, r):
     assert np.array_equal(f.dperm.cpu().numpy().reshape(-1, m), fo.dpiv.perm)
     ks = f.kswaps.cpu().numpy().reshape(-1, 2 * r)
     assert np.array_equal(ks, np.concatenate([kp.swaps for kp in fo.kpiv]))
-    assert rel(f.Y.cpu().numpy(), fo.Y) <= 1e-4
     x = hb.solve(f, b)
     assert x.dtype == np.float32
-    assert rel(x, orc.solve(fo, b, threads=8)) <= 1e-4
+    ey, ex = rel(f.Y.cpu().numpy(), fo.Y), rel(x, orc.solve(fo, b, threads=8))
+    record_parity(f"fp32/n{n}_m{m}_r{r}", y=ey, x=ex, gate_x=1e-4)
+    assert ey <= 1e-4
+    assert ex <= 1e-4
 
 
 def test_fp32_multi_rhs_columns_bitwise_equal_single():

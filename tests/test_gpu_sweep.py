@@ -1,7 +1,8 @@
 """GPU: a seeded sweep over shapes the fused and generic paths dispatch on --
 leaf m, rank r, depth L, pivoting regime s, nrhs -- against the CPU oracle
-(leaf / K pivots bit-exact, x within 1e-9 of the oracle, relres within 4x of
-the oracle's own residual)."""
+(leaf / K pivots bit-exact; x within 1e-10 of the oracle for s = 1, within
+max(1e-10, 4 x the oracle's own 1-ulp sensitivity) for the hard-pivoting
+s = 16 regime; relres within 4x of the oracle's own residual)."""
 
 from __future__ import annotations
 
@@ -13,6 +14,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import hodlr_oracle as orc  # noqa: E402
 import paper_2208_06290_b200 as hb  # noqa: E402
+from tests.conftest import record_parity  # noqa: E402
 
 
 def _cases():
@@ -45,7 +47,16 @@ def test_sweep_against_oracle(m, r, L, s, nrhs, seed):
         assert np.array_equal(f.kswaps.cpu().numpy()[: ((1 << L) - 1) * 2 * r].reshape(-1, 2 * r),
                               np.concatenate([p.swaps for p in fo.kpiv]))
     rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
-    assert rel <= 1e-9, rel
+    if s <= 4:
+        gate, sens = 1e-10, None
+    else:  # the oracle's own change under a 1-ulp perturbation of U
+        h2 = h.copy()
+        h2.U *= 1 + 1e-16 * np.random.default_rng(0).standard_normal(h2.U.size)
+        xo2 = orc.solve(orc.factorize(h2), b)
+        sens = np.linalg.norm(xo2 - xo) / np.linalg.norm(xo)
+        gate = max(1e-10, 4 * sens)
+    record_parity(f"sweep/m{m}_r{r}_L{L}_s{s:g}_nrhs{nrhs}", x=rel, gate_x=gate, sens_x=sens)
+    assert rel <= gate, (rel, gate)
     bt = torch.from_numpy(b).cuda()
 
     def relres(xx):
@@ -69,4 +80,5 @@ def test_sweep_fp32_against_oracle(m, r, L, nrhs):
     assert np.array_equal(f.dperm.cpu().numpy().reshape(-1, m), fo.dpiv.perm)
     x = hb.solve(f, b)
     rel = np.linalg.norm(x.astype(np.float64) - xo) / np.linalg.norm(xo)
+    record_parity(f"sweep_fp32/m{m}_r{r}_L{L}_nrhs{nrhs}", x=rel, gate_x=1e-4)
     assert rel <= 1e-4, rel

@@ -163,3 +163,20 @@ def test_matvec_spec_examples_and_dense():
     X = np.random.default_rng(2).standard_normal((n, 3))
     A = orc.dense(h)
     assert np.linalg.norm(orc.matvec(h, X) - A @ X) <= 1e-13 * np.linalg.norm(A @ X)
+
+
+def test_oracle_reproduces_reference_on_cfg2_subtree():
+    # the cfg2 operator's leading 2^14-row subtree: the oracle's assembly equals the
+    # reference's compress() inputs and its factorize/solve the reference's outputs, bit for bit
+    from oracle import build_oracle as bo
+    from tests.golden.make_cfg_golden import digest, sketches
+
+    g = np.load(GOLDEN / "cfg2_laplace_sub14.npz")
+    n, m, r = int(g["n"]), int(g["m"]), int(g["r"])
+    D, U, V = bo.assemble(bo.LaplaceDL(int(g["n_total"])), n, m, r)
+    assert digest(D, U, V) == str(g["in_sha"])
+    f = orc.factorize(orc.HodlrData(orc.Layout(n, m, r), D, U, V), threads=8)
+    assert np.array_equal(orc.solve(f, g["b"], threads=8), g["x"])
+    assert digest(f.D) == str(g["d_lu_sha"])
+    ys, ks = sketches(f.Y, np.concatenate(f.K), n, r, f.lay.L)
+    assert np.array_equal(ys, g["y_sketch"]) and np.array_equal(ks, g["k_sketch"])
