@@ -123,7 +123,7 @@ def oracle_sensitivity(h, b):
 @pytest.mark.parametrize(
     "n,m,r,s",
     [(1 << 14, 64, 32, 4.0), (1 << 14, 64, 32, 16.0), (1 << 13, 64, 16, 1.0), (1 << 12, 32, 8, 16.0),
-     (1 << 11, 16, 32, 16.0), (1 << 12, 64, 64, 4.0), (1 << 14, 64, 64, 16.0), (1 << 13, 32, 32, 4.0),
+     (1 << 11, 16, 32, 16.0), (1 << 12, 64, 64, 2.0), (1 << 14, 64, 64, 16.0), (1 << 13, 32, 32, 4.0),
      (1 << 13, 32, 16, 16.0)],
 )
 def test_random_vs_oracle(n, m, r, s):
