@@ -368,12 +368,17 @@ def run_ours(args):
         hw.D.copy_(h0.D)
         hw.U.copy_(h0.U)
 
-    def step():
+    # the public repeated-factorization API: one eager factorization, then the
+    # captured launch sequence (CUDA graph) replayed on the restored buffers;
+    # the solve replays its own captured graph (hb.solve(graph=True))
+    plan = hb.FactorPlan(hw, check=False)
+
+    def step(graph=True):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
-        f = hb.factorize(hw, check=False)
+        f = plan.refactor(check=False) if graph else hb.factorize(hw, check=False)
         e1.record()
-        x = hb.solve(f, b)
+        x = hb.solve(f, b, graph=graph)
         e2.record()
         return f, x, (e0, e1, e2)
 
@@ -403,11 +408,21 @@ def run_ours(args):
     ts = sum(ev[1].elapsed_time(ev[2]) for ev in tf_ms) / args.steps
     t_step = tf + ts
 
-    # per-phase event profile + launch count of one step (after the timed loop)
+    # the same steps launched eagerly (no graphs), for comparison
+    eager = []
+    for _ in range(3):
+        restore()
+        _, _, ev = step(graph=False)
+        eager.append(ev)
+    torch.cuda.synchronize()
+    eager_f = statistics.median(ev[0].elapsed_time(ev[1]) for ev in eager)
+    eager_s = statistics.median(ev[1].elapsed_time(ev[2]) for ev in eager)
+
+    # per-phase event profile + launch count of one (eager) step (after the timed loop)
     restore()
     lib.hodlr_profile_enable(1)
     c0 = lib.hodlr_launch_count()
-    f, x, _ = step()
+    f, x, _ = step(graph=False)
     torch.cuda.synchronize()
     launches_per_step = lib.hodlr_launch_count() - c0
     ph = (C.c_double * 9)()
@@ -485,6 +500,8 @@ def run_ours(args):
                                    + PROBLEM_DESC[args.problem], "N": n, "leaf": m, "rank": r, "L": L, "nrhs": 1,
                        "parallelism": f"replicas{world}", "l2_flush": "inputs 8 GB > L2"},
             "t_factor_ms": tf, "t_solve_ms": ts, "factor_tflops": f_flops / (tf * 1e-3) / 1e12, "build_ms": build_ms,
+            "launch": "CUDA graphs (hb.FactorPlan.refactor + hb.solve(graph=True))",
+            "eager_ms": {"factor": eager_f, "solve": eager_s},
             "step_ms_min_med_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
             "solve_gbps": (8 * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 16 * n) / (ts * 1e-3) / 1e9,
             "relres": relres, "flops_factor": f_flops, "flops_solve": s_flops,

@@ -23,6 +23,7 @@ from .backend import (  # noqa: F401
     parse_executor,
 )
 from .hodlr import (  # noqa: F401
+    FactorPlan,
     HodlrFactorization,
     HodlrMatrix,
     HodlrSingularError,

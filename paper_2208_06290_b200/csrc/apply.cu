@@ -630,7 +630,7 @@ hodlr_status tri_apply_f32(int s, int ncols, int batch, const float* lu, int64_t
   constexpr int S = 64, PT = Apply2Cfg<S>::PT;
   auto go = [&](auto kern, int twr_) -> hodlr_status {
     const size_t smem = (size_t)(S + twr_) * PT * sizeof(double) + (size_t)S * 8 * sizeof(double);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_attr(kern, (int)smem);
     const int G = (int)ceil_div(ncols, 8);
     int cpb = 1;
     while ((int64_t)batch * cpb < 2 * 148 && cpb * 8 < G) cpb *= 2;

@@ -1,5 +1,7 @@
 // Shared device helpers for the HODLR B200 kernels (sm_100a).
 #pragma once
+#include <mutex>
+#include <unordered_map>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -83,6 +85,22 @@ __host__ __device__ inline int64_t inv_block_elems(int s) {
   return (s == 32 || s == 64 || s == 128) ? (int64_t)8 * s : s == 16 ? (int64_t)s * s : 0;
 }
 
+}  // namespace hodlr
+
+namespace hodlr {
+// cudaFuncSetAttribute once per (kernel, size): repeated calls would also land
+// inside CUDA-graph captures of later factorize / solve calls
+template <typename K>
+inline void smem_attr(K kern, int bytes, cudaFuncAttribute what = cudaFuncAttributeMaxDynamicSharedMemorySize) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  int& v = done[reinterpret_cast<const void*>(kern)];
+  if (v < bytes + 1) {
+    cudaFuncSetAttribute(kern, what, bytes);
+    v = bytes + 1;
+  }
+}
 }  // namespace hodlr
 
 // records the CUDA error string for hodlr_last_error(); defined in hodlr.cu

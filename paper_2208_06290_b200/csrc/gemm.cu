@@ -205,7 +205,7 @@ static hodlr_status run_cfg(GemmArgs g, cudaStream_t st) {
   auto kern = gemm_f64_kernel<BM, BN, WM, WN, TA, VEC>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_attr(kern, (int)smem);
     attr_set = true;
   }
   g.tiles_m = (int)ceil_div(g.M, BM);

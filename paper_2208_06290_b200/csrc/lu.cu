@@ -519,13 +519,13 @@ hodlr_status launch_getrf(int s, int batch, int mode, const T* src, int64_t lds,
                                   stridei, st);
   size_t sm = getrf_smem<T>(s);
   if (sm > 227 * 1024) return HODLR_ERR_ARG;
-  cudaFuncSetAttribute(getrf_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  smem_attr(getrf_kernel<T>, (int)sm);
   getrf_kernel<T><<<batch, 256, sm, st>>>(s, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info);
   HODLR_CHECK_LAUNCH();
   if (tinv) {
     const size_t sm2 = (size_t)2 * s * (s + 1) * sizeof(T);
     if (sm2 > 227 * 1024) return HODLR_ERR_ARG;
-    cudaFuncSetAttribute(trtri_packed_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    smem_attr(trtri_packed_kernel<T>, (int)sm2);
     trtri_packed_kernel<T><<<batch, 128, sm2, st>>>(s, out, ldo, strideo, tinv, ldi, stridei);
     HODLR_CHECK_LAUNCH();
   }
@@ -723,7 +723,7 @@ static hodlr_status run_getrs_col(int nrhs, int batch, const T* LU, int64_t lda,
   const int64_t grid = (int64_t)batch * cpb;
   if (grid > 2147483647LL) return HODLR_ERR_ARG;
   static const bool carve = [] {
-    cudaFuncSetAttribute(getrs_col_kernel<T, S>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    smem_attr(getrs_col_kernel<T, S>, 100, cudaFuncAttributePreferredSharedMemoryCarveout);
     return true;
   }();
   (void)carve;
@@ -754,7 +754,7 @@ hodlr_status launch_getrs(int s, int nrhs, int batch, const T* LU, int64_t lda, 
   if (sm > 227 * 1024) return HODLR_ERR_ARG;
   const int64_t grid = (int64_t)batch * ((nrhs + cw - 1) / cw);
   if (grid > 2147483647LL) return HODLR_ERR_ARG;
-  cudaFuncSetAttribute(getrs_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  smem_attr(getrs_kernel<T>, (int)sm);
   getrs_kernel<T><<<(unsigned)grid, 256, sm, st>>>(s, nrhs, cw, LU, lda, strideA, perm, B, ldb, strideB, X, ldx,
                                                     strideX, identity);
   HODLR_CHECK_LAUNCH();

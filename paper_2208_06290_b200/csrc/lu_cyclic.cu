@@ -570,31 +570,28 @@ static hodlr_status run_reg(int batch, int mode, const double* src, int64_t lds,
 // Factorization-internal LU (fp64, s in {32, 64}): factors + diagonal-block
 // inverses (8 s doubles per block at dbi + b * stridedbi) instead of the
 // packed full inverses -- the apply kernels run blocked substitutions.
-// s = 64 batches up to this size use the shared-row kernel, larger ones the
-// register-row kernel (cfg2: K levels 0..10; same-box A/B: factor 23.61 -> 23.39 ms)
-constexpr int kSmallLuBatch = 1024;
+// s = 64 batches up to this size use the sliding-window kernel, larger ones the
+// register-row kernel (tools/micro/lu_win_bench: window 1.12-1.34x faster up
+// to 2048 blocks, 0.96x at 8192)
+constexpr int kSmallLuBatch = 2048;
 static int small_lu_batch() { return kSmallLuBatch; }
+
+template <typename T>
+hodlr_status launch_getrf_win(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out,
+                              int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, double* dbi,
+                              int64_t stridedbi, cudaStream_t st);
 
 hodlr_status launch_getrf_dbi_f64(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides,
                                   double* out, int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm,
                                   int32_t* info, double* dbi, int64_t stridedbi, cudaStream_t st) {
   if (batch == 0) return HODLR_OK;
-  if (s == 64 && batch <= small_lu_batch()) {
-    // less than a wave of blocks: the step latency of one block decides, and the
-    // fully unrolled register kernel's ~100 KB body is fetched cold each step;
-    // the shared-row kernel's runtime step loop stays in the instruction cache
-    constexpr int S = 64, RP = S + 2;
-    constexpr size_t rows = (size_t)S * RP * sizeof(double);
-    constexpr size_t inv = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(double);
-    constexpr size_t smem = rows > inv ? rows : inv;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(getrf_sr_kernel<double, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
-    getrf_sr_kernel<double, S><<<batch, S, smem, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info,
-                                                         dbi, 0, stridedbi, 1);
-  } else if (s == 64)
+  if (s == 64 && batch <= small_lu_batch())
+    // less than a few waves of blocks: per-block step latency decides -- the
+    // compact sliding-window kernel (lu_win.cu; 1.2-1.3x faster than the
+    // shared-row kernel for 1..2048 blocks, same bits); full waves: register rows
+    return launch_getrf_win<double>(s, batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, dbi,
+                                    stridedbi, st);
+  if (s == 64)
     getrf_reg_kernel<64><<<batch, 64, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, dbi,
                                               stridedbi);
   else if (s == 32)

@@ -281,6 +281,25 @@ def solve_flops(n: int, m: int, r: int, nrhs: int = 1) -> int:
     return nrhs * (2 * m * n + 4 * r * n * L + 8 * r * r * ((1 << L) - 1))
 
 
+def _alloc_factorization(h: HodlrMatrix, variant: str = "pivoted_standard") -> HodlrFactorization:
+    """Output buffers of a factorization of ``h`` (Y / D overwrite h's U / D)."""
+    torch = _torch()
+    dev = h.D.device
+    fp64 = h.D.dtype == torch.float64
+    n, m, r, L = h.n, h.m, h.rank, h.L
+    nl = 1 << L
+    nk = nl - 1
+    i32 = dict(dtype=torch.int32, device=dev)
+    return HodlrFactorization(
+        tree=h.tree, rank=r, D=h.D, Dinv=torch.empty(_dinv_size(nl, m, fp64), dtype=h.D.dtype, device=dev),
+        Y=h.U, V=h.V, K=torch.empty(nk * 4 * r * r, dtype=h.D.dtype, device=dev),
+        Kinv=torch.empty(_dinv_size(nk, 2 * r, fp64), dtype=h.D.dtype, device=dev),
+        dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
+        kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
+        kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r),
+    )
+
+
 def factorize(h: HodlrMatrix, variant: str = "pivoted_standard", check: bool = True, stream=None) -> HodlrFactorization:
     """Level-wise batched factorization (PAPER Alg. 3).  Consumes ``h``.
 
@@ -294,19 +313,7 @@ def factorize(h: HodlrMatrix, variant: str = "pivoted_standard", check: bool = T
         raise TypeError(f"unsupported dtype {h.D.dtype} (float64: DMMA path; float32: preconditioner path)")
     lib = _lib.load()
     dev = h.D.device
-    fp64 = h.D.dtype == torch.float64
-    n, m, r, L = h.n, h.m, h.rank, h.L
-    nl = 1 << L
-    nk = nl - 1
-    i32 = dict(dtype=torch.int32, device=dev)
-    f = HodlrFactorization(
-        tree=h.tree, rank=r, D=h.D, Dinv=torch.empty(_dinv_size(nl, m, fp64), dtype=h.D.dtype, device=dev),
-        Y=h.U, V=h.V, K=torch.empty(nk * 4 * r * r, dtype=h.D.dtype, device=dev),
-        Kinv=torch.empty(_dinv_size(nk, 2 * r, fp64), dtype=h.D.dtype, device=dev),
-        dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
-        kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
-        kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r),
-    )
+    f = _alloc_factorization(h, variant)
     desc = h.desc()
     wsb = lib.hodlr_factorize_workspace(C.byref(desc))
     so = stream or torch.cuda.current_stream(dev)
@@ -401,9 +408,52 @@ def _raise_if_singular(f: HodlrFactorization) -> None:
             raise HodlrSingularError("K", lv, np.flatnonzero(seg).tolist())
 
 
-def solve(fact: HodlrFactorization, b, stream=None):
+class _SolveGraph:
+    """One captured ``hodlr_solve`` (CUDA graph) of a factorization for a fixed
+    nrhs on one stream: its own X buffer and workspace (the graph bakes their
+    addresses), replayed after the rhs is copied in."""
+
+    def __init__(self, fact, nrhs: int, stream):
+        torch = _torch()
+        lib = _lib.load()
+        n, dev = fact.n, fact.D.device
+        self.nrhs = nrhs
+        desc = fact.desc()
+        wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
+        with torch.cuda.device(dev), torch.cuda.stream(stream):
+            self.X = torch.zeros(nrhs, n, dtype=fact.D.dtype, device=dev)  # column-major N x nrhs
+            self.ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        cf = fact.cfactors()
+        self._args = (C.byref(desc), C.byref(cf), C.c_void_p(self.X.data_ptr()), n, nrhs,
+                      C.c_void_p(self.ws.data_ptr()), wsb)
+        self._keep = (desc, cf)
+        # one eager launch first: kernel attributes / lazy module loading happen
+        # outside the capture
+        _lib.check(lib.hodlr_solve(*self._args, C.c_void_p(stream.cuda_stream)), "hodlr_solve")
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(stream)
+        with torch.cuda.graph(self.graph, stream=side):
+            _lib.check(lib.hodlr_solve(*self._args, C.c_void_p(side.cuda_stream)), "hodlr_solve (capture)")
+        stream.wait_stream(side)
+
+    def run(self, x_cm, stream):
+        """x_cm: (nrhs, N) contiguous on the device; overwritten with the solution."""
+        torch = _torch()
+        with torch.cuda.stream(stream):
+            self.X.copy_(x_cm)
+            self.graph.replay()
+            x_cm.copy_(self.X)
+
+
+def solve(fact: HodlrFactorization, b, stream=None, graph: bool = True):
     """x = A^-1 b (PAPER Alg. 4).  ``b``: (N,) or (N, k), torch (device or host)
-    or numpy; the result has the same kind/shape and ``b`` is not modified."""
+    or numpy; the result has the same kind/shape and ``b`` is not modified.
+
+    graph=True (default): the level-by-level launch sequence of ``hodlr_solve``
+    is captured once per (nrhs, stream) as a CUDA graph and replayed (no host
+    enqueue gaps between the ~4 L small launches); graph=False launches it
+    eagerly.  Both run the same kernels on the same data, bit for bit."""
     torch = _torch()
     lib = _lib.load()
     is_np = isinstance(b, np.ndarray)
@@ -414,22 +464,32 @@ def solve(fact: HodlrFactorization, b, stream=None):
     nrhs = 1 if bt.dim() == 1 else bt.shape[1]
     dev = fact.D.device
     so = stream or torch.cuda.current_stream(dev)
-    with torch.cuda.stream(so):
+    with torch.cuda.device(dev), torch.cuda.stream(so):
         # upload first (a pinned host rhs is one async DMA), then lay out column-major
         # on the device: (nrhs, n) row-major == (n, nrhs) column-major
         bd = bt.to(device=dev, non_blocking=True) if bt.device != dev else bt
         x = bd.reshape(n, nrhs).t().to(dtype=fact.D.dtype).contiguous()
         if x.data_ptr() == bt.data_ptr():
             x = x.clone()
-        desc = fact.desc()
-        wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
-        ws = _workspace(wsb, dev, so)
-        cf = fact.cfactors()
-        _lib.check(
-            lib.hodlr_solve(C.byref(desc), C.byref(cf), C.c_void_p(x.data_ptr()), n, nrhs,
-                            C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(so.cuda_stream)),
-            "hodlr_solve",
-        )
+        if nrhs == 0:
+            pass
+        elif graph and not torch.cuda.is_current_stream_capturing():
+            graphs = fact.__dict__.setdefault("_solve_graphs", {})
+            key = (nrhs, so.cuda_stream)
+            g = graphs.get(key)
+            if g is None:
+                g = graphs[key] = _SolveGraph(fact, nrhs, so)
+            g.run(x, so)
+        else:
+            desc = fact.desc()
+            wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
+            ws = _workspace(wsb, dev, so)
+            cf = fact.cfactors()
+            _lib.check(
+                lib.hodlr_solve(C.byref(desc), C.byref(cf), C.c_void_p(x.data_ptr()), n, nrhs,
+                                C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(so.cuda_stream)),
+                "hodlr_solve",
+            )
         out = x.t().reshape(bt.shape)
         if bt.device == dev:
             return out
@@ -438,6 +498,64 @@ def solve(fact: HodlrFactorization, b, stream=None):
         host.copy_(out, non_blocking=True)
         so.synchronize()
     return host.numpy() if is_np else host
+
+
+class FactorPlan:
+    """Repeated factorizations of one HodlrMatrix's buffers through a captured
+    CUDA graph (e.g. time stepping, or refactoring after the
+    operator's entries change in place).
+
+    ``FactorPlan(h)`` factors ``h`` once eagerly (``self.factorization`` is
+    valid afterwards) and captures the same launch sequence of
+    ``hodlr_factorize`` on the same buffers.  Refill ``h``'s D / U / V in place
+    (``load``) and call ``refactor()``: the graph replays every level's
+    kernels with no host enqueue between them; results are bit-identical to
+    ``factorize``.  The plan owns its workspace."""
+
+    def __init__(self, h: HodlrMatrix, check: bool = True, stream=None):
+        torch = _torch()
+        lib = _lib.load()
+        dev = h.D.device
+        self.h = h
+        so = stream or torch.cuda.current_stream(dev)
+        desc = h.desc()
+        wsb = lib.hodlr_factorize_workspace(C.byref(desc))
+        with torch.cuda.device(dev), torch.cuda.stream(so):
+            self.ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+            self.pristine = None
+            f = _alloc_factorization(h)
+        self.factorization = f
+        cf = f.cfactors()
+        self._keep = (desc, cf)
+        self._args = (C.byref(desc), C.byref(cf), C.c_void_p(self.ws.data_ptr()), wsb)
+        _lib.check(lib.hodlr_factorize(*self._args, C.c_void_p(so.cuda_stream)), "hodlr_factorize")
+        if check:
+            _raise_if_singular(f)
+        # capture on a side stream over the SAME buffers (their contents are
+        # overwritten during capture only symbolically: nothing executes)
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(so)
+        with torch.cuda.graph(self.graph, stream=side):
+            _lib.check(lib.hodlr_factorize(*self._args, C.c_void_p(side.cuda_stream)), "hodlr_factorize (capture)")
+        so.wait_stream(side)
+        f.__dict__.pop("_solve_graphs", None)
+
+    def load(self, D=None, U=None, V=None) -> None:
+        """Copy new operator entries (same layout / sizes) into the plan's buffers."""
+        for dst, src in ((self.h.D, D), (self.h.U, U), (self.h.V, V)):
+            if src is not None:
+                dst.copy_(_torch().as_tensor(src).reshape(-1), non_blocking=True)
+
+    def refactor(self, check: bool = True, stream=None) -> HodlrFactorization:
+        """Replay the captured factorization on the current contents of h."""
+        torch = _torch()
+        so = stream or torch.cuda.current_stream(self.h.D.device)
+        with torch.cuda.stream(so):
+            self.graph.replay()
+        if check:
+            _raise_if_singular(self.factorization)
+        return self.factorization
 
 
 def logdet(fact: HodlrFactorization):

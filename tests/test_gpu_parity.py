@@ -254,3 +254,45 @@ def test_factorize_from_host_equals_device_path():
         assert torch.equal(getattr(f1, name), getattr(f2, name)), name
     b = np.random.default_rng(3).standard_normal(n)
     assert np.array_equal(hb.solve(f1, b), hb.solve(f2, b))
+
+
+@pytest.mark.parametrize("nrhs", [1, 3, 20])
+def test_solve_graph_replay_bitwise_equals_eager(nrhs):
+    # the CUDA-graph solve (captured once per (nrhs, stream), replayed) == the eager launches
+    n, m, r = 1 << 13, 64, 32
+    f = hb.factorize(hb.random_hodlr(n, m, r, seed=31, s=4.0))
+    g = torch.Generator("cuda").manual_seed(7)
+    for _ in range(3):  # first call captures, later calls replay with new right-hand sides
+        B = torch.randn(n, nrhs, dtype=torch.float64, device="cuda", generator=g)
+        keep = B.clone()
+        xg = hb.solve(f, B, graph=True)
+        xe = hb.solve(f, B, graph=False)
+        assert torch.equal(xg, xe)
+        assert torch.equal(B, keep)
+
+
+def test_factor_plan_refactor_bitwise_equals_factorize():
+    # FactorPlan: eager factorization + captured graph; refactor() after loading new entries
+    n, m, r = 1 << 13, 64, 32
+    h1 = hb.random_hodlr(n, m, r, seed=41, s=16.0)
+    h2 = hb.random_hodlr(n, m, r, seed=42, s=16.0)
+    plan = hb.FactorPlan(h1.clone())
+    for h in (h1, h2, h1):
+        plan.load(h.D, h.U, h.V)
+        fp = plan.refactor()
+        fr = hb.factorize(h.clone())
+        for name in ("D", "Y", "K", "kswaps", "dperm", "Dinv", "Kinv"):
+            assert torch.equal(getattr(fp, name), getattr(fr, name)), name
+        b = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
+        assert torch.equal(hb.solve(fp, b), hb.solve(fr, b))
+
+
+def test_factor_plan_raises_on_singular_refactor():
+    n, m, r = 1 << 10, 32, 8
+    h = hb.random_hodlr(n, m, r, seed=5)
+    plan = hb.FactorPlan(h.clone())
+    D = h.D.clone()
+    D[5 * m * m : 6 * m * m] = 0.0
+    plan.load(D, h.U, h.V)
+    with pytest.raises(hb.HodlrSingularError, match=r"leaf block at level 5, node\(s\) \[5\]"):
+        plan.refactor()

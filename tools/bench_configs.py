@@ -26,24 +26,41 @@ def solve_bytes(n, m, r, es, nrhs):
     return es * (m * n + 2 * n * r * L + 4 * r * r * ((1 << L) - 1)) + 2 * n * nrhs * es
 
 
-def time_factor_solve(n, m, r, dtype, reps=5, nrhs=1, h0=None):
+def time_factor_solve(n, m, r, dtype, reps=5, nrhs=1, h0=None, graph=True):
+    """(t_factor, t_solve, relres, eager) medians; graph=True times the captured
+    launch sequences (hb.FactorPlan.refactor + hb.solve(graph=True)) and also
+    returns the eager times for comparison."""
     if h0 is None:
         h0 = hb.random_hodlr(n, m, r, seed=0, s=1.0, dtype=dtype)
     b = torch.randn(n, nrhs, dtype=dtype, device="cuda").squeeze(1) if nrhs == 1 else torch.randn(n, nrhs, dtype=dtype, device="cuda")
-    tf, ts = [], []
-    for it in range(reps + 2):
-        h = h0.clone()
-        torch.cuda.synchronize()
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        e[0].record(); f = hb.factorize(h, check=False); e[1].record(); x = hb.solve(f, b); e[2].record()
-        torch.cuda.synchronize()
-        if it >= 2:
-            tf.append(e[0].elapsed_time(e[1])); ts.append(e[1].elapsed_time(e[2]))
-        del f
+
+    def run(use_graph):
+        tf, ts = [], []
+        plan = hb.FactorPlan(h0.clone(), check=False) if use_graph else None
+        for it in range(reps + 2):
+            if use_graph:
+                plan.load(h0.D, h0.U)
+            else:
+                h = h0.clone()
+            torch.cuda.synchronize()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record()
+            f = plan.refactor(check=False) if use_graph else hb.factorize(h, check=False)
+            e[1].record(); x = hb.solve(f, b, graph=use_graph); e[2].record()
+            torch.cuda.synchronize()
+            if it >= 2:
+                tf.append(e[0].elapsed_time(e[1])); ts.append(e[1].elapsed_time(e[2]))
+        return statistics.median(tf), statistics.median(ts), x
+
+    tf_e, ts_e, x = run(False)
+    eager = {"t_factor_ms": round(tf_e, 3), "t_solve_ms": round(ts_e, 3)}
+    if graph:
+        tf, ts, x = run(True)
+    else:
+        tf, ts = tf_e, ts_e
     res = float(torch.linalg.norm(h0.matvec(x) - b) / torch.linalg.norm(b))
-    del h0, h
     torch.cuda.empty_cache()
-    return statistics.median(tf), statistics.median(ts), res
+    return tf, ts, res, eager
 
 
 def line(cfg, n, m, r, dtype_name, tf, ts, res, extra=None):
@@ -61,9 +78,9 @@ which = sys.argv[1:] or ["cfg1", "cfg3", "cfg4", "cfg5"]
 if "cfg1" in which:
     # the cfg1 operator: Gaussian kernel (h = 0.1, lambda = 1) on 2^14 kd-ordered 2-D points, assembled on the device
     h1 = hb.gaussian_hodlr(1 << 14, 64, 32, dim=2, h=0.1, lam=1.0)
-    tf, ts, res = time_factor_solve(1 << 14, 64, 32, torch.float64, h0=h1)
+    tf, ts, res, eager = time_factor_solve(1 << 14, 64, 32, torch.float64, h0=h1, reps=20)
     # the reference's own CPU path on the same operator (its batched kernels, all host threads)
-    extra = None
+    extra = {"eager": eager, "launch": "CUDA graphs"}
     try:
         import os, time as _t
         import numpy as np
@@ -77,22 +94,22 @@ if "cfg1" in which:
             t1 = _t.perf_counter()
             rd.ref_solve(D, dpiv, U, V, Ks, kp, bb, 1 << 14, 64, 32, 8, rd.executor(thr))
             t2 = _t.perf_counter()
-            extra = {"reference_cpu": {"t_factor_ms": round(1e3 * (t1 - t0), 1), "t_solve_ms": round(1e3 * (t2 - t1), 1),
-                                       "threads": thr}}
+            extra["reference_cpu"] = {"t_factor_ms": round(1e3 * (t1 - t0), 1), "t_solve_ms": round(1e3 * (t2 - t1), 1),
+                                      "threads": thr}
     except Exception as e:  # noqa: BLE001
-        extra = {"reference_cpu": f"unavailable: {e}"}
+        extra["reference_cpu"] = f"unavailable: {e}"
     line("cfg1 (Gaussian kernel, 2^14 2-D points)", 1 << 14, 64, 32, "f64", tf, ts, res, extra)
 if "cfg3" in which:
     # per-GPU share of cfg3 at P = 2: Gaussian kernel on 2^21 kd-ordered 3-D points, rank 64
     h3 = hb.gaussian_hodlr(1 << 21, 64, 64, dim=3, h=0.1, lam=1.0)
-    tf, ts, res = time_factor_solve(1 << 21, 64, 64, torch.float64, reps=3, h0=h3)
+    tf, ts, res, eager = time_factor_solve(1 << 21, 64, 64, torch.float64, reps=3, h0=h3, graph=False)
     del h3
     torch.cuda.empty_cache()
     line("cfg3-shape (Gaussian kernel, 2^21 3-D points: per-GPU share of N=2^22 at P=2)", 1 << 21, 64, 64, "f64",
          tf, ts, res)
 if "cfg4" in which:
-    tf, ts, res = time_factor_solve(1 << 21, 64, 8, torch.float32)
-    line("cfg4", 1 << 21, 64, 8, "f32", tf, ts, res)
+    tf, ts, res, eager = time_factor_solve(1 << 21, 64, 8, torch.float32)
+    line("cfg4", 1 << 21, 64, 8, "f32", tf, ts, res, {"eager": eager, "launch": "CUDA graphs"})
 if "cfg4r" in which or "cfg4" in which:
     # cfg4 as a preconditioner: fp32 factorization + fp64-operator refinement
     n, m, r = 1 << 21, 64, 8
@@ -111,7 +128,7 @@ if "cfg4r" in which or "cfg4" in which:
         del f32
     tf = statistics.median(t[0] for t in runs); tr = statistics.median(t[1] for t in runs)
     res = runs[-1][2]
-    tf64, ts64, res64 = time_factor_solve(n, m, r, torch.float64, reps=3)
+    tf64, ts64, res64, _ = time_factor_solve(n, m, r, torch.float64, reps=3, graph=False)
     print(json.dumps({"config": "cfg4 preconditioner: fp32 factor + fp64 refinement", "N": n, "leaf": m, "rank": r,
                       "t_factor_f32_ms": round(tf, 3), "t_refine_ms": round(tr, 3),
                       "iterations": res.iterations, "relres_history": res.history,

@@ -1,4 +1,4 @@
-"""cfg5 multi-RHS solve times for a list of nrhs (dev A/B with HODLR_SOLVE_WIDE)."""
+"""cfg5 multi-RHS solve times for a list of nrhs (dev timing tool)."""
 import os, statistics, sys
 sys.path.insert(0, ".")
 import torch
