@@ -27,11 +27,13 @@ from .hodlr import (  # noqa: F401
     HodlrFactorization,
     HodlrMatrix,
     HodlrSingularError,
+    LevelPanel,
     RefinementResult,
     factorize,
     factorize_from_host,
     flop_report,
     logdet,
+    pad_level_panels,
     random_hodlr,
     solve,
     solve_flops,
@@ -50,5 +52,6 @@ from .construct import (  # noqa: F401
     laplace_dl_hodlr,
 )
 from ._lib import HodlrNativeError, LIB_PATH  # noqa: F401
+from .io import dump, load  # noqa: F401
 
 __version__ = "0.1.0"

@@ -53,6 +53,85 @@ def _dtype_tag(t) -> int:
 
 
 @dataclass
+class LevelPanel:
+    """One level's basis panel in the SPEC's ragged layout:
+    an n x width column-major buffer; node a of the level owns rows I_a and
+    columns [col_offsets[a], col_offsets[a] + node_ranks[a])."""
+
+    level: int
+    data: "object"  # (n, width) array or flat column-major n * width
+    col_offsets: "object"
+    node_ranks: "object"
+
+    @property
+    def uniform(self) -> bool:
+        nr = np.asarray(self.node_ranks)
+        return bool(nr.size == 0 or (nr == nr[0]).all())
+
+
+def _round_rank(r: int) -> int:
+    """The fused kernels' ranks (16 / 32 / 64); other ranks run the generic path."""
+    for q in (16, 32, 64):
+        if r <= q:
+            return q if r > 8 else r
+    return r
+
+
+def _host(x):
+    return np.asarray(x.detach().cpu() if hasattr(x, "detach") else x)
+
+
+def pad_level_panels(n: int, m: int, u_panels, v_panels, rank: int | None = None, round_rank: bool = True):
+    """Ragged LevelPanels (levels 1..L, per-node column offsets and ranks) ->
+    (r, U, V): the uniform slabs of this engine, every node's basis zero-padded
+    to rank r = the largest node rank (``rank`` overrides it; ``round_rank``
+    rounds it up to a fused-kernel rank 16 / 32 / 64).  The padding changes
+    nothing: padded U columns meet zero V columns, and K_p = [[T_a, I], [I,
+    T_b]] stays invertible (its padded part is a permutation), so the oracle
+    run on the same padded layout gives the same pivots."""
+    L = int(round(math.log2(n // m))) if n >= m else 0
+    if n != m << L:
+        raise ValueError(f"GPU layout needs N = m 2^L (got N={n}, m={m})")
+    ups = {int(p.level): p for p in u_panels}
+    vps = {int(p.level): p for p in v_panels}
+    if set(ups) != set(range(1, L + 1)) or set(vps) != set(range(1, L + 1)):
+        raise ValueError(f"need one u and one v panel per level 1..{L}")
+    rmax = 0
+    for lv in range(1, L + 1):
+        for p in (ups[lv], vps[lv]):
+            nr = np.asarray(p.node_ranks, dtype=np.int64)
+            if nr.shape != (1 << lv,):
+                raise ValueError(f"level {lv}: node_ranks must have 2^{lv} entries")
+            rmax = max(rmax, int(nr.max(initial=0)))
+        # A(I_a, I_b) = U_a V_b^*: node a's U columns pair with its sibling's V columns
+        if not np.array_equal(np.asarray(ups[lv].node_ranks).reshape(-1, 2),
+                              np.asarray(vps[lv].node_ranks).reshape(-1, 2)[:, ::-1]):
+            raise ValueError(f"level {lv}: U_a and V_b of a sibling pair need equal column counts")
+    r = rank if rank is not None else (_round_rank(rmax) if round_rank else rmax)
+    if r < rmax:
+        raise ValueError(f"rank {r} < the largest node rank {rmax}")
+    dt = _host(ups[1].data).dtype if L else np.float64
+    U = np.zeros((L, r, n), dtype=dt)  # level-major; level l is an n x r column-major panel
+    V = np.zeros((L, r, n), dtype=dt)
+    for lv in range(1, L + 1):
+        nl = n >> lv
+        for dst, p in ((U, ups[lv]), (V, vps[lv])):
+            a = _host(p.data).reshape(-1)
+            width = a.size // n if n else 0
+            if a.size != n * width:
+                raise ValueError(f"level {lv}: panel has {a.size} entries, not a multiple of n = {n}")
+            cols = a.reshape(width, n)  # column-major: column j at j n
+            off = np.asarray(p.col_offsets, dtype=np.int64)
+            nr = np.asarray(p.node_ranks, dtype=np.int64)
+            for node in range(1 << lv):
+                k, c0 = int(nr[node]), int(off[node])
+                if c0 < 0 or c0 + k > width:
+                    raise ValueError(f"level {lv} node {node}: columns [{c0}, {c0 + k}) outside the panel")
+                dst[lv - 1, :k, node * nl : (node + 1) * nl] = cols[c0 : c0 + k, node * nl : (node + 1) * nl]
+    return r, U.reshape(-1), V.reshape(-1)
+
+
+@dataclass
 class HodlrMatrix:
     """Uniform-rank HODLR matrix in the concatenated big-matrix layout."""
 
@@ -97,6 +176,15 @@ class HodlrMatrix:
             return t.contiguous()
 
         return cls(tree, r, dev(D, (1 << L) * m * m, "D"), dev(U, n * r * L, "U"), dev(V, n * r * L, "V"))
+
+    @classmethod
+    def from_level_panels(cls, n: int, m: int, d_big, u_panels, v_panels, rank: int | None = None,
+                          round_rank: bool = True, device="cuda") -> "HodlrMatrix":
+        """Ingest the SPEC's ragged representation (SPEC.md:147-160, 208-211);
+        see :func:`pad_level_panels`."""
+        r, U, V = pad_level_panels(n, m, u_panels, v_panels, rank, round_rank)
+        D = np.asarray(d_big.cpu() if hasattr(d_big, "cpu") else d_big)
+        return cls.from_buffers(n, m, r, D, U.astype(D.dtype, copy=False), V.astype(D.dtype, copy=False), device=device)
 
     def clone(self) -> "HodlrMatrix":
         return HodlrMatrix(self.tree, self.rank, self.D.clone(), self.U.clone(), self.V.clone())

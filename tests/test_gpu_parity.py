@@ -296,3 +296,25 @@ def test_factor_plan_raises_on_singular_refactor():
     plan.load(D, h.U, h.V)
     with pytest.raises(hb.HodlrSingularError, match=r"leaf block at level 5, node\(s\) \[5\]"):
         plan.refactor()
+
+
+def test_ragged_level_panels_vs_oracle_on_the_padded_layout():
+    # SPEC.md:147-160 ragged panels (per-node ranks 0..24, scattered column offsets) ingested by
+    # HodlrMatrix.from_level_panels (zero-pad to rank 32, the fused-kernel rank): K pivots bit-exact
+    # vs the oracle on the same padded layout, x within 1e-10, and the ragged dense matrix solved
+    from tests.test_ragged_cpu import ragged
+
+    n, m, L = 1 << 12, 64, 6
+    D, ups, vps, A = ragged(n, m, L, seed=5, width=32, kmax=24)
+    h = hb.HodlrMatrix.from_level_panels(n, m, D, ups, vps)
+    assert h.rank == 32
+    r, U, V = hb.pad_level_panels(n, m, ups, vps)
+    fo = orc.factorize(orc.HodlrData(orc.Layout(n, m, r), D.copy(), U, V))
+    f = hb.factorize(h)
+    assert np.array_equal(f.kswaps.cpu().numpy().reshape(-1, 2 * r), np.concatenate([p.swaps for p in fo.kpiv]))
+    b = np.random.default_rng(2).standard_normal(n)
+    x = hb.solve(f, b)
+    ex = rel(x, orc.solve(fo, b.reshape(-1, 1))[:, 0])
+    record_parity("ragged/n4096_m64_kmax24_pad32", x=ex, gate_x=TOL)
+    assert ex <= TOL
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) < 1e-12
