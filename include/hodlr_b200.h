@@ -198,6 +198,12 @@ hodlr_status hodlr_build_gaussian(const hodlr_desc* d, const double* pts, int di
                                   void* U, void* V, void* work, size_t work_bytes, void* stream);
 hodlr_status hodlr_build_dense(const hodlr_desc* d, const double* A, int64_t lda, void* D, void* U, void* V,
                                void* work, size_t work_bytes, void* stream);
+/* Schur-complement surrogate of BASELINE cfg4 (no reference counterpart): the
+ * hypersingular kernel -1 / (pi r^3) of a planar separator's half-space
+ * Dirichlet-to-Neumann map on 2-D grid points pts (dim-major, cluster order),
+ * diagonal 2.8755 (lattice row sum) + sigma. */
+hodlr_status hodlr_build_schur_plane(const hodlr_desc* d, const double* pts, double sigma, void* D, void* U,
+                                     void* V, void* work, size_t work_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * Row-sharded (multi-GPU) schedule, SURVEY.md §8e.  The caller holds the rows

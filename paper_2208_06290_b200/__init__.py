@@ -50,8 +50,11 @@ from .construct import (  # noqa: F401
     kd_points,
     laplace_dl_geometry,
     laplace_dl_hodlr,
+    schur_surrogate_hodlr,
+    separator_grid,
 )
 from ._lib import HodlrNativeError, LIB_PATH  # noqa: F401
 from .io import dump, load  # noqa: F401
+from .krylov import GmresResult, gmres, gmres_hodlr  # noqa: F401
 
 __version__ = "0.1.0"

@@ -76,6 +76,7 @@ SIGNATURES = {
     "hodlr_build_laplace_dl": (_i, [C.POINTER(Desc), _p, _p, _p, _p, _p, _sz, _p]),
     "hodlr_build_dense": (_i, [C.POINTER(Desc), _p, _i64, _p, _p, _p, _p, _sz, _p]),
     "hodlr_build_gaussian": (_i, [C.POINTER(Desc), _p, _i, _d, _d, _p, _p, _p, _p, _sz, _p]),
+    "hodlr_build_schur_plane": (_i, [C.POINTER(Desc), _p, _d, _p, _p, _p, _p, _sz, _p]),
 }
 
 _lib = None

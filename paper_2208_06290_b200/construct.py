@@ -107,6 +107,13 @@ def kd_points(n: int, dim: int, L: int, seed: int = 0, device=None) -> np.ndarra
         pts = xorshift_uniform_device(n * dim, seed, device).cpu().numpy().reshape(n, dim)
     else:
         pts = xorshift_uniform(n * dim, seed).reshape(n, dim)
+    return kd_order(pts, L)
+
+
+def kd_order(pts: np.ndarray, L: int) -> np.ndarray:
+    """(n, dim) points -> (dim, n) in cluster order: the level-l node range is
+    sorted (stably) along axis l mod dim and split at ceil(len / 2)."""
+    n, dim = pts.shape
     order = np.arange(n)
     starts = np.array([0])
     lens = np.array([n])
@@ -179,6 +186,42 @@ def gaussian_hodlr(n: int, m: int, r: int, dim: int = 2, h: float = 0.1, lam: fl
     _lib.check(lib.hodlr_build_gaussian(C.byref(desc), C.c_void_p(pts.data_ptr()), dim, float(h), float(lam),
                                         C.c_void_p(D.data_ptr()), C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()),
                                         C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(st)), "hodlr_build_gaussian")
+    return _finish(n, m, r, L, D, U, V)
+
+
+def separator_grid(n: int, L: int) -> np.ndarray:
+    """(2, n) unit-spaced points of an nx x ny separator plane (nx = 2^ceil(b/2),
+    ny = 2^floor(b/2) for n = 2^b), in cluster (kd) order."""
+    b = int(round(math.log2(n)))
+    if n != 1 << b:
+        raise ValueError("separator grid: n must be a power of two")
+    nx, ny = 1 << ((b + 1) // 2), 1 << (b // 2)
+    gx, gy = np.meshgrid(np.arange(nx, dtype=np.float64), np.arange(ny, dtype=np.float64), indexing="ij")
+    return kd_order(np.stack([gx.ravel(), gy.ravel()], axis=1), L)
+
+
+def schur_surrogate_hodlr(n: int, m: int, r: int, sigma: float = 0.1, device="cuda", stream=None,
+                          points=None) -> HodlrMatrix:
+    """BASELINE cfg4's operator: the Schur-complement surrogate of a sparse
+    (3-D 7-point Laplacian) factorization on a planar separator -- the
+    hypersingular DtN kernel -1 / (pi r^3) on an n-point separator grid,
+    diagonal 2.8755 + sigma (``hodlr_build_schur_plane``) -- assembled on
+    the device at uniform rank ``r`` (ACA rook, tol = 0)."""
+    torch = _torch()
+    lib = _lib.load()
+    L, D, U, V = _alloc(n, m, r, device)
+    P = separator_grid(n, L) if points is None else np.ascontiguousarray(points, dtype=np.float64)
+    if P.shape != (2, n):
+        raise ValueError(f"points must be (2, {n})")
+    pts = torch.from_numpy(P).to(device)
+    desc = _lib.Desc(n, m, r, L, 0)
+    wsb = lib.hodlr_build_workspace(C.byref(desc))
+    so = stream or torch.cuda.current_stream(pts.device)
+    ws = _workspace(wsb, pts.device, so)
+    _lib.check(lib.hodlr_build_schur_plane(C.byref(desc), C.c_void_p(pts.data_ptr()), float(sigma),
+                                           C.c_void_p(D.data_ptr()), C.c_void_p(U.data_ptr()), C.c_void_p(V.data_ptr()),
+                                           C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(so.cuda_stream)),
+               "hodlr_build_schur_plane")
     return _finish(n, m, r, L, D, U, V)
 
 

@@ -71,6 +71,29 @@ struct GaussianPts {
   }
 };
 
+// Sparse-factorization Schur-complement surrogate (BASELINE cfg4; no reference
+// counterpart -- the reference has no sparse solver): eliminating
+// the two subdomains of a 3-D 7-point Laplacian onto a planar separator leaves
+// (asymptotically) twice the half-space Dirichlet-to-Neumann map, the
+// hypersingular kernel S_ij = -1 / (pi r_ij^3) on the separator grid (unit
+// spacing, dim-major 2-D coordinates), with diagonal c_0 + sigma: c_0 =
+// (1/pi) sum_{k in Z^2 \ 0} |k|^-3 = 2.8755 is the lattice row sum (rows are
+// diagonally dominant, the matrix SPD) and sigma the zeroth-order term the
+// eliminated subdomains contribute.  Off-diagonal blocks of a kd-ordered
+// plane are numerically low-rank, with ranks growing toward the top levels --
+// the regime where a rank-8 HODLR is a low-accuracy preconditioner.
+struct SchurPlane {
+  const double* p;
+  int64_t n;
+  double diag;
+  __device__ __forceinline__ double operator()(int64_t i, int64_t j) const {
+    if (i == j) return diag;
+    const double dx = __dsub_rn(p[i], p[j]), dy = __dsub_rn(p[n + i], p[n + j]);
+    const double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+    return -1.0 / (3.141592653589793 * r2 * sqrt(r2));
+  }
+};
+
 // Entries of a dense column-major matrix on the device (tests, small n).
 struct DenseOracle {
   const double* A;
@@ -575,6 +598,15 @@ extern "C" hodlr_status hodlr_build_gaussian(const hodlr_desc* d, const double* 
     return HODLR_ERR_ARG;
   if (d->L > 0 && d->r > 0 && (!U || !V)) return HODLR_ERR_ARG;
   GaussianPts A{pts, d->n, dim, h * h, lambda};
+  return build_run(d, A, (double*)D, (double*)U, (double*)V, static_cast<char*>(work), static_cast<cudaStream_t>(stream));
+}
+
+extern "C" hodlr_status hodlr_build_schur_plane(const hodlr_desc* d, const double* pts, double sigma, void* D,
+                                                 void* U, void* V, void* work, size_t work_bytes, void* stream) {
+  if (!build_desc_ok(d) || !pts || !(sigma >= 0.0) || !D || !work || work_bytes < build_ws(d).total)
+    return HODLR_ERR_ARG;
+  if (d->L > 0 && d->r > 0 && (!U || !V)) return HODLR_ERR_ARG;
+  SchurPlane A{pts, d->n, 2.8754826265883277 + sigma};
   return build_run(d, A, (double*)D, (double*)U, (double*)V, static_cast<char*>(work), static_cast<cudaStream_t>(stream));
 }
 

@@ -14,6 +14,8 @@
 // and written once per level, and V^T C never re-reads C from HBM.  Segments
 // shorter than the node write partial sums that a fixed-order reduction kernel
 // adds (deterministic).
+#include <cuda.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -472,10 +474,242 @@ __global__ void __launch_bounds__(256, 2) level_update4_kernel(LevelArgs g) {
 #ifndef LEVEL4_LATE
 #define LEVEL4_LATE 1
 #endif
+constexpr bool LEVEL4_LATE_DEFAULT = LEVEL4_LATE;
+// ---------------------------------------------------------------------------
+// TMA-fed variant of level_update4_kernel (factorization mode): the A1 / V
+// panels of each 64-row chunk arrive by two 2-D tensor copies
+// (cp.async.bulk.tensor, box = (CH + 2) rows x R ranks, so the boxes land with
+// the conflict-free pitch P = CH + 2 of the cp.async layout -- the 2 extra rows
+// are read, or zero-filled past the slab end, into the padding) issued by one
+// thread into a 3-stage ring; completion is an mbarrier transaction count
+// ("full"), and stage reuse is an 8-warp arrival barrier ("empty"), so warps
+// never wait on each other at a __syncthreads: a warp waits only for its
+// chunk's bytes, and the issuing thread only for the warps still reading the
+// stage it refills.  Arithmetic and per-column operation order are those of
+// level_update4_kernel (bit-identical results).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int R, int GPW, bool LATE>
+__global__ void __launch_bounds__(256, 2)
+    level_update5_kernel(LevelArgs g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV) {
+  using Cfg = Level4Cfg<R, false>;
+  constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8, NI = Cfg::NI, NS = 3;
+  constexpr uint32_t PANEL_BYTES = (uint32_t)Cfg::PANEL * sizeof(double);  // = box bytes (P x R)
+  extern __shared__ __align__(1024) double sm5[];  // TMA destinations: 128-byte aligned stages
+  double* sm = sm5;
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int seg = blockIdx.x / g.ncg, cg = blockIdx.x % g.ncg;
+  const int64_t seg0 = (int64_t)seg * g.seg_rows;
+  const int nch = g.seg_rows / CH;
+  const int G = g.ncols >> 3;
+  const int gb = cg * g.tpc, ge = min(G, gb + g.tpc);
+
+  if (t == 0) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int ch) {
+    const int st = ch % NS;
+    double* As = sm + st * Cfg::STAGE;
+    mbar_expect_tx(&full[st], 2 * PANEL_BYTES);
+    const int row = (int)(seg0 + (int64_t)ch * CH);
+    tma_load_2d(As, &tmA, row, 0, &full[st]);
+    tma_load_2d(As + Cfg::PANEL, &tmV, row, 0, &full[st]);
+  };
+  if (t == 0)
+    for (int c = 0; c < NS - 1 && c < nch; ++c) issue(c);
+
+  double tw[GPW][RT][2];
+#pragma unroll
+  for (int q = 0; q < GPW; ++q)
+#pragma unroll
+    for (int jr = 0; jr < RT; ++jr) tw[q][jr][0] = tw[q][jr][1] = 0.0;
+
+  for (int ch = 0; ch < nch; ++ch) {
+    const int s = ch % NS;
+    mbar_wait(&full[s], (uint32_t)((ch / NS) & 1));
+    const double* As = sm + s * Cfg::STAGE;
+    const double* Vs = As + Cfg::PANEL;
+    const int64_t row0 = seg0 + (int64_t)ch * CH;
+    const int c = (int)(row0 / g.n_c);
+    const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
+#pragma unroll
+    for (int q = 0; q < GPW; ++q) {
+      const int grp = gb + warp + 8 * q;
+      if (grp < ge) {
+        const int col = grp * 8 + ar;
+        double* cptr = g.C + row0 + (int64_t)col * g.ldc + 4 * ac;
+        double acc[2 * NI][2], cin[2 * NI][2];
+        if constexpr (LATE) {
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            ldg_v4(cptr + 16 * i, cin[2 * i][0], cin[2 * i + 1][0], cin[2 * i][1], cin[2 * i + 1][1]);
+            acc[2 * i][0] = acc[2 * i][1] = acc[2 * i + 1][0] = acc[2 * i + 1][1] = 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NI; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+        }
+        const double* wc = Wp + (int64_t)col * (2 * R) + 2 * ac;
+#pragma unroll
+        for (int kt = 0; kt < R / 8; ++kt) {
+          const double2 w2 = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const double a = -(u ? w2.y : w2.x);
+            const double* ak = As + (8 * kt + 2 * ac + u) * P + 2 * ar;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+              const double2 b2 = *reinterpret_cast<const double2*>(ak + 16 * i);
+              dmma_8x8x4(acc[2 * i][0], acc[2 * i][1], a, b2.x);
+              dmma_8x8x4(acc[2 * i + 1][0], acc[2 * i + 1][1], a, b2.y);
+            }
+          }
+        }
+        if constexpr (LATE) {
+#pragma unroll
+          for (int i = 0; i < 2 * NI; ++i) acc[i][0] = cin[i][0] + acc[i][0], acc[i][1] = cin[i][1] + acc[i][1];
+        }
+#pragma unroll
+        for (int i = 0; i < NI; ++i) stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int jr = 0; jr < RT; ++jr) {
+              const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
+              dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i][h], v2.x);
+              dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i + 1][h], v2.y);
+            }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // refill: chunk ch + NS - 1 into the stage chunk ch - 1 used (released by all 8 warps)
+    if (t == 0 && ch + NS - 1 < nch) {
+      const int c2 = ch + NS - 1;
+      if (c2 >= NS) mbar_wait(&empty[c2 % NS], (uint32_t)((c2 / NS - 1) & 1));
+      issue(c2);
+    }
+  }
+  const int64_t qn = seg0 / g.node_rows;
+  double* out;
+  int64_t ld;
+  if (g.partial) {
+    out = g.TW + (int64_t)seg * R * g.ncols;
+    ld = R;
+  } else {
+    out = g.TW + (qn >> 1) * g.tw_stride + (qn & 1) * R;
+    ld = 2 * R;
+  }
+#pragma unroll
+  for (int q = 0; q < GPW; ++q) {
+    const int grp = gb + warp + 8 * q;
+    if (grp < ge) {
+      const int col = grp * 8 + ar;
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr)
+        *reinterpret_cast<double2*>(out + 8 * jr + 2 * ac + (int64_t)col * ld) = make_double2(tw[q][jr][0], tw[q][jr][1]);
+    }
+  }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// panel = rows [0, rows) x R columns of a column-major slab (ld lda); box = (CH + 2) x R
+template <int R>
+static bool panel_map(CUtensorMap* m, const double* base, int64_t rows, int64_t lda) {
+  using Cfg = Level4Cfg<R, false>;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) || ((lda * 8) & 15)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)R};
+  const cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)Cfg::P, (cuuint32_t)R};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int R, int GPW>
+static hodlr_status launch_level5(const LevelArgs& g, int64_t nseg, int64_t rows, cudaStream_t st) {
+  using Cfg = Level4Cfg<R, false>;
+  constexpr bool LATE = GPW <= 2 && LEVEL4_LATE_DEFAULT;
+  constexpr size_t smem = (size_t)3 * Cfg::STAGE * sizeof(double);
+  CUtensorMap ta, tv;
+  if (!panel_map<R>(&ta, g.A1, rows, g.lda) || !panel_map<R>(&tv, g.V, rows, g.lda)) return HODLR_ERR_ARG;
+  smem_attr(level_update5_kernel<R, GPW, LATE>, (int)smem);
+  level_update5_kernel<R, GPW, LATE><<<(unsigned)(nseg * g.ncg), 256, smem, st>>>(g, ta, tv);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+template <int R>
+static hodlr_status run_level5(const LevelArgs& g, int64_t nseg, int64_t rows, cudaStream_t st) {
+  const int gpw = (g.tpc + 7) / 8;
+  if (gpw <= 1) return launch_level5<R, 1>(g, nseg, rows, st);
+  if (gpw <= 2) return launch_level5<R, 2>(g, nseg, rows, st);
+  if constexpr (R <= 32) {
+    if (gpw <= 4) return launch_level5<R, 4>(g, nseg, rows, st);
+  }
+  if constexpr (R <= 16) {
+    if (gpw <= 7) return launch_level5<R, 7>(g, nseg, rows, st);
+  }
+  return HODLR_ERR_ARG;
+}
+
 template <int R, int GPW>
 static hodlr_status launch_level4(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
   using Cfg = Level4Cfg<R>;
-  constexpr bool LATE = GPW <= 2 && LEVEL4_LATE;
+  constexpr bool LATE = GPW <= 2 && LEVEL4_LATE_DEFAULT;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(level_update4_kernel<R, GPW, LATE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -747,6 +981,12 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   return HODLR_OK;
 }
 
+// factorization level step fed by TMA (level_update5_kernel) or by cp.async (level_update4_kernel)
+#ifndef HODLR_LEVEL_TMA
+#define HODLR_LEVEL_TMA 1
+#endif
+constexpr bool kLevelTma = HODLR_LEVEL_TMA;
+
 // column groups of 8 per level-kernel CTA: the [W|T] partials live in registers
 static int level4_maxg(int r) { return r <= 16 ? 56 : r <= 32 ? 32 : 16; }
 
@@ -822,9 +1062,9 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   const bool small = ncols <= 8;
   hodlr_status s;
   switch (r) {
-    case 16: s = small ? run_level<16, 8>(g, nseg, st) : v4 ? run_level4<16>(g, nseg, st) : run_level<16, 64>(g, nseg, st); break;
-    case 32: s = small ? run_level<32, 8>(g, nseg, st) : v4 ? run_level4<32>(g, nseg, st) : run_level<32, 64>(g, nseg, st); break;
-    case 64: if (!v4) return HODLR_ERR_ARG; s = run_level4<64>(g, nseg, st); break;
+    case 16: s = small ? run_level<16, 8>(g, nseg, st) : v4 ? (kLevelTma ? run_level5<16>(g, nseg, n, st) : run_level4<16>(g, nseg, st)) : run_level<16, 64>(g, nseg, st); break;
+    case 32: s = small ? run_level<32, 8>(g, nseg, st) : v4 ? (kLevelTma ? run_level5<32>(g, nseg, n, st) : run_level4<32>(g, nseg, st)) : run_level<32, 64>(g, nseg, st); break;
+    case 64: if (!v4) return HODLR_ERR_ARG; s = kLevelTma ? run_level5<64>(g, nseg, n, st) : run_level4<64>(g, nseg, st); break;
     default: return HODLR_ERR_ARG;  // r = 64: generic path (fused tiles exceed shared memory)
   }
   if (s != HODLR_OK || !split) return s;

@@ -496,6 +496,24 @@ def _raise_if_singular(f: HodlrFactorization) -> None:
             raise HodlrSingularError("K", lv, np.flatnonzero(seg).tolist())
 
 
+def _capture(launch, stream, dev):
+    """CUDA graph of ``launch(cuda_stream)`` captured on a side stream ordered
+    after ``stream`` (thread-local capture mode: other threads' CUDA calls are
+    unaffected)."""
+    torch = _torch()
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        g.capture_begin(capture_error_mode="thread_local")
+        try:
+            launch(side.cuda_stream)
+        finally:
+            g.capture_end()
+    stream.wait_stream(side)
+    return g
+
+
 class _SolveGraph:
     """One captured ``hodlr_solve`` (CUDA graph) of a factorization for a fixed
     nrhs on one stream: its own X buffer and workspace (the graph bakes their
@@ -515,15 +533,10 @@ class _SolveGraph:
         self._args = (C.byref(desc), C.byref(cf), C.c_void_p(self.X.data_ptr()), n, nrhs,
                       C.c_void_p(self.ws.data_ptr()), wsb)
         self._keep = (desc, cf)
-        # one eager launch first: kernel attributes / lazy module loading happen
-        # outside the capture
-        _lib.check(lib.hodlr_solve(*self._args, C.c_void_p(stream.cuda_stream)), "hodlr_solve")
-        self.graph = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(device=dev)
-        side.wait_stream(stream)
-        with torch.cuda.graph(self.graph, stream=side):
-            _lib.check(lib.hodlr_solve(*self._args, C.c_void_p(side.cuda_stream)), "hodlr_solve (capture)")
-        stream.wait_stream(side)
+        # kernel attributes / lazy module loading happened in the caller's eager
+        # first call; capture directly (no torch.cuda.graph gc / cache flush)
+        self.graph = _capture(lambda st: _lib.check(lib.hodlr_solve(*self._args, C.c_void_p(st)),
+                                                    "hodlr_solve (capture)"), stream, dev)
 
     def run(self, x_cm, stream):
         """x_cm: (nrhs, N) contiguous on the device; overwritten with the solution."""
@@ -534,14 +547,25 @@ class _SolveGraph:
             x_cm.copy_(self.X)
 
 
-def solve(fact: HodlrFactorization, b, stream=None, graph: bool = True):
+def _solve_eager(lib, fact, x, nrhs, dev, so):
+    desc = fact.desc()
+    wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
+    ws = _workspace(wsb, dev, so)
+    cf = fact.cfactors()
+    _lib.check(lib.hodlr_solve(C.byref(desc), C.byref(cf), C.c_void_p(x.data_ptr()), fact.n, nrhs,
+                               C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(so.cuda_stream)), "hodlr_solve")
+
+
+def solve(fact: HodlrFactorization, b, stream=None, graph: bool | None = None):
     """x = A^-1 b (PAPER Alg. 4).  ``b``: (N,) or (N, k), torch (device or host)
     or numpy; the result has the same kind/shape and ``b`` is not modified.
 
-    graph=True (default): the level-by-level launch sequence of ``hodlr_solve``
-    is captured once per (nrhs, stream) as a CUDA graph and replayed (no host
-    enqueue gaps between the ~4 L small launches); graph=False launches it
-    eagerly.  Both run the same kernels on the same data, bit for bit."""
+    The level-by-level launch sequence of ``hodlr_solve`` (~4 L small
+    launches) can run as a CUDA graph captured per (factorization, nrhs,
+    stream): graph=None (default) launches the first solve of a key eagerly and
+    captures from the second on (repeated solves replay, one-shot solves pay no
+    capture); graph=True captures at once; graph=False always launches
+    eagerly.  All run the same kernels on the same data, bit for bit."""
     torch = _torch()
     lib = _lib.load()
     is_np = isinstance(b, np.ndarray)
@@ -559,25 +583,19 @@ def solve(fact: HodlrFactorization, b, stream=None, graph: bool = True):
         x = bd.reshape(n, nrhs).t().to(dtype=fact.D.dtype).contiguous()
         if x.data_ptr() == bt.data_ptr():
             x = x.clone()
-        if nrhs == 0:
-            pass
-        elif graph and not torch.cuda.is_current_stream_capturing():
-            graphs = fact.__dict__.setdefault("_solve_graphs", {})
+        if nrhs > 0:
             key = (nrhs, so.cuda_stream)
-            g = graphs.get(key)
-            if g is None:
-                g = graphs[key] = _SolveGraph(fact, nrhs, so)
-            g.run(x, so)
-        else:
-            desc = fact.desc()
-            wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
-            ws = _workspace(wsb, dev, so)
-            cf = fact.cfactors()
-            _lib.check(
-                lib.hodlr_solve(C.byref(desc), C.byref(cf), C.c_void_p(x.data_ptr()), n, nrhs,
-                                C.c_void_p(ws.data_ptr()), wsb, C.c_void_p(so.cuda_stream)),
-                "hodlr_solve",
-            )
+            graphs = fact.__dict__.setdefault("_solve_graphs", {})
+            g = graphs.get(key) if graph is not False else None
+            if g is not None and not torch.cuda.is_current_stream_capturing():
+                g.run(x, so)
+            else:
+                _solve_eager(lib, fact, x, nrhs, dev, so)
+                if graph is not False and not torch.cuda.is_current_stream_capturing():
+                    calls = fact.__dict__.setdefault("_solve_calls", {})
+                    calls[key] = calls.get(key, 0) + 1
+                    if graph or calls[key] >= 2:  # capture after the eager call(s): later calls replay
+                        graphs[key] = _SolveGraph(fact, nrhs, so)
         out = x.t().reshape(bt.shape)
         if bt.device == dev:
             return out
@@ -610,7 +628,6 @@ class FactorPlan:
         wsb = lib.hodlr_factorize_workspace(C.byref(desc))
         with torch.cuda.device(dev), torch.cuda.stream(so):
             self.ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
-            self.pristine = None
             f = _alloc_factorization(h)
         self.factorization = f
         cf = f.cfactors()
@@ -619,15 +636,9 @@ class FactorPlan:
         _lib.check(lib.hodlr_factorize(*self._args, C.c_void_p(so.cuda_stream)), "hodlr_factorize")
         if check:
             _raise_if_singular(f)
-        # capture on a side stream over the SAME buffers (their contents are
-        # overwritten during capture only symbolically: nothing executes)
-        self.graph = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(device=dev)
-        side.wait_stream(so)
-        with torch.cuda.graph(self.graph, stream=side):
-            _lib.check(lib.hodlr_factorize(*self._args, C.c_void_p(side.cuda_stream)), "hodlr_factorize (capture)")
-        so.wait_stream(side)
-        f.__dict__.pop("_solve_graphs", None)
+        # capture over the SAME buffers (nothing executes during capture)
+        self.graph = _capture(lambda st: _lib.check(lib.hodlr_factorize(*self._args, C.c_void_p(st)),
+                                                    "hodlr_factorize (capture)"), so, dev)
 
     def load(self, D=None, U=None, V=None) -> None:
         """Copy new operator entries (same layout / sizes) into the plan's buffers."""

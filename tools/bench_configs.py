@@ -136,6 +136,41 @@ if "cfg4r" in which or "cfg4" in which:
           flush=True)
     del h64, h32
     torch.cuda.empty_cache()
+if "cfg4g" in which or "cfg4" in which:
+    # BASELINE cfg4 as specified: rank-8 fp32 HODLR preconditioner for the Schur-complement
+    # surrogate (planar-separator DtN kernel, N = 2^21), inside GMRES, to relres 1e-10
+    import time as _t
+    n, m = 1 << 21, 64
+    torch.cuda.synchronize(); t0 = _t.perf_counter()
+    op = hb.schur_surrogate_hodlr(n, m, 32, sigma=0.1)
+    p8 = hb.schur_surrogate_hodlr(n, m, 8, sigma=0.1)
+    torch.cuda.synchronize(); t_build = _t.perf_counter() - t0
+    h32 = hb.HodlrMatrix(p8.tree, 8, p8.D.float(), p8.U.float(), p8.V.float())
+    del p8
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(0))
+    runs = []
+    for it in range(3):
+        torch.cuda.synchronize()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(); prec = hb.factorize(h32.clone(), check=False); e[1].record()
+        res = hb.gmres_hodlr(op, prec, b, tol=1e-10, restart=30); e[2].record()
+        torch.cuda.synchronize()
+        runs.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), res))
+        del prec
+    tf = statistics.median(t[0] for t in runs); tg = statistics.median(t[1] for t in runs)
+    res = runs[-1][2]
+    # fp64 direct solve of the same rank-32 operator, for comparison
+    tf64, ts64, res64, _ = time_factor_solve(n, m, 32, torch.float64, reps=3, h0=op, graph=False)
+    print(json.dumps({"config": "cfg4: GMRES on the Schur-complement surrogate (planar-separator DtN kernel, fp64 "
+                                "rank-32 HODLR operator) preconditioned by a rank-8 fp32 HODLR factorization",
+                      "N": n, "leaf": m, "rank_prec": 8, "rank_op": 32, "build_s": round(t_build, 2),
+                      "t_prec_factor_ms": round(tf, 3), "t_gmres_ms": round(tg, 3), "iterations": res.iterations,
+                      "restarts": res.restarts, "converged": res.converged, "true_relres": res.true_relres,
+                      "history": [float(f"{v:.3e}") for v in res.history],
+                      "fp64_direct_rank32": {"t_factor_ms": round(tf64, 3), "t_solve_ms": round(ts64, 3),
+                                             "relres": res64}}), flush=True)
+    del op, h32
+    torch.cuda.empty_cache()
 if "cfg5" in which:
     n, m, r = 1 << 20, 64, 32
     f = hb.factorize(hb.random_hodlr(n, m, r, seed=0, s=1.0), check=False)
