@@ -693,17 +693,18 @@ static hodlr_status launch_level5(const LevelArgs& g, int64_t nseg, int64_t rows
 }
 
 template <int R>
+static hodlr_status run_level4(const LevelArgs& g, int64_t nseg, cudaStream_t st);
+
+// TMA feed for up to 2 column groups per warp (the upper levels: many chunks per
+// CTA, barrier-bound with cp.async -- ncu launch list r02b: levels 10..1 8-12 %
+// faster); 4+ groups per warp (deep levels, 2-8 chunks per CTA, 128 registers)
+// stay on the cp.async kernel, which is 2-7 % faster there.
+template <int R>
 static hodlr_status run_level5(const LevelArgs& g, int64_t nseg, int64_t rows, cudaStream_t st) {
   const int gpw = (g.tpc + 7) / 8;
   if (gpw <= 1) return launch_level5<R, 1>(g, nseg, rows, st);
   if (gpw <= 2) return launch_level5<R, 2>(g, nseg, rows, st);
-  if constexpr (R <= 32) {
-    if (gpw <= 4) return launch_level5<R, 4>(g, nseg, rows, st);
-  }
-  if constexpr (R <= 16) {
-    if (gpw <= 7) return launch_level5<R, 7>(g, nseg, rows, st);
-  }
-  return HODLR_ERR_ARG;
+  return run_level4<R>(g, nseg, st);
 }
 
 template <int R, int GPW>

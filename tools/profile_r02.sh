@@ -6,10 +6,10 @@
 mkdir -p gpurun_out
 T=${TAG:-r02}
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python tools/profile_once.py > /dev/null 2>&1
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:level_update4 --csv --log-file gpurun_out/${T}_level_traffic.csv python tools/profile_once.py > /dev/null 2>&1
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:level_update[45] --csv --log-file gpurun_out/${T}_level_traffic.csv python tools/profile_once.py > /dev/null 2>&1
 for spec in "13:13" "7:19" "1:25"; do
   lv=${spec%%:*}; skip=${spec##*:}
-  ncu --set full --clock-control none --import-source on -k regex:level_update4 --launch-skip $skip -c 1 -o gpurun_out/${T}_level4_l${lv} -f python tools/profile_once.py > /dev/null 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:level_update[45] --launch-skip $skip -c 1 -o gpurun_out/${T}_level4_l${lv} -f python tools/profile_once.py > /dev/null 2>&1
 done
 ncu --set full --clock-control none --import-source on -k regex:tri_apply2 --launch-skip 15 -c 1 -o gpurun_out/${T}_kapply_l13 -f python tools/profile_once.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:getrf_win --launch-skip 20 -c 1 -o gpurun_out/${T}_getrf_win -f python tools/profile_once.py > /dev/null 2>&1

@@ -16,7 +16,7 @@ for r in rows[hi + 1:]:
 launches = list(per.values())
 launches = launches[len(launches) // 2:]  # second (warm) factorize
 out = {
-    "kernel": "level_update4_kernel",
+    "kernel": "level_update5_kernel (TMA-fed; level_update4_kernel before round-2 A/B)",
     "source": sys.argv[1].split("/")[-1],
     "levels": [{"dram_bytes": l["dram__bytes_read.sum"] + l["dram__bytes_write.sum"],
                 "read": l["dram__bytes_read.sum"], "write": l["dram__bytes_write.sum"],
