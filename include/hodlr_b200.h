@@ -9,6 +9,8 @@
  *   U/Y N x rL slab, ld N, level l' in 1..L at columns [(l'-1) r, l' r)
  *   V   same as U
  *   K   level l (0..L-1) at ((2^l)-1)*(2r)^2, parent p at +p*(2r)^2 (2r x 2r)
+ * (uniform rank r; with per-level ranks (hodlr_desc.ranks) the slabs have
+ * sum(ranks) columns and the per-level blocks follow each other, see below).
  *
  * Each entry point replaces a reference interface (file:line under
  * /root/reference); see INTEGRATION.md for the Python/ctypes binding.
@@ -113,9 +115,18 @@ hodlr_status hodlr_gemm_batched(int dtype, int transA, int M, int N, int K, doub
 typedef struct {
   int64_t n;     /* matrix dimension N = m * 2^L                   */
   int32_t m;     /* leaf size                                      */
-  int32_t r;     /* uniform off-diagonal rank (ragged -> zero-pad) */
+  int32_t r;     /* uniform rank, or the max of ranks[]            */
   int32_t L;     /* tree depth                                     */
   int32_t dtype; /* HODLR_F64 / HODLR_F32                          */
+  const int32_t* ranks; /* NULL: rank r at every level.  Else ranks[l'-1] =
+                     rank of level l' (1..L), each node of a level zero-
+                     padded to its level's rank (SPEC.md:147-160 ragged
+                     panels).  Level l' then owns slab columns
+                     [c_l', c_l' + ranks[l'-1]) with c_l' = sum of the ranks
+                     above; parent level l's K blocks are 2 ranks[l] square,
+                     stored level after level.  fp64 factorize / solve /
+                     matvec; the builders and the row-sharded entry points
+                     take uniform ranks only. */
 } hodlr_desc;
 
 /* Device buffers of a factorization (all owned by the caller). */

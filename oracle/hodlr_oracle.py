@@ -204,17 +204,36 @@ def _chunks(nitems: int, threads: int, body) -> None:
 
 @dataclass
 class Layout:
+    """N = m 2^L rows; rank r at every level, or per-level ``ranks`` (level
+    l' = 1..L at ranks[l'-1], SPEC.md:147-160 ragged panels padded per level):
+    level l' then owns slab columns [c(l'), c(l') + rk(l'))."""
+
     n: int
     m: int
     r: int
+    ranks: tuple | None = None
 
     @property
     def L(self) -> int:
         return int(round(math.log2(self.n // self.m)))
 
+    def rk(self, lp: int) -> int:
+        return self.r if self.ranks is None else int(self.ranks[lp - 1])
+
+    def c(self, lp: int) -> int:
+        return (lp - 1) * self.r if self.ranks is None else int(sum(self.ranks[: lp - 1]))
+
+    @property
+    def C(self) -> int:
+        return self.c(self.L + 1)
+
     def __post_init__(self):
         if self.n % self.m or (self.n // self.m) & (self.n // self.m - 1):
             raise ValueError("oracle layout needs N = m * 2^L")
+        if self.ranks is not None:
+            self.ranks = tuple(int(x) for x in self.ranks)
+            if len(self.ranks) != self.L:
+                raise ValueError("per-level ranks: one per level 1..L")
 
 
 @dataclass
@@ -228,25 +247,26 @@ class HodlrData:
         return HodlrData(self.lay, self.D.copy(), self.U.copy(), self.V.copy())
 
 
-def make_exact_hodlr(n: int, m: int, r: int, seed: int = 0, s: float = 1.0, dtype=np.float64) -> HodlrData:
+def make_exact_hodlr(n: int, m: int, r: int, seed: int = 0, s: float = 1.0, dtype=np.float64,
+                     ranks=None) -> HodlrData:
     """Seeded exact uniform-rank HODLR (SURVEY.md §8d stand-in generator).
 
     D_a = N(0,1)/sqrt(m) + 4 I; level-l U entries N(0, s^2/n_l), V entries
     N(0, 1/n_l) with n_l = N/2^l rows per node.  s=1: trivial K pivots;
     s=16: most K pivots are real partial-pivot choices.
     """
-    lay = Layout(n, m, r)
+    lay = Layout(n, m, r if ranks is None else max(ranks, default=0), ranks)
     L = lay.L
     rng = np.random.default_rng(seed)
     nleaf = 1 << L
     D = rng.standard_normal(nleaf * m * m) / math.sqrt(m)
     diag = (np.arange(nleaf)[:, None] * m * m + np.arange(m)[None, :] * (m + 1)).ravel()
     D[diag] += 4.0
-    U = rng.standard_normal(n * r * L)
-    V = rng.standard_normal(n * r * L)
+    U = rng.standard_normal(n * lay.C)
+    V = rng.standard_normal(n * lay.C)
     for lv in range(1, L + 1):
         nl = n >> lv
-        sl = slice((lv - 1) * r * n, lv * r * n)
+        sl = slice(lay.c(lv) * n, (lay.c(lv) + lay.rk(lv)) * n)
         U[sl] *= s / math.sqrt(nl)
         V[sl] *= 1.0 / math.sqrt(nl)
     return HodlrData(lay, D.astype(dtype), U.astype(dtype), V.astype(dtype))
@@ -261,12 +281,13 @@ def dense(h: HodlrData) -> np.ndarray:
         A[a * m : (a + 1) * m, a * m : (a + 1) * m] = bview(h.D, a * m * m, m, m, m)
     for lv in range(1, L + 1):
         nl = n >> lv
+        r, c0 = lay.rk(lv), lay.c(lv) * n
         for k in range(1 << (lv - 1)):
             ia, ib = 2 * k * nl, (2 * k + 1) * nl
-            Ua = bview(h.U, (lv - 1) * r * n + ia, nl, r, n)
-            Ub = bview(h.U, (lv - 1) * r * n + ib, nl, r, n)
-            Va = bview(h.V, (lv - 1) * r * n + ia, nl, r, n)
-            Vb = bview(h.V, (lv - 1) * r * n + ib, nl, r, n)
+            Ua = bview(h.U, c0 + ia, nl, r, n)
+            Ub = bview(h.U, c0 + ib, nl, r, n)
+            Va = bview(h.V, c0 + ia, nl, r, n)
+            Vb = bview(h.V, c0 + ib, nl, r, n)
             A[ia : ia + nl, ib : ib + nl] = Ua @ Vb.T
             A[ib : ib + nl, ia : ia + nl] = Ub @ Va.T
     return A
@@ -283,8 +304,9 @@ def matvec(h: HodlrData, x: np.ndarray) -> np.ndarray:
     y = np.einsum("aij,ajk->aik", Dm, X.reshape(1 << L, m, -1)).reshape(n, -1)
     for lv in range(1, L + 1):
         nl = n >> lv
-        U = h.U[(lv - 1) * r * n : lv * r * n].reshape(r, n).T.reshape(1 << (lv - 1), 2, nl, r)
-        V = h.V[(lv - 1) * r * n : lv * r * n].reshape(r, n).T.reshape(1 << (lv - 1), 2, nl, r)
+        r, c0 = lay.rk(lv), lay.c(lv) * n
+        U = h.U[c0 : c0 + r * n].reshape(r, n).T.reshape(1 << (lv - 1), 2, nl, r)
+        V = h.V[c0 : c0 + r * n].reshape(r, n).T.reshape(1 << (lv - 1), 2, nl, r)
         w = np.einsum("pcir,pcik->pcrk", V, X.reshape(1 << (lv - 1), 2, nl, -1))  # V_c^T x_c
         y += np.einsum("pcir,pcrk->pcik", U, w[:, ::-1]).reshape(n, -1)  # child 0 gets U_0 w_1
     return y.reshape(np.shape(x))
@@ -334,18 +356,25 @@ def factorize(h: HodlrData, threads: int = 1) -> Factorization:
 
     # (2) leaf getrs on all Y rows (Alg.3 l.3)
     if L > 0:
-        yst = sview(Y, 0, m, nleaf, m, r * L, n)
+        yst = sview(Y, 0, m, nleaf, m, lay.C, n)
         _chunks(nleaf, threads, lambda lo, hi: lu_solve(dst[lo:hi], pm[lo:hi], yst[lo:hi]))
-        fl["leaf_getrs"] = lu_solve_flops(m, r * L) * nleaf
+        fl["leaf_getrs"] = lu_solve_flops(m, lay.C) * nleaf
 
     # (3) levels
     for lv in range(L - 1, -1, -1):
         nch = 1 << (lv + 1)
         npar = 1 << lv
         nc = n >> (lv + 1)
-        ncol = r * (lv + 1)
+        r = lay.rk(lv + 1)  # rank of the children (level lv + 1)
+        c1 = lay.c(lv + 1)  # their panel's first column = the columns of levels 1..lv
+        ncol = c1 + r
+        if r == 0:  # rank-0 level: empty K blocks, no update
+            fact.K.insert(0, np.zeros(0, dtype=Y.dtype))
+            fact.kpiv.insert(0, Pivots(np.zeros((npar, 0), np.int64), np.zeros((npar, 0), np.int64),
+                                       np.zeros(npar, bool)))
+            continue
         tw = np.zeros(nch * r * ncol, dtype=Y.dtype)
-        va = sview(V, lv * r * n, nc, nch, nc, r, n)
+        va = sview(V, c1 * n, nc, nch, nc, r, n)
         yb = sview(Y, 0, nc, nch, nc, ncol, n)
         tc = sview(tw, 0, r * ncol, nch, r, ncol, r)
         _chunks(nch, threads, lambda lo, hi: gemm_into(va[lo:hi], yb[lo:hi], tc[lo:hi], conj_a=True))
@@ -354,8 +383,8 @@ def factorize(h: HodlrData, threads: int = 1) -> Factorization:
         K = np.zeros(npar * 4 * r * r, dtype=Y.dtype)
         for p in range(npar):
             kb = bview(K, p * 4 * r * r, 2 * r, 2 * r, 2 * r)
-            kb[:r, :r] = bview(tw, 2 * p * r * ncol + lv * r * r, r, r, r)
-            kb[r:, r:] = bview(tw, (2 * p + 1) * r * ncol + lv * r * r, r, r, r)
+            kb[:r, :r] = bview(tw, 2 * p * r * ncol + c1 * r, r, r, r)
+            kb[r:, r:] = bview(tw, (2 * p + 1) * r * ncol + c1 * r, r, r, r)
             kb[:r, r:] = np.eye(r)
             kb[r:, :r] = np.eye(r)
         kst = sview(K, 0, 4 * r * r, npar, 2 * r, 2 * r, 2 * r)
@@ -373,9 +402,9 @@ def factorize(h: HodlrData, threads: int = 1) -> Factorization:
         fact.kpiv.insert(0, Pivots(ksw, kpm, ksg))
         if ksg.any():
             raise SingularError("K", lv, np.flatnonzero(ksg).tolist())
-        if lv == 0:
+        if lv == 0 or c1 == 0:
             continue
-        wcols = r * lv
+        wcols = c1
         W = np.zeros(npar * 2 * r * wcols, dtype=Y.dtype)
         for c in range(nch):
             bview(W, (c // 2) * 2 * r * wcols + (c % 2) * r, r, wcols, 2 * r)[...] = bview(
@@ -388,7 +417,7 @@ def factorize(h: HodlrData, threads: int = 1) -> Factorization:
         # update: W operand offsets alternate -> reference generic per-item path
         def u_body(lo, hi):
             for c in range(lo, hi):
-                a = bview(Y, lv * r * n + c * nc, nc, r, n)[None]
+                a = bview(Y, c1 * n + c * nc, nc, r, n)[None]
                 b = bview(W, (c // 2) * 2 * r * wcols + (c % 2) * r, r, wcols, 2 * r)[None]
                 cc = bview(Y, c * nc, nc, wcols, n)[None]
                 gemm_into(a, b, cc, alpha=-1.0, beta=1.0)
@@ -412,12 +441,15 @@ def solve(fact: Factorization, b: np.ndarray, threads: int = 1) -> np.ndarray:
     _chunks(nleaf, threads, lambda lo, hi: lu_solve(dst[lo:hi], fact.dpiv.perm[lo:hi], xst[lo:hi]))
     for lv in range(L - 1, -1, -1):
         nch, npar, nc = 1 << (lv + 1), 1 << lv, n >> (lv + 1)
+        r, c1 = lay.rk(lv + 1), lay.c(lv + 1)
+        if r == 0:
+            continue
         w = np.zeros(npar * 2 * r * nrhs, dtype=x.dtype)
 
         def w_body(lo, hi):
             for c in range(lo, hi):
                 gemm_into(
-                    bview(fact.V, lv * r * n + c * nc, nc, r, n)[None],
+                    bview(fact.V, c1 * n + c * nc, nc, r, n)[None],
                     bview(x, c * nc, nc, nrhs, n)[None],
                     bview(w, (c // 2) * 2 * r * nrhs + (c % 2) * r, r, nrhs, 2 * r)[None],
                     conj_a=True,
@@ -431,7 +463,7 @@ def solve(fact: Factorization, b: np.ndarray, threads: int = 1) -> np.ndarray:
         def x_body(lo, hi):
             for c in range(lo, hi):
                 gemm_into(
-                    bview(fact.Y, lv * r * n + c * nc, nc, r, n)[None],
+                    bview(fact.Y, c1 * n + c * nc, nc, r, n)[None],
                     bview(w, (c // 2) * 2 * r * nrhs + (c % 2) * r, r, nrhs, 2 * r)[None],
                     bview(x, c * nc, nc, nrhs, n)[None],
                     alpha=-1.0,
@@ -457,6 +489,9 @@ def logdet(fact: Factorization):
     sign = float(np.prod(fact.dpiv.sign()) * np.prod(np.sign(dd)))
     for lv in range(L):
         npar = 1 << lv
+        r = lay.rk(lv + 1)
+        if r == 0:
+            continue
         kd = np.stack([np.diagonal(bview(fact.K[lv], p * 4 * r * r, 2 * r, 2 * r, 2 * r)) for p in range(npar)])
         logabs += float(np.log(np.abs(kd)).sum())
         sign *= float(np.prod(fact.kpiv[lv].sign()) * np.prod(np.sign(kd)))

@@ -47,23 +47,38 @@ def executor(threads: int):
     return SERIAL if threads <= 1 else ThreadedExecutor(threads)
 
 
-def ref_factorize(D, Y, V, n, m, r, L, ex=None):
-    """Appendix-B recipe through the reference kernels; returns pivots + K."""
+def _level_ranks(r, L, ranks):
+    rk = [r] * L if ranks is None else [int(x) for x in ranks]
+    c = [0]
+    for k in rk:
+        c.append(c[-1] + k)
+    return rk, c  # rank of level l' = rk[l'-1], its first column c[l'-1]; c[L] = total
+
+
+def ref_factorize(D, Y, V, n, m, r, L, ex=None, ranks=None):
+    """Appendix-B recipe through the reference kernels; returns pivots + K.
+    ``ranks``: per-level ranks (level l' at ranks[l'-1], panels padded per level)."""
     ex = ex or SERIAL
+    rk, cc = _level_ranks(r, L, ranks)
     nleaf = 1 << L
     drefs = [BlockRef(D, a * m * m, m, m, m) for a in range(nleaf)]
     dpiv, _ = batched_lu_factor_inplace(drefs, executor=ex)
     assert not dpiv.singular
-    if L > 0:
-        batched_lu_solve_inplace(drefs, dpiv, [BlockRef(Y, a * m, m, r * L, n) for a in range(nleaf)], executor=ex)
+    if L > 0 and cc[L]:
+        batched_lu_solve_inplace(drefs, dpiv, [BlockRef(Y, a * m, m, cc[L], n) for a in range(nleaf)], executor=ex)
     Ks, kpivs = [None] * L, [None] * L
     for lv in range(L - 1, -1, -1):
-        nch, npar, nc, ncol = 1 << (lv + 1), 1 << lv, n >> (lv + 1), r * (lv + 1)
+        nch, npar, nc = 1 << (lv + 1), 1 << lv, n >> (lv + 1)
+        r, c1 = rk[lv], cc[lv]  # rank / first column of level lv + 1
+        ncol = c1 + r
+        if r == 0:
+            Ks[lv], kpivs[lv] = np.zeros(0), None
+            continue
         tw = np.zeros(nch * r * ncol)
         batched_gemm(
             [
                 (
-                    BlockRef(V, lv * r * n + c * nc, nc, r, n),
+                    BlockRef(V, c1 * n + c * nc, nc, r, n),
                     BlockRef(Y, c * nc, nc, ncol, n),
                     BlockRef(tw, c * r * ncol, r, ncol, r),
                 )
@@ -75,17 +90,17 @@ def ref_factorize(D, Y, V, n, m, r, L, ex=None):
         K = np.zeros(npar * 4 * r * r)
         for p in range(npar):
             kb = BlockRef(K, p * 4 * r * r, 2 * r, 2 * r, 2 * r).view()
-            kb[:r, :r] = BlockRef(tw, 2 * p * r * ncol + lv * r * r, r, r, r).view()
-            kb[r:, r:] = BlockRef(tw, (2 * p + 1) * r * ncol + lv * r * r, r, r, r).view()
+            kb[:r, :r] = BlockRef(tw, 2 * p * r * ncol + c1 * r, r, r, r).view()
+            kb[r:, r:] = BlockRef(tw, (2 * p + 1) * r * ncol + c1 * r, r, r, r).view()
             kb[:r, r:] = np.eye(r)
             kb[r:, :r] = np.eye(r)
         krefs = [BlockRef(K, p * 4 * r * r, 2 * r, 2 * r, 2 * r) for p in range(npar)]
         kpiv, _ = batched_lu_factor_inplace(krefs, executor=ex)
         assert not kpiv.singular
         Ks[lv], kpivs[lv] = K, kpiv
-        if lv == 0:
+        if lv == 0 or c1 == 0:
             continue
-        wc = r * lv
+        wc = c1
         W = np.zeros(npar * 2 * r * wc)
         for c in range(nch):
             BlockRef(W, (c // 2) * 2 * r * wc + (c % 2) * r, r, wc, 2 * r).view()[...] = BlockRef(
@@ -95,7 +110,7 @@ def ref_factorize(D, Y, V, n, m, r, L, ex=None):
         batched_gemm(
             [
                 (
-                    BlockRef(Y, lv * r * n + c * nc, nc, r, n),
+                    BlockRef(Y, c1 * n + c * nc, nc, r, n),
                     BlockRef(W, (c // 2) * 2 * r * wc + (c % 2) * r, r, wc, 2 * r),
                     BlockRef(Y, c * nc, nc, wc, n),
                 )
@@ -108,8 +123,9 @@ def ref_factorize(D, Y, V, n, m, r, L, ex=None):
     return dpiv, Ks, kpivs
 
 
-def ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L, ex=None):
+def ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L, ex=None, ranks=None):
     ex = ex or SERIAL
+    rk, cc = _level_ranks(r, L, ranks)
     nrhs = b.shape[1]
     x = np.asfortranarray(b).ravel(order="F").copy()
     nleaf = 1 << L
@@ -117,24 +133,25 @@ def ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L, ex=None):
     batched_lu_solve_inplace(drefs, dpiv, [BlockRef(x, a * m, m, nrhs, n) for a in range(nleaf)], executor=ex)
     for lv in range(L - 1, -1, -1):
         nch, npar, nc = 1 << (lv + 1), 1 << lv, n >> (lv + 1)
+        r, c1 = rk[lv], cc[lv]
+        if r == 0:
+            continue
         w = np.zeros(npar * 2 * r * nrhs)
-        wref = lambda c: BlockRef(w, (c // 2) * 2 * r * nrhs + (c % 2) * r, r, nrhs, 2 * r)  # noqa: E731
+        wref = lambda c, r=r: BlockRef(w, (c // 2) * 2 * r * nrhs + (c % 2) * r, r, nrhs, 2 * r)  # noqa: E731
         batched_gemm(
-            [(BlockRef(V, lv * r * n + c * nc, nc, r, n), BlockRef(x, c * nc, nc, nrhs, n), wref(c)) for c in range(nch)],
+            [(BlockRef(V, c1 * n + c * nc, nc, r, n), BlockRef(x, c * nc, nc, nrhs, n), wref(c)) for c in range(nch)],
             transpose_a="conj_transpose",
             executor=ex,
         )
         krefs = [BlockRef(Ks[lv], p * 4 * r * r, 2 * r, 2 * r, 2 * r) for p in range(npar)]
         batched_lu_solve_inplace(krefs, kpivs[lv], [BlockRef(w, p * 2 * r * nrhs, 2 * r, nrhs, 2 * r) for p in range(npar)], executor=ex)
         batched_gemm(
-            [(BlockRef(Y, lv * r * n + c * nc, nc, r, n), wref(c), BlockRef(x, c * nc, nc, nrhs, n)) for c in range(nch)],
+            [(BlockRef(Y, c1 * n + c * nc, nc, r, n), wref(c), BlockRef(x, c * nc, nc, nrhs, n)) for c in range(nch)],
             alpha=-1.0,
             beta=1.0,
             executor=ex,
         )
     return x.reshape(nrhs, n).T.copy()
-
-
 
 
 def ref_assemble(entry, n: int, m: int, r: int):

@@ -34,6 +34,7 @@ from .hodlr import (  # noqa: F401
     flop_report,
     logdet,
     pad_level_panels,
+    truncate_ranks,
     random_hodlr,
     solve,
     solve_flops,

@@ -32,7 +32,19 @@ class HodlrNativeError(RuntimeError):
 
 
 class Desc(C.Structure):
-    _fields_ = [("n", C.c_int64), ("m", C.c_int32), ("r", C.c_int32), ("L", C.c_int32), ("dtype", C.c_int32)]
+    _fields_ = [("n", C.c_int64), ("m", C.c_int32), ("r", C.c_int32), ("L", C.c_int32), ("dtype", C.c_int32),
+                ("ranks", C.c_void_p)]
+
+
+def make_desc(n: int, m: int, r: int, L: int, dtype: int, ranks=None) -> Desc:
+    """hodlr_desc; ``ranks`` (per-level ranks, level l' at ranks[l'-1]) is kept
+    alive on the returned structure."""
+    d = Desc(n, m, r, L, dtype, None)
+    if ranks is not None:
+        arr = (C.c_int32 * len(ranks))(*[int(x) for x in ranks])
+        d.ranks = C.cast(arr, C.c_void_p)
+        d._ranks_keep = arr
+    return d
 
 
 class Factors(C.Structure):

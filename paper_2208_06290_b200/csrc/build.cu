@@ -458,7 +458,7 @@ BuildWs build_ws(const hodlr_desc* d) {
 }
 
 bool build_desc_ok(const hodlr_desc* d) {
-  return d && d->dtype == HODLR_F64 && d->m >= 1 && d->r >= 0 && d->L >= 0 && d->L <= 30 &&
+  return d && d->ranks == nullptr && d->dtype == HODLR_F64 && d->m >= 1 && d->r >= 0 && d->L >= 0 && d->L <= 30 &&
          d->n == (int64_t)d->m << d->L;
 }
 

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "ranks.cuh"
 
 namespace hodlr {
 template <typename T>
@@ -207,9 +208,15 @@ static bool tri_size_ok(int s) { return s == 16 || s == 32 || s == 64 || s == 12
 static bool desc_ok(const hodlr_desc* d) {
   if (!d || d->m < 1 || d->r < 0 || d->L < 0 || d->L > 30) return false;
   if (d->m > 119 && !tri_size_ok(d->m)) return false;
-  if (d->L > 0 && 2 * d->r > 119 && !tri_size_ok(2 * d->r)) return false;
+  LevelRanks q;
+  if (!make_ranks(d, q)) return false;
+  for (int l = 1; l <= d->L; ++l)
+    if (2 * q.r[l] > 119 && !tri_size_ok(2 * q.r[l])) return false;
+  if (!q.uniform && d->dtype != HODLR_F64) return false;  // per-level ranks: the fp64 drivers
   return d->n == (int64_t)d->m << d->L;
 }
+// the row-sharded entry points and the fp32 drivers take uniform ranks
+static bool uniform_desc(const hodlr_desc* d) { return d->ranks == nullptr; }
 
 // Factor s x s blocks; for DMMA-supported sizes also emit the packed
 // triangular inverses used by lu_apply.
@@ -311,8 +318,11 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
   double* W = reinterpret_cast<double*>(wp + ws.split + ws.tw);
   double* part = reinterpret_cast<double*>(wp + ws.split + ws.tw + ws.w);
 
+  LevelRanks q;
+  if (!make_ranks(d, q)) return HODLR_ERR_ARG;
   const int64_t N = d->n, n = n_loc;
-  const int m = d->m, r = d->r, L = d->L;
+  const int m = d->m, L = d->L;
+  const int64_t C = q.cols();  // slab columns (r L when uniform)
   const int64_t nleaf = n / m;
   double* D = (double*)f->D;
   double* Dinv = (double*)f->Dinv;
@@ -321,26 +331,27 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
   double* K = (double*)f->K;
   double* Kinv = (double*)f->Kinv;
 
-  // (1) leaf getrf (bit-exact) + packed triangular inverses     Alg.3 l.2
+  // (1) leaf getrf (bit-exact) + diagonal-block inverses          Alg.3 l.2
   if (vready && L > 0 && cudaStreamWaitEvent(st, vready[L], 0) != cudaSuccess)  // D, U and V^(L) resident
     return hodlr_set_cuda_error(cudaGetLastError());
   {
     Phase ph(HODLR_PHASE_LEAF_GETRF, st);
     TRY(lu_factor(m, (int)nleaf, 0, D, m, (int64_t)m * m, D, (int64_t)m * m, f->dswaps, f->dperm, f->dinfo, Dinv, st));
   }
-  if (L == 0 || r == 0) return HODLR_OK;
+  if (L == 0 || C == 0) return HODLR_OK;
   // (2) Y(I_a, :) <- D_a^-1 U(I_a, :) for all levels at once       Alg.3 l.3
-  //     fused with the level-(L-1) [W|T]_a = V_a^T Y(I_a, 0:rL)   Alg.3 l.5-6
+  //     fused with the level-(L-1) [W|T]_a = V_a^T Y(I_a, 0:C)      Alg.3 l.5-6
   bool tw_ready = false;
   {
     Phase ph(HODLR_PHASE_LEAF_APPLY, st);
-    if (tri_size_ok(m)) {
-      hodlr_status s = tri_apply_f64(m, r * L, (int)nleaf, D, Dinv, m, (int64_t)m * m, f->dperm, Y, n, m, 0, Y, n, m, 0,
-                                     1, st, V + (int64_t)(L - 1) * r * n, n, m, r, TW, (int64_t)2 * r * r * L);
+    const int rL = q.r[L];
+    if (tri_size_ok(m) && rL > 0) {
+      hodlr_status s = tri_apply_f64(m, (int)C, (int)nleaf, D, Dinv, m, (int64_t)m * m, f->dperm, Y, n, m, 0, Y, n, m, 0,
+                                     1, st, V + q.c[L] * n, n, m, rL, TW, (int64_t)2 * rL * C);
       if (s == HODLR_OK) tw_ready = true;
       else if (s != HODLR_ERR_ARG) return s;
     }
-    if (!tw_ready) TRY(lu_apply(m, r * L, (int)nleaf, D, Dinv, f->dperm, Y, n, m, Y, n, m, st));
+    if (!tw_ready) TRY(lu_apply(m, (int)C, (int)nleaf, D, Dinv, f->dperm, Y, n, m, Y, n, m, st));
   }
 
   // (3) levels                                                     Alg.3 l.4-10
@@ -348,37 +359,48 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
     const int64_t nc = N >> (lv + 1);
     const int nch = (int)(n / nc), npar = nch / 2;
     const int64_t p0 = row0 / (2 * nc);  // global index of the first local parent
-    const int ncol = r * (lv + 1), wc = r * lv;
-    const int64_t kblk = ((int64_t)1 << lv) - 1 + p0;  // first local K block (global layout)
-    const int64_t koff = kblk * 4 * r * r, kioff = kblk * inv_block_elems(2 * r);
+    const int r = q.r[lv + 1];           // rank of the children (level lv + 1)
+    const int ncol = (int)q.c[lv + 2], wc = (int)q.c[lv + 1];
+    const int64_t kblk = ((int64_t)1 << lv) - 1 + p0;  // first local K block (global numbering)
+    const int64_t koff = q.koff[lv] + p0 * 4 * r * r, kioff = q.kioff[lv] + p0 * inv_block_elems(2 * r);
+    const int64_t kpoff = q.kpoff[lv] + p0 * 2 * r;
+    if (r == 0) {  // a rank-0 level: K_p is the empty matrix, nothing to update
+      tw_ready = false;
+      continue;
+    }
     if (!tw_ready) {
       Phase ph(HODLR_PHASE_GEMM, st);
-      // [W|T]_c = V_c^T Y(I_c, 0:r(l+1)), paired per parent: 2r x ncol, ld 2r
-      TRY(gemm_f64(1, r, ncol, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, Y, n, 2 * nc, nc, 0.0, TW,
-                   2 * r, (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
+      // [W|T]_c = V_c^T Y(I_c, 0:ncol), paired per parent: 2r x ncol, ld 2r
+      TRY(gemm_f64(1, r, ncol, (int)nc, 1.0, V + q.c[lv + 1] * n, n, 2 * nc, nc, Y, n, 2 * nc, nc, 0.0, TW, 2 * r,
+                   (int64_t)2 * r * ncol, r, nch, 2, split, ws.split, st));
     }
-    // K_p = [[T_2p, I], [I, T_2p+1]] assembled + factored (bit-exact) + packed inverses
-    int32_t* kperm = f->kperm + kblk * 2 * r;
+    // K_p = [[T_2p, I], [I, T_2p+1]] assembled + factored (bit-exact) + diagonal-block inverses
+    int32_t* kperm = f->kperm + kpoff;
     {
       Phase ph(HODLR_PHASE_K_GETRF, st);
       TRY(lu_factor(2 * r, npar, 1, TW + (int64_t)wc * 2 * r, 2 * r, (int64_t)2 * r * ncol, K + koff,
-                    (int64_t)4 * r * r, f->kswaps + kblk * 2 * r, kperm, f->kinfo + kblk, Kinv + kioff, st));
+                    (int64_t)4 * r * r, f->kswaps + kpoff, kperm, f->kinfo + kblk, Kinv + kioff, st));
     }
     if (lv == 0) break;
+    if (wc == 0) {  // rank-0 levels above: no columns to update
+      tw_ready = false;
+      continue;
+    }
     // W_p <- K_p^-1 [W_2p; W_2p+1]
     {
       Phase ph(HODLR_PHASE_K_APPLY, st);
       TRY(lu_apply(2 * r, wc, npar, K + koff, Kinv + kioff, kperm, TW, 2 * r, (int64_t)2 * r * ncol, W, 2 * r,
                    (int64_t)2 * r * wc, st));
     }
-    // Y(I_c, 0:rl) -= Y_c^{l+1} W_c, fused with the next level's [W|T] (V^{(l)T} Y(I_q, 0:rl))
+    // Y(I_c, 0:wc) -= Y_c^{l+1} W_c, fused with the next level's [W|T] (V^{(l)T} Y(I_q, 0:wc))
+    // when both levels have the same rank (the fused kernel holds one rank)
     if (vready && cudaStreamWaitEvent(st, vready[lv], 0) != cudaSuccess)  // V^(lv) resident (streamed upload)
       return hodlr_set_cuda_error(cudaGetLastError());
-    hodlr_status s;
-    {
+    hodlr_status s = HODLR_ERR_ARG;
+    if (q.r[lv] == r) {
       Phase ph(HODLR_PHASE_LEVEL, st);
-      s = level_update_f64(r, n, nc, 2 * nc, Y, n, Y + (int64_t)lv * r * n, V + (int64_t)(lv - 1) * r * n, n, W,
-                           (int64_t)2 * r * wc, wc, TW, (int64_t)2 * r * wc, part, ws.part, st, true);
+      s = level_update_f64(r, n, nc, 2 * nc, Y, n, Y + q.c[lv + 1] * n, V + q.c[lv] * n, n, W, (int64_t)2 * r * wc,
+                           wc, TW, (int64_t)2 * r * wc, part, ws.part, st, true);
     }
     if (s == HODLR_OK) {
       tw_ready = true;
@@ -387,19 +409,20 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
     if (s != HODLR_ERR_ARG) return s;
     tw_ready = false;
     Phase ph(HODLR_PHASE_GEMM, st);
-    TRY(gemm_f64(0, (int)nc, wc, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, W, 2 * r, (int64_t)2 * r * wc, r,
-                 1.0, Y, n, 2 * nc, nc, nch, 2, split, ws.split, st));
+    TRY(gemm_f64(0, (int)nc, wc, r, -1.0, Y + q.c[lv + 1] * n, n, 2 * nc, nc, W, 2 * r, (int64_t)2 * r * wc, r, 1.0,
+                 Y, n, 2 * nc, nc, nch, 2, split, ws.split, st));
   }
   if (!tw_ready && lv_stop > 0) {
-    // the caller wants the level-lv_stop [W|T] in the workspace
+    // the caller wants the level-lv_stop [W|T] in the workspace (uniform ranks: the sharded path)
     const int lv = lv_stop - 1;
     const int64_t nc = N >> (lv + 1);
     const int nch = (int)(n / nc);
-    if (nch >= 1 && nc <= n) {
+    const int r = q.r[lv + 1];
+    if (nch >= 1 && nc <= n && r > 0) {
       Phase ph(HODLR_PHASE_GEMM, st);
-      const int ncol = r * (lv + 1);
-      TRY(gemm_f64(1, r, ncol, (int)std::min<int64_t>(nc, n), 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, Y, n,
-                   2 * nc, nc, 0.0, TW, 2 * r, (int64_t)2 * r * ncol, r, std::max(nch, 1), 2, split, ws.split, st));
+      const int ncol = (int)q.c[lv + 2];
+      TRY(gemm_f64(1, r, ncol, (int)std::min<int64_t>(nc, n), 1.0, V + q.c[lv + 1] * n, n, 2 * nc, nc, Y, n, 2 * nc,
+                   nc, 0.0, TW, 2 * r, (int64_t)2 * r * ncol, r, std::max(nch, 1), 2, split, ws.split, st));
     }
   }
   return HODLR_OK;
@@ -627,7 +650,7 @@ static std::map<int, std::vector<cudaEvent_t>> g_up_ev;  // per device: events l
 extern "C" hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hodlr_factors* f, const void* D_host,
                                                   const void* U_host, const void* V_host, void* work,
                                                   size_t work_bytes, void* stream, void* copy_stream) {
-  if (!desc_ok(d) || !f || !D_host || !U_host || !V_host) return HODLR_ERR_ARG;
+  if (!desc_ok(d) || !uniform_desc(d) || !f || !D_host || !U_host || !V_host) return HODLR_ERR_ARG;
   if (d->dtype != HODLR_F64) return HODLR_ERR_ARG;
   const FactWs ws = fact_ws(d);
   if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
@@ -669,7 +692,7 @@ extern "C" hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hod
 extern "C" hodlr_status hodlr_factorize_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
                                               int lv_stop, double* tw_out, void* work, size_t work_bytes,
                                               void* stream) {
-  if (!desc_ok(d) || !f || !local_ok(d, n_loc, row0)) return HODLR_ERR_ARG;
+  if (!desc_ok(d) || !uniform_desc(d) || !f || !local_ok(d, n_loc, row0)) return HODLR_ERR_ARG;
   if (d->dtype != HODLR_F64 || lv_stop < 0 || lv_stop > d->L) return HODLR_ERR_ARG;
   if ((d->n >> lv_stop) > n_loc) return HODLR_ERR_ARG;  // levels >= lv_stop must be local
   const FactWs ws = fact_ws_local(d, n_loc);
@@ -696,7 +719,7 @@ extern "C" hodlr_status hodlr_factorize_local(const hodlr_desc* d, const hodlr_f
 extern "C" hodlr_status hodlr_factorize_top(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
                                             int lv, const double* tw_all, double* tw_out, void* work,
                                             size_t work_bytes, void* stream) {
-  if (!desc_ok(d) || !f || !local_ok(d, n_loc, row0) || !tw_all) return HODLR_ERR_ARG;
+  if (!desc_ok(d) || !uniform_desc(d) || !f || !local_ok(d, n_loc, row0) || !tw_all) return HODLR_ERR_ARG;
   if (d->dtype != HODLR_F64 || lv < 0 || lv >= d->L || (d->n >> (lv + 1)) < n_loc) return HODLR_ERR_ARG;
   const FactWs ws = fact_ws_local(d, n_loc);
   if (work_bytes < ws.total || !work) return HODLR_ERR_ARG;
@@ -750,9 +773,11 @@ extern "C" hodlr_status hodlr_factorize_top(const hodlr_desc* d, const hodlr_fac
 // (paired layout, local node 0) when lv_stop > 0.
 static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0, int lv_stop,
                                 double* X, int64_t ldx, int nrhs, char* wp, cudaStream_t st) {
+  LevelRanks q;
+  if (!make_ranks(d, q)) return HODLR_ERR_ARG;
   const int64_t N = d->n, n = n_loc;
-  const int m = d->m, r = d->r, L = d->L;
-  const size_t wsz = align_up(sizeof(double) * (size_t)std::max<int64_t>((int64_t)1 << L, 2) * r * nrhs);
+  const int m = d->m, L = d->L;
+  const size_t wsz = align_up(sizeof(double) * (size_t)std::max<int64_t>((int64_t)1 << L, 2) * q.rmax * nrhs);
   void* split = wp;
   double* w = reinterpret_cast<double*>(wp + kSplitBytes);
   double* w2 = reinterpret_cast<double*>(wp + kSplitBytes + wsz);
@@ -766,10 +791,11 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
   bool w_ready = false;
   {
     Phase ph(HODLR_PHASE_SOLVE_LEAF, st);
-    if (r > 0 && L > 0 && tri_size_ok(m)) {
-      hodlr_status s = tri_apply_f64(m, nrhs, (int)nleaf, (const double*)f->D, (const double*)f->Dinv, m, (int64_t)m * m, f->dperm, X, ldx,
-                                     m, 0, X, ldx, m, 0, 1, st, V + (int64_t)(L - 1) * r * n, n, m, r, w,
-                                     (int64_t)2 * r * nrhs);
+    const int rL = L > 0 ? q.r[L] : 0;
+    if (rL > 0 && tri_size_ok(m)) {
+      hodlr_status s = tri_apply_f64(m, nrhs, (int)nleaf, (const double*)f->D, (const double*)f->Dinv, m,
+                                     (int64_t)m * m, f->dperm, X, ldx, m, 0, X, ldx, m, 0, 1, st, V + q.c[L] * n, n, m,
+                                     rL, w, (int64_t)2 * rL * nrhs);
       if (s == HODLR_OK) w_ready = true;
       else if (s != HODLR_ERR_ARG) return s;
     }
@@ -777,54 +803,63 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
       TRY(lu_apply(m, nrhs, (int)nleaf, (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m, X, ldx, m,
                    st));
   }
-  if (r == 0 || L == 0) return HODLR_OK;
+  if (q.cols() == 0 || L == 0) return HODLR_OK;
   for (int lv = L - 1; lv >= lv_stop; --lv) {
     const int64_t nc = N >> (lv + 1);
     const int nch = (int)(n / nc), npar = nch / 2;
     const int64_t p0 = row0 / (2 * nc);
-    const int64_t kblk = ((int64_t)1 << lv) - 1 + p0;
-    const int64_t koff = kblk * 4 * r * r, kioff = kblk * inv_block_elems(2 * r);
+    const int r = q.r[lv + 1];
+    if (r == 0) {
+      w_ready = false;
+      continue;
+    }
+    const int64_t koff = q.koff[lv] + p0 * 4 * r * r, kioff = q.kioff[lv] + p0 * inv_block_elems(2 * r);
+    const int64_t kpoff = q.kpoff[lv] + p0 * 2 * r;
     // w_c = V_c^T x_c  (paired per parent, 2r x nrhs, ld 2r)       Alg.4 l.5
     if (!w_ready) {
       Phase ph(HODLR_PHASE_GEMM, st);
-      TRY(gemm_f64(1, r, nrhs, (int)nc, 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w,
-                   2 * r, (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
+      TRY(gemm_f64(1, r, nrhs, (int)nc, 1.0, V + q.c[lv + 1] * n, n, 2 * nc, nc, X, ldx, 2 * nc, nc, 0.0, w, 2 * r,
+                   (int64_t)2 * r * nrhs, r, nch, 2, split, kSplitBytes, st));
     }
     // w_p <- K_p^-1 w_p                                              Alg.4 l.6
     {
       Phase ph(HODLR_PHASE_SOLVE_K, st);
-      TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + kioff, f->kperm + kblk * 2 * r, w, 2 * r,
+      TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + kioff, f->kperm + kpoff, w, 2 * r,
                    (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st));
     }
     // x_c -= Y_c w_c  fused with the next level's w = V^{(l)T} x    Alg.4 l.7 (+ l.5 of level l-1)
+    // (fused when the next level has the same rank)
+    const bool next_same = lv == 0 || q.r[lv] == r;
+    const double* Vn = lv > 0 && next_same ? V + q.c[lv] * n : nullptr;
     hodlr_status s;
     {
       Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
-      s = solve_level_f64(r, n, nc, 2 * nc, X, ldx, Y + (int64_t)lv * r * n,
-                          lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
+      s = solve_level_f64(r, n, nc, 2 * nc, X, ldx, Y + q.c[lv + 1] * n, Vn, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
                           (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st);
       if (s == HODLR_ERR_ARG)
-        s = level_update_f64(r, n, nc, 2 * nc, X, ldx, Y + (int64_t)lv * r * n,
-                             lv > 0 ? V + (int64_t)(lv - 1) * r * n : nullptr, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
+        s = level_update_f64(r, n, nc, 2 * nc, X, ldx, Y + q.c[lv + 1] * n, Vn, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
                              (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st, false);
     }
     if (s == HODLR_OK) {
-      w_ready = lv > 0;
+      w_ready = lv > 0 && Vn != nullptr;
       continue;
     }
     if (s != HODLR_ERR_ARG) return s;
     w_ready = false;
     Phase ph(HODLR_PHASE_GEMM, st);
-    TRY(gemm_f64(0, (int)nc, nrhs, r, -1.0, Y + (int64_t)lv * r * n, n, 2 * nc, nc, w2, 2 * r, (int64_t)2 * r * nrhs,
-                 r, 1.0, X, ldx, 2 * nc, nc, nch, 2, split, kSplitBytes, st));
+    TRY(gemm_f64(0, (int)nc, nrhs, r, -1.0, Y + q.c[lv + 1] * n, n, 2 * nc, nc, w2, 2 * r, (int64_t)2 * r * nrhs, r,
+                 1.0, X, ldx, 2 * nc, nc, nch, 2, split, kSplitBytes, st));
   }
   if (!w_ready && lv_stop > 0) {
     const int lv = lv_stop - 1;
     const int64_t nc = N >> (lv + 1);
-    Phase ph(HODLR_PHASE_GEMM, st);
-    TRY(gemm_f64(1, r, nrhs, (int)std::min<int64_t>(nc, n), 1.0, V + (int64_t)lv * r * n, n, 2 * nc, nc, X, ldx,
-                 2 * nc, nc, 0.0, w, 2 * r, (int64_t)2 * r * nrhs, r, std::max<int>((int)(n / nc), 1), 2, split,
-                 kSplitBytes, st));
+    const int r = q.r[lv + 1];
+    if (r > 0) {
+      Phase ph(HODLR_PHASE_GEMM, st);
+      TRY(gemm_f64(1, r, nrhs, (int)std::min<int64_t>(nc, n), 1.0, V + q.c[lv + 1] * n, n, 2 * nc, nc, X, ldx,
+                   2 * nc, nc, 0.0, w, 2 * r, (int64_t)2 * r * nrhs, r, std::max<int>((int)(n / nc), 1), 2, split,
+                   kSplitBytes, st));
+    }
   }
   return HODLR_OK;
 }
@@ -843,7 +878,7 @@ extern "C" hodlr_status hodlr_solve(const hodlr_desc* d, const hodlr_factors* f,
 extern "C" hodlr_status hodlr_solve_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
                                           int lv_stop, void* Xv, int64_t ldx, int nrhs, double* w_out, void* work,
                                           size_t work_bytes, void* stream) {
-  if (!desc_ok(d) || !f || !local_ok(d, n_loc, row0) || nrhs < 0 || ldx < n_loc) return HODLR_ERR_ARG;
+  if (!desc_ok(d) || !uniform_desc(d) || !f || !local_ok(d, n_loc, row0) || nrhs < 0 || ldx < n_loc) return HODLR_ERR_ARG;
   if (d->dtype != HODLR_F64 || lv_stop < 0 || lv_stop > d->L || (d->n >> lv_stop) > n_loc) return HODLR_ERR_ARG;
   if (nrhs == 0) return HODLR_OK;
   if (work_bytes < hodlr_solve_workspace(d, nrhs) || !work) return HODLR_ERR_ARG;
@@ -866,7 +901,7 @@ extern "C" hodlr_status hodlr_solve_local(const hodlr_desc* d, const hodlr_facto
 extern "C" hodlr_status hodlr_solve_top(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0,
                                         int lv, const double* w_all, double* w_out, void* Xv, int64_t ldx, int nrhs,
                                         void* work, size_t work_bytes, void* stream) {
-  if (!desc_ok(d) || !f || !local_ok(d, n_loc, row0) || !w_all || nrhs <= 0 || ldx < n_loc) return HODLR_ERR_ARG;
+  if (!desc_ok(d) || !uniform_desc(d) || !f || !local_ok(d, n_loc, row0) || !w_all || nrhs <= 0 || ldx < n_loc) return HODLR_ERR_ARG;
   if (d->dtype != HODLR_F64 || lv < 0 || lv >= d->L || (d->n >> (lv + 1)) < n_loc) return HODLR_ERR_ARG;
   if (work_bytes < hodlr_solve_workspace(d, nrhs) || !work) return HODLR_ERR_ARG;
   cudaStream_t st = S(stream);

@@ -23,6 +23,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "ranks.cuh"
 
 namespace hodlr {
 namespace {
@@ -403,9 +404,58 @@ bool mv_shape_ok(const hodlr_desc* d) {
 }  // namespace
 }  // namespace hodlr
 
+namespace hodlr {
+hodlr_status gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, int64_t lda, int64_t sA_hi,
+                      int64_t sA_lo, const double* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double beta,
+                      double* C, int64_t ldc, int64_t sC_hi, int64_t sC_lo, int batch, int bdiv, void* work,
+                      size_t work_bytes, cudaStream_t st);
+namespace {
+constexpr size_t kMvSplitBytes = size_t(64) << 20;
+
+// Per-level-rank (ragged) matvec: the batched DMMA GEMMs level by level --
+// Y_a = D_a X_a, then per level w_c = V_c^T X_c and Y_c += U_c w_sibling(c).
+// (The fused two-sweep kernels above assume one rank for every level.)
+size_t mv_ragged_w_elems(const LevelRanks& q, int nrhs) {
+  size_t e = 0;
+  for (int l = 1; l <= q.L; ++l) e += ((size_t)1 << l) * q.r[l] * nrhs;
+  return e;
+}
+hodlr_status mv_ragged(const hodlr_desc* d, const LevelRanks& q, const double* D, const double* U, const double* V,
+                       const double* X, int64_t ldx, double* Y, int64_t ldy, int nrhs, char* ws, cudaStream_t st) {
+  const int64_t N = d->n;
+  const int m = d->m, L = d->L;
+  void* split = ws;
+  double* w = reinterpret_cast<double*>(ws + kMvSplitBytes);
+  hodlr_status s = gemm_f64(0, m, nrhs, m, 1.0, D, m, (int64_t)m * m, 0, X, ldx, m, 0, 0.0, Y, ldy, m, 0, 1 << L, 1,
+                            split, kMvSplitBytes, st);
+  if (s != HODLR_OK) return s;
+  for (int l = 1; l <= L; ++l) {
+    const int k = q.r[l];
+    if (k == 0) continue;
+    const int64_t nl = N >> l;
+    const int nb = 1 << l;
+    s = gemm_f64(1, k, nrhs, (int)nl, 1.0, V + q.c[l] * N, N, nl, 0, X, ldx, nl, 0, 0.0, w, k, (int64_t)k * nrhs, 0,
+                 nb, 1, split, kMvSplitBytes, st);
+    if (s != HODLR_OK) return s;
+    // child b reads its sibling's w: b = 2p -> w[2p + 1], b = 2p + 1 -> w[2p]
+    const int64_t per = (int64_t)k * nrhs;
+    s = gemm_f64(0, (int)nl, nrhs, k, 1.0, U + q.c[l] * N, N, 2 * nl, nl, w + per, k, 2 * per, -per, 1.0, Y, ldy, 2 * nl, nl,
+                 nb, 2, split, kMvSplitBytes, st);
+    if (s != HODLR_OK) return s;
+  }
+  return HODLR_OK;
+}
+}  // namespace
+}  // namespace hodlr
+
 using namespace hodlr;
 
 extern "C" size_t hodlr_matvec_workspace(const hodlr_desc* d, int nrhs) {
+  if (d && d->ranks) {
+    LevelRanks q;
+    if (!mv_shape_ok(d) || nrhs < 0 || d->dtype != HODLR_F64 || !make_ranks(d, q)) return 0;
+    return kMvSplitBytes + ((mv_ragged_w_elems(q, std::max(nrhs, 1)) * sizeof(double) + 255) & ~(size_t)255);
+  }
   if (!mv_shape_ok(d) || nrhs < 0) return 0;
   const MvGeom g = mv_geom(d, std::max(nrhs, 1));
   const size_t b = mv_ws_elems(g) * (d->dtype == HODLR_F64 ? sizeof(double) : sizeof(float));
@@ -420,6 +470,12 @@ extern "C" hodlr_status hodlr_matvec(const hodlr_desc* d, const void* D, const v
   if (!D || !X || !Y || X == Y || (d->r > 0 && d->L > 0 && (!U || !V))) return HODLR_ERR_ARG;
   const size_t need = hodlr_matvec_workspace(d, nrhs);
   if (work_bytes < need || (need && !work)) return HODLR_ERR_ARG;
+  if (d->ranks) {
+    LevelRanks q;
+    if (d->dtype != HODLR_F64 || !make_ranks(d, q) || !need) return HODLR_ERR_ARG;
+    return mv_ragged(d, q, (const double*)D, (const double*)U, (const double*)V, (const double*)X, ldx, (double*)Y,
+                     ldy, nrhs, static_cast<char*>(work), static_cast<cudaStream_t>(stream));
+  }
   const size_t es = d->dtype == HODLR_F64 ? sizeof(double) : sizeof(float);
   // vector loads (V 4 scalars, U / D 2 scalars) when the layout allows them
   const bool vec = d->m % 4 == 0 && (uintptr_t)V % (4 * es) == 0 && (uintptr_t)U % (2 * es) == 0 &&

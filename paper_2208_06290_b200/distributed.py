@@ -73,6 +73,8 @@ def make_shard(h, rank: int, world: int) -> Shard:
     import torch
 
     n, m, r, L = h.n, h.m, h.rank, h.L
+    if getattr(h, "ranks", None) is not None:
+        raise ValueError("the row-sharded path takes one rank per matrix (per-level ranks: single GPU)")
     if world < 1 or world & (world - 1) or world > (1 << L):
         raise ValueError(f"world size {world} must be a power of two <= 2^L")
     if not 0 <= rank < world:

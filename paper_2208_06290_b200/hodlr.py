@@ -81,7 +81,8 @@ def _host(x):
     return np.asarray(x.detach().cpu() if hasattr(x, "detach") else x)
 
 
-def pad_level_panels(n: int, m: int, u_panels, v_panels, rank: int | None = None, round_rank: bool = True):
+def pad_level_panels(n: int, m: int, u_panels, v_panels, rank: int | None = None, round_rank: bool = True,
+                     per_level: bool = False, with_ranks: bool = False):
     """Ragged LevelPanels (levels 1..L, per-node column offsets and ranks) ->
     (r, U, V): the uniform slabs of this engine, every node's basis zero-padded
     to rank r = the largest node rank (``rank`` overrides it; ``round_rank``
@@ -110,12 +111,23 @@ def pad_level_panels(n: int, m: int, u_panels, v_panels, rank: int | None = None
     r = rank if rank is not None else (_round_rank(rmax) if round_rank else rmax)
     if r < rmax:
         raise ValueError(f"rank {r} < the largest node rank {rmax}")
+    if per_level:  # each level padded to its own largest node rank (rounded)
+        lr = []
+        for lv in range(1, L + 1):
+            k = int(max(np.asarray(ups[lv].node_ranks).max(initial=0), np.asarray(vps[lv].node_ranks).max(initial=0)))
+            lr.append(_round_rank(k) if (round_rank and k > 0) else k)
+        ranks = tuple(lr)
+        r = max(ranks, default=0)
+    else:
+        ranks = (r,) * L
     dt = _host(ups[1].data).dtype if L else np.float64
-    U = np.zeros((L, r, n), dtype=dt)  # level-major; level l is an n x r column-major panel
-    V = np.zeros((L, r, n), dtype=dt)
+    cc = np.concatenate([[0], np.cumsum(ranks)]).astype(np.int64)
+    U = np.zeros((int(cc[-1]), n), dtype=dt)  # level l's n x ranks[l-1] column-major panel at rows cc[l-1]
+    V = np.zeros((int(cc[-1]), n), dtype=dt)
     for lv in range(1, L + 1):
         nl = n >> lv
-        for dst, p in ((U, ups[lv]), (V, vps[lv])):
+        for dstall, p in ((U, ups[lv]), (V, vps[lv])):
+            dst = dstall[cc[lv - 1] : cc[lv]]
             a = _host(p.data).reshape(-1)
             width = a.size // n if n else 0
             if a.size != n * width:
@@ -127,7 +139,9 @@ def pad_level_panels(n: int, m: int, u_panels, v_panels, rank: int | None = None
                 k, c0 = int(nr[node]), int(off[node])
                 if c0 < 0 or c0 + k > width:
                     raise ValueError(f"level {lv} node {node}: columns [{c0}, {c0 + k}) outside the panel")
-                dst[lv - 1, :k, node * nl : (node + 1) * nl] = cols[c0 : c0 + k, node * nl : (node + 1) * nl]
+                dst[:k, node * nl : (node + 1) * nl] = cols[c0 : c0 + k, node * nl : (node + 1) * nl]
+    if with_ranks:
+        return r, U.reshape(-1), V.reshape(-1), (ranks if per_level else None)
     return r, U.reshape(-1), V.reshape(-1)
 
 
@@ -138,8 +152,17 @@ class HodlrMatrix:
     tree: ClusterTree
     rank: int
     D: "object"  # torch (2^L m^2,)  leaf a at a*m*m, column-major
-    U: "object"  # torch (N r L,)   ld N, level l' at columns (l'-1) r
-    V: "object"  # torch (N r L,)
+    U: "object"  # torch (N C,)  ld N, level l' at columns [c_l', c_l' + r_l') (uniform: (l'-1) r)
+    V: "object"  # torch (N C,)
+    ranks: tuple | None = None  # per-level ranks (level l' at ranks[l'-1]); None: ``rank`` everywhere
+
+    @property
+    def level_ranks(self) -> tuple:
+        return tuple(self.ranks) if self.ranks is not None else (self.rank,) * self.L
+
+    @property
+    def cols(self) -> int:
+        return sum(self.level_ranks)
 
     @property
     def n(self) -> int:
@@ -158,16 +181,26 @@ class HodlrMatrix:
         return self.D.dtype
 
     def desc(self) -> _lib.Desc:
-        return _lib.Desc(self.n, self.m, self.rank, self.L, _dtype_tag(self.D))
+        return _lib.make_desc(self.n, self.m, self.rank, self.L, _dtype_tag(self.D), self.ranks)
 
     @classmethod
-    def from_buffers(cls, n: int, m: int, r: int, D, U, V, device="cuda") -> "HodlrMatrix":
-        """Wrap flat buffers (numpy or torch) in the reference layout; copies to ``device``."""
+    def from_buffers(cls, n: int, m: int, r: int, D, U, V, device="cuda", ranks=None) -> "HodlrMatrix":
+        """Wrap flat buffers (numpy or torch) in the reference layout; copies to
+        ``device``.  ``ranks``: per-level ranks (level l' at ranks[l'-1]; the
+        slabs then have sum(ranks) columns and ``r`` is ignored)."""
         torch = _torch()
         L = int(round(math.log2(n // m))) if n >= m else 0
         if n != m << L:
             raise ValueError(f"GPU layout needs N = m 2^L (got N={n}, m={m})")
         tree = ClusterTree(n, L)
+        if ranks is not None:
+            ranks = tuple(int(x) for x in ranks)
+            if len(ranks) != L or min(ranks, default=0) < 0:
+                raise ValueError(f"ranks: {L} non-negative per-level ranks expected (got {ranks})")
+            r = max(ranks, default=0)
+            if len(set(ranks)) <= 1 and (not ranks or ranks[0] == r):
+                ranks = None  # uniform
+        C_ = sum(ranks) if ranks is not None else r * L
 
         def dev(x, size, name):
             t = torch.as_tensor(x).reshape(-1).to(device)
@@ -175,31 +208,35 @@ class HodlrMatrix:
                 raise ValueError(f"{name} has {t.numel()} entries, expected {size}")
             return t.contiguous()
 
-        return cls(tree, r, dev(D, (1 << L) * m * m, "D"), dev(U, n * r * L, "U"), dev(V, n * r * L, "V"))
+        return cls(tree, r, dev(D, (1 << L) * m * m, "D"), dev(U, n * C_, "U"), dev(V, n * C_, "V"), ranks)
 
     @classmethod
     def from_level_panels(cls, n: int, m: int, d_big, u_panels, v_panels, rank: int | None = None,
-                          round_rank: bool = True, device="cuda") -> "HodlrMatrix":
+                          round_rank: bool = True, device="cuda", per_level: bool = True) -> "HodlrMatrix":
         """Ingest the SPEC's ragged representation (SPEC.md:147-160, 208-211);
-        see :func:`pad_level_panels`."""
-        r, U, V = pad_level_panels(n, m, u_panels, v_panels, rank, round_rank)
+        see :func:`pad_level_panels`.  per_level=True pads each level to its own
+        (rounded) rank -- the per-level-rank layout of ``hodlr_desc.ranks`` --
+        else every level to one rank."""
+        r, U, V, ranks = pad_level_panels(n, m, u_panels, v_panels, rank, round_rank, per_level=per_level,
+                                          with_ranks=True)
         D = np.asarray(d_big.cpu() if hasattr(d_big, "cpu") else d_big)
-        return cls.from_buffers(n, m, r, D, U.astype(D.dtype, copy=False), V.astype(D.dtype, copy=False), device=device)
+        return cls.from_buffers(n, m, r, D, U.astype(D.dtype, copy=False), V.astype(D.dtype, copy=False), device=device,
+                                ranks=ranks)
 
     def clone(self) -> "HodlrMatrix":
-        return HodlrMatrix(self.tree, self.rank, self.D.clone(), self.U.clone(), self.V.clone())
+        return HodlrMatrix(self.tree, self.rank, self.D.clone(), self.U.clone(), self.V.clone(), self.ranks)
 
     def storage_report(self) -> dict:
         """Scalar counts vs Thm. 2: diag m N, bases 2 r N L."""
-        n, m, r, L = self.n, self.m, self.rank, self.L
+        n, m, C_ = self.n, self.m, self.cols
         es = self.D.element_size()
         return {
             "scalars_diagonal": m * n,
-            "scalars_bases": 2 * r * n * L,
+            "scalars_bases": 2 * C_ * n,
             "bytes_diagonal": m * n * es,
-            "bytes_bases": 2 * r * n * L * es,
-            "formula_prediction": m * n + 2 * r * n * L,
-            "factorization_scalars_thm2": m * n + r * n * L,
+            "bytes_bases": 2 * C_ * n * es,
+            "formula_prediction": m * n + 2 * C_ * n,
+            "factorization_scalars_thm2": m * n + C_ * n,
         }
 
     def matvec(self, x, stream=None):
@@ -269,6 +306,21 @@ class HodlrFactorization:
     kinfo: "object"
     variant: str = "pivoted_standard"
     flops: dict = field(default_factory=dict)
+    ranks: tuple | None = None  # per-level ranks (as the factored HodlrMatrix)
+
+    @property
+    def level_ranks(self) -> tuple:
+        return tuple(self.ranks) if self.ranks is not None else (self.rank,) * self.L
+
+    def _k_offsets(self, level: int):
+        """(K offset, pivot offset, rank) of parent level ``level``'s blocks."""
+        ko = kp = 0
+        rk = self.level_ranks
+        for lv in range(level):
+            s = 2 * rk[lv]
+            ko += (1 << lv) * s * s
+            kp += (1 << lv) * s
+        return ko, kp, rk[level]
 
     @property
     def n(self):
@@ -283,7 +335,7 @@ class HodlrFactorization:
         return self.tree.n >> self.tree.depth
 
     def desc(self) -> _lib.Desc:
-        return _lib.Desc(self.n, self.m, self.rank, self.L, _dtype_tag(self.D))
+        return _lib.make_desc(self.n, self.m, self.rank, self.L, _dtype_tag(self.D), self.ranks)
 
     def cfactors(self) -> _lib.Factors:
         p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
@@ -299,16 +351,16 @@ class HodlrFactorization:
         return LuPivots(sw, pm, [int(i) for i in np.flatnonzero(self.dinfo.cpu().numpy())])
 
     def k_pivots(self, level: int) -> LuPivots:
-        r2, npar = 2 * self.rank, 1 << level
-        lo = (npar - 1) * r2
+        _, lo, r = self._k_offsets(level)
+        r2, npar = 2 * r, 1 << level
         sw = self.kswaps[lo : lo + npar * r2].view(npar, r2).cpu().numpy().astype(np.int64)
         pm = self.kperm[lo : lo + npar * r2].view(npar, r2).cpu().numpy().astype(np.int64)
         info = self.kinfo[npar - 1 : 2 * npar - 1].cpu().numpy()
         return LuPivots(sw, pm, [int(i) for i in np.flatnonzero(info)])
 
     def k_block(self, level: int):
-        r2, npar = 2 * self.rank, 1 << level
-        lo = (npar - 1) * r2 * r2
+        lo, _, r = self._k_offsets(level)
+        r2, npar = 2 * r, 1 << level
         return self.K[lo : lo + npar * r2 * r2]
 
 
@@ -341,23 +393,32 @@ def _workspace(nbytes: int, device, stream=None):
     return buf
 
 
-def flop_report(n: int, m: int, r: int) -> dict:
-    """Per-phase factor flops with the reference counters (backend.py:240-251)."""
+def flop_report(n: int, m: int, r: int, ranks=None) -> dict:
+    """Per-phase factor flops with the reference counters (backend.py:240-251);
+    ``ranks``: per-level ranks (level l' at ranks[l'-1])."""
     L = int(round(math.log2(n // m)))
     nl = 1 << L
+    rk = list(ranks) if ranks is not None else [r] * L
+    cc = [0]
+    for k in rk:
+        cc.append(cc[-1] + k)
     rep = {
         "leaf_getrf": lu_factor_flops(m) * nl,
-        "leaf_getrs": lu_solve_flops(m, r * L) * nl if L else 0,
+        "leaf_getrs": lu_solve_flops(m, cc[L]) * nl if L else 0,
         "tw_gemm": 0, "k_getrf": 0, "k_getrs": 0, "update_gemm": 0, "per_level_gemm": {},
     }
     for lv in range(L):
         nc = n >> (lv + 1)
-        tw = gemm_flops(r, nc, r * (lv + 1)) * (1 << (lv + 1))
-        up = gemm_flops(nc, r, r * lv) * (1 << (lv + 1)) if lv else 0
+        k, wc = rk[lv], cc[lv]  # rank of level lv + 1, columns of levels 1..lv
+        if k == 0:
+            rep["per_level_gemm"][lv] = 0
+            continue
+        tw = gemm_flops(k, nc, wc + k) * (1 << (lv + 1))
+        up = gemm_flops(nc, k, wc) * (1 << (lv + 1)) if lv and wc else 0
         rep["tw_gemm"] += tw
         rep["update_gemm"] += up
-        rep["k_getrf"] += lu_factor_flops(2 * r) * (1 << lv)
-        rep["k_getrs"] += lu_solve_flops(2 * r, r * lv) * (1 << lv) if lv else 0
+        rep["k_getrf"] += lu_factor_flops(2 * k) * (1 << lv)
+        rep["k_getrs"] += lu_solve_flops(2 * k, wc) * (1 << lv) if lv and wc else 0
         rep["per_level_gemm"][lv] = tw + up
     rep["total"] = sum(v for k, v in rep.items() if k != "per_level_gemm")
     return rep
@@ -377,14 +438,19 @@ def _alloc_factorization(h: HodlrMatrix, variant: str = "pivoted_standard") -> H
     n, m, r, L = h.n, h.m, h.rank, h.L
     nl = 1 << L
     nk = nl - 1
+    rk = h.level_ranks
+    ksz = sum((1 << lv) * (2 * rk[lv]) ** 2 for lv in range(L))
+    kps = sum((1 << lv) * 2 * rk[lv] for lv in range(L))
+    kis = sum(_dinv_size(1 << lv, 2 * rk[lv], fp64) for lv in range(L)) if L else 1
     i32 = dict(dtype=torch.int32, device=dev)
     return HodlrFactorization(
         tree=h.tree, rank=r, D=h.D, Dinv=torch.empty(_dinv_size(nl, m, fp64), dtype=h.D.dtype, device=dev),
-        Y=h.U, V=h.V, K=torch.empty(nk * 4 * r * r, dtype=h.D.dtype, device=dev),
-        Kinv=torch.empty(_dinv_size(nk, 2 * r, fp64), dtype=h.D.dtype, device=dev),
+        Y=h.U, V=h.V, K=torch.empty(ksz, dtype=h.D.dtype, device=dev),
+        Kinv=torch.empty(max(kis, 1), dtype=h.D.dtype, device=dev),
         dswaps=torch.empty(nl * m, **i32), dperm=torch.empty(nl * m, **i32), dinfo=torch.zeros(nl, **i32),
-        kswaps=torch.empty(max(nk, 1) * 2 * r, **i32), kperm=torch.empty(max(nk, 1) * 2 * r, **i32),
-        kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r),
+        kswaps=torch.empty(max(kps, 1), **i32), kperm=torch.empty(max(kps, 1), **i32),
+        kinfo=torch.zeros(max(nk, 1), **i32), variant=variant, flops=flop_report(n, m, r, ranks=h.ranks),
+        ranks=h.ranks,
     )
 
 
@@ -399,6 +465,8 @@ def factorize(h: HodlrMatrix, variant: str = "pivoted_standard", check: bool = T
         raise ValueError(f"unknown variant {variant!r} (supported: {VARIANTS})")
     if h.D.dtype not in (torch.float64, torch.float32):
         raise TypeError(f"unsupported dtype {h.D.dtype} (float64: DMMA path; float32: preconditioner path)")
+    if h.ranks is not None and h.D.dtype != torch.float64:
+        raise TypeError("per-level ranks: float64 only (the fp32 preconditioner path takes one rank)")
     lib = _lib.load()
     dev = h.D.device
     f = _alloc_factorization(h, variant)
@@ -671,7 +739,8 @@ def logdet(fact: HodlrFactorization):
     neg = (dd < 0).sum()
     ar = torch.arange(m, device=dd.device, dtype=torch.int32)
     nswap = (fact.dswaps.view(nl, m) != ar).sum()
-    if L:
+    blockswap = 0
+    if L and fact.ranks is None:
         nk, r2 = nl - 1, 2 * r
         kd = fact.K.view(nk, r2, r2).diagonal(dim1=1, dim2=2)
         logabs = logabs + torch.log(kd.abs()).sum()
@@ -679,8 +748,18 @@ def logdet(fact: HodlrFactorization):
         ak = torch.arange(r2, device=dd.device, dtype=torch.int32)
         nswap = nswap + (fact.kswaps[: nk * r2].view(nk, r2) != ak).sum()
         blockswap = nk * (r * r % 2)
-    else:
-        blockswap = 0
+    elif L:  # per-level ranks: level by level
+        for lv in range(L):
+            ko, kp, k = fact._k_offsets(lv)
+            if k == 0:
+                continue
+            npar, r2 = 1 << lv, 2 * k
+            kd = fact.K[ko : ko + npar * r2 * r2].view(npar, r2, r2).diagonal(dim1=1, dim2=2)
+            logabs = logabs + torch.log(kd.abs()).sum()
+            neg = neg + (kd < 0).sum()
+            ak = torch.arange(r2, device=dd.device, dtype=torch.int32)
+            nswap = nswap + (fact.kswaps[kp : kp + npar * r2].view(npar, r2) != ak).sum()
+            blockswap += npar * (k * k % 2)
     parity = (int(neg) + int(nswap) + blockswap) % 2
     return float(logabs), (-1.0 if parity else 1.0)
 
@@ -748,8 +827,10 @@ def solve_with_refinement(fact: HodlrFactorization, h: HodlrMatrix, b, max_iters
 # ---------------------------------------------------------------------------
 
 
-def random_hodlr(n: int, m: int, r: int, seed: int = 0, s: float = 1.0, device="cuda", dtype=None) -> HodlrMatrix:
-    """Seeded exact uniform-rank HODLR generated directly in HBM.
+def random_hodlr(n: int, m: int, r: int, seed: int = 0, s: float = 1.0, device="cuda", dtype=None,
+                 ranks=None) -> HodlrMatrix:
+    """Seeded exact HODLR generated directly in HBM (uniform rank r, or
+    per-level ``ranks``, level l' at ranks[l'-1]).
 
     D_a = N(0,1)/sqrt(m) + 4 I; level-l U ~ N(0, s^2/n_l), V ~ N(0, 1/n_l).
     (Same distribution as the oracle's numpy generator; different stream.)
@@ -759,20 +840,46 @@ def random_hodlr(n: int, m: int, r: int, seed: int = 0, s: float = 1.0, device="
     L = int(round(math.log2(n // m)))
     if n != m << L:
         raise ValueError("need N = m 2^L")
+    rk = tuple(int(x) for x in ranks) if ranks is not None else (r,) * L
+    if len(rk) != L:
+        raise ValueError(f"ranks: {L} per-level ranks expected")
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     nl = 1 << L
     D = torch.randn(nl * m * m, generator=g, device=device, dtype=dtype).mul_(1.0 / math.sqrt(m))
     D.view(nl, m, m).diagonal(dim1=1, dim2=2).add_(4.0)
-    U = torch.randn(n * r * L, generator=g, device=device, dtype=dtype)
-    V = torch.randn(n * r * L, generator=g, device=device, dtype=dtype)
+    C_ = sum(rk)
+    U = torch.randn(n * C_, generator=g, device=device, dtype=dtype)
+    V = torch.randn(n * C_, generator=g, device=device, dtype=dtype)
+    c0 = 0
     for lv in range(1, L + 1):
         nlv = n >> lv
-        sl = slice((lv - 1) * r * n, lv * r * n)
+        sl = slice(c0 * n, (c0 + rk[lv - 1]) * n)
         U[sl].mul_(s / math.sqrt(nlv))
         V[sl].mul_(1.0 / math.sqrt(nlv))
-    return HodlrMatrix(ClusterTree(n, L), r, D, U, V)
+        c0 += rk[lv - 1]
+    if ranks is None:
+        return HodlrMatrix(ClusterTree(n, L), r, D, U, V)
+    return HodlrMatrix.from_buffers(n, m, 0, D, U, V, device=device, ranks=rk)
 
 
 def tree_for(n: int, leaf_size: int) -> ClusterTree:
     return build_tree(n, leaf_size)
+
+
+def truncate_ranks(h: HodlrMatrix, ranks) -> HodlrMatrix:
+    """Per-level rank truncation of a uniform-rank HodlrMatrix: level l' keeps
+    its first ranks[l'-1] basis columns (ACA crosses are ordered by
+    selection, so the leading ones form the rank-k approximation), giving the
+    per-level-rank layout of ``hodlr_desc.ranks`` (e.g. the paper's rank
+    profiles, PAPER.md appendix).  A new matrix; ``h`` is unchanged."""
+    torch = _torch()
+    L, n, r = h.L, h.n, h.rank
+    rk = tuple(int(x) for x in ranks)
+    if len(rk) != L or any(k < 0 or k > r for k in rk):
+        raise ValueError(f"ranks: {L} per-level ranks in [0, {r}] expected")
+    if h.ranks is not None:
+        raise ValueError("truncate_ranks expects a uniform-rank matrix")
+    U = torch.cat([h.U.view(L, r, n)[lv, : rk[lv]].reshape(-1) for lv in range(L)]) if L else h.U[:0]
+    V = torch.cat([h.V.view(L, r, n)[lv, : rk[lv]].reshape(-1) for lv in range(L)]) if L else h.V[:0]
+    return HodlrMatrix.from_buffers(n, h.m, 0, h.D.clone(), U, V, device=h.D.device, ranks=rk)

@@ -27,9 +27,10 @@ Layout (little-endian throughout)::
                     (2^l - 1)(2r)^2), Dinv / Kinv solve aids
                     (hodlr_inv_elems per block; fp64 only)
 
-This engine stores uniform ranks (ragged inputs are zero-padded per level,
-SURVEY §8a), so every ranks[l] equals r; the field is kept per level so the
-format is the SPEC's.  Scalars are written as stored (no conversion).
+Ranks are per level (uniform matrices repeat r; ragged nodes are zero-padded
+to their level's rank); with per-level ranks the K blocks of parent
+level l are 2 ranks[l] square, stored level after level.  Scalars are written
+as stored (no conversion).
 """
 
 from __future__ import annotations
@@ -96,14 +97,15 @@ def payload_layout(hdr: dict, inv_elems=None):
     nl, nk = 1 << L, (1 << L) - 1
     lay = [("D", dt, nl * m * m), ("U", dt, n * sum(ranks)), ("V", dt, n * sum(ranks))]
     if hdr["kind"] == KIND_FACTORIZATION:
-        if len(set(ranks)) > 1:
-            raise ValueError("factorization dumps carry a uniform rank")
-        r = ranks[0] if ranks else 0
-        lay += [("dswaps", i4, nl * m), ("dperm", i4, nl * m), ("kswaps", i4, max(nk, 1) * 2 * r),
-                ("kperm", i4, max(nk, 1) * 2 * r), ("K", dt, nk * 4 * r * r)]
+        # per parent level lv the K blocks are 2 ranks[lv] square (uniform: 2r)
+        kps = sum((1 << lv) * 2 * ranks[lv] for lv in range(L))
+        ksz = sum((1 << lv) * (2 * ranks[lv]) ** 2 for lv in range(L))
+        lay += [("dswaps", i4, nl * m), ("dperm", i4, nl * m), ("kswaps", i4, max(kps, 1)),
+                ("kperm", i4, max(kps, 1)), ("K", dt, ksz)]
         if hdr["field"] == FIELD_F64:
             ie = inv_elems or (lambda s: 8 * s if s in (32, 64, 128) else (s * s if s == 16 else 0))
-            lay += [("Dinv", dt, max(nl * ie(m), 1)), ("Kinv", dt, max(nk * ie(2 * r), 1))]
+            kis = sum(max((1 << lv) * ie(2 * ranks[lv]), 1) for lv in range(L)) if L else 1
+            lay += [("Dinv", dt, max(nl * ie(m), 1)), ("Kinv", dt, max(kis, 1))]
     return lay
 
 
@@ -136,9 +138,10 @@ def dump(obj, path) -> None:
         return t.detach().cpu().numpy()
 
     field = FIELD_F64 if str(obj.D.dtype).endswith("float64") else FIELD_F32
-    L, n, m, r = obj.L, obj.n, obj.m, obj.rank
+    L, n, m = obj.L, obj.n, obj.m
+    ranks = list(obj.level_ranks)
     if isinstance(obj, HodlrMatrix):
-        write_raw(path, KIND_MATRIX, field, n, m, [r] * L, [host(obj.D), host(obj.U), host(obj.V)])
+        write_raw(path, KIND_MATRIX, field, n, m, ranks, [host(obj.D), host(obj.U), host(obj.V)])
         return
     if not isinstance(obj, HodlrFactorization):
         raise TypeError(f"cannot dump {type(obj).__name__}")
@@ -148,7 +151,7 @@ def dump(obj, path) -> None:
             host(obj.kperm), host(obj.K)]
     if field == FIELD_F64:
         bufs += [host(obj.Dinv), host(obj.Kinv)]
-    write_raw(path, KIND_FACTORIZATION, field, n, m, [r] * L, bufs)
+    write_raw(path, KIND_FACTORIZATION, field, n, m, ranks, bufs)
 
 
 def load(path, device="cuda"):
@@ -164,14 +167,13 @@ def load(path, device="cuda"):
     hdr, buf = read_raw(path, inv_elems=lambda s: int(lib.hodlr_inv_elems(s)))
     n, m, L = hdr["n"], hdr["m"], hdr["L"]
     ranks = [int(x) for x in hdr["ranks"]]
-    if len(set(ranks)) > 1:
-        raise ValueError("ragged per-level ranks: pad to the maximum with HodlrMatrix.from_level_panels")
-    r = ranks[0] if ranks else 0
+    r = max(ranks, default=0)
+    per_level = tuple(ranks) if len(set(ranks)) > 1 else None
     dev = torch.device(device)
     t = {k: torch.from_numpy(v.copy()).to(dev) for k, v in buf.items()}
     tree = ClusterTree(n, L)
     if hdr["kind"] == KIND_MATRIX:
-        return HodlrMatrix(tree, r, t["D"], t["U"], t["V"])
+        return HodlrMatrix(tree, r, t["D"], t["U"], t["V"], per_level)
     nl, nk = 1 << L, (1 << L) - 1
     i32 = dict(dtype=torch.int32, device=dev)
     dt = t["D"].dtype
@@ -179,7 +181,7 @@ def load(path, device="cuda"):
         tree=tree, rank=r, D=t["D"], Dinv=t.get("Dinv", torch.empty(1, dtype=dt, device=dev)), Y=t["U"], V=t["V"],
         K=t["K"], Kinv=t.get("Kinv", torch.empty(1, dtype=dt, device=dev)), dswaps=t["dswaps"], dperm=t["dperm"],
         dinfo=torch.zeros(nl, **i32), kswaps=t["kswaps"], kperm=t["kperm"], kinfo=torch.zeros(max(nk, 1), **i32),
-        flops=flop_report(n, m, r),
+        flops=flop_report(n, m, r, ranks=per_level), ranks=per_level,
     )
 
 

@@ -32,11 +32,15 @@ from oracle import hodlr_oracle as orc  # noqa: E402
 from oracle.ref_driver import BlockRef, ref_factorize, ref_solve  # noqa: E402  (reference kernels)
 
 CASES = [
-    # name, N, m, r, s(U scale), seed, nrhs
+    # name, N, m, r, s(U scale), seed, nrhs[, per-level ranks (level 1..L)]
     ("n256_m16_r4_s1", 256, 16, 4, 1.0, 11, 3),
     ("n512_m32_r8_s16", 512, 32, 8, 16.0, 12, 2),
     ("n1024_m64_r16_s16", 1024, 64, 16, 16.0, 13, 1),
     ("n512_m16_r32_s16", 512, 16, 32, 16.0, 14, 2),
+    # per-level ranks (SPEC.md:147-160 ragged panels padded per level; the paper's
+    # Laplace rank profiles fall from the top levels and rise again near the leaves)
+    ("ragged_n2048_m32_r16-8-16-32-16-32", 2048, 32, 32, 4.0, 15, 2, (16, 8, 16, 32, 16, 32)),
+    ("ragged_n1024_m64_r32-0-16-16", 1024, 64, 32, 16.0, 16, 1, (32, 0, 16, 16)),
 ]
 
 
@@ -48,8 +52,10 @@ def digest(*arrays) -> str:
 
 
 def main():
-    for name, n, m, r, s, seed, nrhs in CASES:
-        h = orc.make_exact_hodlr(n, m, r, seed=seed, s=s)
+    for case in CASES:
+        name, n, m, r, s, seed, nrhs = case[:7]
+        ranks = case[7] if len(case) > 7 else None
+        h = orc.make_exact_hodlr(n, m, r, seed=seed, s=s, ranks=ranks)
         L = h.lay.L
         in_digest = digest(h.D, h.U, h.V)
         b = np.random.default_rng(seed + 1000).standard_normal((n, nrhs))
@@ -57,15 +63,16 @@ def main():
 
         # reference kernels
         D, Y, V = h.D.copy(), h.U.copy(), h.V.copy()
-        dpiv, Ks, kpivs = ref_factorize(D, Y, V, n, m, r, L)
-        x = ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L)
+        dpiv, Ks, kpivs = ref_factorize(D, Y, V, n, m, r, L, ranks=ranks)
+        x = ref_solve(D, dpiv, Y, V, Ks, kpivs, b, n, m, r, L, ranks=ranks)
 
         # oracle restatement must be bit-identical
         fo = orc.factorize(h.copy())
         assert fo.D.tobytes() == D.tobytes(), name
         assert fo.Y.tobytes() == Y.tobytes(), name
         assert np.array_equal(fo.dpiv.perm, dpiv.perm) and np.array_equal(fo.dpiv.swaps, dpiv.swaps)
-        for lv in range(L):
+        live = [lv for lv in range(L) if kpivs[lv] is not None]  # rank-0 levels have no K blocks
+        for lv in live:
             assert fo.K[lv].tobytes() == Ks[lv].tobytes(), (name, lv)
             assert np.array_equal(fo.kpiv[lv].swaps, kpivs[lv].swaps), (name, lv)
         xo = orc.solve(fo, b)
@@ -77,14 +84,20 @@ def main():
         la, sg = orc.logdet(fo)
         sd, ld = np.linalg.slogdet(A)
         assert abs(la - ld) <= 1e-9 * max(1.0, abs(ld)) and sg == sd, (name, la, ld, sg, sd)
-        nontrivial = int(sum((kp.swaps[:, :r] != (np.arange(r) + r)).sum() for kp in kpivs))
+        nontrivial = int(sum((kpivs[lv].swaps[:, : h.lay.rk(lv + 1)] != (np.arange(h.lay.rk(lv + 1)) + h.lay.rk(lv + 1))).sum()
+                             for lv in live))
+        extra = {} if ranks is None else {"ranks": np.array(ranks)}
         np.savez_compressed(
             HERE / f"{name}.npz",
             n=n, m=m, r=r, s=s, seed=seed, nrhs=nrhs, input_sha256=in_digest,
             D_lu=D, d_swaps=dpiv.swaps, d_perm=dpiv.perm, Y=Y,
-            K=np.concatenate(Ks), k_swaps=np.concatenate([kp.swaps for kp in kpivs]),
-            k_perm=np.concatenate([kp.perm for kp in kpivs]),
-            b=b, x=x, logdet=la, logdet_sign=sg, dense_err=err,
+            K=np.concatenate([Ks[lv] for lv in live]),
+            # uniform: (nK, 2r) stacks; per-level ranks: flat, level after level
+            k_swaps=(np.concatenate([kpivs[lv].swaps for lv in live]) if ranks is None
+                     else np.concatenate([kpivs[lv].swaps.ravel() for lv in live])),
+            k_perm=(np.concatenate([kpivs[lv].perm for lv in live]) if ranks is None
+                    else np.concatenate([kpivs[lv].perm.ravel() for lv in live])),
+            b=b, x=x, logdet=la, logdet_sign=sg, dense_err=err, **extra,
         )
         print(f"{name}: L={L} oracle==reference bitwise; dense err {err:.2e}; "
               f"logdet {la:.6f} ({sg:+.0f}); nontrivial K pivots {nontrivial}")

@@ -306,8 +306,8 @@ def test_ragged_level_panels_vs_oracle_on_the_padded_layout():
 
     n, m, L = 1 << 12, 64, 6
     D, ups, vps, A = ragged(n, m, L, seed=5, width=32, kmax=24)
-    h = hb.HodlrMatrix.from_level_panels(n, m, D, ups, vps)
-    assert h.rank == 32
+    h = hb.HodlrMatrix.from_level_panels(n, m, D, ups, vps, per_level=False)
+    assert h.rank == 32 and h.ranks is None
     r, U, V = hb.pad_level_panels(n, m, ups, vps)
     fo = orc.factorize(orc.HodlrData(orc.Layout(n, m, r), D.copy(), U, V))
     f = hb.factorize(h)

@@ -171,6 +171,27 @@ if "cfg4g" in which or "cfg4" in which:
                                              "relres": res64}}), flush=True)
     del op, h32
     torch.cuda.empty_cache()
+if "profile" in which:
+    # the Laplace operator at N = 2^22 with the paper's rank profile (PAPER.md appendix:
+    # 24 22 15 14 13 13 13 13 14 14 15 16 16 17 17 18, levels 1..16), per-level ranks padded
+    # to the fused-kernel ranks, vs the same operator at uniform rank 32
+    n, m = 1 << 22, 64
+    prof = (24, 22, 15, 14, 13, 13, 13, 13, 14, 14, 15, 16, 16, 17, 17, 18)
+    padded = tuple(16 if k <= 16 else 32 for k in prof)
+    h32 = hb.laplace_dl_hodlr(n, m, 32)
+    rows = []
+    for name, h in (("uniform 32", h32), ("per-level (paper profile, padded)", hb.truncate_ranks(h32, padded))):
+        tf, ts, res, eager = time_factor_solve(n, m, 32, torch.float64, reps=3, h0=h, graph=False)
+        fl = hb.flop_report(n, m, 32, ranks=h.ranks)["total"]
+        rows.append({"layout": name, "ranks": list(h.level_ranks), "t_factor_ms": round(tf, 3),
+                     "t_solve_ms": round(ts, 3), "factor_gflop": round(fl / 1e9, 1), "relres": res,
+                     "bytes_UV": 2 * h.U.numel() * 8})
+        if h is not h32:
+            del h
+    print(json.dumps({"config": "Laplace DL N=2^22 at the paper's rank profile vs uniform rank 32", "runs": rows}),
+          flush=True)
+    del h32
+    torch.cuda.empty_cache()
 if "cfg5" in which:
     n, m, r = 1 << 20, 64, 32
     f = hb.factorize(hb.random_hodlr(n, m, r, seed=0, s=1.0), check=False)
