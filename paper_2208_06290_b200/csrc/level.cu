@@ -515,10 +515,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <int R, int GPW, bool LATE>
+// SOLVE: the multi-RHS solve step (columns = right-hand sides, ragged last
+// group masked, V may be null at the last level) with the reduction order of
+// solve_level_kernel (each 64-row chunk's [W|T] contribution a DMMA chain from
+// zero, added to the running sum in row order) -- bit-identical to it.
+template <int R, int GPW, bool LATE, bool SOLVE = false>
 __global__ void __launch_bounds__(256, 2)
     level_update5_kernel(LevelArgs g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV) {
-  using Cfg = Level4Cfg<R, false>;
+  using Cfg = Level4Cfg<R, SOLVE>;
   constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8, NI = Cfg::NI, NS = 3;
   constexpr uint32_t PANEL_BYTES = (uint32_t)Cfg::PANEL * sizeof(double);  // = box bytes (P x R)
   extern __shared__ __align__(1024) double sm5[];  // TMA destinations: 128-byte aligned stages
@@ -529,8 +533,9 @@ __global__ void __launch_bounds__(256, 2)
   const int seg = blockIdx.x / g.ncg, cg = blockIdx.x % g.ncg;
   const int64_t seg0 = (int64_t)seg * g.seg_rows;
   const int nch = g.seg_rows / CH;
-  const int G = g.ncols >> 3;
+  const int G = SOLVE ? (g.ncols + 7) >> 3 : g.ncols >> 3;
   const int gb = cg * g.tpc, ge = min(G, gb + g.tpc);
+  const bool want_tw = !SOLVE || g.V != nullptr;
 
   if (t == 0) {
 #pragma unroll
@@ -544,10 +549,10 @@ __global__ void __launch_bounds__(256, 2)
   auto issue = [&](int ch) {
     const int st = ch % NS;
     double* As = sm + st * Cfg::STAGE;
-    mbar_expect_tx(&full[st], 2 * PANEL_BYTES);
+    mbar_expect_tx(&full[st], (want_tw ? 2 : 1) * PANEL_BYTES);
     const int row = (int)(seg0 + (int64_t)ch * CH);
     tma_load_2d(As, &tmA, row, 0, &full[st]);
-    tma_load_2d(As + Cfg::PANEL, &tmV, row, 0, &full[st]);
+    if (want_tw) tma_load_2d(As + Cfg::PANEL, &tmV, row, 0, &full[st]);
   };
   if (t == 0)
     for (int c = 0; c < NS - 1 && c < nch; ++c) issue(c);
@@ -571,9 +576,19 @@ __global__ void __launch_bounds__(256, 2)
       const int grp = gb + warp + 8 * q;
       if (grp < ge) {
         const int col = grp * 8 + ar;
-        double* cptr = g.C + row0 + (int64_t)col * g.ldc + 4 * ac;
+        const bool cok = !SOLVE || col < g.ncols;
+        double* cptr = g.C + row0 + (int64_t)(cok ? col : 0) * g.ldc + 4 * ac;
         double acc[2 * NI][2], cin[2 * NI][2];
-        if constexpr (LATE) {
+        if constexpr (SOLVE) {
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            if (cok) {
+              ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+            } else {
+              acc[2 * i][0] = acc[2 * i + 1][0] = acc[2 * i][1] = acc[2 * i + 1][1] = 0.0;
+            }
+          }
+        } else if constexpr (LATE) {
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
             ldg_v4(cptr + 16 * i, cin[2 * i][0], cin[2 * i + 1][0], cin[2 * i][1], cin[2 * i + 1][1]);
@@ -583,10 +598,11 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
           for (int i = 0; i < NI; ++i) ldg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
         }
-        const double* wc = Wp + (int64_t)col * (2 * R) + 2 * ac;
+        const double* wc = Wp + (int64_t)(cok ? col : 0) * (2 * R) + 2 * ac;
 #pragma unroll
         for (int kt = 0; kt < R / 8; ++kt) {
-          const double2 w2 = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
+          double2 w2 = make_double2(0.0, 0.0);
+          if (cok) w2 = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const double a = -(u ? w2.y : w2.x);
@@ -599,22 +615,44 @@ __global__ void __launch_bounds__(256, 2)
             }
           }
         }
-        if constexpr (LATE) {
+        if constexpr (LATE && !SOLVE) {
 #pragma unroll
           for (int i = 0; i < 2 * NI; ++i) acc[i][0] = cin[i][0] + acc[i][0], acc[i][1] = cin[i][1] + acc[i][1];
         }
+        if (cok) {
 #pragma unroll
-        for (int i = 0; i < NI; ++i) stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+          for (int i = 0; i < NI; ++i)
+            stg_v4(cptr + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+        }
+        if (!want_tw) continue;
+        if constexpr (SOLVE) {
+          double pp[RT][2];
 #pragma unroll
-        for (int i = 0; i < NI; ++i)
+          for (int jr = 0; jr < RT; ++jr) pp[jr][0] = pp[jr][1] = 0.0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+          for (int i = 0; i < NI; ++i)
 #pragma unroll
-            for (int jr = 0; jr < RT; ++jr) {
-              const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
-              dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i][h], v2.x);
-              dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i + 1][h], v2.y);
-            }
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int jr = 0; jr < RT; ++jr) {
+                const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
+                dmma_8x8x4(pp[jr][0], pp[jr][1], acc[2 * i][h], v2.x);
+                dmma_8x8x4(pp[jr][0], pp[jr][1], acc[2 * i + 1][h], v2.y);
+              }
+#pragma unroll
+          for (int jr = 0; jr < RT; ++jr) tw[q][jr][0] += pp[jr][0], tw[q][jr][1] += pp[jr][1];
+        } else {
+#pragma unroll
+          for (int i = 0; i < NI; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int jr = 0; jr < RT; ++jr) {
+                const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
+                dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i][h], v2.x);
+                dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i + 1][h], v2.y);
+              }
+        }
       }
     }
     __syncwarp();
@@ -626,6 +664,7 @@ __global__ void __launch_bounds__(256, 2)
       issue(c2);
     }
   }
+  if (!want_tw) return;
   const int64_t qn = seg0 / g.node_rows;
   double* out;
   int64_t ld;
@@ -639,7 +678,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
   for (int q = 0; q < GPW; ++q) {
     const int grp = gb + warp + 8 * q;
-    if (grp < ge) {
+    if (grp < ge && (!SOLVE || grp * 8 + ar < g.ncols)) {
       const int col = grp * 8 + ar;
 #pragma unroll
       for (int jr = 0; jr < RT; ++jr)
@@ -665,9 +704,9 @@ static EncodeTiledFn encode_tiled() {
 }
 
 // panel = rows [0, rows) x R columns of a column-major slab (ld lda); box = (CH + 2) x R
-template <int R>
+template <int R, bool SOLVE = false>
 static bool panel_map(CUtensorMap* m, const double* base, int64_t rows, int64_t lda) {
-  using Cfg = Level4Cfg<R, false>;
+  using Cfg = Level4Cfg<R, SOLVE>;
   EncodeTiledFn enc = encode_tiled();
   if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) || ((lda * 8) & 15)) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)R};
@@ -896,6 +935,12 @@ __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
   }
 }
 
+// the shared-panel multi-RHS solve step fed by TMA (level_update5_kernel, solve mode)
+#ifndef HODLR_SOLVE_TMA
+#define HODLR_SOLVE_TMA 1
+#endif
+constexpr bool kSolveTma = HODLR_SOLVE_TMA;
+
 // 9-16 RHS at r <= 32: two 8-column groups share every panel load (12 RHS 4.17 -> 3.41 ms)
 constexpr bool kSolvePairs = true;
 
@@ -907,6 +952,38 @@ static hodlr_status run_solve_level(const LevelArgs& g, int64_t nblk, cudaStream
     solve_level_kernel<R, 1><<<(unsigned)nblk, 256, 0, st>>>(g);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
+}
+
+// multi-RHS solve step on the TMA-fed kernel (solve mode), one column group per
+// warp at R = 64 (register budget), up to 2 at R <= 32
+template <int R, int GPW>
+static hodlr_status launch_level5_solve(const LevelArgs& g, int64_t nseg, int64_t rows, cudaStream_t st) {
+  using Cfg = Level4Cfg<R, true>;
+  constexpr size_t smem = (size_t)3 * Cfg::STAGE * sizeof(double);
+  CUtensorMap ta, tv;
+  if (!panel_map<R, true>(&ta, g.A1, rows, g.lda)) return HODLR_ERR_ARG;
+  if (g.V != nullptr) {
+    if (!panel_map<R, true>(&tv, g.V, rows, g.lda)) return HODLR_ERR_ARG;
+  } else {
+    tv = ta;  // unused (no next-level w)
+  }
+  smem_attr(level_update5_kernel<R, GPW, false, true>, (int)smem);
+  level_update5_kernel<R, GPW, false, true><<<(unsigned)(nseg * g.ncg), 256, smem, st>>>(g, ta, tv);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+template <int R>
+static hodlr_status run_level4_solve(const LevelArgs& g, int64_t nseg, cudaStream_t st);
+
+template <int R>
+static hodlr_status run_level5_solve(const LevelArgs& g, int64_t nseg, int64_t rows, cudaStream_t st) {
+  const int gpw = (g.tpc + 7) / 8;
+  if (gpw <= 1) return launch_level5_solve<R, 1>(g, nseg, rows, st);
+  if constexpr (R <= 32) {
+    if (gpw <= 2) return launch_level5_solve<R, 2>(g, nseg, rows, st);
+  }
+  return run_level4_solve<R>(g, nseg, st);
 }
 
 template <int R>
@@ -964,9 +1041,16 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
     g.ncg = (G + gpc - 1) / gpc;
     g.tpc = gpc;
     const int64_t nseg = n / g.seg_rows;
-    s = r == 16 ? run_level4_solve<16>(g, nseg, st)
-        : r == 32 ? run_level4_solve<32>(g, nseg, st)
-                  : run_level4_solve<64>(g, nseg, st);
+    // TMA feed: rank 64 at any nrhs (5-10 % faster), rank <= 32 up to 32 RHS (2-3 %);
+    // 64-128 RHS at rank 32 stay on cp.async (4 % faster there; profiles/r02_ab_solve.txt)
+    if (kSolveTma && (r >= 64 || nrhs <= 32))
+      s = r == 16 ? run_level5_solve<16>(g, nseg, n, st)
+          : r == 32 ? run_level5_solve<32>(g, nseg, n, st)
+                    : run_level5_solve<64>(g, nseg, n, st);
+    else
+      s = r == 16 ? run_level4_solve<16>(g, nseg, st)
+          : r == 32 ? run_level4_solve<32>(g, nseg, st)
+                    : run_level4_solve<64>(g, nseg, st);
   } else {
     s = r == 16 ? run_solve_level<16>(g, nblk, st)
         : r == 32 ? run_solve_level<32>(g, nblk, st)

@@ -16,4 +16,4 @@ for nrhs in [int(x) for x in sys.argv[1:]]:
         if it >= 2:
             ts.append(e0.elapsed_time(e1))
     out.append(f"{nrhs}:{statistics.median(ts):.2f}")
-print("WIDE=" + os.environ.get("HODLR_SOLVE_WIDE", "1"), " ".join(out))
+print(" ".join(out))
