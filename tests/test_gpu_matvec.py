@@ -183,3 +183,25 @@ def test_dump_load_roundtrip_matrix_and_factorization(tmp_path):
     f32 = hb.factorize(h32)
     hb.dump(f32, tmp_path / "f32.hodlr")
     assert torch.equal(hb.solve(f32, b.float()), hb.solve(hb.load(tmp_path / "f32.hodlr"), b.float()))
+
+
+def test_hodlr_bench_cli_cells(tmp_path):
+    # SPEC.md:537-574 harness on the device: records, the 14 CSV columns, and byte-identical
+    # output (timing columns excluded) for identical config + seed
+    from paper_2208_06290_b200 import cli
+
+    cfg = tmp_path / "cells.txt"
+    cfg.write_text("[cell]\nproblem=laplace\nn=4096\nrank=16\nruns=2\n[cell]\nproblem=standin\nn=4096\nrank=16\n"
+                   "precision=single\nruns=2\n")
+    outs = []
+    for k in range(2):
+        out = tmp_path / f"r{k}.csv"
+        assert cli.main(["--config", str(cfg), "--out", str(out), "--seed", "3"]) == 0
+        recs = cli.parse_results(out.read_text(), "csv")
+        assert [r["problem"] for r in recs] == ["laplace", "standin"]
+        assert recs[0]["relres"] < 1e-13 and recs[1]["relres"] < 1e-5
+        assert recs[0]["ranks"] == "/".join(["16"] * 6)
+        for r in recs:
+            r.pop("t_f_seconds"), r.pop("t_s_seconds")
+        outs.append(recs)
+    assert outs[0] == outs[1]
