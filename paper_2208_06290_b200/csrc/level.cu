@@ -22,6 +22,15 @@
 
 namespace hodlr {
 
+// factorization level steps with <= 4 column groups per CTA: two warps per group
+// (row halves), so all 8 warps work (level 1 at cfg2: level phase 14.36 -> 14.31
+// ms same-box; letting the schedule prefer <= 4 groups per CTA at the other
+// levels was slower, 14.96 ms -- profiles/r02_ab_rowsplit.txt)
+#ifndef HODLR_LEVEL_ROWSPLIT
+#define HODLR_LEVEL_ROWSPLIT 1
+#endif
+constexpr bool kLevelRowSplit = HODLR_LEVEL_ROWSPLIT;
+
 struct LevelArgs {
   double* C;  // rows [0, n) of the updated block, column-major
   int64_t ldc;
@@ -519,11 +528,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 // group masked, V may be null at the last level) with the reduction order of
 // solve_level_kernel (each 64-row chunk's [W|T] contribution a DMMA chain from
 // zero, added to the running sum in row order) -- bit-identical to it.
-template <int R, int GPW, bool LATE, bool SOLVE = false>
+template <int R, int GPW, bool LATE, bool SOLVE = false, int RS = 1>
 __global__ void __launch_bounds__(256, 2)
     level_update5_kernel(LevelArgs g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV) {
   using Cfg = Level4Cfg<R, SOLVE>;
-  constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8, NI = Cfg::NI, NS = 3;
+  constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8, NS = 3;
+  // RS = 2 (factorization, <= 4 column groups per CTA): warps w and w + 4 share
+  // group w, each on half of the chunk's 16-row bands; their [W|T] partials
+  // are added at the end (half 0 + half 1)
+  static_assert(RS == 1 || (RS == 2 && !SOLVE && GPW == 1), "row split: factorization, one group per warp");
+  constexpr int NI = Cfg::NI / RS;
   constexpr uint32_t PANEL_BYTES = (uint32_t)Cfg::PANEL * sizeof(double);  // = box bytes (P x R)
   extern __shared__ __align__(1024) double sm5[];  // TMA destinations: 128-byte aligned stages
   double* sm = sm5;
@@ -536,6 +550,8 @@ __global__ void __launch_bounds__(256, 2)
   const int G = SOLVE ? (g.ncols + 7) >> 3 : g.ncols >> 3;
   const int gb = cg * g.tpc, ge = min(G, gb + g.tpc);
   const bool want_tw = !SOLVE || g.V != nullptr;
+  const int wg = RS == 1 ? warp : (warp & 3);    // group slot of this warp
+  const int band0 = RS == 1 ? 0 : (warp >> 2) * NI;  // first 16-row band of this warp's half
 
   if (t == 0) {
 #pragma unroll
@@ -573,11 +589,11 @@ __global__ void __launch_bounds__(256, 2)
     const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
 #pragma unroll
     for (int q = 0; q < GPW; ++q) {
-      const int grp = gb + warp + 8 * q;
+      const int grp = gb + wg + 8 * q;
       if (grp < ge) {
         const int col = grp * 8 + ar;
         const bool cok = !SOLVE || col < g.ncols;
-        double* cptr = g.C + row0 + (int64_t)(cok ? col : 0) * g.ldc + 4 * ac;
+        double* cptr = g.C + row0 + 16 * band0 + (int64_t)(cok ? col : 0) * g.ldc + 4 * ac;
         double acc[2 * NI][2], cin[2 * NI][2];
         if constexpr (SOLVE) {
 #pragma unroll
@@ -606,7 +622,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const double a = -(u ? w2.y : w2.x);
-            const double* ak = As + (8 * kt + 2 * ac + u) * P + 2 * ar;
+            const double* ak = As + (8 * kt + 2 * ac + u) * P + 2 * ar + 16 * band0;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
               const double2 b2 = *reinterpret_cast<const double2*>(ak + 16 * i);
@@ -635,7 +651,7 @@ __global__ void __launch_bounds__(256, 2)
             for (int h = 0; h < 2; ++h)
 #pragma unroll
               for (int jr = 0; jr < RT; ++jr) {
-                const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
+                const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * (i + band0) + 4 * ac + 2 * h);
                 dmma_8x8x4(pp[jr][0], pp[jr][1], acc[2 * i][h], v2.x);
                 dmma_8x8x4(pp[jr][0], pp[jr][1], acc[2 * i + 1][h], v2.y);
               }
@@ -648,7 +664,7 @@ __global__ void __launch_bounds__(256, 2)
             for (int h = 0; h < 2; ++h)
 #pragma unroll
               for (int jr = 0; jr < RT; ++jr) {
-                const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * i + 4 * ac + 2 * h);
+                const double2 v2 = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * (i + band0) + 4 * ac + 2 * h);
                 dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i][h], v2.x);
                 dmma_8x8x4(tw[q][jr][0], tw[q][jr][1], acc[2 * i + 1][h], v2.y);
               }
@@ -675,9 +691,27 @@ __global__ void __launch_bounds__(256, 2)
     out = g.TW + (qn >> 1) * g.tw_stride + (qn & 1) * R;
     ld = 2 * R;
   }
+  if constexpr (RS == 2) {  // half 1 hands its partials to half 0 (the pipeline smem is free now)
+    __syncthreads();
+    double* xs = sm + (warp & 3) * (32 * RT * 2);
+    if (warp >= 4) {
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr) {
+        xs[(jr * 2) * 32 + lane] = tw[0][jr][0];
+        xs[(jr * 2 + 1) * 32 + lane] = tw[0][jr][1];
+      }
+    }
+    __syncthreads();
+    if (warp >= 4) return;
+#pragma unroll
+    for (int jr = 0; jr < RT; ++jr) {
+      tw[0][jr][0] += xs[(jr * 2) * 32 + lane];
+      tw[0][jr][1] += xs[(jr * 2 + 1) * 32 + lane];
+    }
+  }
 #pragma unroll
   for (int q = 0; q < GPW; ++q) {
-    const int grp = gb + warp + 8 * q;
+    const int grp = gb + wg + 8 * q;
     if (grp < ge && (!SOLVE || grp * 8 + ar < g.ncols)) {
       const int col = grp * 8 + ar;
 #pragma unroll
@@ -718,15 +752,15 @@ static bool panel_map(CUtensorMap* m, const double* base, int64_t rows, int64_t 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int R, int GPW>
+template <int R, int GPW, int RS = 1>
 static hodlr_status launch_level5(const LevelArgs& g, int64_t nseg, int64_t rows, cudaStream_t st) {
   using Cfg = Level4Cfg<R, false>;
   constexpr bool LATE = GPW <= 2 && LEVEL4_LATE_DEFAULT;
   constexpr size_t smem = (size_t)3 * Cfg::STAGE * sizeof(double);
   CUtensorMap ta, tv;
   if (!panel_map<R>(&ta, g.A1, rows, g.lda) || !panel_map<R>(&tv, g.V, rows, g.lda)) return HODLR_ERR_ARG;
-  smem_attr(level_update5_kernel<R, GPW, LATE>, (int)smem);
-  level_update5_kernel<R, GPW, LATE><<<(unsigned)(nseg * g.ncg), 256, smem, st>>>(g, ta, tv);
+  smem_attr(level_update5_kernel<R, GPW, LATE, false, RS>, (int)smem);
+  level_update5_kernel<R, GPW, LATE, false, RS><<<(unsigned)(nseg * g.ncg), 256, smem, st>>>(g, ta, tv);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
@@ -741,6 +775,7 @@ static hodlr_status run_level4(const LevelArgs& g, int64_t nseg, cudaStream_t st
 template <int R>
 static hodlr_status run_level5(const LevelArgs& g, int64_t nseg, int64_t rows, cudaStream_t st) {
   const int gpw = (g.tpc + 7) / 8;
+  if (g.tpc <= 4 && kLevelRowSplit) return launch_level5<R, 1, 2>(g, nseg, rows, st);  // 8 warps on <= 4 groups
   if (gpw <= 1) return launch_level5<R, 1>(g, nseg, rows, st);
   if (gpw <= 2) return launch_level5<R, 2>(g, nseg, rows, st);
   return run_level4<R>(g, nseg, st);
@@ -1032,7 +1067,7 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   LevelArgs g{X, ldx, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)cta_rows,
               node_rows, nrhs, 1, 1};
   hodlr_status s;
-  if (nrhs >= (r >= 64 ? 25 : 17)) {  // crossovers measured (cfg5 sweeps; 9-16 RHS: paired streaming)
+  if (nrhs >= 17) {  // crossover measured (cfg5 sweeps, profiles/r02_ab_x9.txt; 9-16 RHS: streaming kernel)
     // many right-hand sides: shared-memory panels reused by every column group
     // (same segments and reduction order as solve_level_kernel)
     const int G = (nrhs + 7) / 8;

@@ -615,6 +615,9 @@ class _SolveGraph:
             x_cm.copy_(self.X)
 
 
+_GRAPH_AUTO_BYTES = 1 << 28  # graph=None: capture solves whose rhs block is <= 256 MB
+
+
 def _solve_eager(lib, fact, x, nrhs, dev, so):
     desc = fact.desc()
     wsb = lib.hodlr_solve_workspace(C.byref(desc), nrhs)
@@ -631,9 +634,10 @@ def solve(fact: HodlrFactorization, b, stream=None, graph: bool | None = None):
     The level-by-level launch sequence of ``hodlr_solve`` (~4 L small
     launches) can run as a CUDA graph captured per (factorization, nrhs,
     stream): graph=None (default) launches the first solve of a key eagerly and
-    captures from the second on (repeated solves replay, one-shot solves pay no
-    capture); graph=True captures at once; graph=False always launches
-    eagerly.  All run the same kernels on the same data, bit for bit."""
+    captures from the second on when the rhs block is at most 256 MB (repeated
+    latency-bound solves replay, one-shot solves pay no capture, big multi-RHS
+    solves stay eager); graph=True captures at once; graph=False always
+    launches eagerly.  All run the same kernels on the same data, bit for bit."""
     torch = _torch()
     lib = _lib.load()
     is_np = isinstance(b, np.ndarray)
@@ -662,7 +666,10 @@ def solve(fact: HodlrFactorization, b, stream=None, graph: bool | None = None):
                 if graph is not False and not torch.cuda.is_current_stream_capturing():
                     calls = fact.__dict__.setdefault("_solve_calls", {})
                     calls[key] = calls.get(key, 0) + 1
-                    if graph or calls[key] >= 2:  # capture after the eager call(s): later calls replay
+                    # capture after the eager call(s) -- later calls replay.  graph=None captures
+                    # only latency-bound sizes (the graph owns an N x nrhs buffer + workspace)
+                    small = n * nrhs * x.element_size() <= _GRAPH_AUTO_BYTES
+                    if graph or (calls[key] >= 2 and small):
                         graphs[key] = _SolveGraph(fact, nrhs, so)
         out = x.t().reshape(bt.shape)
         if bt.device == dev:
