@@ -528,11 +528,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 // group masked, V may be null at the last level) with the reduction order of
 // solve_level_kernel (each 64-row chunk's [W|T] contribution a DMMA chain from
 // zero, added to the running sum in row order) -- bit-identical to it.
-template <int R, int GPW, bool LATE, bool SOLVE = false, int RS = 1>
+template <int R, int GPW, bool LATE, bool SOLVE = false, int RS = 1, int NS = 3>
 __global__ void __launch_bounds__(256, 2)
     level_update5_kernel(LevelArgs g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV) {
   using Cfg = Level4Cfg<R, SOLVE>;
-  constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8, NS = 3;
+  constexpr int CH = Cfg::CH, P = Cfg::P, RT = R / 8;
   // RS = 2 (factorization, <= 4 column groups per CTA): warps w and w + 4 share
   // group w, each on half of the chunk's 16-row bands; their [W|T] partials
   // are added at the end (half 0 + half 1)
@@ -752,15 +752,15 @@ static bool panel_map(CUtensorMap* m, const double* base, int64_t rows, int64_t 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int R, int GPW, int RS = 1>
+template <int R, int GPW, int RS = 1, int NS = 3>
 static hodlr_status launch_level5(const LevelArgs& g, int64_t nseg, int64_t rows, cudaStream_t st) {
   using Cfg = Level4Cfg<R, false>;
   constexpr bool LATE = GPW <= 2 && LEVEL4_LATE_DEFAULT;
-  constexpr size_t smem = (size_t)3 * Cfg::STAGE * sizeof(double);
+  constexpr size_t smem = (size_t)NS * Cfg::STAGE * sizeof(double);
   CUtensorMap ta, tv;
   if (!panel_map<R>(&ta, g.A1, rows, g.lda) || !panel_map<R>(&tv, g.V, rows, g.lda)) return HODLR_ERR_ARG;
-  smem_attr(level_update5_kernel<R, GPW, LATE, false, RS>, (int)smem);
-  level_update5_kernel<R, GPW, LATE, false, RS><<<(unsigned)(nseg * g.ncg), 256, smem, st>>>(g, ta, tv);
+  smem_attr(level_update5_kernel<R, GPW, LATE, false, RS, NS>, (int)smem);
+  level_update5_kernel<R, GPW, LATE, false, RS, NS><<<(unsigned)(nseg * g.ncg), 256, smem, st>>>(g, ta, tv);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
