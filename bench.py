@@ -304,8 +304,10 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
     workload = args.workload or ("cfg3" if (args.gpus > 1 or world > 1) else "cfg2")
-    N, r = WORKLOADS[workload]
+    N, r = WORKLOADS[workload][:2]
     n = CPU_SAMPLE_N if workload == "cfg2" else CPU_SAMPLE_N // 2
+    if args.cpu_sample_rows:
+        n = args.cpu_sample_rows
     cpu_reference(1 << 12, threads)  # warm-up (imports, thread pool)
     t0 = time.perf_counter()
     sample = cpu_sample(n, args.problem) if workload == "cfg2" else cfg3_cpu_sample(n)  # outside the timed steps
@@ -710,6 +712,7 @@ def main():
     ap.add_argument("--no-relres", action="store_true", help="sharded run: skip the full-operator residual")
     ap.add_argument("--sharded", action="store_true", help="use the row-sharded path even on one GPU")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (single-GPU testing)")
+    ap.add_argument("--cpu-sample-rows", type=int, default=None, help=argparse.SUPPRESS)  # tests: smaller CPU sample
     args = ap.parse_args()
     if args.impl == "reference":
         if dist_env()[0] == 0:
