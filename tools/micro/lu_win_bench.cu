@@ -37,10 +37,6 @@ static int run(int S, int batch, int mode, bool fp32) {
                                                i1, nullptr, 0, 0, 0);
   };
   auto win = [&]() {
-    if constexpr (sizeof(T) == 8)
-      if (S == 64 && getenv("WIN2"))
-        return hodlr::launch_getrf_win2(batch, mode, A, S, (int64_t)S * S, O2, S, (int64_t)S * S, s2, p2, i2, D2,
-                                        8 * S, 0);
     return hodlr::launch_getrf_win<T>(S, batch, mode, A, S, (int64_t)S * S, O2, S, (int64_t)S * S, s2, p2, i2,
                                       sizeof(T) == 8 ? D2 : nullptr, 8 * S, 0);
   };
@@ -88,12 +84,6 @@ static int run(int S, int batch, int mode, bool fp32) {
 
 int main() {
   int bad = 0;
-  if (getenv("WIN2")) {  // s = 64 two-threads-per-row kernel vs production
-    for (int mode : {0, 1})
-      for (int batch : {1, 8, 128, 1024, 2048, 4096, 8192, 16384}) bad += run<double>(64, batch, mode, false);
-    printf("%s\n", bad ? "MISMATCHES" : "all bitwise equal");
-    return bad != 0;
-  }
   for (int S : {64, 32})
     for (int mode : {0, 1})
       for (int batch : {1, 4, 32, 128, 512, 1024, 2048, 8192, 16384}) bad += run<double>(S, batch, mode, false);
