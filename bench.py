@@ -659,6 +659,8 @@ def run_sharded(args):
     value = (f_flops + s_flops) / (t_step * 1e-3) / 1e12
     if rank == 0:
         desc = WORKLOADS[workload][2] + (PROBLEM_DESC[args.problem] if workload == "cfg2" else "")
+        if n != WORKLOADS[workload][0]:
+            desc += f"; run at N=2^{int(round(math.log2(n)))} (--rows)"
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
@@ -702,7 +704,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=None, help="matrix size (default: the workload's)")
+    ap.add_argument("--rows", dest="n", type=int, default=None, help="matrix size N (default: the workload's)")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default=None,
                     help="cfg2 (default at N=1) or cfg3 (default for the sharded N>1 run)")
     ap.add_argument("--problem", choices=("laplace", "standin"), default="laplace",
