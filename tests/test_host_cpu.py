@@ -169,3 +169,24 @@ def test_product_path_has_no_cpu_fallback():
         pytest.skip("GPU present")
     with pytest.raises(_lib.HodlrNativeError):
         hb.HodlrMatrix.from_buffers(128, 16, 2, np.zeros(8 * 256), np.zeros(128 * 6), np.zeros(128 * 6))
+
+
+def test_per_level_rank_descriptors_without_gpu():
+    # hodlr_desc.ranks: workspace sizing, validation (max must equal r; fp32 takes one rank),
+    # and the per-level flop counters vs the oracle's instrumented counts
+    from oracle import hodlr_oracle as orc
+
+    lib = _lib.load()
+    ranks = (16, 32, 0, 16, 32, 64)
+    d = _lib.make_desc(4096, 64, 64, 6, _lib.F64, ranks)
+    assert lib.hodlr_factorize_workspace(ctypes.byref(d)) > 0
+    assert lib.hodlr_solve_workspace(ctypes.byref(d), 3) > 0
+    assert lib.hodlr_matvec_workspace(ctypes.byref(d), 3) > 0
+    assert lib.hodlr_factorize_workspace(ctypes.byref(_lib.make_desc(4096, 64, 32, 6, _lib.F64, ranks))) == 0
+    assert lib.hodlr_factorize_workspace(ctypes.byref(_lib.make_desc(4096, 64, 64, 6, _lib.F32, ranks))) == 0
+    assert lib.hodlr_build_workspace(ctypes.byref(d)) == 0  # the builders take one rank
+    h = orc.make_exact_hodlr(4096, 64, 64, seed=2, ranks=ranks)
+    f = orc.factorize(h)
+    rep = hb.flop_report(4096, 64, 64, ranks=ranks)
+    for k in ("leaf_getrf", "leaf_getrs", "tw_gemm", "k_getrf", "k_getrs", "update_gemm"):
+        assert rep[k] == f.flops[k], k
