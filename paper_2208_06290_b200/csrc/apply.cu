@@ -456,7 +456,7 @@ static bool apply2_ok(const ApplyArgs& g) {
 }
 
 
-// Narrow variant (ncols <= 8, the solve phase): one warp per block, the same
+// Narrow variant (the solve phase: up to narrow_cols right-hand sides): one warp per block, the same
 // DMMA instruction sequence per column as tri_apply2_kernel (so a column of a
 // multi-RHS solve is bit-identical to the single-vector solve), with the
 // packed inverses, the permutation and the V panel read straight from global
@@ -465,14 +465,17 @@ template <int S, int TWR>
 __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply_narrow_kernel(ApplyArgs g) {
   constexpr int NJ = S / 8, RT = TWR / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b = blockIdx.x * (AP_THREADS / 32) + warp;
+  // warp -> (block, column group): the groups of a block are consecutive warps,
+  // so the block's factors come from HBM once and from L1 for its other groups
+  const int64_t gw = (int64_t)blockIdx.x * (AP_THREADS / 32) + warp;
+  const int b = (int)(gw / g.groups);
   if (b >= g.batch) return;
   const int ar = lane >> 2, ac = lane & 3;
   const double* ti = g.tinv + (int64_t)b * g.strideI;
   const int32_t* pmb = g.perm + (int64_t)b * S;
   const double* Bb = g.B + aoff(b, g.bdiv, g.sB_hi, g.sB_lo);
   double* Xb = g.X + aoff(b, g.bdiv, g.sX_hi, g.sX_lo);
-  const int col = ar;
+  const int col = (int)(gw % g.groups) * 8 + ar;
   const bool ok = col < g.ncols;
   double bv[NJ][2];
   {
@@ -561,7 +564,9 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply_narrow
 
 template <int S, int TWR>
 static hodlr_status run_apply_narrow(ApplyArgs g, cudaStream_t st) {
-  const int64_t grid = ceil_div(g.batch, AP_THREADS / 32);
+  g.groups = (int)ceil_div(g.ncols, 8);
+  const int64_t grid = ceil_div((int64_t)g.batch * g.groups, AP_THREADS / 32);
+  if (grid > 2147483647LL) return HODLR_ERR_ARG;
   tri_apply_narrow_kernel<S, TWR><<<(unsigned)grid, AP_THREADS, 0, st>>>(g);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
@@ -649,12 +654,12 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const 
                            const int32_t* perm, const double* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double* X,
                            int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st,
                            const double* V = nullptr, int64_t ldv = 0, int64_t vstride = 0, int twr = 0,
-                           double* TW = nullptr, int64_t tw_stride = 0) {
+                           double* TW = nullptr, int64_t tw_stride = 0, int narrow_cols = 8) {
   if (batch == 0 || ncols == 0 || s == 0) return HODLR_OK;
   if ((ldi & 1) || (reinterpret_cast<uintptr_t>(tinv) & 15) || (strideT & 1)) return HODLR_ERR_ARG;
   ApplyArgs g{tinv, lu, ldi, strideT, inv_block_elems(s), perm, B, ldb, sB_hi, sB_lo, X, ldx, sX_hi, sX_lo, ncols, batch, bdiv, 1,
               V, ldv, vstride, TW, tw_stride};
-  const bool narrow = ncols <= 8;
+  const bool narrow = ncols <= narrow_cols;
   if (s == 128) {  // diagonal-block-inverse format, no fused reduction
     if (V || lu == nullptr || (reinterpret_cast<uintptr_t>(tinv) & 15)) return HODLR_ERR_ARG;
     if (narrow && apply_narrow_ok(g)) return run_apply_narrow<128, 0>(g, st);

@@ -23,7 +23,7 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const 
                            const int32_t* perm, const double* B, int64_t ldb, int64_t sB_hi, int64_t sB_lo, double* X,
                            int64_t ldx, int64_t sX_hi, int64_t sX_lo, int bdiv, cudaStream_t st,
                            const double* V = nullptr, int64_t ldv = 0, int64_t vstride = 0, int twr = 0,
-                           double* TW = nullptr, int64_t tw_stride = 0);
+                           double* TW = nullptr, int64_t tw_stride = 0, int narrow_cols = 8);
 hodlr_status tri_apply_f32(int s, int ncols, int batch, const float* lu, int64_t strideT, const int32_t* perm, float* Y,
                            int64_t ldy, int64_t sY, const float* V, int64_t ldv, int64_t vstride, int twr, float* TW,
                            int64_t tw_stride, cudaStream_t st);
@@ -234,10 +234,10 @@ static hodlr_status lu_factor(int s, int batch, int mode, const double* src, int
 // packed inverses, or row substitution for other block sizes.
 static hodlr_status lu_apply(int s, int ncols, int batch, const double* LU, const double* tinv, const int32_t* perm,
                              const double* B, int64_t ldb, int64_t sB, double* X, int64_t ldx, int64_t sX,
-                             cudaStream_t st) {
+                             cudaStream_t st, int narrow_cols = 8) {
   if (tri_size_ok(s)) {
     const hodlr_status r = tri_apply_f64(s, ncols, batch, LU, tinv, s, (int64_t)s * s, perm, B, ldb, sB, 0, X, ldx, sX,
-                                         0, 1, st);
+                                         0, 1, st, nullptr, 0, 0, 0, nullptr, 0, narrow_cols);
     if (r != HODLR_ERR_ARG) return r;
   }
   return launch_getrs<double>(s, ncols, batch, LU, s, (int64_t)s * s, perm, B, ldb, sB, X, ldx, sX, 0, st);
@@ -768,6 +768,13 @@ extern "C" hodlr_status hodlr_factorize_top(const hodlr_desc* d, const hodlr_fac
                   1, wp, ws.split, st);
 }
 
+// right-hand sides up to which the solve's triangular applies use the narrow
+// kernel (a warp per block and 8-column group; the block's factors read once)
+#ifndef HODLR_SOLVE_NARROW_COLS
+#define HODLR_SOLVE_NARROW_COLS 32
+#endif
+constexpr int kSolveNarrowCols = HODLR_SOLVE_NARROW_COLS;
+
 // Leaf solve + levels L-1 .. lv_stop over the caller's rows of X (ld ldx).
 // On return the workspace w region holds w of the local level-lv_stop node
 // (paired layout, local node 0) when lv_stop > 0.
@@ -795,13 +802,13 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
     if (rL > 0 && tri_size_ok(m)) {
       hodlr_status s = tri_apply_f64(m, nrhs, (int)nleaf, (const double*)f->D, (const double*)f->Dinv, m,
                                      (int64_t)m * m, f->dperm, X, ldx, m, 0, X, ldx, m, 0, 1, st, V + q.c[L] * n, n, m,
-                                     rL, w, (int64_t)2 * rL * nrhs);
+                                     rL, w, (int64_t)2 * rL * nrhs, kSolveNarrowCols);
       if (s == HODLR_OK) w_ready = true;
       else if (s != HODLR_ERR_ARG) return s;
     }
     if (!w_ready)
       TRY(lu_apply(m, nrhs, (int)nleaf, (const double*)f->D, (const double*)f->Dinv, f->dperm, X, ldx, m, X, ldx, m,
-                   st));
+                   st, kSolveNarrowCols));
   }
   if (q.cols() == 0 || L == 0) return HODLR_OK;
   for (int lv = L - 1; lv >= lv_stop; --lv) {
@@ -825,7 +832,7 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
     {
       Phase ph(HODLR_PHASE_SOLVE_K, st);
       TRY(lu_apply(2 * r, nrhs, npar, (const double*)f->K + koff, Kinv + kioff, f->kperm + kpoff, w, 2 * r,
-                   (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st));
+                   (int64_t)2 * r * nrhs, w2, 2 * r, (int64_t)2 * r * nrhs, st, kSolveNarrowCols));
     }
     // x_c -= Y_c w_c  fused with the next level's w = V^{(l)T} x    Alg.4 l.7 (+ l.5 of level l-1)
     // (fused when the next level has the same rank)
@@ -918,7 +925,7 @@ extern "C" hodlr_status hodlr_solve_top(const hodlr_desc* d, const hodlr_factors
   {
     Phase ph(HODLR_PHASE_SOLVE_K, st);
     TRY(lu_apply(2 * r, nrhs, 1, (const double*)f->K + kblk * 4 * r * r, (const double*)f->Kinv + kblk * inv_block_elems(2 * r),
-                 f->kperm + kblk * 2 * r, w_all + p * 2 * r * nrhs, 2 * r, 0, w2, 2 * r, 0, st));
+                 f->kperm + kblk * 2 * r, w_all + p * 2 * r * nrhs, 2 * r, 0, w2, 2 * r, 0, st, kSolveNarrowCols));
   }
   const double* Y = (const double*)f->Y;
   const double* V = (const double*)f->V;

@@ -970,6 +970,132 @@ __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
   }
 }
 
+// Multi-RHS solve level step, band-major: the same per-column DMMA chains as
+// solve_level_kernel (x tile chain over the ranks; w partial chain over the
+// chunk's rows in band order, each chunk partial from zero, summed in chunk
+// order), so every column is bit-identical to the single-vector solve, but each
+// warp walks its 64-row chunk one 16-row band at a time and applies every panel
+// fragment it loads to NG column groups at once.  Per group only the band's x
+// tiles (4 doubles) and the w partial (2 RT doubles) are live, so NG = 4 fits
+// the two-CTA register budget at R = 64: the Y / V panels stream from HBM once
+// per NG * 8 right-hand sides (solve_level_kernel re-reads them per 8 at R = 64).
+template <int R, int NG, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) solve_multi_kernel(LevelArgs g) {
+  constexpr int RT = R / 8;
+  __shared__ double ps[8][R * 8];  // chunk partials of one group: [chunk][col_local * R + rank]
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int64_t cta0 = (int64_t)blockIdx.x * g.seg_rows;
+  const int nchunk = g.seg_rows / 64;
+  const int64_t row0 = cta0 + 64 * warp;
+  const bool has_chunk = warp < nchunk;
+  const int c = has_chunk ? (int)(row0 / g.n_c) : 0;
+  const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
+  const bool want_w = g.V != nullptr;
+  const int G = (g.ncols + 7) >> 3;
+  const int cpn = (int)(g.node_rows / 64 < nchunk ? g.node_rows / 64 : nchunk);  // chunks per output unit
+  const int units = nchunk / cpn;
+  for (int gp = 0; gp < G; gp += NG) {
+    double p[NG][RT][2];
+#pragma unroll
+    for (int q = 0; q < NG; ++q)
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr) p[q][jr][0] = p[q][jr][1] = 0.0;
+    if (has_chunk) {
+      bool ok[NG];
+      const double* wq[NG];
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        const int col = (gp + q) * 8 + ar;
+        ok[q] = col < g.ncols;
+        wq[q] = Wp + (int64_t)(ok[q] ? col : 0) * (2 * R) + 2 * ac;
+      }
+#pragma unroll 1
+      for (int i = 0; i < 4; ++i) {
+        double acc[NG][2][2];
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+          if (ok[q]) {
+            ldg_v4(g.C + row0 + 16 * i + (int64_t)((gp + q) * 8 + ar) * g.ldc + 4 * ac, acc[q][0][0], acc[q][1][0],
+                   acc[q][0][1], acc[q][1][1]);
+          } else {
+            acc[q][0][0] = acc[q][1][0] = acc[q][0][1] = acc[q][1][1] = 0.0;
+          }
+        }
+        // ---- x^T += (-w'^T) Y^T over this band ----
+        const double* a1 = g.A1 + row0 + 16 * i + 2 * ar;
+#pragma unroll 2
+        for (int kt = 0; kt < R / 8; ++kt) {
+          double2 w2[NG];
+#pragma unroll
+          for (int q = 0; q < NG; ++q) {
+            w2[q] = make_double2(0.0, 0.0);
+            if (ok[q]) w2[q] = __ldg(reinterpret_cast<const double2*>(wq[q] + 8 * kt));
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const double2 b2 = __ldcs(reinterpret_cast<const double2*>(a1 + (int64_t)(8 * kt + 2 * ac + u) * g.lda));
+#pragma unroll
+            for (int q = 0; q < NG; ++q) {
+              const double a = -(u ? w2[q].y : w2[q].x);
+              dmma_8x8x4(acc[q][0][0], acc[q][0][1], a, b2.x);
+              dmma_8x8x4(acc[q][1][0], acc[q][1][1], a, b2.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NG; ++q)
+          if (ok[q])
+            stg_v4(g.C + row0 + 16 * i + (int64_t)((gp + q) * 8 + ar) * g.ldc + 4 * ac, acc[q][0][0], acc[q][1][0],
+                   acc[q][0][1], acc[q][1][1]);
+        if (want_w) {
+          // ---- this band's terms of the chunk partial p^T += x_new^T V ----
+          const double* vb = g.V + row0 + 16 * i + 4 * ac;
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int jr = 0; jr < RT; ++jr) {
+              const double2 v2 = __ldcs(reinterpret_cast<const double2*>(vb + (int64_t)(8 * jr + ar) * g.lda + 2 * h));
+#pragma unroll
+              for (int q = 0; q < NG; ++q) {
+                dmma_8x8x4(p[q][jr][0], p[q][jr][1], acc[q][0][h], v2.x);
+                dmma_8x8x4(p[q][jr][0], p[q][jr][1], acc[q][1][h], v2.y);
+              }
+            }
+        }
+      }
+    }
+    if (!want_w) continue;
+    // ---- fixed-order sums of the chunk partials per output node / CTA segment, one group at a time ----
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {
+      if (gp + q >= G) break;
+      if (has_chunk) {
+#pragma unroll
+        for (int jr = 0; jr < RT; ++jr)
+          *reinterpret_cast<double2*>(&ps[warp][ar * R + 8 * jr + 2 * ac]) = make_double2(p[q][jr][0], p[q][jr][1]);
+      }
+      __syncthreads();
+      for (int e = t; e < units * 8 * R; e += 256) {
+        const int uidx = e / (8 * R), mn = e % (8 * R);
+        const int cl = mn / R, rank = mn % R;
+        const int colg = (gp + q) * 8 + cl;
+        double sacc = 0.0;
+        for (int k = 0; k < cpn; ++k) sacc += ps[uidx * cpn + k][mn];
+        if (colg < g.ncols) {
+          if (g.partial) {
+            g.TW[(int64_t)blockIdx.x * R * g.ncols + rank + (int64_t)colg * R] = sacc;
+          } else {
+            const int64_t qn = (cta0 + (int64_t)uidx * cpn * 64) / g.node_rows;
+            g.TW[(qn >> 1) * g.tw_stride + (qn & 1) * R + rank + (int64_t)colg * 2 * R] = sacc;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // the shared-panel multi-RHS solve step fed by TMA (level_update5_kernel, solve mode)
 #ifndef HODLR_SOLVE_TMA
 #define HODLR_SOLVE_TMA 1
@@ -985,6 +1111,24 @@ static hodlr_status run_solve_level(const LevelArgs& g, int64_t nblk, cudaStream
     solve_level_kernel<R, R <= 32 ? 2 : 1><<<(unsigned)nblk, 256, 0, st>>>(g);
   else
     solve_level_kernel<R, 1><<<(unsigned)nblk, 256, 0, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+// most column groups (of 8 right-hand sides) the band-major streaming kernel takes
+#ifndef HODLR_SOLVE_MULTI_MAXG
+#define HODLR_SOLVE_MULTI_MAXG 3
+#endif
+constexpr int kSolveMultiMaxG = HODLR_SOLVE_MULTI_MAXG;
+
+template <int R>
+static hodlr_status run_solve_multi(const LevelArgs& g, int64_t nblk, int ng, cudaStream_t st) {
+  switch (ng) {
+    case 1: solve_multi_kernel<R, 1><<<(unsigned)nblk, 256, 0, st>>>(g); break;
+    case 2: solve_multi_kernel<R, 2><<<(unsigned)nblk, 256, 0, st>>>(g); break;
+    case 3: solve_multi_kernel<R, 3, R >= 64 ? 1 : 2><<<(unsigned)nblk, 256, 0, st>>>(g); break;
+    default: solve_multi_kernel<R, 4, R >= 32 ? 1 : 2><<<(unsigned)nblk, 256, 0, st>>>(g); break;
+  }
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
@@ -1067,10 +1211,17 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
   LevelArgs g{X, ldx, A1, V, lda, W, wstride, split ? part : TW, tw_stride, split ? 1 : 0, (int)n_c, (int)cta_rows,
               node_rows, nrhs, 1, 1};
   hodlr_status s;
-  if (nrhs >= 17) {  // crossover measured (cfg5 sweeps, profiles/r02_ab_x9.txt; 9-16 RHS: streaming kernel)
+  const int G = (nrhs + 7) / 8;
+  if (r >= 64 && G >= 2 && G <= kSolveMultiMaxG) {
+    // rank 64, 9-24 RHS: the band-major kernel, every group in one pass (r <= 32: the
+    // kt-major streaming kernel in pairs is faster; 25+ RHS: the shared-panel kernel)
+    const int passes = (G + 3) / 4, ng = (G + passes - 1) / passes;
+    s = r == 16 ? run_solve_multi<16>(g, nblk, ng, st)
+        : r == 32 ? run_solve_multi<32>(g, nblk, ng, st)
+                  : run_solve_multi<64>(g, nblk, ng, st);
+  } else if (nrhs >= 17) {  // crossover measured (cfg5 sweeps, profiles/r02_ab_x9.txt; 9-16 RHS: streaming kernel)
     // many right-hand sides: shared-memory panels reused by every column group
     // (same segments and reduction order as solve_level_kernel)
-    const int G = (nrhs + 7) / 8;
     const int gpc = std::min(G, r >= 64 ? 8 : 32);  // R = 64: one group per warp (register budget)
     g.seg_rows = (int)std::min<int64_t>(node_rows, cta_rows);
     g.ncg = (G + gpc - 1) / gpc;
