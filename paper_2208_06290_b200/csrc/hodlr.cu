@@ -47,6 +47,13 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
                              int nrhs, double* TW, int64_t tw_stride, double* part, size_t part_bytes,
                              cudaStream_t st);
 int64_t level_segment_rows(int64_t n, int64_t node, int sms);
+hodlr_status level_reduce_f64(const double* part, double* TW, int r, int ncols, int segs, int nnodes, int64_t tw_stride,
+                              cudaStream_t st);
+hodlr_status solve_step_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, double* X, int64_t ldx, const double* Y,
+                            const double* V, int64_t lda, const double* W, int64_t wstride, int nrhs, double* TW,
+                            int64_t tw_stride, double* part, size_t part_bytes, int sms, bool* used_partial,
+                            cudaStream_t st);
+int device_sm_count();
 hodlr_status level_f32(int r, int64_t n, int64_t n_c, int64_t node_rows, float* C, int64_t ldc, const float* A1,
                        const float* V, int64_t lda, const float* W, int64_t wstride, int ncols, float* TW,
                        int64_t tw_stride, float* part, size_t part_bytes, cudaStream_t st, int seg_max = 1024);
@@ -768,6 +775,12 @@ extern "C" hodlr_status hodlr_factorize_top(const hodlr_desc* d, const hodlr_fac
                   1, wp, ws.split, st);
 }
 
+// the TMA-fed persistent solve level step (solve.cu) before the streaming kernels
+#ifndef HODLR_SOLVE_STEP_TMA
+#define HODLR_SOLVE_STEP_TMA 1
+#endif
+constexpr bool kSolveStepTma = HODLR_SOLVE_STEP_TMA;
+
 // right-hand sides up to which the solve's triangular applies use the narrow
 // kernel (a warp per block and 8-column group; the block's factors read once)
 #ifndef HODLR_SOLVE_NARROW_COLS
@@ -841,8 +854,17 @@ static hodlr_status solve_local(const hodlr_desc* d, const hodlr_factors* f, int
     hodlr_status s;
     {
       Phase ph(HODLR_PHASE_SOLVE_LEVEL, st);
-      s = solve_level_f64(r, n, nc, 2 * nc, X, ldx, Y + q.c[lv + 1] * n, Vn, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
-                          (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st);
+      s = HODLR_ERR_ARG;
+      if (kSolveStepTma) {
+        bool used_partial = false;
+        s = solve_step_f64(r, n, nc, 2 * nc, X, ldx, Y + q.c[lv + 1] * n, Vn, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
+                           (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), device_sm_count(), &used_partial, st);
+        if (s == HODLR_OK && used_partial)
+          s = level_reduce_f64(part, w, r, nrhs, (int)(2 * nc / 512), (int)(n / (2 * nc)), (int64_t)2 * r * nrhs, st);
+      }
+      if (s == HODLR_ERR_ARG)
+        s = solve_level_f64(r, n, nc, 2 * nc, X, ldx, Y + q.c[lv + 1] * n, Vn, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
+                            (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st);
       if (s == HODLR_ERR_ARG)
         s = level_update_f64(r, n, nc, 2 * nc, X, ldx, Y + q.c[lv + 1] * n, Vn, n, w2, (int64_t)2 * r * nrhs, nrhs, w,
                              (int64_t)2 * r * nrhs, part, solve_part_bytes(d, nrhs), st, false);

@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace hodlr {
 
@@ -66,6 +67,8 @@ static int sm_count() {
   }
   return n;
 }
+
+int device_sm_count() { return sm_count(); }
 
 constexpr int LV_THREADS = 512;  // 16 warps: two per scheduler slot of each SMSP pair
 
@@ -497,33 +500,6 @@ constexpr bool LEVEL4_LATE_DEFAULT = LEVEL4_LATE;
 // stage it refills.  Arithmetic and per-column operation order are those of
 // level_update4_kernel (bit-identical results).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // SOLVE: the multi-RHS solve step (columns = right-hand sides, ragged last
 // group masked, V may be null at the last level) with the reduction order of
 // solve_level_kernel (each 64-row chunk's [W|T] contribution a DMMA chain from
@@ -721,35 +697,10 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    return reinterpret_cast<EncodeTiledFn>(p);
-  }();
-  return fn;
-}
-
 // panel = rows [0, rows) x R columns of a column-major slab (ld lda); box = (CH + 2) x R
 template <int R, bool SOLVE = false>
 static bool panel_map(CUtensorMap* m, const double* base, int64_t rows, int64_t lda) {
-  using Cfg = Level4Cfg<R, SOLVE>;
-  EncodeTiledFn enc = encode_tiled();
-  if (!enc || (reinterpret_cast<uintptr_t>(base) & 15) || ((lda * 8) & 15)) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)R};
-  const cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)Cfg::P, (cuuint32_t)R};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return panel_map_f64(m, base, rows, R, lda, Level4Cfg<R, SOLVE>::P);
 }
 
 template <int R, int GPW, int RS = 1, int NS = 3>
@@ -970,132 +921,6 @@ __global__ void __launch_bounds__(256, 2) solve_level_kernel(LevelArgs g) {
   }
 }
 
-// Multi-RHS solve level step, band-major: the same per-column DMMA chains as
-// solve_level_kernel (x tile chain over the ranks; w partial chain over the
-// chunk's rows in band order, each chunk partial from zero, summed in chunk
-// order), so every column is bit-identical to the single-vector solve, but each
-// warp walks its 64-row chunk one 16-row band at a time and applies every panel
-// fragment it loads to NG column groups at once.  Per group only the band's x
-// tiles (4 doubles) and the w partial (2 RT doubles) are live, so NG = 4 fits
-// the two-CTA register budget at R = 64: the Y / V panels stream from HBM once
-// per NG * 8 right-hand sides (solve_level_kernel re-reads them per 8 at R = 64).
-template <int R, int NG, int MINB = 2>
-__global__ void __launch_bounds__(256, MINB) solve_multi_kernel(LevelArgs g) {
-  constexpr int RT = R / 8;
-  __shared__ double ps[8][R * 8];  // chunk partials of one group: [chunk][col_local * R + rank]
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int ar = lane >> 2, ac = lane & 3;
-  const int64_t cta0 = (int64_t)blockIdx.x * g.seg_rows;
-  const int nchunk = g.seg_rows / 64;
-  const int64_t row0 = cta0 + 64 * warp;
-  const bool has_chunk = warp < nchunk;
-  const int c = has_chunk ? (int)(row0 / g.n_c) : 0;
-  const double* Wp = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R;
-  const bool want_w = g.V != nullptr;
-  const int G = (g.ncols + 7) >> 3;
-  const int cpn = (int)(g.node_rows / 64 < nchunk ? g.node_rows / 64 : nchunk);  // chunks per output unit
-  const int units = nchunk / cpn;
-  for (int gp = 0; gp < G; gp += NG) {
-    double p[NG][RT][2];
-#pragma unroll
-    for (int q = 0; q < NG; ++q)
-#pragma unroll
-      for (int jr = 0; jr < RT; ++jr) p[q][jr][0] = p[q][jr][1] = 0.0;
-    if (has_chunk) {
-      bool ok[NG];
-      const double* wq[NG];
-#pragma unroll
-      for (int q = 0; q < NG; ++q) {
-        const int col = (gp + q) * 8 + ar;
-        ok[q] = col < g.ncols;
-        wq[q] = Wp + (int64_t)(ok[q] ? col : 0) * (2 * R) + 2 * ac;
-      }
-#pragma unroll 1
-      for (int i = 0; i < 4; ++i) {
-        double acc[NG][2][2];
-#pragma unroll
-        for (int q = 0; q < NG; ++q) {
-          if (ok[q]) {
-            ldg_v4(g.C + row0 + 16 * i + (int64_t)((gp + q) * 8 + ar) * g.ldc + 4 * ac, acc[q][0][0], acc[q][1][0],
-                   acc[q][0][1], acc[q][1][1]);
-          } else {
-            acc[q][0][0] = acc[q][1][0] = acc[q][0][1] = acc[q][1][1] = 0.0;
-          }
-        }
-        // ---- x^T += (-w'^T) Y^T over this band ----
-        const double* a1 = g.A1 + row0 + 16 * i + 2 * ar;
-#pragma unroll 2
-        for (int kt = 0; kt < R / 8; ++kt) {
-          double2 w2[NG];
-#pragma unroll
-          for (int q = 0; q < NG; ++q) {
-            w2[q] = make_double2(0.0, 0.0);
-            if (ok[q]) w2[q] = __ldg(reinterpret_cast<const double2*>(wq[q] + 8 * kt));
-          }
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const double2 b2 = __ldcs(reinterpret_cast<const double2*>(a1 + (int64_t)(8 * kt + 2 * ac + u) * g.lda));
-#pragma unroll
-            for (int q = 0; q < NG; ++q) {
-              const double a = -(u ? w2[q].y : w2[q].x);
-              dmma_8x8x4(acc[q][0][0], acc[q][0][1], a, b2.x);
-              dmma_8x8x4(acc[q][1][0], acc[q][1][1], a, b2.y);
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < NG; ++q)
-          if (ok[q])
-            stg_v4(g.C + row0 + 16 * i + (int64_t)((gp + q) * 8 + ar) * g.ldc + 4 * ac, acc[q][0][0], acc[q][1][0],
-                   acc[q][0][1], acc[q][1][1]);
-        if (want_w) {
-          // ---- this band's terms of the chunk partial p^T += x_new^T V ----
-          const double* vb = g.V + row0 + 16 * i + 4 * ac;
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int jr = 0; jr < RT; ++jr) {
-              const double2 v2 = __ldcs(reinterpret_cast<const double2*>(vb + (int64_t)(8 * jr + ar) * g.lda + 2 * h));
-#pragma unroll
-              for (int q = 0; q < NG; ++q) {
-                dmma_8x8x4(p[q][jr][0], p[q][jr][1], acc[q][0][h], v2.x);
-                dmma_8x8x4(p[q][jr][0], p[q][jr][1], acc[q][1][h], v2.y);
-              }
-            }
-        }
-      }
-    }
-    if (!want_w) continue;
-    // ---- fixed-order sums of the chunk partials per output node / CTA segment, one group at a time ----
-#pragma unroll
-    for (int q = 0; q < NG; ++q) {
-      if (gp + q >= G) break;
-      if (has_chunk) {
-#pragma unroll
-        for (int jr = 0; jr < RT; ++jr)
-          *reinterpret_cast<double2*>(&ps[warp][ar * R + 8 * jr + 2 * ac]) = make_double2(p[q][jr][0], p[q][jr][1]);
-      }
-      __syncthreads();
-      for (int e = t; e < units * 8 * R; e += 256) {
-        const int uidx = e / (8 * R), mn = e % (8 * R);
-        const int cl = mn / R, rank = mn % R;
-        const int colg = (gp + q) * 8 + cl;
-        double sacc = 0.0;
-        for (int k = 0; k < cpn; ++k) sacc += ps[uidx * cpn + k][mn];
-        if (colg < g.ncols) {
-          if (g.partial) {
-            g.TW[(int64_t)blockIdx.x * R * g.ncols + rank + (int64_t)colg * R] = sacc;
-          } else {
-            const int64_t qn = (cta0 + (int64_t)uidx * cpn * 64) / g.node_rows;
-            g.TW[(qn >> 1) * g.tw_stride + (qn & 1) * R + rank + (int64_t)colg * 2 * R] = sacc;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 // the shared-panel multi-RHS solve step fed by TMA (level_update5_kernel, solve mode)
 #ifndef HODLR_SOLVE_TMA
 #define HODLR_SOLVE_TMA 1
@@ -1111,24 +936,6 @@ static hodlr_status run_solve_level(const LevelArgs& g, int64_t nblk, cudaStream
     solve_level_kernel<R, R <= 32 ? 2 : 1><<<(unsigned)nblk, 256, 0, st>>>(g);
   else
     solve_level_kernel<R, 1><<<(unsigned)nblk, 256, 0, st>>>(g);
-  HODLR_CHECK_LAUNCH();
-  return HODLR_OK;
-}
-
-// most column groups (of 8 right-hand sides) the band-major streaming kernel takes
-#ifndef HODLR_SOLVE_MULTI_MAXG
-#define HODLR_SOLVE_MULTI_MAXG 3
-#endif
-constexpr int kSolveMultiMaxG = HODLR_SOLVE_MULTI_MAXG;
-
-template <int R>
-static hodlr_status run_solve_multi(const LevelArgs& g, int64_t nblk, int ng, cudaStream_t st) {
-  switch (ng) {
-    case 1: solve_multi_kernel<R, 1><<<(unsigned)nblk, 256, 0, st>>>(g); break;
-    case 2: solve_multi_kernel<R, 2><<<(unsigned)nblk, 256, 0, st>>>(g); break;
-    case 3: solve_multi_kernel<R, 3, R >= 64 ? 1 : 2><<<(unsigned)nblk, 256, 0, st>>>(g); break;
-    default: solve_multi_kernel<R, 4, R >= 32 ? 1 : 2><<<(unsigned)nblk, 256, 0, st>>>(g); break;
-  }
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
@@ -1189,6 +996,9 @@ size_t solve_level_partial_bytes(int64_t n, int r, int nrhs) {
   return (size_t)(n / kSolveCtaRows + 1) * r * nrhs * sizeof(double);
 }
 
+hodlr_status level_reduce_f64(const double* part, double* TW, int r, int ncols, int segs, int nnodes, int64_t tw_stride,
+                              cudaStream_t st);
+
 // One solve level step over n rows of X (see solve_level_kernel).  Returns
 // ERR_ARG for unsupported shapes (caller falls back).
 hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, double* X, int64_t ldx,
@@ -1212,14 +1022,7 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
               node_rows, nrhs, 1, 1};
   hodlr_status s;
   const int G = (nrhs + 7) / 8;
-  if (r >= 64 && G >= 2 && G <= kSolveMultiMaxG) {
-    // rank 64, 9-24 RHS: the band-major kernel, every group in one pass (r <= 32: the
-    // kt-major streaming kernel in pairs is faster; 25+ RHS: the shared-panel kernel)
-    const int passes = (G + 3) / 4, ng = (G + passes - 1) / passes;
-    s = r == 16 ? run_solve_multi<16>(g, nblk, ng, st)
-        : r == 32 ? run_solve_multi<32>(g, nblk, ng, st)
-                  : run_solve_multi<64>(g, nblk, ng, st);
-  } else if (nrhs >= 17) {  // crossover measured (cfg5 sweeps, profiles/r02_ab_x9.txt; 9-16 RHS: streaming kernel)
+  if (nrhs >= 17) {  // crossover measured (cfg5 sweeps, profiles/r02_ab_x9.txt; 9-16 RHS: streaming kernel)
     // many right-hand sides: shared-memory panels reused by every column group
     // (same segments and reduction order as solve_level_kernel)
     const int gpc = std::min(G, r >= 64 ? 8 : 32);  // R = 64: one group per warp (register budget)
@@ -1243,11 +1046,15 @@ hodlr_status solve_level_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, d
                   : run_solve_level<64>(g, nblk, st);
   }
   if (s != HODLR_OK || !split) return s;
-  const int nnodes = (int)(n / node_rows);
-  const int64_t total = (int64_t)r * nrhs * nnodes;
-  const int segs = (int)(node_rows / cta_rows);
+  return level_reduce_f64(part, TW, r, nrhs, (int)(node_rows / cta_rows), (int)(n / node_rows), tw_stride, st);
+}
+
+// fixed-order sum of per-segment partials into the paired [W|T] / w layout
+hodlr_status level_reduce_f64(const double* part, double* TW, int r, int ncols, int segs, int nnodes, int64_t tw_stride,
+                              cudaStream_t st) {
+  const int64_t total = (int64_t)r * ncols * nnodes;
   const int64_t blocks = std::min<int64_t>(ceil_div(segs > 32 ? total * 32 : total, 256), 8 * (int64_t)sm_count());
-  level_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, TW, r, nrhs, segs, nnodes, tw_stride);
+  level_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, TW, r, ncols, segs, nnodes, tw_stride);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
