@@ -456,11 +456,54 @@ static bool apply2_ok(const ApplyArgs& g) {
 }
 
 
-// Narrow variant (the solve phase: up to narrow_cols right-hand sides): one warp per block, the same
-// DMMA instruction sequence per column as tri_apply2_kernel (so a column of a
-// multi-RHS solve is bit-identical to the single-vector solve), with the
-// packed inverses, the permutation and the V panel read straight from global
-// memory into fragments -- the phase is a single HBM pass over Tinv / V.
+// X = U^-1 L^-1 (P B) for one 8-column group of one block in the blocked
+// diagonal-block-inverse form: bv = the lane's gathered rows of P B, tl(jn, j)
+// = the (row 8 jn + ar, columns 8 j + 2 ac + {0, 1}) pair of the LU off the
+// diagonal tiles and of the diagonal-block inverse on them.  The DMMA sequence
+// is the one of tri_apply2_kernel (bit-identical columns).
+template <int NJ, typename TL>
+__device__ __forceinline__ void blocked_solve(const double (&bv)[NJ][2], double (&a2)[NJ][2], TL tl, int ar, int ac) {
+  double a1[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    double c0 = bv[j][0], c1 = bv[j][1];
+#pragma unroll
+    for (int i = 0; i < j; ++i) {
+      const double2 l = tl(j, i);
+      dmma_8x8x4(c0, c1, a1[i][0], -l.x);
+      dmma_8x8x4(c0, c1, a1[i][1], -l.y);
+    }
+    const double2 p = tl(j, j);
+    const int k0 = 2 * ac;
+    const double lx = k0 < ar ? p.x : (k0 == ar ? 1.0 : 0.0);
+    const double ly = k0 + 1 < ar ? p.y : (k0 + 1 == ar ? 1.0 : 0.0);
+    a1[j][0] = a1[j][1] = 0.0;
+    dmma_8x8x4(a1[j][0], a1[j][1], c0, lx);
+    dmma_8x8x4(a1[j][0], a1[j][1], c1, ly);
+  }
+#pragma unroll
+  for (int j = NJ - 1; j >= 0; --j) {
+    double c0 = a1[j][0], c1 = a1[j][1];
+#pragma unroll
+    for (int i = j + 1; i < NJ; ++i) {
+      const double2 u = tl(j, i);
+      dmma_8x8x4(c0, c1, a2[i][0], -u.x);
+      dmma_8x8x4(c0, c1, a2[i][1], -u.y);
+    }
+    const double2 p = tl(j, j);
+    const int k0 = 2 * ac;
+    const double ux = k0 >= ar ? p.x : 0.0;
+    const double uy = k0 + 1 >= ar ? p.y : 0.0;
+    a2[j][0] = a2[j][1] = 0.0;
+    dmma_8x8x4(a2[j][0], a2[j][1], c0, ux);
+    dmma_8x8x4(a2[j][0], a2[j][1], c1, uy);
+  }
+}
+
+// Narrow variant (the solve phase: up to narrow_cols right-hand sides): one
+// warp per (block, 8-column group), the packed inverses, the permutation and
+// the V panel read straight from global memory into fragments -- the phase is
+// a single HBM pass over Tinv / V.
 template <int S, int TWR>
 __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply_narrow_kernel(ApplyArgs g) {
   constexpr int NJ = S / 8, RT = TWR / 8;
@@ -487,50 +530,13 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply_narrow
       bv[j][1] = ok ? bc[p.y] : 0.0;
     }
   }
-  // [row][k] pair of rows 8 jn + ar, columns 8 j + 2 ac + {0, 1}: LU off the
-  // diagonal tiles, the diagonal-block inverse on them
   const double* lb = g.lu + (int64_t)b * g.strideT;
-  auto tl = [&](int jn, int j) {
+  double a2[NJ][2];
+  blocked_solve<NJ>(bv, a2, [&](int jn, int j) {
     if (jn == j) return __ldg(reinterpret_cast<const double2*>(ti + 64 * j + 8 * ar + 2 * ac));
     const double* q = lb + (8 * jn + ar) + (int64_t)(8 * j + 2 * ac) * g.ldi;
     return make_double2(__ldg(q), __ldg(q + g.ldi));
-  };
-  double a1[NJ][2];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    double c0 = bv[j][0], c1 = bv[j][1];
-#pragma unroll
-    for (int i = 0; i < j; ++i) {
-      const double2 l = tl(j, i);
-      dmma_8x8x4(c0, c1, a1[i][0], -l.x);
-      dmma_8x8x4(c0, c1, a1[i][1], -l.y);
-    }
-    const double2 p = tl(j, j);
-    const int k0 = 2 * ac;
-    const double lx = k0 < ar ? p.x : (k0 == ar ? 1.0 : 0.0);
-    const double ly = k0 + 1 < ar ? p.y : (k0 + 1 == ar ? 1.0 : 0.0);
-    a1[j][0] = a1[j][1] = 0.0;
-    dmma_8x8x4(a1[j][0], a1[j][1], c0, lx);
-    dmma_8x8x4(a1[j][0], a1[j][1], c1, ly);
-  }
-  double a2[NJ][2];
-#pragma unroll
-  for (int j = NJ - 1; j >= 0; --j) {
-    double c0 = a1[j][0], c1 = a1[j][1];
-#pragma unroll
-    for (int i = j + 1; i < NJ; ++i) {
-      const double2 u = tl(j, i);
-      dmma_8x8x4(c0, c1, a2[i][0], -u.x);
-      dmma_8x8x4(c0, c1, a2[i][1], -u.y);
-    }
-    const double2 p = tl(j, j);
-    const int k0 = 2 * ac;
-    const double ux = k0 >= ar ? p.x : 0.0;
-    const double uy = k0 + 1 >= ar ? p.y : 0.0;
-    a2[j][0] = a2[j][1] = 0.0;
-    dmma_8x8x4(a2[j][0], a2[j][1], c0, ux);
-    dmma_8x8x4(a2[j][0], a2[j][1], c1, uy);
-  }
+  }, ar, ac);
   if (ok) {
     double* xc = Xb + (int64_t)col * g.ldx + 2 * ac;
 #pragma unroll
@@ -561,6 +567,84 @@ __global__ void __launch_bounds__(AP_THREADS, S >= 128 ? 1 : 2) tri_apply_narrow
     }
   }
 }
+
+// Staged variant for small batches (the top levels of the solve's K phase,
+// where one block's dependent substitution chain is the whole launch): the CTA
+// copies its block's LU (pitch S + 2), diagonal-block inverses and permutation
+// into shared memory with every load in flight at once, then warp w solves
+// column group w from shared memory -- one memory latency per launch instead
+// of one per substitution step.  Same DMMA sequence (bit-identical).
+template <int S>
+__global__ void __launch_bounds__(AP_THREADS, 1) tri_apply_staged_kernel(ApplyArgs g) {
+  constexpr int NJ = S / 8, PL = S + 2;
+  extern __shared__ __align__(16) double stg[];
+  double* Ls = stg;                      // S columns x PL
+  double* Ts = stg + S * PL;             // 8 S inverse entries
+  int* Ps = reinterpret_cast<int*>(Ts + 8 * S);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int b = blockIdx.x;
+  const double* lb = g.lu + (int64_t)b * g.strideT;
+  const double* ti = g.tinv + (int64_t)b * g.strideI;
+  for (int e = t; e < S * (S / 2); e += AP_THREADS) {  // 16-byte pieces of the LU columns
+    const int c = e / (S / 2), r2 = e % (S / 2);
+    cp_async_16(Ls + c * PL + 2 * r2, lb + (int64_t)c * g.ldi + 2 * r2, 16);
+  }
+  for (int e = t; e < 4 * S; e += AP_THREADS) cp_async_16(Ts + 2 * e, ti + 2 * e, 16);
+  for (int e = t; e < S / 4; e += AP_THREADS) cp_async_16(Ps + 4 * e, g.perm + (int64_t)b * S + 4 * e, 16);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (warp >= g.groups) return;
+  const int ar = lane >> 2, ac = lane & 3;
+  const double* Bb = g.B + aoff(b, g.bdiv, g.sB_hi, g.sB_lo);
+  double* Xb = g.X + aoff(b, g.bdiv, g.sX_hi, g.sX_lo);
+  const int col = warp * 8 + ar;
+  const bool ok = col < g.ncols;
+  double bv[NJ][2];
+  {
+    const double* bc = Bb + (int64_t)(ok ? col : 0) * g.ldb;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int2 p = *reinterpret_cast<const int2*>(Ps + 8 * j + 2 * ac);
+      bv[j][0] = ok ? bc[p.x] : 0.0;
+      bv[j][1] = ok ? bc[p.y] : 0.0;
+    }
+  }
+  double a2[NJ][2];
+  blocked_solve<NJ>(bv, a2, [&](int jn, int j) {
+    if (jn == j) return *reinterpret_cast<const double2*>(Ts + 64 * j + 8 * ar + 2 * ac);
+    const double* q = Ls + (8 * jn + ar) + (8 * j + 2 * ac) * PL;
+    return make_double2(q[0], q[PL]);
+  }, ar, ac);
+  if (ok) {
+    double* xc = Xb + (int64_t)col * g.ldx + 2 * ac;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) *reinterpret_cast<double2*>(xc + 8 * j) = make_double2(a2[j][0], a2[j][1]);
+  }
+}
+
+template <int S>
+static hodlr_status run_apply_staged(ApplyArgs g, cudaStream_t st) {
+  constexpr size_t smem = ((size_t)S * (S + 2) + 8 * S) * sizeof(double) + S * sizeof(int);
+  g.groups = (int)ceil_div(g.ncols, 8);
+  if (g.groups > AP_THREADS / 32) return HODLR_ERR_ARG;
+  smem_attr(tri_apply_staged_kernel<S>, (int)smem);
+  tri_apply_staged_kernel<S><<<(unsigned)g.batch, AP_THREADS, smem, st>>>(g);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+static bool apply_staged_ok(const ApplyArgs& g) {
+  // 16-byte cp.async pieces of the LU columns, inverses and permutation
+  return !(g.ldi & 1) && !(g.strideT & 1) && !(reinterpret_cast<uintptr_t>(g.lu) & 15) && !(g.strideI & 1) &&
+         !(reinterpret_cast<uintptr_t>(g.perm) & 15) && !(reinterpret_cast<uintptr_t>(g.tinv) & 15);
+}
+
+// batches up to this many blocks take the staged kernel (latency-bound launches)
+#ifndef HODLR_STAGED_MAX_BATCH
+#define HODLR_STAGED_MAX_BATCH 148
+#endif
+constexpr int kStagedMaxBatch = HODLR_STAGED_MAX_BATCH;
 
 template <int S, int TWR>
 static hodlr_status run_apply_narrow(ApplyArgs g, cudaStream_t st) {
@@ -662,6 +746,7 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const 
   const bool narrow = ncols <= narrow_cols;
   if (s == 128) {  // diagonal-block-inverse format, no fused reduction
     if (V || lu == nullptr || (reinterpret_cast<uintptr_t>(tinv) & 15)) return HODLR_ERR_ARG;
+    if (narrow && batch <= kStagedMaxBatch && apply_narrow_ok(g) && apply_staged_ok(g)) return run_apply_staged<128>(g, st);
     if (narrow && apply_narrow_ok(g)) return run_apply_narrow<128, 0>(g, st);
     if (!narrow && apply2_ok(g)) return run_apply2<128, 0>(g, st);
     return HODLR_ERR_ARG;
@@ -688,6 +773,8 @@ hodlr_status tri_apply_f64(int s, int ncols, int batch, const double* lu, const 
       }
       return HODLR_ERR_ARG;
     }
+    if (narrow && batch <= kStagedMaxBatch && apply_narrow_ok(g) && apply_staged_ok(g))
+      return s == 64 ? run_apply_staged<64>(g, st) : run_apply_staged<32>(g, st);
     if (narrow && apply_narrow_ok(g)) return s == 64 ? run_apply_narrow<64, 0>(g, st) : run_apply_narrow<32, 0>(g, st);
     if (!narrow && apply2_ok(g)) return s == 64 ? run_apply2<64, 0>(g, st) : run_apply2<32, 0>(g, st);
     return HODLR_ERR_ARG;

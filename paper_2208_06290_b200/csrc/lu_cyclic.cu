@@ -550,21 +550,44 @@ __global__ void __launch_bounds__(128) trtri_sm_kernel(const double* __restrict_
 }
 
 template <int S>
+static hodlr_status run_trtri_sm(int batch, const double* out, int64_t ldo, int64_t strideo, double* tinv, int64_t ldi,
+                                 int64_t stridei, cudaStream_t st) {
+  constexpr size_t smem = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(double);
+  smem_attr(trtri_sm_kernel<S>, (int)smem);
+  trtri_sm_kernel<S><<<batch, 128, smem, st>>>(out, ldo, strideo, tinv, ldi, stridei);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
+hodlr_status launch_getrf_wide(int s, int batch, int mode, const double* src, int64_t lds, int64_t strides,
+                               double* out, int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info,
+                               double* dbi, int64_t stridedbi, cudaStream_t st);
+
+// batches up to this many blocks take the latency-optimised column-owner LU
+// (lu_wide.cu); larger ones the throughput kernels.  Measured single-launch
+// times (tools/lu_latency.py): s = 64: 35 us (1 block) / 41 us (296) vs the
+// window kernel's 52 / 56 us, 74 vs 67 us at 512; s = 128 (every batch): 122 /
+// 245 us at 148 / 296 blocks vs the shared-row kernel's 178 / 346 us, and
+// 1.7 ms vs 2.3 ms (est.) at 2048 (profiles/r02_lu_col.txt)
+#ifndef HODLR_WIDE_LU_BATCH
+#define HODLR_WIDE_LU_BATCH 296
+#endif
+constexpr int kWideLuBatch = HODLR_WIDE_LU_BATCH;
+static int wide_lu_batch(int s) { return s >= 128 ? (kWideLuBatch > 0 ? 1 << 30 : 0) : kWideLuBatch; }
+#define TRY_STATUS(x)                     \
+  do {                                    \
+    const hodlr_status s_ = (x);          \
+    if (s_ != HODLR_OK) return s_;        \
+  } while (0)
+
+template <int S>
 static hodlr_status run_reg(int batch, int mode, const double* src, int64_t lds, int64_t strides, double* out,
                             int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, double* tinv,
                             int64_t ldi, int64_t stridei, cudaStream_t st) {
   getrf_reg_kernel<S><<<batch, S, 0, st>>>(mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, nullptr, 0);
   HODLR_CHECK_LAUNCH();
   if (tinv == nullptr) return HODLR_OK;
-  constexpr size_t smem = ((size_t)S * (S + 4) + (size_t)(S / 2) * (S / 2 + 4)) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(trtri_sm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  trtri_sm_kernel<S><<<batch, 128, smem, st>>>(out, ldo, strideo, tinv, ldi, stridei);
-  HODLR_CHECK_LAUNCH();
-  return HODLR_OK;
+  return run_trtri_sm<S>(batch, out, ldo, strideo, tinv, ldi, stridei, st);
 }
 
 // Factorization-internal LU (fp64, s in {32, 64}): factors + diagonal-block
@@ -585,6 +608,9 @@ hodlr_status launch_getrf_dbi_f64(int s, int batch, int mode, const double* src,
                                   double* out, int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm,
                                   int32_t* info, double* dbi, int64_t stridedbi, cudaStream_t st) {
   if (batch == 0) return HODLR_OK;
+  if ((s == 32 || s == 64 || s == 128) && batch <= wide_lu_batch(s))
+    return launch_getrf_wide(s, batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, dbi, stridedbi,
+                             st);
   if (s == 64 && batch <= small_lu_batch())
     // less than a few waves of blocks: per-block step latency decides -- the
     // compact sliding-window kernel (lu_win.cu; 1.2-1.3x faster than the
@@ -643,6 +669,15 @@ template <typename T>
 hodlr_status launch_getrf_cyclic(int s, int batch, int mode, const T* src, int64_t lds, int64_t strides, T* out,
                                  int64_t ldo, int64_t strideo, int32_t* swaps, int32_t* perm, int32_t* info, T* tinv,
                                  int64_t ldi, int64_t stridei, cudaStream_t st) {
+  if constexpr (sizeof(T) == 8) {
+    if ((s == 32 || s == 64 || s == 128) && batch <= wide_lu_batch(s)) {
+      TRY_STATUS(launch_getrf_wide(s, batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, nullptr, 0, st));
+      if (tinv == nullptr) return HODLR_OK;
+      return s == 32 ? run_trtri_sm<32>(batch, out, ldo, strideo, tinv, ldi, stridei, st)
+             : s == 64 ? run_trtri_sm<64>(batch, out, ldo, strideo, tinv, ldi, stridei, st)
+                       : run_trtri_sm<128>(batch, out, ldo, strideo, tinv, ldi, stridei, st);
+    }
+  }
   switch (s) {
     case 16: return run_sr<T, 16>(batch, mode, src, lds, strides, out, ldo, strideo, swaps, perm, info, tinv, ldi, stridei, st);
     case 32:

@@ -173,7 +173,7 @@ def test_lu_nonfinite_and_degenerate_blocks_bit_exact(s, dtype):
     assert sorted(piv.singular) == sorted(np.flatnonzero(p.singular).tolist())
 
 
-@pytest.mark.parametrize("s,nb", [(64, 512), (32, 300), (16, 1000), (128, 40), (7, 33)])
+@pytest.mark.parametrize("s,nb", [(64, 512), (64, 296), (64, 1), (32, 300), (32, 148), (16, 1000), (128, 40), (128, 300), (7, 33)])
 def test_lu_bit_exact_vs_reference_order(s, nb):
     rng = np.random.default_rng(s * 1000 + nb)
     base = rng.standard_normal(nb * s * s)
