@@ -697,6 +697,218 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent factorization level step with C staged by TMA (round 2,
+// level_update6): the same per-column arithmetic as level_update4_kernel (C
+// loaded into the accumulators, C^T += (-W'^T) A1^T, then TW^T += C^T V), but
+// every operand of a chunk -- the A1 and V panels AND the chunk's C tile
+// (CH + 2 rows x the item's columns, one 2-D tensor copy) -- arrives through an
+// NS-stage mbarrier ring, so no warp ever waits on a global load of C (ncu
+// stall sampling of level_update4/5: 15-19 % of the samples on the C loads,
+// 16 % on the per-chunk barrier).  The last warp done with a stage (a
+// monotonic shared counter) refills it, so no warp waits for the others.
+//
+// Work item = (row segment, block of 16 column groups of 8; the last block of
+// a segment holds the remainder, its C box the next power of two of groups);
+// warp w owns group w of the item.  The CTA walks items blockIdx.x,
+// + gridDim.x, ... as one flat stream of CH-row chunks.  Levels whose
+// remainder block would leave too many warps idle keep level_update4/5
+// (level6_efficient).  [W|T] partials stay in registers for the item and
+// are written in the paired layout, or as per-segment partials that
+// level_reduce_kernel sums in a fixed order.  Deterministic, no atomics on data.
+// ---------------------------------------------------------------------------
+constexpr int kL6Warps = 16;
+template <int R>
+struct Level6Cfg {
+  static constexpr int CH = R >= 64 ? 32 : 64;  // rows per chunk
+  static constexpr int NI = CH / 16;            // 16-row bands per chunk
+  static constexpr int P = CH + 2;              // row pitch of every tile (LDS.128 conflict-free)
+  static constexpr int GC = kL6Warps;           // column groups of a full item
+  static constexpr int PANEL = R * P;
+  static constexpr int CTILE = GC * 8 * P;
+  static constexpr int STAGE = 2 * PANEL + CTILE;
+  static constexpr int NS = (int)((227 * 1024 - 1024) / 8) / STAGE;
+  static constexpr size_t SMEM = (size_t)NS * STAGE * sizeof(double);
+  static constexpr int THREADS = kL6Warps * 32;
+};
+
+// item -> (segment, first group, groups, C box kind: 16 >> kind groups >= gi)
+struct L6Item {
+  int64_t seg;
+  int gb, gi, kind;
+};
+__device__ __forceinline__ L6Item l6_item(int64_t item, int ncg, int G) {
+  L6Item it;
+  it.seg = item / ncg;
+  it.gb = 16 * (int)(item - it.seg * ncg);
+  it.gi = min(16, G - it.gb);
+  it.kind = it.gi > 8 ? 0 : it.gi > 4 ? 1 : it.gi > 2 ? 2 : it.gi > 1 ? 3 : 4;
+  return it;
+}
+
+struct L6Maps {
+  CUtensorMap a, v, c[5];  // A1 / V panels; C boxes of 16 / 8 / 4 / 2 / 1 groups
+};
+
+// one chunk of one warp: group `slot` of the item (the lane's C column `col`)
+template <int R>
+__device__ __forceinline__ void level6_chunk(const LevelArgs& g, const double* As, const double* Vs, const double* Cs,
+                                             const double2 (&wf)[R / 8], double (&tw)[R / 8][2], int64_t row0,
+                                             int slot, int col, int ar, int ac) {
+  constexpr int P = Level6Cfg<R>::P, RT = R / 8, NB = Level6Cfg<R>::NI, b0 = 0;
+  double acc[2 * NB][2];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const double* ci = Cs + (slot * 8 + ar) * P + 16 * (b0 + i) + 4 * ac;
+    const double2 x01 = *reinterpret_cast<const double2*>(ci);
+    const double2 x23 = *reinterpret_cast<const double2*>(ci + 2);
+    acc[2 * i][0] = x01.x, acc[2 * i + 1][0] = x01.y, acc[2 * i][1] = x23.x, acc[2 * i + 1][1] = x23.y;
+  }
+  // ---- C^T += (-W'^T) A1^T ----
+#pragma unroll
+  for (int kt = 0; kt < RT; ++kt)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double a = -(u ? wf[kt].y : wf[kt].x);
+      const double* ak = As + (8 * kt + 2 * ac + u) * P + 2 * ar + 16 * b0;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const double2 b2 = *reinterpret_cast<const double2*>(ak + 16 * i);
+        dmma_8x8x4(acc[2 * i][0], acc[2 * i][1], a, b2.x);
+        dmma_8x8x4(acc[2 * i + 1][0], acc[2 * i + 1][1], a, b2.y);
+      }
+    }
+  double* cp = g.C + row0 + 16 * b0 + (int64_t)col * g.ldc + 4 * ac;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) stg_v4(cp + 16 * i, acc[2 * i][0], acc[2 * i + 1][0], acc[2 * i][1], acc[2 * i + 1][1]);
+  // ---- TW^T += C^T V: per (band, half) the RT first products, then the second ones ----
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double2 v2[RT];
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr)
+        v2[jr] = *reinterpret_cast<const double2*>(Vs + (8 * jr + ar) * P + 16 * (b0 + i) + 4 * ac + 2 * h);
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr) dmma_8x8x4(tw[jr][0], tw[jr][1], acc[2 * i][h], v2[jr].x);
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr) dmma_8x8x4(tw[jr][0], tw[jr][1], acc[2 * i + 1][h], v2[jr].y);
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(Level6Cfg<R>::THREADS, 1)
+    level_update6_kernel(LevelArgs g, int64_t nitems, const __grid_constant__ L6Maps tm) {
+  using Cfg = Level6Cfg<R>;
+  constexpr int CH = Cfg::CH, NI = Cfg::NI, P = Cfg::P, NS = Cfg::NS, RT = R / 8, NW = kL6Warps;
+  extern __shared__ __align__(1024) double sm6[];
+  __shared__ __align__(8) uint64_t full[NS];
+  __shared__ int released[NS];  // warps done with the stage (monotonic; the NW-th of a use refills it)
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const int G = g.ncols >> 3;
+  const int cps = g.seg_rows / CH;  // chunks per item
+  const int64_t nmine = nitems > (int64_t)blockIdx.x ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = nmine * cps;
+
+  auto issue = [&](int64_t item, int cu, int s) {
+    const L6Item it = l6_item(item, g.ncg, G);
+    const int row = (int)(it.seg * g.seg_rows + (int64_t)cu * CH);
+    double* st = sm6 + (size_t)s * Cfg::STAGE;
+    mbar_expect_tx(&full[s], (uint32_t)((2 * Cfg::PANEL + (16 >> it.kind) * 8 * P) * sizeof(double)));
+    tma_load_2d(st, &tm.a, row, 0, &full[s]);
+    tma_load_2d(st + Cfg::PANEL, &tm.v, row, 0, &full[s]);
+    tma_load_2d(st + 2 * Cfg::PANEL, &tm.c[it.kind], row, it.gb * 8, &full[s]);
+  };
+  if (t == 0) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      released[q] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    int64_t item = blockIdx.x;
+    int cu = 0;
+    for (int f = 0; f < NS && f < total; ++f) {
+      issue(item, cu, f);
+      if (++cu == cps) cu = 0, item += gridDim.x;
+    }
+  }
+  __syncthreads();
+
+  double tw[RT][2];
+#pragma unroll
+  for (int jr = 0; jr < RT; ++jr) tw[jr][0] = tw[jr][1] = 0.0;
+  // W' fragments of chunk f (loaded one chunk ahead, L1 / L2)
+  double2 wf[RT];
+  auto load_w = [&](double2 (&w)[RT], int64_t item, int cu) {
+    const L6Item it = l6_item(item, g.ncg, G);
+    const int64_t row0 = it.seg * g.seg_rows + (int64_t)cu * CH;
+    const int c = (int)(row0 / g.n_c);
+    const int col = (warp < it.gi ? it.gb + warp : 0) * 8 + ar;
+    const double* wc = g.W + (int64_t)(c >> 1) * g.wstride + (c & 1) * R + (int64_t)col * (2 * R) + 2 * ac;
+#pragma unroll
+    for (int kt = 0; kt < RT; ++kt) w[kt] = __ldg(reinterpret_cast<const double2*>(wc + 8 * kt));
+  };
+  int64_t item = blockIdx.x;
+  int cu = 0;
+  if (total > 0) load_w(wf, item, cu);
+  for (int64_t f = 0; f < total; ++f) {
+    const int s = (int)(f % NS);
+    const L6Item it = l6_item(item, g.ncg, G);
+    const bool on = warp < it.gi;
+    const int col = (it.gb + warp) * 8 + ar;
+    const int64_t row0 = it.seg * g.seg_rows + (int64_t)cu * CH;
+    int64_t item_n = item;
+    int cu_n = cu + 1;
+    if (cu_n == cps) cu_n = 0, item_n += gridDim.x;
+    double2 wn[RT];
+    if (f + 1 < total) load_w(wn, item_n, cu_n);
+    mbar_wait(&full[s], (uint32_t)((f / NS) & 1));
+    const double* As = sm6 + (size_t)s * Cfg::STAGE;
+    const double* Vs = As + Cfg::PANEL;
+    const double* Cs = Vs + Cfg::PANEL;
+    if (on) level6_chunk<R>(g, As, Vs, Cs, wf, tw, row0, warp, col, ar, ac);
+    __syncwarp();
+    if (lane == 0) {  // the last warp done with stage s refills it with chunk f + NS
+      __threadfence_block();
+      const int old = atomicAdd(&released[s], 1);
+      if ((old + 1) % NW == 0 && f + NS < total) {
+        int64_t it2 = item;
+        int cu2 = cu + NS;
+        it2 += (int64_t)(cu2 / cps) * gridDim.x;
+        cu2 %= cps;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(it2, cu2, s);
+      }
+    }
+    if (cu_n == 0) {  // item done: [W|T] (or partial) out, running sums reset
+      if (on) {
+        double* out;
+        int64_t ld;
+        if (g.partial) {
+          out = g.TW + it.seg * R * g.ncols;
+          ld = R;
+        } else {
+          const int64_t qn = it.seg * g.seg_rows / g.node_rows;
+          out = g.TW + (qn >> 1) * g.tw_stride + (qn & 1) * R;
+          ld = 2 * R;
+        }
+#pragma unroll
+        for (int jr = 0; jr < RT; ++jr)
+          *reinterpret_cast<double2*>(out + 8 * jr + 2 * ac + (int64_t)col * ld) = make_double2(tw[jr][0], tw[jr][1]);
+      }
+#pragma unroll
+      for (int jr = 0; jr < RT; ++jr) tw[jr][0] = tw[jr][1] = 0.0;
+    }
+    item = item_n;
+    cu = cu_n;
+#pragma unroll
+    for (int kt = 0; kt < RT; ++kt) wf[kt] = wn[kt];
+  }
+}
+
 // panel = rows [0, rows) x R columns of a column-major slab (ld lda); box = (CH + 2) x R
 template <int R, bool SOLVE = false>
 static bool panel_map(CUtensorMap* m, const double* base, int64_t rows, int64_t lda) {
@@ -1106,6 +1318,74 @@ size_t level_partial_bytes(int64_t n, int m, int r, int L) {
   return best;
 }
 
+// level_update6_kernel: items of 16 column groups; rows per item = the whole
+// node unless that leaves the persistent CTAs unbalanced (then a power-of-two
+// split with partial sums, at most kMaxSegs segments, preferring larger
+// segments unless a split balances the waves >= 2 % better)
+#ifndef HODLR_LEVEL6
+#define HODLR_LEVEL6 1
+#endif
+// level_update6 where its items keep >= 80 % of the warps busy (rank 32; the
+// same-box launch list: levels 13, 12, 11, 8, 7, 4 of cfg2 faster than
+// level_update4/5, levels 6, 5 slower with half-empty remainder items; rank 64
+// loses with 2 stages of 70 KB -- profiles/r02_level6.txt)
+static bool level6_efficient(int r, int G) {
+  return HODLR_LEVEL6 && r == 32 && G >= 16 && 5 * G >= 4 * 16 * (int)ceil_div(G, 16);
+}
+
+static int64_t level6_segment_rows(int64_t n, int64_t node, int64_t ncg, int sms, int ch) {
+  int64_t best = node;
+  double best_eff = -1.0;
+  for (int64_t seg = node; seg >= ch && node % seg == 0; seg >>= 1) {
+    const int64_t nseg = n / seg;
+    if (seg < node && nseg > kMaxSegs) break;
+    const int64_t items = nseg * ncg;
+    const double eff = (double)items / (double)(ceil_div(items, sms) * sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = seg;
+    }
+    if (seg % (2 * ch)) break;
+  }
+  return best;
+}
+
+template <int R>
+static hodlr_status run_level6(LevelArgs g, int64_t n, int64_t node, double* part, size_t part_bytes, double* TW,
+                               cudaStream_t st) {
+  using Cfg = Level6Cfg<R>;
+  const int G = g.ncols / 8;
+  const int64_t ncg = ceil_div(G, Cfg::GC);  // items per segment
+  const int sms = sm_count();
+  const int64_t seg = level6_segment_rows(n, node, ncg, sms, Cfg::CH);
+  if (seg % Cfg::CH || (g.n_c < n && g.n_c % Cfg::CH) || n > 2147483647LL - Cfg::P) return HODLR_ERR_ARG;
+  const int64_t nseg = n / seg;
+  const bool split = seg < node;
+  if (split && (size_t)nseg * R * g.ncols * sizeof(double) > part_bytes) return HODLR_ERR_ARG;
+  g.seg_rows = (int)seg;
+  g.ncg = (int)ncg;
+  g.tpc = Cfg::GC;
+  g.partial = split ? 1 : 0;
+  g.TW = split ? part : TW;
+  L6Maps tm;
+  if (!panel_map_f64(&tm.a, g.A1, n, R, g.lda, Cfg::P) || !panel_map_f64(&tm.v, g.V, n, R, g.lda, Cfg::P))
+    return HODLR_ERR_ARG;
+  for (int k = 0; k < 5; ++k)
+    if (!tensor_map_f64(&tm.c[k], g.C, n, g.ncols, g.ldc, Cfg::P, (Cfg::GC >> k) * 8)) return HODLR_ERR_ARG;
+  const int64_t items = nseg * ncg;
+  smem_attr(level_update6_kernel<R>, (int)Cfg::SMEM);
+  level_update6_kernel<R><<<(unsigned)std::min<int64_t>(items, sms), Cfg::THREADS, Cfg::SMEM, st>>>(g, items, tm);
+  HODLR_CHECK_LAUNCH();
+  if (!split) return HODLR_OK;
+  const int nnodes = (int)(n / node);
+  const int64_t total = (int64_t)R * g.ncols * nnodes;
+  const int segs = (int)(node / seg);
+  const int64_t blocks = std::min<int64_t>(ceil_div(segs > 32 ? total * 32 : total, 256), 8 * (int64_t)sms);
+  level_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, TW, R, g.ncols, segs, nnodes, g.tw_stride);
+  HODLR_CHECK_LAUNCH();
+  return HODLR_OK;
+}
+
 // One fused level step over all n rows.  Returns ERR_ARG when the shape is not
 // supported (caller falls back to the generic batched GEMM path).
 // reg_resident selects the register-resident kernel, which accumulates the
@@ -1129,6 +1409,13 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   // factorization: the column-group kernel (32-byte aligned C columns, groups of 8)
   const bool v4 = fact && ncols % 8 == 0 && !(ldc & 3) && !(reinterpret_cast<uintptr_t>(C) & 31);
   if (fact && !v4) return HODLR_ERR_ARG;  // generic GEMM path
+  if (v4 && level6_efficient(r, ncols / 8)) {  // persistent, C staged by TMA
+    LevelArgs g6{C, ldc, A1, V, lda, W, wstride, TW, tw_stride, 0, (int)n_c, 0, node, ncols, 0, 0};
+    const hodlr_status s6 = r == 16   ? run_level6<16>(g6, n, node, part, part_bytes, TW, st)
+                            : r == 32 ? run_level6<32>(g6, n, node, part, part_bytes, TW, st)
+                                      : run_level6<64>(g6, n, node, part, part_bytes, TW, st);
+    if (s6 != HODLR_ERR_ARG) return s6;
+  }
   if (v4) fs = level4_schedule(n, node, ncols / 8, sm_count(), level4_maxg(r));
   const int64_t seg = fs.seg;
   const int64_t nseg = n / seg;
