@@ -523,12 +523,13 @@ def run_ours(args):
             "matvec": {"ms": mv_t, "GB_per_s": mv_bytes / (mv_t * 1e-3) / 1e9, "bytes": mv_bytes,
                        "frac_hbm": (mv_bytes / (mv_t * 1e-3) / 1e9 / peaks["hbm_gbs"]) if peaks.get("hbm_gbs") else None},
             "phase_ms": phases, "gpu_launches": launches_per_step * args.steps,
-            "roofline": {"bound": "tensor", "kernel": "level_update4_kernel (fused Y update + next-level [W|T]); traffic = "
-                                   "mean DRAM bytes per level_update4 launch (ncu, profiles/traffic.json)",
+            "roofline": {"bound": "tensor", "kernel": "level phase: level_update6_kernel (persistent, C tile + panels by TMA) and "
+                                   "level_update4/5 (remainder groups, small levels), fused Y update + next-level [W|T]; "
+                                   "traffic = mean DRAM bytes per level launch (ncu, profiles/traffic.json)",
                          "achieved": lvl_achieved, "peak": dgemm, "unit": "TFLOP/s",
                          "frac": (lvl_achieved / dgemm) if (lvl_achieved and dgemm) else None,
                          "peak_source": "measured cuBLAS DGEMM 8192^3 in this run (MEASURED_PEAKS.json has no fp64)",
-                         "traffic": traffic, "launches_per_step": level_launches,
+                         "traffic": traffic, "level_steps_per_step": level_launches,
                          "flops_per_step": level_flops(n, m, r)},
             "clocks": clk.summary(), "wall_s_timed": wall,
             "hbm_peak_measured_gbps": peaks.get("hbm_gbs"),
@@ -670,7 +671,7 @@ def run_sharded(args):
                        "l2_flush": "inputs > L2 (126 MB)"},
             "t_factor_ms": tf, "t_solve_ms": ts, "relres": relres, "phase_ms_rank0": phases, "build_ms": build_ms,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "wall_s_timed": wall,
-            "roofline": {"bound": "tensor", "kernel": "level_update4_kernel", "achieved":
+            "roofline": {"bound": "tensor", "kernel": "level phase (level_update6/4/5)", "achieved":
                          (level_flops(n // world, m, r) / (phases["level"] * 1e-3) / 1e12) if phases["level"] else None,
                          "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None,
                          "note": "rank 0's local level phase; the per-kernel roofline is reported by the N=1 run"},

@@ -1325,12 +1325,14 @@ size_t level_partial_bytes(int64_t n, int m, int r, int L) {
 #ifndef HODLR_LEVEL6
 #define HODLR_LEVEL6 1
 #endif
-// level_update6 where its items keep >= 80 % of the warps busy (rank 32; the
-// same-box launch list: levels 13, 12, 11, 8, 7, 4 of cfg2 faster than
-// level_update4/5, levels 6, 5 slower with half-empty remainder items; rank 64
-// loses with 2 stages of 70 KB -- profiles/r02_level6.txt)
-static bool level6_efficient(int r, int G) {
-  return HODLR_LEVEL6 && r == 32 && G >= 16 && 5 * G >= 4 * 16 * (int)ceil_div(G, 16);
+// level_update6 at rank 32 (G >= 16 groups): a remainder of G mod 16 >= 12
+// groups is one ragged level6 item (>= 75 % of its warps busy); a smaller
+// remainder (4 or 8 groups) takes level_update4/5 in a second launch, since a
+// mostly empty level6 item costs a full item's time (same-box launch lists,
+// profiles/r02_level6.txt).  Rank 64 loses with 2 stages of 70 KB.
+static int level6_groups(int r, int G) {
+  if (!HODLR_LEVEL6 || r != 32 || G < 16) return 0;
+  return G % 16 >= 12 ? G : G & ~15;
 }
 
 static int64_t level6_segment_rows(int64_t n, int64_t node, int64_t ncg, int sms, int ch) {
@@ -1409,12 +1411,17 @@ hodlr_status level_update_f64(int r, int64_t n, int64_t n_c, int64_t node_rows, 
   // factorization: the column-group kernel (32-byte aligned C columns, groups of 8)
   const bool v4 = fact && ncols % 8 == 0 && !(ldc & 3) && !(reinterpret_cast<uintptr_t>(C) & 31);
   if (fact && !v4) return HODLR_ERR_ARG;  // generic GEMM path
-  if (v4 && level6_efficient(r, ncols / 8)) {  // persistent, C staged by TMA
-    LevelArgs g6{C, ldc, A1, V, lda, W, wstride, TW, tw_stride, 0, (int)n_c, 0, node, ncols, 0, 0};
-    const hodlr_status s6 = r == 16   ? run_level6<16>(g6, n, node, part, part_bytes, TW, st)
-                            : r == 32 ? run_level6<32>(g6, n, node, part, part_bytes, TW, st)
-                                      : run_level6<64>(g6, n, node, part, part_bytes, TW, st);
-    if (s6 != HODLR_ERR_ARG) return s6;
+  if (v4 && level6_groups(r, ncols / 8) > 0) {  // persistent, C staged by TMA
+    const int c6 = 8 * level6_groups(r, ncols / 8);
+    LevelArgs g6{C, ldc, A1, V, lda, W, wstride, TW, tw_stride, 0, (int)n_c, 0, node, c6, 0, 0};
+    const hodlr_status s6 = run_level6<32>(g6, n, node, part, part_bytes, TW, st);
+    if (s6 != HODLR_OK || c6 == ncols) {
+      if (s6 != HODLR_ERR_ARG) return s6;
+    } else {  // remainder columns [c6, ncols): same step on the column-offset operands
+      return level_update_f64(r, n, n_c, node_rows, C + (int64_t)c6 * ldc, ldc, A1, V, lda, W + (int64_t)c6 * 2 * r,
+                              wstride, ncols - c6, TW + (int64_t)c6 * 2 * r, tw_stride, part, part_bytes, st,
+                              reg_resident);
+    }
   }
   if (v4) fs = level4_schedule(n, node, ncols / 8, sm_count(), level4_maxg(r));
   const int64_t seg = fs.seg;
