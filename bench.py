@@ -525,7 +525,7 @@ def run_ours(args):
             "phase_ms": phases, "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "tensor", "kernel": "level phase: level_update6_kernel (persistent, C tile + panels by TMA) and "
                                    "level_update4/5 (remainder groups, small levels), fused Y update + next-level [W|T]; "
-                                   "traffic = mean DRAM bytes per level launch (ncu, profiles/traffic.json)",
+                                   "traffic = mean DRAM bytes per level step (ncu, profiles/traffic.json)",
                          "achieved": lvl_achieved, "peak": dgemm, "unit": "TFLOP/s",
                          "frac": (lvl_achieved / dgemm) if (lvl_achieved and dgemm) else None,
                          "peak_source": "measured cuBLAS DGEMM 8192^3 in this run (MEASURED_PEAKS.json has no fp64)",

@@ -25,7 +25,9 @@ for rep in sys.argv[1:]:
         tensor = [h for h in hdr if ("dmma" in h or "pipe_tensor" in h or "pipe_fp64" in h or "pipe_shared" in h
                                      or "pipe_lsu" in h) and ("pct" in h or h.endswith(".ratio"))]
         for h in tensor:
-            print(f"   {h} = {d[h]} {units[hdr.index(h)]}")
+            v = d[h].replace(",", "")
+            if ".avg." in h and "elapsed" not in h and v not in ("", "0") and float(v) != 0.0:
+                print(f"   {h} = {d[h]} {units[hdr.index(h)]}")
         for h in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                   "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
                   "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
