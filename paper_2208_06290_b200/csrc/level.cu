@@ -1188,17 +1188,18 @@ template <int R>
 static hodlr_status run_level4_solve(const LevelArgs& g, int64_t nseg, cudaStream_t st) {
   using Cfg = Level4Cfg<R, true>;
   const int gpw = (g.tpc + 7) / 8;
-  static bool attr = false;  // set once, outside any graph capture of a later call
-  if (!attr) {
-    cudaFuncSetAttribute(level_update4_kernel<R, 1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaFuncSetAttribute(level_update4_kernel<R, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaFuncSetAttribute(level_update4_kernel<R, 4, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    attr = true;
+  auto launch = [&](auto kern) {
+    smem_attr(kern, (int)Cfg::SMEM);
+    kern<<<(unsigned)(nseg * g.ncg), 256, Cfg::SMEM, st>>>(g);
+  };
+  if (gpw <= 1) {
+    launch(level_update4_kernel<R, 1, false, true>);
+  } else if constexpr (R <= 32) {  // rank 64 solves run one column group per warp (solve_level_f64)
+    if (gpw <= 2) launch(level_update4_kernel<R, 2, false, true>);
+    else launch(level_update4_kernel<R, 4, false, true>);
+  } else {
+    return HODLR_ERR_ARG;
   }
-  auto launch = [&](auto kern) { kern<<<(unsigned)(nseg * g.ncg), 256, Cfg::SMEM, st>>>(g); };
-  if (gpw <= 1) launch(level_update4_kernel<R, 1, false, true>);
-  else if (gpw <= 2) launch(level_update4_kernel<R, 2, false, true>);
-  else launch(level_update4_kernel<R, 4, false, true>);
   HODLR_CHECK_LAUNCH();
   return HODLR_OK;
 }
