@@ -6,10 +6,15 @@
 // additionally the packed triangular inverses strict_lower(L^-1) + upper(U^-1)
 // of every leaf and K block, so every triangular solve of the factor and solve
 // phases becomes a pair of batched DMMA GEMMs (apply.cu).
+#include <climits>
+#include <condition_variable>
 #include <cstdio>
+#include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 
 #include "common.cuh"
 #include "ranks.cuh"
@@ -312,6 +317,31 @@ extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
     if (s_ != HODLR_OK) return s_;        \
   } while (0)
 
+// Host-side gate between a staging upload (pageable host inputs) and the
+// thread enqueueing the factorization: vready[l'] may only be waited on once
+// the uploader has recorded it (an unrecorded event would not order anything).
+struct UploadGate {
+  std::mutex mu;
+  std::condition_variable cv;
+  int ready = INT_MAX;  // vready[l'] recorded for every l' >= ready
+  bool failed = false;
+  void publish(int lv) {
+    std::lock_guard<std::mutex> lk(mu);
+    ready = lv;
+    cv.notify_all();
+  }
+  void fail() {
+    std::lock_guard<std::mutex> lk(mu);
+    failed = true;
+    cv.notify_all();
+  }
+  bool wait(int lv) {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return failed || ready <= lv; });
+    return !failed;
+  }
+};
+
 // Leaf phase + levels L-1 .. lv_stop over the local rows.  On return the
 // workspace TW region holds [W|T] of the local level-lv_stop node(s) (paired
 // layout, local node 0 first) unless lv_stop == 0.
@@ -319,7 +349,8 @@ extern "C" size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs) {
 // (columns (l'-1) r .. l' r) is resident; the leaf phase needs vready[L],
 // level l's update kernel vready[l] (streamed host upload, hodlr_factorize_from_host).
 static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, int64_t n_loc, int64_t row0, int lv_stop,
-                                 char* wp, const FactWs& ws, cudaStream_t st, const cudaEvent_t* vready = nullptr) {
+                                 char* wp, const FactWs& ws, cudaStream_t st, const cudaEvent_t* vready = nullptr,
+                                 UploadGate* gate = nullptr) {
   void* split = wp;
   double* TW = reinterpret_cast<double*>(wp + ws.split);
   double* W = reinterpret_cast<double*>(wp + ws.split + ws.tw);
@@ -339,6 +370,7 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
   double* Kinv = (double*)f->Kinv;
 
   // (1) leaf getrf (bit-exact) + diagonal-block inverses          Alg.3 l.2
+  if (gate && L > 0 && !gate->wait(L)) return HODLR_ERR_CUDA;
   if (vready && L > 0 && cudaStreamWaitEvent(st, vready[L], 0) != cudaSuccess)  // D, U and V^(L) resident
     return hodlr_set_cuda_error(cudaGetLastError());
   {
@@ -401,6 +433,7 @@ static hodlr_status factor_local(const hodlr_desc* d, const hodlr_factors* f, in
     }
     // Y(I_c, 0:wc) -= Y_c^{l+1} W_c, fused with the next level's [W|T] (V^{(l)T} Y(I_q, 0:wc))
     // when both levels have the same rank (the fused kernel holds one rank)
+    if (gate && !gate->wait(lv)) return HODLR_ERR_CUDA;
     if (vready && cudaStreamWaitEvent(st, vready[lv], 0) != cudaSuccess)  // V^(lv) resident (streamed upload)
       return hodlr_set_cuda_error(cudaGetLastError());
     hodlr_status s = HODLR_ERR_ARG;
@@ -647,13 +680,101 @@ extern "C" hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors
   return factor_local(d, f, d->n, 0, 0, static_cast<char*>(work), ws, S(stream));
 }
 
-// Factorization from host (pinned) buffers with the upload overlapped: D, U and
-// V^(L) are copied first on copy_stream, then the V panels in the order the
-// levels consume them (V^(L-1) ... V^(1)); the compute on `stream` waits per
-// level, so all but the first 4.6 GB (cfg2) of the transfer hide behind the
+// Factorization from host buffers with the upload overlapped: D, U and V^(L)
+// are copied first on copy_stream, then the V panels in the order the levels
+// consume them (V^(L-1) ... V^(1)); the compute on `stream` waits per level,
+// so all but the first 4.6 GB (cfg2) of the transfer hide behind the
 // factorization.  f's D / Y / V are the device destinations (Y receives U).
+//
+// Pinned inputs are copied directly.  Pageable inputs (e.g. numpy arrays) go
+// through a pinned staging ring: kStageThreads host threads copy each 64 MB
+// chunk into a free slot, the caller's thread issues that slot's H2D copy and
+// records the event gating the slot's reuse; meanwhile a second host thread
+// enqueues the factorization, blocking (UploadGate) until each level's V
+// panel event has been recorded.  The call returns once every byte has left
+// the caller's buffers (they may be freed at once).
 static std::mutex g_up_mu;
 static std::map<int, std::vector<cudaEvent_t>> g_up_ev;  // per device: events live in that device's context
+
+namespace {
+constexpr int kStageSlots = 4;
+constexpr size_t kStageBytes = (size_t)64 << 20;
+struct StageRing {
+  void* slot[kStageSlots] = {};
+  cudaEvent_t ev[kStageSlots] = {};
+  int next = 0;
+  bool ready = false;
+};
+std::map<int, StageRing> g_stage;  // per device, under g_up_mu; kept for the process
+
+// memcpy of one chunk split over T host threads (the caller is thread 0)
+class CopyPool {
+ public:
+  explicit CopyPool(int T) : T_(T) {
+    for (int i = 1; i < T_; ++i) th_.emplace_back([this, i] { worker(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      quit_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void copy(char* dst, const char* src, size_t len) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = dst, src_ = src, len_ = len, pending_ = T_ - 1, ++gen_;
+    }
+    cv_.notify_all();
+    piece(0, dst, src, len);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  void piece(int i, char* dst, const char* src, size_t len) const {
+    const size_t per = ((len + T_ - 1) / T_ + 4095) & ~(size_t)4095;
+    const size_t off = (size_t)i * per;
+    if (off < len) std::memcpy(dst + off, src + off, std::min(per, len - off));
+  }
+  void worker(int i) {
+    int seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return quit_ || gen_ != seen; });
+      if (quit_) return;
+      seen = gen_;
+      char* d = dst_;
+      const char* s = src_;
+      const size_t l = len_;
+      lk.unlock();
+      piece(i, d, s, l);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  int T_;
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t len_ = 0;
+  int gen_ = 0, pending_ = 0;
+  bool quit_ = false;
+};
+
+bool host_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+}  // namespace
+
 extern "C" hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hodlr_factors* f, const void* D_host,
                                                   const void* U_host, const void* V_host, void* work,
                                                   size_t work_bytes, void* stream, void* copy_stream) {
@@ -675,23 +796,69 @@ extern "C" hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hod
     ev.push_back(e);
   }
   auto ok_ = [](cudaError_t e) { return e == cudaSuccess; };
+  const bool pD = host_pageable(D_host), pU = host_pageable(U_host), pV = host_pageable(V_host);
+  const bool staged = pD || pU || pV;
+  StageRing* ring = nullptr;
+  if (staged) {
+    ring = &g_stage[dev];
+    if (!ring->ready) {
+      for (int k = 0; k < kStageSlots; ++k)
+        if (cudaHostAlloc(&ring->slot[k], kStageBytes, cudaHostAllocDefault) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ring->ev[k], cudaEventDisableTiming) != cudaSuccess)
+          return hodlr_set_cuda_error(cudaGetLastError());
+      ring->ready = true;
+    }
+  }
   // the copies must not start before the caller's prior work on `stream`
   if (!ok_(cudaEventRecord(ev[L + 1], st)) || !ok_(cudaStreamWaitEvent(cs, ev[L + 1], 0)))
     return hodlr_set_cuda_error(cudaGetLastError());
-  auto cp = [&](void* dst, const void* src, size_t bytes) {
-    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs) == cudaSuccess;
+  const int nthreads = staged ? (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency())) : 1;
+  std::unique_ptr<CopyPool> pool(staged ? new CopyPool(nthreads) : nullptr);
+  auto cp = [&](void* dst, const void* src, size_t bytes, bool pageable) {
+    if (!pageable) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs) == cudaSuccess;
+    for (size_t off = 0; off < bytes; off += kStageBytes) {
+      const size_t len = std::min(kStageBytes, bytes - off);
+      const int k = ring->next;
+      ring->next = (k + 1) % kStageSlots;
+      if (cudaEventSynchronize(ring->ev[k]) != cudaSuccess) return false;  // the slot's previous copy has landed
+      pool->copy(static_cast<char*>(ring->slot[k]), static_cast<const char*>(src) + off, len);
+      if (cudaMemcpyAsync(static_cast<char*>(dst) + off, ring->slot[k], len, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+          cudaEventRecord(ring->ev[k], cs) != cudaSuccess)
+        return false;
+    }
+    return true;
+  };
+  // staged: the factorization is enqueued by a second host thread while this one uploads
+  UploadGate gate;
+  hodlr_status fs = HODLR_OK;
+  std::thread compute;
+  if (staged && L > 0)
+    compute = std::thread([&] {
+      if (cudaSetDevice(dev) != cudaSuccess) {
+        fs = hodlr_set_cuda_error(cudaGetLastError());
+        return;
+      }
+      fs = factor_local(d, f, n, 0, 0, static_cast<char*>(work), ws, st, ev.data(), &gate);
+    });
+  auto finish = [&](hodlr_status s) {
+    if (s != HODLR_OK) gate.fail();
+    if (compute.joinable()) compute.join();
+    return s != HODLR_OK ? s : fs;
   };
   const size_t panel = (size_t)n * r * es;
-  bool ok = cp(f->D, D_host, (size_t)n * m * es) && cp(f->Y, U_host, (size_t)L * panel);
+  bool ok = cp(f->D, D_host, (size_t)n * m * es, pD) && cp(f->Y, U_host, (size_t)L * panel, pU);
   if (L > 0)
-    ok = ok && cp((char*)f->V + (size_t)(L - 1) * panel, (const char*)V_host + (size_t)(L - 1) * panel, panel);
+    ok = ok && cp((char*)f->V + (size_t)(L - 1) * panel, (const char*)V_host + (size_t)(L - 1) * panel, panel, pV);
   ok = ok && ok_(cudaEventRecord(ev[L > 0 ? L : 0], cs));
-  if (!ok) return hodlr_set_cuda_error(cudaGetLastError());
+  if (!ok) return finish(hodlr_set_cuda_error(cudaGetLastError()));
+  gate.publish(L);
   for (int lv = L - 1; lv >= 1; --lv) {
-    if (!cp((char*)f->V + (size_t)(lv - 1) * panel, (const char*)V_host + (size_t)(lv - 1) * panel, panel) ||
+    if (!cp((char*)f->V + (size_t)(lv - 1) * panel, (const char*)V_host + (size_t)(lv - 1) * panel, panel, pV) ||
         !ok_(cudaEventRecord(ev[lv], cs)))
-      return hodlr_set_cuda_error(cudaGetLastError());
+      return finish(hodlr_set_cuda_error(cudaGetLastError()));
+    gate.publish(lv);
   }
+  if (compute.joinable()) return finish(HODLR_OK);
   if (L == 0 && !ok_(cudaStreamWaitEvent(st, ev[0], 0))) return hodlr_set_cuda_error(cudaGetLastError());
   return factor_local(d, f, n, 0, 0, static_cast<char*>(work), ws, st, ev.data());
 }

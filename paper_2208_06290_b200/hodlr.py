@@ -491,9 +491,12 @@ def factorize_from_host(n: int, m: int, r: int, D, U, V, variant: str = "pivoted
     """Factorize a HODLR matrix held in host memory (reference layout, fp64),
     overlapping the upload with the factorization: D, U and the last level's V
     go first, then the V panels in the order the levels consume them, on a
-    side copy stream (``hodlr_factorize_from_host``).  Host buffers should be
-    pinned (``tensor.pin_memory()``); pageable inputs are pinned first (a copy).
-    Equivalent to ``factorize(HodlrMatrix.from_buffers(...))``."""
+    side copy stream (``hodlr_factorize_from_host``).  Pinned host buffers
+    (``tensor.pin_memory()``) are copied directly; pageable ones (numpy arrays)
+    stream through the library's pinned staging ring (multi-threaded host
+    copies, the factorization enqueued as the level panels arrive), and may be
+    freed as soon as this returns.  Equivalent to
+    ``factorize(HodlrMatrix.from_buffers(...))``."""
     torch = _torch()
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r} (supported: {VARIANTS})")
@@ -511,8 +514,7 @@ def factorize_from_host(n: int, m: int, r: int, D, U, V, variant: str = "pivoted
             raise ValueError(f"{name} has {t.numel()} entries, expected {size}")
         if t.is_cuda:
             raise ValueError(f"{name} is already on the device; use HodlrMatrix.from_buffers")
-        t = t.contiguous()
-        return t if t.is_pinned() else t.pin_memory()
+        return t.contiguous()
 
     Dh, Uh, Vh = host(D, nl * m * m, "D"), host(U, n * r * L, "U"), host(V, n * r * L, "V")
     dev = torch.device(device)

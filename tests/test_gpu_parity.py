@@ -256,6 +256,22 @@ def test_factorize_from_host_equals_device_path():
     assert np.array_equal(hb.solve(f1, b), hb.solve(f2, b))
 
 
+@pytest.mark.parametrize("pinned_d", [False, True])
+def test_factorize_from_host_pageable_equals_device_path(pinned_d):
+    # pageable (numpy) inputs stream through the pinned staging ring (369 MB
+    # slabs: several 64 MB chunks, the 4-slot ring wraps) while a second host
+    # thread enqueues the factorization; also mixed pinned / pageable inputs
+    n, m, r = 1 << 17, 64, 32
+    h = hb.random_hodlr(n, m, r, seed=5, s=4.0)
+    Dn, Un, Vn = (x.cpu().numpy().copy() for x in (h.D, h.U, h.V))
+    f1 = hb.factorize(h.clone())
+    Dh = torch.from_numpy(Dn).pin_memory() if pinned_d else Dn
+    f2 = hb.factorize_from_host(n, m, r, Dh, Un, Vn)
+    del Dn, Un, Vn  # the call returns once the host buffers have been consumed
+    for name in ("D", "Y", "K", "kswaps", "dperm"):
+        assert torch.equal(getattr(f1, name), getattr(f2, name)), name
+
+
 @pytest.mark.parametrize("nrhs", [1, 3, 20])
 def test_solve_graph_replay_bitwise_equals_eager(nrhs):
     # the CUDA-graph solve (captured once per (nrhs, stream), replayed) == the eager launches
