@@ -69,9 +69,17 @@ __device__ __forceinline__ void stg_x4(double* p, double x, double y, double z, 
 // Warp roles: warps 0-3 (A) update x (phase 1), warps 4-7 (B) form the w
 // partials (phase 2) of the previous chunk at the same time, warp 8 issues the
 // tensor copies.  Barriers: full[s] (TMA bytes landed), empty[s] (8 consumer
-// warps done with the stage), xready[b] / xfree[b] (double-buffered shared x
-// tile handed from A to B and back).
+// warps done with the stage) -- mbarriers; the double-buffered shared x tile
+// is handed from A to B and back with named barriers (producer bar.arrive,
+// consumer bar.sync over the 8 compute warps: ready[b] = 1 + b, free[b] = 3 + b).
 constexpr int kSolveA = 4, kSolveB = 4, kSolveThreads = 32 * (kSolveA + kSolveB + 1);
+constexpr int kSolveAB = 32 * (kSolveA + kSolveB);
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 template <int R, int GB, int CH, int NS>
 __global__ void __launch_bounds__(kSolveThreads, 1)
@@ -86,7 +94,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
   extern __shared__ __align__(1024) double sms[];
   double* ring = sms;                   // NS x [Y panel | V panel | x tile | w' tile]
   double* xs0 = sms + NS * Cfg::STAGE;  // 2 x [GB * 8 columns][PX]: the updated x of a chunk
-  __shared__ __align__(8) uint64_t full[NS], empty[NS], xready[2], xfree[2];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ar = lane >> 2, ac = lane & 3;
   const bool want_w = g.out != nullptr;
@@ -99,10 +107,6 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
     for (int q = 0; q < NS; ++q) {
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], want_w ? kSolveA + kSolveB : kSolveA);
-    }
-    for (int q = 0; q < 2; ++q) {
-      mbar_init(&xready[q], kSolveA);
-      mbar_init(&xfree[q], kSolveB);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
       const int64_t row0 = p.unit * g.unit_rows + (int64_t)p.cu * CH;
       double* xb = xs0 + (f & 1) * (GB * 8 * PX);
       mbar_wait(&full[s], (uint32_t)(use & 1));
-      if (want_w && f >= 2) mbar_wait(&xfree[f & 1], (uint32_t)(((f >> 1) - 1) & 1));
+      if (want_w && f >= 2) nbar_sync(3 + (f & 1), kSolveAB);  // B is done with this x buffer (use f - 2)
       const double* Ys = ring + s * Cfg::STAGE;
       const double* Xs = Ys + 2 * Cfg::PANEL;
       const double* Ws = Xs + Cfg::XT;
@@ -193,10 +197,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) {
-        if (want_w) mbar_arrive(&xready[f & 1]);
-        mbar_arrive(&empty[s]);
-      }
+      if (want_w) nbar_arrive(1 + (f & 1), kSolveAB);  // x tile of chunk f ready for B
+      if (lane == 0) mbar_arrive(&empty[s]);
       advance(p);
       if (++s == NS) s = 0, ++use;
     }
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
     const int sub = p.cu % NSUB;  // TMA chunk within the canonical 64-row chunk
     const double* xb = xs0 + (f & 1) * (GB * 8 * PX);
     mbar_wait(&full[s], (uint32_t)(use & 1));
-    mbar_wait(&xready[f & 1], (uint32_t)((f >> 1) & 1));
+    nbar_sync(1 + (f & 1), kSolveAB);
     const double* Vs = ring + s * Cfg::STAGE + Cfg::PANEL;
 #pragma unroll
     for (int k = 0; k < T2; ++k) {
@@ -237,10 +239,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
       }
     }
     __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&xfree[f & 1]);
-      mbar_arrive(&empty[s]);
-    }
+    nbar_arrive(3 + (f & 1), kSolveAB);
+    if (lane == 0) mbar_arrive(&empty[s]);
     if (p.cu == cpu - 1) {  // unit complete: its w (or partial) out, running sums reset
 #pragma unroll
       for (int k = 0; k < T2; ++k) {
