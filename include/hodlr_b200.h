@@ -159,11 +159,15 @@ size_t hodlr_solve_workspace(const hodlr_desc* d, int nrhs);
 hodlr_status hodlr_factorize(const hodlr_desc* d, const hodlr_factors* f, void* work,
                              size_t work_bytes, void* stream);
 
-/* Alg. 3 from host memory: D / U / V (pinned host buffers in the reference
- * layout) are uploaded on copy_stream in the order the factorization consumes
- * them (D, U, V^(L), then V^(L-1) .. V^(1)) while the factorization runs on
- * `stream`, each level waiting only for its own V panel.  f->D / f->Y / f->V are
- * the device destinations (f->Y receives U).  fp64. */
+/* Alg. 3 from host memory: D / U / V (host buffers in the reference layout)
+ * are uploaded on copy_stream in the order the factorization consumes them (D,
+ * U, V^(L), then V^(L-1) .. V^(1)) while the factorization runs on `stream`,
+ * each level waiting only for its own V panel.  f->D / f->Y / f->V are the
+ * device destinations (f->Y receives U).  fp64.  Pinned buffers are copied
+ * directly (keep them alive until `stream` has passed the call); pageable ones
+ * stream through a library-owned pinned ring (host copy threads, the
+ * factorization enqueued by a second host thread as the panels land) and are
+ * no longer read once the call returns.  Calls are serialised per process. */
 hodlr_status hodlr_factorize_from_host(const hodlr_desc* d, const hodlr_factors* f, const void* D_host,
                                        const void* U_host, const void* V_host, void* work, size_t work_bytes,
                                        void* stream, void* copy_stream);
