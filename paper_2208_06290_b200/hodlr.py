@@ -608,13 +608,14 @@ class _SolveGraph:
         self.graph = _capture(lambda st: _lib.check(lib.hodlr_solve(*self._args, C.c_void_p(st)),
                                                     "hodlr_solve (capture)"), stream, dev)
 
-    def run(self, x_cm, stream):
-        """x_cm: (nrhs, N) contiguous on the device; overwritten with the solution."""
+    def run_from(self, b_cm, stream):
+        """b_cm: (nrhs, N) view of the rhs (any strides / dtype); returns a new
+        (nrhs, N) contiguous solution."""
         torch = _torch()
         with torch.cuda.stream(stream):
-            self.X.copy_(x_cm)
+            self.X.copy_(b_cm)
             self.graph.replay()
-            x_cm.copy_(self.X)
+            return self.X.clone()
 
 
 _GRAPH_AUTO_BYTES = 1 << 28  # graph=None: capture solves whose rhs block is <= 256 MB
@@ -654,25 +655,27 @@ def solve(fact: HodlrFactorization, b, stream=None, graph: bool | None = None):
         # upload first (a pinned host rhs is one async DMA), then lay out column-major
         # on the device: (nrhs, n) row-major == (n, nrhs) column-major
         bd = bt.to(device=dev, non_blocking=True) if bt.device != dev else bt
-        x = bd.reshape(n, nrhs).t().to(dtype=fact.D.dtype).contiguous()
-        if x.data_ptr() == bt.data_ptr():
-            x = x.clone()
-        if nrhs > 0:
-            key = (nrhs, so.cuda_stream)
-            graphs = fact.__dict__.setdefault("_solve_graphs", {})
-            g = graphs.get(key) if graph is not False else None
-            if g is not None and not torch.cuda.is_current_stream_capturing():
-                g.run(x, so)
-            else:
-                _solve_eager(lib, fact, x, nrhs, dev, so)
-                if graph is not False and not torch.cuda.is_current_stream_capturing():
-                    calls = fact.__dict__.setdefault("_solve_calls", {})
-                    calls[key] = calls.get(key, 0) + 1
-                    # capture after the eager call(s) -- later calls replay.  graph=None captures
-                    # only latency-bound sizes (the graph owns an N x nrhs buffer + workspace)
-                    small = n * nrhs * x.element_size() <= _GRAPH_AUTO_BYTES
-                    if graph or (calls[key] >= 2 and small):
-                        graphs[key] = _SolveGraph(fact, nrhs, so)
+        key = (nrhs, so.cuda_stream)
+        graphs = fact.__dict__.setdefault("_solve_graphs", {})
+        g = graphs.get(key) if (graph is not False and nrhs > 0) else None
+        if g is not None and not torch.cuda.is_current_stream_capturing():
+            # replay: lay b out column-major straight into the graph's buffer,
+            # then one copy out (the graph owns and reuses its X)
+            x = g.run_from(bd.reshape(n, nrhs).t(), so)
+        else:
+            x = bd.reshape(n, nrhs).t().to(dtype=fact.D.dtype).contiguous()
+            if x.data_ptr() == bt.data_ptr():
+                x = x.clone()
+        if nrhs > 0 and (g is None or torch.cuda.is_current_stream_capturing()):
+            _solve_eager(lib, fact, x, nrhs, dev, so)
+            if graph is not False and not torch.cuda.is_current_stream_capturing():
+                calls = fact.__dict__.setdefault("_solve_calls", {})
+                calls[key] = calls.get(key, 0) + 1
+                # capture after the eager call(s) -- later calls replay.  graph=None captures
+                # only latency-bound sizes (the graph owns an N x nrhs buffer + workspace)
+                small = n * nrhs * x.element_size() <= _GRAPH_AUTO_BYTES
+                if graph or (calls[key] >= 2 and small):
+                    graphs[key] = _SolveGraph(fact, nrhs, so)
         out = x.t().reshape(bt.shape)
         if bt.device == dev:
             return out
