@@ -154,12 +154,13 @@ def test_random_vs_oracle(n, m, r, s):
     assert relres(x) <= max(1e-12, 4 * relres(orc.solve(fo, b, threads=8)))
 
 
-@pytest.mark.parametrize("nrhs", [5, 12, 16, 20, 27, 40, 64, 72])
+@pytest.mark.parametrize("nrhs", [5, 12, 16, 20, 27, 40, 64, 72, 131, 257])
 @pytest.mark.parametrize("r", [16, 32, 64])
 def test_multi_rhs_columns_bitwise_equal_single(nrhs, r):
     # column j of a blocked solve == single-vector solve, bit for bit
-    # (<= 8 columns: the streaming kernel; 9-64: the band-major multi-group kernel in
-    # passes of <= 4 groups of 8; more: the shared-panel TMA kernel)
+    # (<= 24/32 columns: the warp-specialized TMA solve step; more: the shared-panel
+    # kernels; rank 32 with >= 128 columns: level_update6 in solve mode for the
+    # leading 16-group blocks + the shared-panel kernel for the rest)
     n, m = 1 << 13, 64
     h = hb.random_hodlr(n, m, r, seed=3, s=16.0)
     f = hb.factorize(h)
