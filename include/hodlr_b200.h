@@ -188,6 +188,12 @@ hodlr_status hodlr_matvec(const hodlr_desc* d, const void* D, const void* U, con
                           int64_t ldx, void* Y, int64_t ldy, int nrhs, void* work, size_t work_bytes,
                           void* stream);
 
+/* Layout helper of the solve API: X[c * ldx + i] = B[i * ldb + c] for i < n,
+ * c < k (a row-major n x k block to column-major, or back with the roles of
+ * n / k swapped), fp64, asynchronous on `stream`. */
+hodlr_status hodlr_transpose_f64(const void* B, int64_t n, int64_t k, int64_t ldb, void* X, int64_t ldx,
+                                 void* stream);
+
 /* HODLR assembly on the device (SPEC.md:163-171 [OP] assemble): leaf blocks
  * D materialized exactly; every sibling off-diagonal block A(I_a, I_b)
  * compressed to U_a V_b^T by ACA with rook pivoting at rank cap r (replaces

@@ -89,6 +89,7 @@ SIGNATURES = {
     "hodlr_build_dense": (_i, [C.POINTER(Desc), _p, _i64, _p, _p, _p, _p, _sz, _p]),
     "hodlr_build_gaussian": (_i, [C.POINTER(Desc), _p, _i, _d, _d, _p, _p, _p, _p, _sz, _p]),
     "hodlr_build_schur_plane": (_i, [C.POINTER(Desc), _p, _d, _p, _p, _p, _p, _sz, _p]),
+    "hodlr_transpose_f64": (_i, [_p, _i64, _i64, _i64, _p, _i64, _p]),
 }
 
 _lib = None

@@ -608,14 +608,29 @@ class _SolveGraph:
         self.graph = _capture(lambda st: _lib.check(lib.hodlr_solve(*self._args, C.c_void_p(st)),
                                                     "hodlr_solve (capture)"), stream, dev)
 
-    def run_from(self, b_cm, stream):
-        """b_cm: (nrhs, N) view of the rhs (any strides / dtype); returns a new
-        (nrhs, N) contiguous solution."""
+    def run_from(self, bd, stream):
+        """bd: the (N,) / (N, nrhs) rhs on the device; returns a new (nrhs, N)
+        contiguous solution (column-major N x nrhs)."""
         torch = _torch()
         with torch.cuda.stream(stream):
-            self.X.copy_(b_cm)
+            _to_column_major(bd, self.X, stream)
             self.graph.replay()
             return self.X.clone()
+
+
+def _to_column_major(bd, out, stream):
+    """out (nrhs, N) contiguous <- the rhs bd (N,) or (N, nrhs): one copy, and for a
+    row-major fp64 block the library's tiled transpose (torch's strided copy of
+    this shape runs at ~0.8 TB/s)."""
+    torch = _torch()
+    n, k = out.shape[1], out.shape[0]
+    b2 = bd.reshape(n, k)
+    if k > 1 and b2.dtype == torch.float64 and out.dtype == torch.float64 and b2.stride(1) == 1 and b2.stride(0) >= k:
+        _lib.check(_lib.load().hodlr_transpose_f64(C.c_void_p(b2.data_ptr()), n, k, b2.stride(0),
+                                                   C.c_void_p(out.data_ptr()), n, C.c_void_p(stream.cuda_stream)),
+                   "hodlr_transpose_f64")
+    else:
+        out.copy_(b2.t())
 
 
 _GRAPH_AUTO_BYTES = 1 << 28  # graph=None: capture solves whose rhs block is <= 256 MB
@@ -661,11 +676,10 @@ def solve(fact: HodlrFactorization, b, stream=None, graph: bool | None = None):
         if g is not None and not torch.cuda.is_current_stream_capturing():
             # replay: lay b out column-major straight into the graph's buffer,
             # then one copy out (the graph owns and reuses its X)
-            x = g.run_from(bd.reshape(n, nrhs).t(), so)
+            x = g.run_from(bd, so)
         else:
-            x = bd.reshape(n, nrhs).t().to(dtype=fact.D.dtype).contiguous()
-            if x.data_ptr() == bt.data_ptr():
-                x = x.clone()
+            x = torch.empty((nrhs, n), dtype=fact.D.dtype, device=dev)
+            _to_column_major(bd, x, so)
         if nrhs > 0 and (g is None or torch.cuda.is_current_stream_capturing()):
             _solve_eager(lib, fact, x, nrhs, dev, so)
             if graph is not False and not torch.cuda.is_current_stream_capturing():
@@ -679,7 +693,12 @@ def solve(fact: HodlrFactorization, b, stream=None, graph: bool | None = None):
         out = x.t().reshape(bt.shape)
         if bt.device == dev:
             return out
-        # host result: async copy into pinned memory, then wait for the stream
+        # host result: back to row-major on the device, async copy into pinned memory, wait
+        if nrhs > 1 and x.dtype == torch.float64:
+            rm = torch.empty((n, nrhs), dtype=x.dtype, device=dev)
+            _lib.check(lib.hodlr_transpose_f64(C.c_void_p(x.data_ptr()), nrhs, n, n, C.c_void_p(rm.data_ptr()), nrhs,
+                                               C.c_void_p(so.cuda_stream)), "hodlr_transpose_f64")
+            out = rm.reshape(bt.shape)
         host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
         host.copy_(out, non_blocking=True)
         so.synchronize()
