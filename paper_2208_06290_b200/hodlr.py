@@ -256,7 +256,9 @@ class HodlrMatrix:
         wsb = lib.hodlr_matvec_workspace(C.byref(desc), nrhs)
         so = stream or torch.cuda.current_stream(dev)
         with torch.cuda.device(dev), torch.cuda.stream(so):
-            X = xt.reshape(n, nrhs).t().to(device=dev, dtype=self.dtype).contiguous()  # column-major N x nrhs
+            xd = xt.to(device=dev, non_blocking=True) if xt.device != dev else xt
+            X = torch.empty((nrhs, n), dtype=self.dtype, device=dev)  # column-major N x nrhs
+            _to_column_major(xd, X, so)
             Y = torch.empty_like(X)
             ws = _workspace(wsb, dev, so) if wsb else None
             _lib.check(
@@ -267,6 +269,11 @@ class HodlrMatrix:
                 "hodlr_matvec",
             )
             out = Y.t().reshape(xt.shape)
+            if (is_np or xt.device != dev) and nrhs > 1 and Y.dtype == torch.float64:
+                rm = torch.empty((n, nrhs), dtype=Y.dtype, device=dev)  # row-major on the device first
+                _lib.check(lib.hodlr_transpose_f64(C.c_void_p(Y.data_ptr()), nrhs, n, n, C.c_void_p(rm.data_ptr()),
+                                                   nrhs, C.c_void_p(so.cuda_stream)), "hodlr_transpose_f64")
+                out = rm.reshape(xt.shape)
             if is_np:
                 res = out.cpu().numpy()  # synchronous on `so`
             elif xt.device != dev:
