@@ -145,12 +145,12 @@ def test_lu_known_answers():  # :261-275
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-@pytest.mark.parametrize("s", [16, 32, 64, 128])
-def test_lu_nonfinite_and_degenerate_blocks_bit_exact(s, dtype):
+@pytest.mark.parametrize("s,nb", [(16, 12), (32, 12), (64, 12), (128, 12), (64, 2053)])
+def test_lu_nonfinite_and_degenerate_blocks_bit_exact(s, nb, dtype):
     # NaN wins the pivot search (np.argmax), +-inf, exact ties, zero columns, duplicate
-    # rows (singular flags) -- factors (NaN-aware), pivots and flags as the reference
+    # rows (singular flags) -- factors (NaN-aware), pivots and flags as the reference;
+    # nb > 2048: the full-wave register-row kernel (blocks in lockstep per CTA, ragged tail)
     rng = np.random.default_rng(s)
-    nb = 12
     base = rng.standard_normal((nb, s, s))
     base[0, 3, 0] = np.nan
     base[1, :, 2] = 0.0
@@ -173,7 +173,7 @@ def test_lu_nonfinite_and_degenerate_blocks_bit_exact(s, dtype):
     assert sorted(piv.singular) == sorted(np.flatnonzero(p.singular).tolist())
 
 
-@pytest.mark.parametrize("s,nb", [(64, 512), (64, 296), (64, 1), (32, 300), (32, 148), (16, 1000), (128, 40), (128, 300), (7, 33)])
+@pytest.mark.parametrize("s,nb", [(64, 512), (64, 296), (64, 1), (64, 4099), (32, 300), (32, 148), (16, 1000), (128, 40), (128, 300), (7, 33)])
 def test_lu_bit_exact_vs_reference_order(s, nb):
     rng = np.random.default_rng(s * 1000 + nb)
     base = rng.standard_normal(nb * s * s)
