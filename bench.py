@@ -546,6 +546,9 @@ def run_ours(args):
                          "achieved": lvl_achieved, "peak": dgemm, "unit": "TFLOP/s",
                          "frac": (lvl_achieved / dgemm) if (lvl_achieved and dgemm) else None,
                          "peak_source": "measured cuBLAS DGEMM 8192^3 in this run (MEASURED_PEAKS.json has no fp64)",
+                         "alt_peak": {"tflops": 37.11, "frac": (lvl_achieved / 37.11) if lvl_achieved else None,
+                                      "source": "DMMA micro-benchmark ceiling (32 warps/SM of independent "
+                                                "mma.m8n8k4.f64, 1965 MHz), profiles/r01_fp64_peak_probe.txt"},
                          "traffic": traffic, "level_steps_per_step": level_launches,
                          "flops_per_step": level_flops(n, m, r)},
             "clocks": clk.summary(), "wall_s_timed": wall,
